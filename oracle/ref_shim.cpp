@@ -1,0 +1,237 @@
+// ref_shim.cpp — extern "C" entry points over the COMPILED REFERENCE (test infrastructure).
+//
+// oracle/Makefile compiles this file together with the reference's own sources, in place under
+// /root/reference/proj/core/src (tensor.cpp, rng.cpp, parallel.cpp, linalg.cpp, attention.cpp),
+// into oracle/_ref/libjagged_ref.so. Nothing here restates arithmetic: each function builds the
+// reference's own JaggedTensor/Jagged2Tensor/DenseTensor and calls the reference operator, so the
+// results are the reference's results. Used to (1) pin oracle/jagged_oracle.c, (2) generate
+// tests/golden fixtures, (3) time the reference CPU path in bench.py (cpu_baseline, --impl reference).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "jagged/attention.hpp"
+#include "jagged/linalg.hpp"
+#include "jagged/rng.hpp"
+#include "jagged/tensor.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+template <typename T>
+std::vector<T> vec(const T* p, int64_t n) {
+  return std::vector<T>(p, p + n);
+}
+
+template <typename T>
+jagged::JaggedTensor<T> jt(const int64_t* off, int64_t B, int64_t dim, const T* v) {
+  return jagged::JaggedTensor<T>(vec(off, B + 1), vec(v, off[B] * dim), dim);
+}
+
+template <typename T>
+jagged::Jagged2Tensor<T> j2(const int64_t* off, int64_t B, const T* v) {
+  std::vector<int64_t> lens(B);
+  int64_t sq = 0;
+  for (int64_t i = 0; i < B; ++i) {
+    lens[i] = off[i + 1] - off[i];
+    sq += lens[i] * lens[i];
+  }
+  return jagged::Jagged2Tensor<T>(lens, vec(v, sq));
+}
+
+template <typename T>
+void put(const std::vector<T>& src, T* dst) {
+  std::memcpy(dst, src.data(), src.size() * sizeof(T));
+}
+
+jagged::KernelOptions kopts(int threads, int64_t block) {
+  jagged::KernelOptions o;
+  o.block = block > 0 ? block : 64;
+  o.threads = threads > 0 ? threads : 1;
+  return o;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+}  // namespace
+
+#define REF_T(T, SUF)                                                                              \
+  extern "C" int ref_jagged_dense_bmm_##SUF(const int64_t* off, int64_t B, int64_t D, int64_t Tt, \
+                                            const T* x, const T* w, int threads, T* out) {         \
+    return guard([&] {                                                                             \
+      auto r = jagged::jagged_dense_bmm(jt(off, B, D, x),                                          \
+                                        jagged::DenseTensor<T>({B, D, Tt}, vec(w, B * D * Tt)),   \
+                                        kopts(threads, 64));                                       \
+      put(r.values(), out);                                                                        \
+    });                                                                                            \
+  }                                                                                                \
+  extern "C" int ref_jagged_jagged_bmm_##SUF(const int64_t* off, int64_t B, int64_t D, int64_t Tt,\
+                                             const T* x, const T* y, int threads, T* out) {        \
+    return guard([&] {                                                                             \
+      auto r = jagged::jagged_jagged_bmm(jt(off, B, D, x), jt(off, B, Tt, y), kopts(threads, 64)); \
+      put(r.data(), out);                                                                          \
+    });                                                                                            \
+  }                                                                                                \
+  extern "C" int ref_jagged_softmax_##SUF(const int64_t* off, int64_t B, int64_t D, const T* x,   \
+                                          int threads, T* out) {                                   \
+    return guard([&] { put(jagged::jagged_softmax(jt(off, B, D, x), kopts(threads, 64)).values(), out); }); \
+  }                                                                                                \
+  extern "C" int ref_jagged_jagged_bmm_jagged_out_##SUF(const int64_t* off, int64_t B, int64_t D,  \
+                                                        const T* q, const T* k, int threads,       \
+                                                        T* out) {                                  \
+    return guard([&] {                                                                             \
+      put(jagged::jagged_jagged_bmm_jagged_out(jt(off, B, D, q), jt(off, B, D, k),                \
+                                               kopts(threads, 64)).values(), out);                 \
+    });                                                                                            \
+  }                                                                                                \
+  extern "C" int ref_array_jagged_bmm_jagged_out_##SUF(const int64_t* off, int64_t B, int64_t D,   \
+                                                       const T* a, const T* v, int threads,        \
+                                                       T* out) {                                   \
+    return guard([&] {                                                                             \
+      put(jagged::array_jagged_bmm_jagged_out(j2(off, B, a), jt(off, B, D, v),                    \
+                                              kopts(threads, 64)).values(), out);                  \
+    });                                                                                            \
+  }                                                                                                \
+  extern "C" int ref_jagged2_softmax_##SUF(const int64_t* off, int64_t B, const T* s, int threads, \
+                                           T* out) {                                               \
+    return guard([&] { put(jagged::jagged2_softmax(j2(off, B, s), kopts(threads, 64)).values(), out); }); \
+  }                                                                                                \
+  extern "C" int ref_jagged_attention_##SUF(const int64_t* off, int64_t B, int64_t D, const T* q,  \
+                                            const T* k, const T* v, int threads, T* out) {         \
+    return guard([&] {                                                                             \
+      put(jagged::jagged_attention(jt(off, B, D, q), jt(off, B, D, k), jt(off, B, D, v),          \
+                                   kopts(threads, 64)).values(), out);                             \
+    });                                                                                            \
+  }                                                                                                \
+  extern "C" int ref_jfa_forward_##SUF(const int64_t* off, int64_t B, int64_t D, const T* q,       \
+                                       const T* k, const T* v, int64_t bq, int64_t bk,             \
+                                       int threads, T* out, T* lse) {                              \
+    return guard([&] {                                                                             \
+      auto s = jagged::jagged_flash_attention_forward(jt(off, B, D, q), jt(off, B, D, k),         \
+                                                      jt(off, B, D, v), bq, bk,                    \
+                                                      kopts(threads, 64));                         \
+      put(s.output.values(), out);                                                                 \
+      put(s.logsumexp, lse);                                                                       \
+    });                                                                                            \
+  }                                                                                                \
+  extern "C" int ref_jfa_backward_##SUF(const int64_t* off, int64_t B, int64_t D, const T* q,      \
+                                        const T* k, const T* v, const T* go, const T* o,           \
+                                        const T* lse, int64_t bq, int64_t bk, int threads, T* dq,  \
+                                        T* dk, T* dv) {                                            \
+    return guard([&] {                                                                             \
+      jagged::JaggedAttentionSaved<T> saved{jt(off, B, D, o), vec(lse, off[B]), bq, bk};           \
+      auto g = jagged::jagged_flash_attention_backward(jt(off, B, D, q), jt(off, B, D, k),        \
+                                                       jt(off, B, D, v), jt(off, B, D, go), saved, \
+                                                       kopts(threads, 64));                        \
+      put(g.dq.values(), dq);                                                                      \
+      put(g.dk.values(), dk);                                                                      \
+      put(g.dv.values(), dv);                                                                      \
+    });                                                                                            \
+  }
+
+REF_T(float, f32)
+REF_T(double, f64)
+
+// VJPs: the reference's registry and gradcheck use the double instantiation.
+extern "C" int ref_jagged_dense_bmm_vjp_f64(const int64_t* off, int64_t B, int64_t D, int64_t T,
+                                            const double* x, const double* w, const double* go,
+                                            double* dx, double* dw) {
+  return guard([&] {
+    auto g = jagged::jagged_dense_bmm_vjp(jt(off, B, D, x),
+                                          jagged::DenseTensor<double>({B, D, T}, vec(w, B * D * T)),
+                                          jt(off, B, T, go));
+    put(g.dx.values(), dx);
+    put(g.dw.data(), dw);
+  });
+}
+extern "C" int ref_jagged_jagged_bmm_vjp_f64(const int64_t* off, int64_t B, int64_t D, int64_t T,
+                                             const double* x, const double* y, const double* go,
+                                             double* dx, double* dy) {
+  return guard([&] {
+    auto g = jagged::jagged_jagged_bmm_vjp(jt(off, B, D, x), jt(off, B, T, y),
+                                           jagged::DenseTensor<double>({B, D, T}, vec(go, B * D * T)));
+    put(g.dx.values(), dx);
+    put(g.dy.values(), dy);
+  });
+}
+extern "C" int ref_jagged_softmax_vjp_f64(const int64_t* off, int64_t B, int64_t D,
+                                          const double* x, const double* go, double* dx) {
+  return guard([&] { put(jagged::jagged_softmax_vjp(jt(off, B, D, x), jt(off, B, D, go)).values(), dx); });
+}
+extern "C" int ref_jagged_jagged_bmm_jagged_out_vjp_f64(const int64_t* off, int64_t B, int64_t D,
+                                                        const double* q, const double* k,
+                                                        const double* go, double* dq, double* dk) {
+  return guard([&] {
+    auto g = jagged::jagged_jagged_bmm_jagged_out_vjp(jt(off, B, D, q), jt(off, B, D, k), j2(off, B, go));
+    put(g.dq.values(), dq);
+    put(g.dk.values(), dk);
+  });
+}
+extern "C" int ref_array_jagged_bmm_jagged_out_vjp_f64(const int64_t* off, int64_t B, int64_t D,
+                                                       const double* a, const double* v,
+                                                       const double* go, double* da, double* dv) {
+  return guard([&] {
+    auto g = jagged::array_jagged_bmm_jagged_out_vjp(j2(off, B, a), jt(off, B, D, v), jt(off, B, D, go));
+    put(g.da.values(), da);
+    put(g.dv.values(), dv);
+  });
+}
+extern "C" int ref_jagged2_softmax_vjp_f64(const int64_t* off, int64_t B, const double* s,
+                                           const double* go, double* ds) {
+  return guard([&] { put(jagged::jagged2_softmax_vjp(j2(off, B, s), j2(off, B, go)).values(), ds); });
+}
+
+// Reference generators (rng.cpp) so the oracle's restated RNG can be pinned bit-exactly.
+extern "C" int ref_gen_lengths(int kind, int64_t max_len, uint64_t seed, int64_t batch,
+                               int64_t* out) {
+  return guard([&] {
+    jagged::LengthDistribution d;
+    d.kind = kind == 0 ? jagged::LengthKind::fixed
+                       : (kind == 1 ? jagged::LengthKind::uniform : jagged::LengthKind::half_mean);
+    d.max_len = max_len;
+    d.seed = seed;
+    put(jagged::gen_lengths(d, batch), out);
+  });
+}
+extern "C" int ref_uniform_values_f64(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+  return guard([&] {
+    jagged::Rng r(seed);
+    put(jagged::uniform_values<double>(r, n, lo, hi), out);
+  });
+}
+extern "C" int ref_uniform_values_f32(uint64_t seed, int64_t n, double lo, double hi, float* out) {
+  return guard([&] {
+    jagged::Rng r(seed);
+    put(jagged::uniform_values<float>(r, n, lo, hi), out);
+  });
+}
+extern "C" int ref_make_offsets(const int64_t* lengths, int64_t B, int64_t* offsets) {
+  return guard([&] {
+    auto x = jagged::make_jagged<double>(std::span<const int64_t>(lengths, B), std::vector<double>(
+        [&] { int64_t s = 0; for (int64_t i = 0; i < B; ++i) s += lengths[i] > 0 ? lengths[i] : 0; return s; }()), 1);
+    put(x.offsets(), offsets);
+  });
+}
+extern "C" int ref_jagged_to_dense_f64(const int64_t* off, int64_t B, int64_t D, const double* x,
+                                       int64_t L, double pad, double* out) {
+  return guard([&] { put(jagged::jagged_to_dense(jt(off, B, D, x), L, pad).data(), out); });
+}
+extern "C" int ref_hardware_threads(void) {
+  return static_cast<int>(std::thread::hardware_concurrency());
+}
+extern "C" const char* ref_last_error(void) { return g_err.c_str(); }
