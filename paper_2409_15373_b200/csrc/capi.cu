@@ -1,0 +1,539 @@
+// capi.cu — the extern "C" boundary (include/jagged_b200.h): argument validation with the
+// reference's error texts, per-op GemmDesc construction, stream-ordered scratch, dispatch to the
+// SIMT or tcgen05 kernels. No host fallback exists: every op either launches device work or fails.
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace jg {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+jg_status fail(jg_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+jg_status cuda_status(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? JG_OUT_OF_MEMORY : JG_CUDA_ERROR;
+}
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int device_sm_count() {
+  static std::mutex mu;
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && cached[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : kNumSMsB200;
+    // keep stream-ordered scratch cached in the default pool between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  return dev < 64 ? cached[dev] : kNumSMsB200;
+}
+
+// RAII stream-ordered scratch
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  jg_status alloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync");
+    return JG_OK;
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+static bool dtype_ok(jg_dtype d) { return d == JG_F32 || d == JG_BF16; }
+static size_t dsize(jg_dtype d) { return d == JG_F32 ? 4 : (d == JG_BF16 ? 2 : 8); }
+
+#define REQUIRE(cond, code, msg) \
+  do {                           \
+    if (!(cond)) return ::jg::fail(code, msg); \
+  } while (0)
+
+#define CHECK_DT(op, dt) \
+  REQUIRE((dt) != JG_F64, JG_UNSUPPORTED, std::string(op) + ": f64 has no device path (no CPU fallback)"); \
+  REQUIRE(dtype_ok(dt), JG_INVALID_ARGUMENT, std::string(op) + ": unknown dtype")
+
+static jg_status gemm(const GemmDesc& g, const int64_t* off, const int64_t* sq, int64_t batch, const void* A,
+                      const void* B, void* C, jg_dtype in_dt, jg_dtype out_dt, cudaStream_t st) {
+  Scratch prefix(st);
+  jg_status rc = prefix.alloc(sizeof(int64_t) * (batch + 1));
+  if (rc) return rc;
+  return launch_grouped_gemm(g, off, sq, batch, A, B, C, in_dt, out_dt, (int64_t*)prefix.p, st);
+}
+
+static GemmDesc desc(Lin M, Lin N, Lin K, Lin a0, Lin sam, Lin sak, Lin b0, Lin sbk, Lin sbn, Lin c0, Lin scm,
+                     Lin scn) {
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K;
+  g.a0 = a0; g.sam = sam; g.sak = sak;
+  g.b0 = b0; g.sbk = sbk; g.sbn = sbn;
+  g.c0 = c0; g.scm = scm; g.scn = scn;
+  return g;
+}
+static Lin OFF(int64_t k, int64_t c = 0) { Lin l; l.off = k; l.c = c; return l; }
+static Lin SQ(int64_t c = 0) { Lin l; l.sq = 1; l.c = c; return l; }
+static Lin IDX(int64_t k) { Lin l; l.idx = k; return l; }
+static Lin C_(int64_t c) { return L_const(c); }
+static Lin BI() { return L_bi(1); }
+
+static jg_status check_out(const char* op, jg_dtype in, jg_dtype out) {
+  CHECK_DT(op, in);
+  REQUIRE(out == in || (in == JG_BF16 && out == JG_F32), JG_INVALID_ARGUMENT,
+          std::string(op) + ": out_dtype must equal in_dtype or be f32 for bf16 inputs");
+  return JG_OK;
+}
+
+}  // namespace jg
+
+using namespace jg;
+
+// ============================================================================ misc
+extern "C" const char* jg_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* jg_version(void) { return "jagged_b200 0.1 (sm_100a)"; }
+extern "C" int64_t jg_launch_count(void) { return g_launches.load(); }
+extern "C" void jg_reset_launch_count(void) { g_launches.store(0); }
+
+// ============================================================================ offsets layer
+extern "C" jg_status jg_make_offsets(const int64_t* lengths, int64_t batch, int64_t* offsets,
+                                     int64_t* bad_sample, void* stream) {
+  REQUIRE(batch >= 0, JG_INVALID_ARGUMENT, "make_jagged: batch must be >= 0");
+  return launch_scan(0, lengths, batch, offsets, bad_sample, as_stream(stream));
+}
+
+extern "C" jg_status jg_segment_lengths(const int64_t* offsets, int64_t batch, int64_t* lengths, void* stream) {
+  REQUIRE(batch >= 0, JG_INVALID_ARGUMENT, "segment_lengths: batch must be >= 0");
+  return launch_lengths(offsets, batch, lengths, as_stream(stream));
+}
+
+extern "C" jg_status jg_sq_offsets(const int64_t* offsets, int64_t batch, int64_t* sq_offsets, void* stream) {
+  REQUIRE(batch >= 0, JG_INVALID_ARGUMENT, "Jagged2Tensor: batch must be >= 0");
+  return launch_scan(1, offsets, batch, sq_offsets, nullptr, as_stream(stream));
+}
+
+struct jg_schedule_s {
+  const int64_t* offsets;
+  int64_t batch, total_rows, max_items;
+  int64_t* lengths;
+  int64_t* sq;
+  int2* items;
+  int64_t* n_items;
+  void* block;
+};
+
+extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, int64_t total_rows, void* stream,
+                                        jg_schedule* out) {
+  REQUIRE(batch >= 0 && total_rows >= 0 && out, JG_INVALID_ARGUMENT, "schedule: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  device_sm_count();
+  auto* s = new jg_schedule_s();
+  s->offsets = offsets;
+  s->batch = batch;
+  s->total_rows = total_rows;
+  s->max_items = total_rows / 128 + batch + 1;
+  const size_t b_len = sizeof(int64_t) * (batch + 1), b_sq = sizeof(int64_t) * (batch + 1),
+               b_items = sizeof(int2) * s->max_items;
+  const size_t bytes = b_len + b_sq + b_items + 64;
+  cudaError_t e = cudaMallocAsync(&s->block, bytes, st);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_status(e, "schedule alloc");
+  }
+  char* p = (char*)s->block;
+  s->lengths = (int64_t*)p; p += b_len;
+  s->sq = (int64_t*)p; p += b_sq;
+  s->n_items = (int64_t*)p; p += 64;
+  s->items = (int2*)p;
+  jg_status rc = JG_OK;
+  if (batch > 0) {
+    if ((rc = launch_lengths(offsets, batch, s->lengths, st))) goto err;
+    if ((rc = launch_scan(1, offsets, batch, s->sq, nullptr, st))) goto err;
+    if ((rc = launch_work_list(offsets, batch, 128, s->items, s->n_items, st))) goto err;
+  } else {
+    JG_CUDA(cudaMemsetAsync(s->n_items, 0, sizeof(int64_t), st));
+    JG_CUDA(cudaMemsetAsync(s->sq, 0, sizeof(int64_t), st));
+  }
+  *out = s;
+  return JG_OK;
+err:
+  cudaFreeAsync(s->block, st);
+  delete s;
+  return rc;
+}
+
+extern "C" jg_status jg_schedule_destroy(jg_schedule s) {
+  if (!s) return JG_OK;
+  cudaError_t e = cudaFree(s->block);
+  delete s;
+  if (e != cudaSuccess) return cuda_status(e, "schedule free");
+  return JG_OK;
+}
+
+extern "C" const int64_t* jg_schedule_sq_offsets(jg_schedule s) { return s ? s->sq : nullptr; }
+
+extern "C" jg_status jg_schedule_work_list(jg_schedule s, int32_t* host_items, int64_t capacity, int64_t* count) {
+  REQUIRE(s && count, JG_INVALID_ARGUMENT, "schedule_work_list: null argument");
+  JG_CUDA(cudaDeviceSynchronize());
+  int64_t n = 0;
+  JG_CUDA(cudaMemcpy(&n, s->n_items, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  *count = n;
+  if (host_items && capacity > 0) {
+    const int64_t m = n < capacity ? n : capacity;
+    JG_CUDA(cudaMemcpy(host_items, s->items, sizeof(int2) * m, cudaMemcpyDeviceToHost));
+  }
+  return JG_OK;
+}
+
+// ============================================================================ conversions
+extern "C" jg_status jg_jagged_to_dense(const int64_t* offsets, int64_t batch, int64_t dim, const void* x,
+                                        int64_t max_len, double pad_value, void* out, jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged_to_dense", dtype);
+  REQUIRE(max_len >= 0, JG_INVALID_ARGUMENT, "jagged_to_dense: max_len must be >= 0");
+  REQUIRE(dim > 0, JG_INVALID_ARGUMENT, "JaggedTensor: dim must be positive");
+  return launch_jagged_to_dense(offsets, batch, dim, x, max_len, pad_value, out, dtype, as_stream(stream));
+}
+
+extern "C" jg_status jg_dense_to_jagged(const void* d, int64_t batch, int64_t max_len, int64_t dim,
+                                        const int64_t* offsets, int64_t total_rows, int64_t max_segment, void* out,
+                                        jg_dtype dtype, void* stream) {
+  CHECK_DT("dense_to_jagged", dtype);
+  REQUIRE(max_segment <= max_len, JG_INVALID_ARGUMENT,
+          "dense_to_jagged: a sample length " + std::to_string(max_segment) + " exceeds max_len " +
+              std::to_string(max_len));
+  return launch_dense_to_jagged(d, batch, max_len, dim, offsets, total_rows, out, dtype, as_stream(stream));
+}
+
+extern "C" jg_status jg_jagged2_to_dense(const int64_t* offsets, const int64_t* sq_offsets, int64_t batch,
+                                         const void* s, int64_t max_len, double pad_value, void* out, jg_dtype dtype,
+                                         void* stream) {
+  CHECK_DT("jagged2_to_dense", dtype);
+  REQUIRE(max_len >= 0, JG_INVALID_ARGUMENT, "jagged2_to_dense: max_len must be >= 0");
+  return launch_jagged2_to_dense(offsets, sq_offsets, batch, s, max_len, pad_value, out, dtype, as_stream(stream));
+}
+
+extern "C" jg_status jg_dense_to_jagged2(const void* d, int64_t batch, int64_t max_len, const int64_t* offsets,
+                                         const int64_t* sq_offsets, int64_t max_segment, void* out, jg_dtype dtype,
+                                         void* stream) {
+  CHECK_DT("dense_to_jagged2", dtype);
+  REQUIRE(max_segment <= max_len, JG_INVALID_ARGUMENT,
+          "dense_to_jagged2: a sample length " + std::to_string(max_segment) + " exceeds max_len " +
+              std::to_string(max_len));
+  return launch_dense_to_jagged2(d, batch, max_len, offsets, sq_offsets, batch * max_len, out, dtype,
+                                 as_stream(stream));
+}
+
+extern "C" jg_status jg_elementwise(int32_t op, const void* a, const void* b, int64_t n, void* out, jg_dtype dtype,
+                                    void* stream) {
+  CHECK_DT("elementwise", dtype);
+  REQUIRE(op >= 0 && op <= 2, JG_INVALID_ARGUMENT, "elementwise: op must be 0 (add), 1 (sub) or 2 (mul)");
+  return launch_elementwise(op, a, b, n, 0.0, out, dtype, as_stream(stream));
+}
+
+extern "C" jg_status jg_scale(const void* a, int64_t n, double s, void* out, jg_dtype dtype, void* stream) {
+  CHECK_DT("scale", dtype);
+  return launch_elementwise(3, a, nullptr, n, s, out, dtype, as_stream(stream));
+}
+
+// ============================================================================ Table-1 operators
+extern "C" jg_status jg_jagged_dense_bmm(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D, int64_t T,
+                                         const void* x, const void* w, void* out, jg_dtype in_dt, jg_dtype out_dt,
+                                         void* stream) {
+  if (jg_status rc = check_out("jagged_dense_bmm", in_dt, out_dt)) return rc;
+  REQUIRE(D > 0 && T > 0, JG_INVALID_ARGUMENT, "jagged_dense_bmm: w must be [B, D, T]");
+  (void)total_rows;
+  GemmDesc g = desc(BI(), C_(T), C_(D), OFF(D), C_(D), C_(1), IDX(D * T), C_(T), C_(1), OFF(T), C_(T), C_(1));
+  return gemm(g, off, nullptr, batch, x, w, out, in_dt, out_dt, as_stream(stream));
+}
+
+extern "C" jg_status jg_jagged_jagged_bmm(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D, int64_t T,
+                                          const void* x, const void* y, void* out, jg_dtype in_dt, jg_dtype out_dt,
+                                          void* stream) {
+  if (jg_status rc = check_out("jagged_jagged_bmm", in_dt, out_dt)) return rc;
+  REQUIRE(D > 0 && T > 0, JG_INVALID_ARGUMENT, "jagged_jagged_bmm: dims must be positive");
+  (void)total_rows;
+  GemmDesc g = desc(C_(D), C_(T), BI(), OFF(D), C_(1), C_(D), OFF(T), C_(T), C_(1), IDX(D * T), C_(T), C_(1));
+  return gemm(g, off, nullptr, batch, x, y, out, in_dt, out_dt, as_stream(stream));
+}
+
+extern "C" jg_status jg_jagged_softmax(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D,
+                                       const void* x, void* out, jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged_softmax", dtype);
+  (void)total_rows;
+  return launch_jagged_softmax(off, batch, D, x, nullptr, out, dtype, false, as_stream(stream));
+}
+
+extern "C" jg_status jg_jagged_jagged_bmm_jagged_out(const int64_t* off, const int64_t* sq, int64_t batch,
+                                                     int64_t total_rows, int64_t D, const void* q, const void* k,
+                                                     void* out, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
+  if (jg_status rc = check_out("jagged_jagged_bmm_jagged_out", in_dt, out_dt)) return rc;
+  REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged_jagged_bmm_jagged_out: sq_offsets required");
+  (void)total_rows;
+  GemmDesc g = desc(BI(), BI(), C_(D), OFF(D), C_(D), C_(1), OFF(D), C_(1), C_(D), SQ(), BI(), C_(1));
+  return gemm(g, off, sq, batch, q, k, out, in_dt, out_dt, as_stream(stream));
+}
+
+extern "C" jg_status jg_array_jagged_bmm_jagged_out(const int64_t* off, const int64_t* sq, int64_t batch,
+                                                    int64_t total_rows, int64_t D, const void* a, const void* v,
+                                                    void* out, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
+  if (jg_status rc = check_out("array_jagged_bmm_jagged_out", in_dt, out_dt)) return rc;
+  REQUIRE(sq, JG_INVALID_ARGUMENT, "array_jagged_bmm_jagged_out: sq_offsets required");
+  (void)total_rows;
+  GemmDesc g = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
+  return gemm(g, off, sq, batch, a, v, out, in_dt, out_dt, as_stream(stream));
+}
+
+extern "C" jg_status jg_jagged2_softmax(const int64_t* off, const int64_t* sq, int64_t batch, const void* s, void* out,
+                                        jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged2_softmax", dtype);
+  REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged2_softmax: sq_offsets required");
+  const int64_t total_rows = -1;  // read from offsets[batch] on device
+  return launch_jagged2_softmax(off, sq, batch, total_rows, s, nullptr, out, dtype, false, as_stream(stream));
+}
+
+// ---------------------------------------------------------------------------- VJPs
+extern "C" jg_status jg_jagged_dense_bmm_vjp(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D,
+                                             int64_t T, const void* x, const void* w, const void* go, void* dx,
+                                             void* dw, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
+  if (jg_status rc = check_out("jagged_dense_bmm_vjp", in_dt, out_dt)) return rc;
+  (void)total_rows;
+  cudaStream_t st = as_stream(stream);
+  GemmDesc gx = desc(BI(), C_(D), C_(T), OFF(T), C_(T), C_(1), IDX(D * T), C_(1), C_(T), OFF(D), C_(D), C_(1));
+  if (jg_status rc = gemm(gx, off, nullptr, batch, go, w, dx, in_dt, out_dt, st)) return rc;
+  GemmDesc gw = desc(C_(D), C_(T), BI(), OFF(D), C_(1), C_(D), OFF(T), C_(T), C_(1), IDX(D * T), C_(T), C_(1));
+  return gemm(gw, off, nullptr, batch, x, go, dw, in_dt, out_dt, st);
+}
+
+extern "C" jg_status jg_jagged_jagged_bmm_vjp(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D,
+                                              int64_t T, const void* x, const void* y, const void* go, void* dx,
+                                              void* dy, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
+  if (jg_status rc = check_out("jagged_jagged_bmm_vjp", in_dt, out_dt)) return rc;
+  (void)total_rows;
+  cudaStream_t st = as_stream(stream);
+  GemmDesc gx = desc(BI(), C_(D), C_(T), OFF(T), C_(T), C_(1), IDX(D * T), C_(1), C_(T), OFF(D), C_(D), C_(1));
+  if (jg_status rc = gemm(gx, off, nullptr, batch, y, go, dx, in_dt, out_dt, st)) return rc;
+  GemmDesc gy = desc(BI(), C_(T), C_(D), OFF(D), C_(D), C_(1), IDX(D * T), C_(T), C_(1), OFF(T), C_(T), C_(1));
+  return gemm(gy, off, nullptr, batch, x, go, dy, in_dt, out_dt, st);
+}
+
+extern "C" jg_status jg_jagged_softmax_vjp(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D,
+                                           const void* x, const void* go, void* dx, jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged_softmax_vjp", dtype);
+  (void)total_rows;
+  return launch_jagged_softmax(off, batch, D, x, go, dx, dtype, true, as_stream(stream));
+}
+
+extern "C" jg_status jg_jagged_jagged_bmm_jagged_out_vjp(const int64_t* off, const int64_t* sq, int64_t batch,
+                                                         int64_t total_rows, int64_t D, const void* q, const void* k,
+                                                         const void* go, void* dq, void* dk, jg_dtype in_dt,
+                                                         jg_dtype out_dt, void* stream) {
+  if (jg_status rc = check_out("jagged_jagged_bmm_jagged_out_vjp", in_dt, out_dt)) return rc;
+  (void)total_rows;
+  cudaStream_t st = as_stream(stream);
+  GemmDesc gq = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
+  if (jg_status rc = gemm(gq, off, sq, batch, go, k, dq, in_dt, out_dt, st)) return rc;
+  GemmDesc gk = desc(BI(), C_(D), BI(), SQ(), C_(1), BI(), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
+  return gemm(gk, off, sq, batch, go, q, dk, in_dt, out_dt, st);
+}
+
+extern "C" jg_status jg_array_jagged_bmm_jagged_out_vjp(const int64_t* off, const int64_t* sq, int64_t batch,
+                                                        int64_t total_rows, int64_t D, const void* a, const void* v,
+                                                        const void* go, void* da, void* dv, jg_dtype in_dt,
+                                                        jg_dtype out_dt, void* stream) {
+  if (jg_status rc = check_out("array_jagged_bmm_jagged_out_vjp", in_dt, out_dt)) return rc;
+  (void)total_rows;
+  cudaStream_t st = as_stream(stream);
+  GemmDesc ga = desc(BI(), BI(), C_(D), OFF(D), C_(D), C_(1), OFF(D), C_(1), C_(D), SQ(), BI(), C_(1));
+  if (jg_status rc = gemm(ga, off, sq, batch, go, v, da, in_dt, out_dt, st)) return rc;
+  GemmDesc gv = desc(BI(), C_(D), BI(), SQ(), C_(1), BI(), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
+  return gemm(gv, off, sq, batch, a, go, dv, in_dt, out_dt, st);
+}
+
+extern "C" jg_status jg_jagged2_softmax_vjp(const int64_t* off, const int64_t* sq, int64_t batch, const void* s,
+                                            const void* go, void* ds, jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged2_softmax_vjp", dtype);
+  const int64_t total_rows = -1;  // read from offsets[batch] on device
+  return launch_jagged2_softmax(off, sq, batch, total_rows, s, go, ds, dtype, true, as_stream(stream));
+}
+
+// ============================================================================ attention
+static bool force_simt() {
+  const char* e = std::getenv("JG_ATTN_IMPL");
+  return e && std::strcmp(e, "simt") == 0;
+}
+
+extern "C" int64_t jg_attention_backward_workspace_size(int64_t total_rows, int32_t num_heads, int32_t head_dim) {
+  const int64_t delta = ((total_rows * num_heads * 4 + 255) / 256) * 256;
+  const int64_t acc = total_rows * num_heads * (int64_t)head_dim * 4;
+  return delta + acc + 256;
+}
+
+extern "C" jg_status jg_jagged_flash_attention_forward(const int64_t* off, int64_t batch, int64_t total_rows,
+                                                       int32_t H, int32_t D, const void* q, const void* k,
+                                                       const void* v, int64_t block_q, int64_t block_k, void* out,
+                                                       float* lse, jg_dtype dtype, jg_schedule sched, void* stream) {
+  CHECK_DT("jagged_flash_attention_forward", dtype);
+  REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
+          "jagged_flash_attention_forward: block sizes must be >= 1");
+  REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_forward: dim mismatch");
+  cudaStream_t st = as_stream(stream);
+  if (total_rows == 0) return JG_OK;
+  if (!force_simt() && attn_sm100_supported(D, dtype)) {
+    jg_schedule own = nullptr;
+    if (!sched) {
+      if (jg_status rc = jg_schedule_create(off, batch, total_rows, stream, &own)) return rc;
+      sched = own;
+    }
+    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items,
+                                         sched->n_items, sched->max_items, st);
+    if (own) {
+      cudaStreamSynchronize(st);
+      jg_schedule_destroy(own);
+    }
+    return rc;
+  }
+  return launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, st);
+}
+
+extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int64_t batch, int64_t total_rows,
+                                                        int32_t H, int32_t D, const void* q, const void* k,
+                                                        const void* v, const void* go, const void* o,
+                                                        const float* lse, int64_t block_q, int64_t block_k, void* dq,
+                                                        void* dk, void* dv, jg_dtype dtype, jg_schedule sched,
+                                                        void* workspace, void* stream) {
+  CHECK_DT("jagged_flash_attention_backward", dtype);
+  REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
+          "jagged_flash_attention_backward: saved state does not match inputs");
+  REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_backward: grad_out layout mismatch");
+  cudaStream_t st = as_stream(stream);
+  if (total_rows == 0) return JG_OK;
+  Scratch ws(st);
+  if (!workspace) {
+    if (jg_status rc = ws.alloc(jg_attention_backward_workspace_size(total_rows, H, D))) return rc;
+    workspace = ws.p;
+  }
+  float* delta = (float*)workspace;
+  float* dq_acc = (float*)((char*)workspace + ((total_rows * H * 4 + 255) / 256) * 256);
+  if (!force_simt() && attn_sm100_supported(D, dtype)) {
+    jg_schedule own = nullptr;
+    if (!sched) {
+      if (jg_status rc = jg_schedule_create(off, batch, total_rows, stream, &own)) return rc;
+      sched = own;
+    }
+    jg_status rc = launch_attn_bwd_sm100(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta,
+                                         dq_acc, sched->items, sched->n_items, sched->max_items, st);
+    if (own) {
+      cudaStreamSynchronize(st);
+      jg_schedule_destroy(own);
+    }
+    return rc;
+  }
+  return launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype, st);
+}
+
+extern "C" jg_status jg_jagged_attention(const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows,
+                                         int64_t sum_sq, int32_t H, int32_t D, const void* q, const void* k,
+                                         const void* v, void* out, jg_dtype dtype, void* scores_ws, void* stream) {
+  CHECK_DT("jagged_attention", dtype);
+  REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged_attention: sq_offsets required");
+  cudaStream_t st = as_stream(stream);
+  if (total_rows == 0) return JG_OK;
+  const size_t es = dsize(dtype);
+  Scratch ws(st);
+  if (!scores_ws) {
+    if (jg_status rc = ws.alloc(2 * es * (size_t)sum_sq * H)) return rc;
+    scores_ws = ws.p;
+  }
+  char* S = (char*)scores_ws;
+  char* P = S + es * (size_t)sum_sq * H;
+  const int64_t RS = (int64_t)H * D;
+  for (int h = 0; h < H; ++h) {
+    const int64_t ho = (int64_t)h * D;
+    char* Sh = S + es * (size_t)sum_sq * h;
+    char* Ph = P + es * (size_t)sum_sq * h;
+    // jagged_jagged_bmm_jagged_out (attention.cpp:167) on head h
+    GemmDesc gs = desc(BI(), BI(), C_(D), OFF(RS, ho), C_(RS), C_(1), OFF(RS, ho), C_(1), C_(RS), SQ(), BI(), C_(1));
+    if (jg_status rc = gemm(gs, off, sq, batch, q, k, Sh, dtype, dtype, st)) return rc;
+  }
+  // scale by 1/sqrt(D), rounded to the element type (attention.cpp:166-167)
+  const double inv = dtype == JG_F32 ? (double)(float)(1.0 / std::sqrt((double)D)) : 1.0 / std::sqrt((double)D);
+  if (jg_status rc = launch_elementwise(3, S, nullptr, sum_sq * H, inv, S, dtype, st)) return rc;
+  for (int h = 0; h < H; ++h) {
+    const int64_t ho = (int64_t)h * D;
+    char* Sh = S + es * (size_t)sum_sq * h;
+    char* Ph = P + es * (size_t)sum_sq * h;
+    if (jg_status rc = launch_jagged2_softmax(off, sq, batch, total_rows, Sh, nullptr, Ph, dtype, false, st)) return rc;
+    GemmDesc go = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(RS, ho), C_(RS), C_(1), OFF(RS, ho), C_(RS), C_(1));
+    if (jg_status rc = gemm(go, off, sq, batch, Ph, v, out, dtype, dtype, st)) return rc;
+  }
+  return JG_OK;
+}
+
+extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_offsets, int64_t batch, int32_t H,
+                                                            int32_t D, const void* q, const void* k, const void* v,
+                                                            const void* go, void* out, float* lse, void* dq, void* dk,
+                                                            void* dv, jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged_flash_attention", dtype);
+  REQUIRE(host_offsets && batch >= 0, JG_INVALID_ARGUMENT, "jagged_flash_attention: offsets required");
+  REQUIRE(host_offsets[0] == 0, JG_INVALID_ARGUMENT, "JaggedTensor: offsets must start with 0");
+  for (int64_t i = 1; i <= batch; ++i)
+    REQUIRE(host_offsets[i] >= host_offsets[i - 1], JG_INVALID_ARGUMENT,
+            "JaggedTensor: offsets must be non-decreasing at index " + std::to_string(i));
+  cudaStream_t st = as_stream(stream);
+  const int64_t S = host_offsets[batch];
+  const size_t tb = (size_t)S * H * D * dsize(dtype);
+  const size_t lb = (size_t)S * H * sizeof(float);
+  const size_t ob = sizeof(int64_t) * (batch + 1);
+  const size_t ws = (size_t)jg_attention_backward_workspace_size(S, H, D);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  Scratch buf(st);
+  if (jg_status rc = buf.alloc(al(ob) + 8 * al(tb) + al(lb) + al(ws))) return rc;
+  char* p = (char*)buf.p;
+  int64_t* d_off = (int64_t*)p; p += al(ob);
+  char* t[8];
+  for (int j = 0; j < 8; ++j) { t[j] = p; p += al(tb); }
+  float* d_lse = (float*)p; p += al(lb);
+  void* d_ws = p;
+  JG_CUDA(cudaMemcpyAsync(d_off, host_offsets, ob, cudaMemcpyHostToDevice, st));
+  JG_CUDA(cudaMemcpyAsync(t[0], q, tb, cudaMemcpyHostToDevice, st));
+  JG_CUDA(cudaMemcpyAsync(t[1], k, tb, cudaMemcpyHostToDevice, st));
+  JG_CUDA(cudaMemcpyAsync(t[2], v, tb, cudaMemcpyHostToDevice, st));
+  JG_CUDA(cudaMemcpyAsync(t[3], go, tb, cudaMemcpyHostToDevice, st));
+  jg_schedule sched = nullptr;
+  if (jg_status rc = jg_schedule_create(d_off, batch, S, stream, &sched)) return rc;
+  jg_status rc = jg_jagged_flash_attention_forward(d_off, batch, S, H, D, t[0], t[1], t[2], 64, 64, t[4], d_lse,
+                                                   dtype, sched, stream);
+  if (!rc)
+    rc = jg_jagged_flash_attention_backward(d_off, batch, S, H, D, t[0], t[1], t[2], t[3], t[4], d_lse, 64, 64, t[5],
+                                            t[6], t[7], dtype, sched, d_ws, stream);
+  if (!rc) {
+    cudaMemcpyAsync(out, t[4], tb, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(lse, d_lse, lb, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dq, t[5], tb, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dk, t[6], tb, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dv, t[7], tb, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_status(e, "fwd_bwd_host");
+  }
+  jg_schedule_destroy(sched);
+  return rc;
+}

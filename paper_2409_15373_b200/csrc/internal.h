@@ -1,0 +1,81 @@
+// internal.h — launcher declarations shared between the kernel files and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "jagged_b200.h"
+
+namespace jg {
+
+// ------------------------------------------------------------------ per-sample affine descriptors
+// Every jagged contraction of the bmm family (and its VJPs) is, per sample i, a strided GEMM
+// C_i[M x N] = sum_k A_i[m,k] B_i[k,n]. Each size/offset/stride is an affine function of the
+// sample's length Bi, row offset off_i, square offset sq_i and index i; one kernel covers all
+// eight contractions of linalg.cpp:34-197 and :283-472.
+struct Lin {
+  int64_t bi = 0, off = 0, sq = 0, idx = 0, c = 0;
+  __host__ __device__ int64_t at(int64_t Bi, int64_t o, int64_t s, int64_t i) const {
+    return bi * Bi + off * o + sq * s + idx * i + c;
+  }
+};
+inline Lin L_const(int64_t c) { Lin l; l.c = c; return l; }
+inline Lin L_bi(int64_t k = 1) { Lin l; l.bi = k; return l; }
+
+struct GemmDesc {
+  Lin M, N, K;
+  Lin a0, sam, sak;  // A(m,k) = A[a0 + m*sam + k*sak]
+  Lin b0, sbk, sbn;  // B(k,n) = B[b0 + k*sbk + n*sbn]
+  Lin c0, scm, scn;  // C(m,n) = C[c0 + m*scm + n*scn]
+};
+
+jg_status launch_scan(int mode, const int64_t* in, int64_t n, int64_t* out, int64_t* bad, cudaStream_t s);
+jg_status launch_lengths(const int64_t* off, int64_t n, int64_t* len, cudaStream_t s);
+jg_status launch_work_list(const int64_t* off, int64_t batch, int tile, int2* items, int64_t* count,
+                           cudaStream_t s);
+
+jg_status launch_jagged_to_dense(const int64_t* off, int64_t batch, int64_t dim, const void* x,
+                                 int64_t max_len, double pad, void* out, jg_dtype dt, cudaStream_t s);
+jg_status launch_dense_to_jagged(const void* d, int64_t batch, int64_t max_len, int64_t dim,
+                                 const int64_t* off, int64_t total_rows, void* out, jg_dtype dt,
+                                 cudaStream_t s);
+jg_status launch_jagged2_to_dense(const int64_t* off, const int64_t* sq, int64_t batch, const void* x,
+                                  int64_t max_len, double pad, void* out, jg_dtype dt, cudaStream_t s);
+jg_status launch_dense_to_jagged2(const void* d, int64_t batch, int64_t max_len, const int64_t* off,
+                                  const int64_t* sq, int64_t total_rows_hint, void* out, jg_dtype dt,
+                                  cudaStream_t s);
+jg_status launch_elementwise(int op, const void* a, const void* b, int64_t n, double sc, void* out,
+                             jg_dtype dt, cudaStream_t s);
+
+jg_status launch_jagged_softmax(const int64_t* off, int64_t batch, int64_t D, const void* x,
+                                const void* g, void* out, jg_dtype dt, bool vjp, cudaStream_t st);
+jg_status launch_jagged2_softmax(const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows,
+                                 const void* s, const void* g, void* out, jg_dtype dt, bool vjp,
+                                 cudaStream_t st);
+
+// Grouped strided GEMM over samples. tile_prefix: device scratch of batch+1 int64.
+jg_status launch_grouped_gemm(const GemmDesc& g, const int64_t* off, const int64_t* sq, int64_t batch,
+                              const void* A, const void* B, void* C, jg_dtype in_dt, jg_dtype out_dt,
+                              int64_t* tile_prefix, cudaStream_t st);
+
+// SIMT attention (fp32 mode, and any head_dim the tensor-core path does not cover)
+jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
+                               const void* q, const void* k, const void* v, void* out, float* lse,
+                               jg_dtype dt, cudaStream_t st);
+jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
+                               const void* q, const void* k, const void* v, const void* go,
+                               const void* o, const float* lse, void* dq, void* dk, void* dv,
+                               float* delta, jg_dtype dt, cudaStream_t st);
+
+// tcgen05 attention (bf16, head_dim 64/128)
+bool attn_sm100_supported(int head_dim, jg_dtype dt);
+jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
+                                const void* q, const void* k, const void* v, void* out, float* lse,
+                                const int2* items, const int64_t* n_items, int64_t max_items,
+                                cudaStream_t st);
+jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
+                                const void* q, const void* k, const void* v, const void* go,
+                                const void* o, const float* lse, void* dq, void* dk, void* dv,
+                                float* delta, float* dq_accum, const int2* items,
+                                const int64_t* n_items, int64_t max_items, cudaStream_t st);
+
+}  // namespace jg

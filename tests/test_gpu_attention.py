@@ -1,0 +1,146 @@
+"""GPU parity of jagged flash attention (forward + backward) and the unfused jagged attention.
+
+All results go through the C-ABI; the oracle (binary64, pinned to the reference) runs per head on
+the same rounded inputs. fp32 mode: 1e-5 relative (norm-wise + RMS-floored elementwise). bf16:
+2e-2 max-abs. Edge cases follow SPEC.md:280-300 (Bi=0 rows do not exist, Bi=1 -> out = v,
+dv = grad_out, dq = dk = 0) and block-size invariance.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import restated as R
+from tests.parity import assert_bf16_close, assert_fp32_close, bf16_round, f32_round
+
+pytestmark = pytest.mark.gpu
+J = pytest.importorskip("paper_2409_15373_b200.jagged")
+DEV = "cuda"
+
+
+def make(ln, H, D, seed, dtype):
+    ln = np.asarray(ln, np.int64)
+    off = R.make_offsets(ln)
+    S = int(off[-1])
+    rnd = f32_round if dtype == torch.float32 else bf16_round
+    vals = rnd(R.Rng(seed + 1).uniform_values(4 * S * H * D))
+    q, k, v, go = (vals[i * S * H * D:(i + 1) * S * H * D].reshape(S, H, D) for i in range(4))
+    toj = lambda a: J.JaggedTensor(torch.from_numpy(off).to(DEV), torch.from_numpy(a).to(dtype).to(DEV), off)  # noqa
+    return off, (q, k, v, go), tuple(toj(a) for a in (q, k, v, go))
+
+
+def oracle_per_head(off, q, k, v, go):
+    S, H, D = q.shape
+    out, lse = np.empty_like(q), np.empty((H, S))
+    dq, dk, dv = np.empty_like(q), np.empty_like(q), np.empty_like(q)
+    for h in range(H):
+        o_h, l_h = R.jfa_forward(off, q[:, h], k[:, h], v[:, h], 64, 64)
+        out[:, h], lse[h] = o_h, l_h
+        dq[:, h], dk[:, h], dv[:, h] = R.jfa_backward(off, q[:, h], k[:, h], v[:, h], go[:, h], o_h, l_h, 64)
+    return out, lse, dq, dk, dv
+
+
+CASES = [
+    ([0, 1, 2, 5, 7, 17, 33, 70, 130, 257], 1, 16),
+    ([3, 0, 128, 129, 255, 1, 64], 2, 64),
+    ([200, 5, 300, 0, 131], 2, 128),
+    (list(R.gen_lengths("zipf", 512, 0, 24, 1.1)), 1, 64),
+]
+
+
+@pytest.mark.parametrize("ln,H,D", CASES)
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_flash_attention_fwd_bwd(ln, H, D, mode):
+    dtype = torch.float32 if mode == "fp32" else torch.bfloat16
+    close = assert_fp32_close if mode == "fp32" else assert_bf16_close
+    off, (q, k, v, go), (Q, K, V, G) = make(ln, H, D, 5, dtype)
+    out, lse, dq, dk, dv = oracle_per_head(off, q, k, v, go)
+    saved = J.jagged_flash_attention_forward(Q, K, V, 64, 64)
+    close(saved.output.values, out, what="out")
+    # lse is always float32; fp32-mode tolerance on it in both modes (bf16 inputs are exact in the oracle)
+    assert_fp32_close(saved.logsumexp, lse, tol=1e-5 if mode == "fp32" else 2e-3, what="lse")
+    # backward uses the oracle's saved state semantics: recompute from q, k, lse of the device forward
+    grads = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+    close(grads.dq.values, dq, what="dq")
+    close(grads.dk.values, dk, what="dk")
+    close(grads.dv.values, dv, what="dv")
+
+
+def test_flash_attention_golden(golden):
+    """The reference's own JFA outputs (tests/golden/attention.npz, binary64 inputs) in fp32 mode."""
+    a = golden["attention"]
+    off = a["offsets"]
+    toj = lambda x: J.JaggedTensor(torch.from_numpy(off).to(DEV), torch.from_numpy(x).float().to(DEV), off)  # noqa
+    Q, K, V, G = (toj(a[n]) for n in ("q", "k", "v", "go"))
+    saved = J.jagged_flash_attention_forward(Q, K, V, 3, 3)
+    assert_fp32_close(saved.output.values, a["out_b3x3"], tol=2e-5, what="out")
+    fin = np.isfinite(a["lse_b3x3"])
+    assert fin.all()  # empty segments have no rows
+    assert_fp32_close(saved.logsumexp.reshape(-1), a["lse_b3x3"], tol=2e-5, what="lse")
+    g = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+    assert_fp32_close(g.dq.values, a["dq_b3x3"], tol=5e-5, what="dq")
+    assert_fp32_close(g.dk.values, a["dk_b3x3"], tol=5e-5, what="dk")
+    assert_fp32_close(g.dv.values, a["dv_b3x3"], tol=5e-5, what="dv")
+    # unfused jagged attention
+    assert_fp32_close(J.jagged_attention(Q, K, V).values, a["jagged_attention"], tol=2e-5, what="unfused")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_single_row_segments(dtype):
+    """Bi=1 everywhere -> out = v, dv = grad_out, dq = dk = 0."""
+    off, (q, k, v, go), (Q, K, V, G) = make([1] * 37, 2, 64, 9, dtype)
+    saved = J.jagged_flash_attention_forward(Q, K, V)
+    torch.testing.assert_close(saved.output.values, V.values, rtol=0, atol=0)
+    g = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+    torch.testing.assert_close(g.dv.values.float(), G.values.float(), rtol=1e-6, atol=1e-6)
+    assert float(g.dq.values.abs().max()) < 1e-5 and float(g.dk.values.abs().max()) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_uniform_keys_average_values(dtype):
+    """all keys equal within a segment -> every output row = mean of the segment's V."""
+    ln = [5, 140, 3]
+    off, (q, k, v, go), (Q, K, V, G) = make(ln, 1, 64, 2, dtype)
+    kk = np.repeat(k[off[:-1]][:, None], 1, 1)
+    kconst = np.concatenate([np.repeat(k[off[i]:off[i] + 1], ln[i], 0) for i in range(3)])
+    Kc = J.JaggedTensor(K.offsets, torch.from_numpy(kconst).to(dtype).to(DEV), off)
+    out = J.jagged_flash_attention_forward(Q, Kc, V).output.values.double().cpu().numpy()
+    for i in range(3):
+        seg = slice(off[i], off[i + 1])
+        np.testing.assert_allclose(out[seg], np.broadcast_to(v[seg].mean(0), out[seg].shape),
+                                   atol=2e-2 if dtype == torch.bfloat16 else 1e-5)
+    del kk
+
+
+def test_zero_grad_out_gives_zero_grads():
+    off, _, (Q, K, V, G) = make([7, 0, 150], 1, 64, 3, torch.bfloat16)
+    Z = J.JaggedTensor(G.offsets, torch.zeros_like(G.values), off)
+    g = J.jagged_flash_attention_backward(Q, K, V, Z, J.jagged_flash_attention_forward(Q, K, V))
+    for t in (g.dq, g.dk, g.dv):
+        assert float(t.values.abs().max()) == 0.0
+
+
+def test_block_size_invariance_and_errors():
+    off, _, (Q, K, V, G) = make([9, 33], 1, 16, 4, torch.float32)
+    a = J.jagged_flash_attention_forward(Q, K, V, 1, 1).output.values
+    b = J.jagged_flash_attention_forward(Q, K, V, 64, 64).output.values
+    assert torch.equal(a, b)
+    with pytest.raises(J.JaggedError, match="block sizes must be >= 1"):
+        J.jagged_flash_attention_forward(Q, K, V, 0, 64)
+    K2 = J.JaggedTensor(torch.from_numpy(R.make_offsets([10, 32])).to(DEV), K.values, R.make_offsets([10, 32]))
+    with pytest.raises(J.JaggedError, match="q, k, v must share offsets"):
+        J.jagged_flash_attention_forward(Q, K2, V)
+    saved = J.jagged_flash_attention_forward(Q, K, V)
+    saved.logsumexp = saved.logsumexp[:, :5]
+    with pytest.raises(J.JaggedError, match="saved state does not match inputs"):
+        J.jagged_flash_attention_backward(Q, K, V, G, saved)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_unfused_matches_flash(dtype):
+    off, (q, k, v, go), (Q, K, V, G) = make([4, 0, 33, 70], 2, 32, 6, dtype)
+    ref = np.stack([R.jagged_attention(off, q[:, h], k[:, h], v[:, h]) for h in range(2)], 1)
+    got = J.jagged_attention(Q, K, V).values
+    if dtype == torch.float32:
+        assert_fp32_close(got, ref, what="unfused")
+    else:
+        assert_bf16_close(got, ref, tol=3e-2, what="unfused (bf16 scores materialized)")

@@ -1,0 +1,81 @@
+"""CPU tests: synthetic-input generator bit-exactness and multi-rank sharding (gloo, world size 2)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import reference as F
+from oracle import restated as R
+from paper_2409_15373_b200 import shard, synth
+
+
+@pytest.mark.parametrize("kind,L,B,seed", [("uniform", 128, 64, 0), ("half-mean", 1024, 1024, 0),
+                                           ("half-mean", 50, 33, 9), ("fixed", 7, 3, 1), ("uniform", 4096, 777, 5)])
+def test_synth_lengths_bit_exact(kind, L, B, seed):
+    got = synth.gen_lengths(kind, L, seed, B)
+    np.testing.assert_array_equal(got, R.gen_lengths(kind, L, seed, B))
+    if F.available():
+        np.testing.assert_array_equal(got, F.gen_lengths(kind, L, seed, B))
+
+
+@pytest.mark.parametrize("alpha,L,B", [(1.1, 512, 256), (0.8, 4096, 4096)])
+def test_synth_zipf_bit_exact(alpha, L, B):
+    np.testing.assert_array_equal(synth.gen_lengths("zipf", L, 0, B, alpha), R.gen_lengths("zipf", L, 0, B, alpha))
+
+
+def test_synth_rng_stream():
+    a, b = synth.Rng(123), R.Rng(123)
+    for _ in range(1000):
+        assert a.next_u64() == b.next_u64()
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_shard_bounds_cover_and_balance(world):
+    ln = synth.gen_lengths("half-mean", 1024, 0, 1024 * world)
+    b = shard.shard_bounds(ln, world)
+    assert b[0] == 0 and b[-1] == len(ln) and (np.diff(b) >= 0).all()
+    cost = np.array([int((ln[b[k]:b[k + 1]] ** 2).sum()) for k in range(world)])
+    assert abs(cost - cost.mean()).max() <= 1024 ** 2  # imbalance bounded by one sample
+    rows = sum(shard.make_shard(ln, world, k).row_end - shard.make_shard(ln, world, k).row_begin for k in range(world))
+    assert rows == ln.sum()
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ln = synth.gen_lengths("half-mean", 1024, 0, 64 * world)
+    sh = shard.make_shard(ln, world, rank)
+    # each rank holds its contiguous value rows; gather them back and check the layout is bit-exact
+    off = synth.offsets_of(ln)
+    vals = torch.arange(int(off[-1]), dtype=torch.int64)[sh.row_begin:sh.row_end]
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([vals.numel()]))
+    mx = int(max(s.item() for s in sizes))
+    buf = torch.full((mx,), -1, dtype=torch.int64)
+    buf[:vals.numel()] = vals
+    outs = [torch.empty(mx, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(outs, buf)
+    full = torch.cat([o[:int(s.item())] for o, s in zip(outs, sizes)])
+    ok = bool(torch.equal(full, torch.arange(int(off[-1]))))
+    rebased_ok = bool((sh.offsets == off[sh.sample_begin:sh.sample_end + 1] - off[sh.sample_begin]).all())
+    # per-rank cost summed over ranks == total
+    c = torch.tensor([int((sh.lengths ** 2).sum())])
+    dist.all_reduce(c)
+    q.put((rank, ok, rebased_ok, int(c.item()) == int((ln ** 2).sum())))
+    dist.destroy_process_group()
+
+
+def test_sharded_layout_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok and rb and tot for _, ok, rb, tot in res), res
