@@ -433,7 +433,7 @@ extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int6
   }
   float* delta = (float*)workspace;
   float* dq_acc = (float*)((char*)workspace + ((total_rows * H * 4 + 255) / 256) * 256);
-  if (!force_simt() && attn_sm100_supported(D, dtype)) {
+  if (!force_simt() && attn_sm100_bwd_supported(D, dtype)) {
     jg_schedule own = nullptr;
     if (!sched) {
       if (jg_status rc = jg_schedule_create(off, batch, total_rows, stream, &own)) return rc;

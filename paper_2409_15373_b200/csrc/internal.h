@@ -68,6 +68,7 @@ jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_
 
 // tcgen05 attention (bf16, head_dim 64/128)
 bool attn_sm100_supported(int head_dim, jg_dtype dt);
+bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt);
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, void* out, float* lse,
                                 const int2* items, const int64_t* n_items, int64_t max_items,

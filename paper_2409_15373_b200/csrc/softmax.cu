@@ -4,7 +4,10 @@
 //
 // Semantics (linalg.cpp:98-120, :199-220, :355-388, :474-507): max-subtracted softmax, empty
 // segments untouched, p recomputed from x in the VJP. fp32 accumulation; exp via ex2.approx on
-// log2(e)-prescaled inputs (relative error ~2^-22, inside the 1e-5 fp32-mode tolerance).
+// log2(e)-prescaled inputs (relative error ~2^-22, inside the 1e-5 fp32-mode tolerance). The
+// prescale is an unfused __fmul_rn so the max pass and the exp pass see the identical value
+// (a contracted FMA would leave the product's rounding error in x*log2e - m, and Bi=1 must
+// give exactly 1.0).
 #include "common.cuh"
 #include "internal.h"
 
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
       float v[VEC];
       VecIO<T, VEC>::load(x + r * D + col, v);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) online_update(m[j], s[j], v[j] * kLog2e);
+      for (int j = 0; j < VEC; ++j) online_update(m[j], s[j], __fmul_rn(v[j], kLog2e));
     }
   }
   combine_ms<VEC>(m, s, sm_m, sm_s, col_local);
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
       float v[VEC];
       VecIO<T, VEC>::load(x + r * D + col, v);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] = exp2f(v[j] * kLog2e - m[j]) * inv[j];
+      for (int j = 0; j < VEC; ++j) v[j] = exp2f(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j];
       VecIO<T, VEC>::store(out + r * D + col, v);
     }
   } else {
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
         VecIO<T, VEC>::load(x + r * D + col, v);
         VecIO<T, VEC>::load(g + r * D + col, gv);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) dot[j] += gv[j] * (exp2f(v[j] * kLog2e - m[j]) * inv[j]);
+        for (int j = 0; j < VEC; ++j) dot[j] += gv[j] * (exp2f(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j]);
       }
     }
     __syncthreads();
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
       VecIO<T, VEC>::load(x + r * D + col, v);
       VecIO<T, VEC>::load(g + r * D + col, gv);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] = exp2f(v[j] * kLog2e - m[j]) * inv[j] * (gv[j] - dot[j]);
+      for (int j = 0; j < VEC; ++j) v[j] = exp2f(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j] * (gv[j] - dot[j]);
       VecIO<T, VEC>::store(out + r * D + col, v);
     }
   }
@@ -192,19 +195,19 @@ __global__ void __launch_bounds__(256) jagged2_softmax_kernel(const int64_t* __r
     const int64_t n = off[i + 1] - off[i], r = R - off[i];
     const int64_t base = sq[i] + r * n;
     float m = -INFINITY, sm = 0.f;
-    for (int64_t c = lane; c < n; c += 32) online_update(m, sm, ld(s + base + c) * kLog2e);
+    for (int64_t c = lane; c < n; c += 32) online_update(m, sm, __fmul_rn(ld(s + base + c), kLog2e));
     const float M = warp_max(m);
     const float S = warp_sum(m == -INFINITY ? 0.f : sm * exp2f(m - M));
     const float inv = 1.0f / S;
     if constexpr (MODE == 0) {
-      for (int64_t c = lane; c < n; c += 32) st(out + base + c, exp2f(ld(s + base + c) * kLog2e - M) * inv);
+      for (int64_t c = lane; c < n; c += 32) st(out + base + c, exp2f(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv);
     } else {
       float dot = 0.f;
       for (int64_t c = lane; c < n; c += 32)
-        dot += ld(g + base + c) * (exp2f(ld(s + base + c) * kLog2e - M) * inv);
+        dot += ld(g + base + c) * (exp2f(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv);
       dot = warp_sum(dot);
       for (int64_t c = lane; c < n; c += 32) {
-        const float p = exp2f(ld(s + base + c) * kLog2e - M) * inv;
+        const float p = exp2f(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv;
         st(out + base + c, p * (ld(g + base + c) - dot));
       }
     }
