@@ -1,0 +1,464 @@
+// attn_bwd_sm100.cu — Jagged Flash Attention backward on tcgen05 tensor cores (bf16, head_dim 128).
+//
+// Semantics: attention.cpp:227-289 (jagged_flash_attention_backward): recompute P = exp(S/sqrt(D) - lse)
+// from (q, k, lse), Delta = rowsum(dO * O), dV = P^T dO, dS = P * (dP - Delta) with dP = dO V^T,
+// dQ = dS K / sqrt(D), dK = dS^T Q / sqrt(D). Per segment only; no padding materialised.
+//
+// Three launches:
+//   1. prologue: Delta[h, r] = sum_d dO*O (fp32) and zero the fp32 dQ accumulator        (HBM-bound)
+//   2. main persistent kernel, key-stationary: a CTA owns 128 key rows of one (sample, head) and
+//      streams the sample's queries in 64-row blocks:
+//        S^T = K Q_j^T, dP^T = V dO_j^T                      (tcgen05, M=128 keys, N=64 queries)
+//        P^T, dS^T in registers -> smem (bf16, SWIZZLE_128B)  (softmax warpgroup, thread = key row)
+//        dV += P^T dO_j, dK += dS^T Q_j                      (accumulated in TMEM across all j)
+//        dQ_j^T = K^T dS^T                                    (M = head_dim, N = 64 queries)
+//      dQ_j^T is drained by a second warpgroup through smem and added into the fp32 accumulator with
+//      bulk async reductions (cp.reduce.async.bulk .add.f32, one 512 B row per query).
+//   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
+// Warps: 0 TMA producer, 1 MMA issuer, 4-7 softmax/dS, 8-11 dQ drain + dK/dV epilogue.
+// TMEM columns: S^T [0,64), dP^T [64,128), dQ^T [128,192), dV [256,384), dK [384,512).
+#include "common.cuh"
+#include "internal.h"
+#include "tc.cuh"
+#include "tma_host.h"
+
+namespace jg {
+namespace fb {
+
+constexpr int BKV = 128;  // key rows per CTA tile
+constexpr int BQ = 64;    // query rows per streamed block
+constexpr int kThreads = 384;
+constexpr int kSmWarp0 = 4, kDqWarp0 = 8;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct Smem {
+  static constexpr int kChunkKV = BKV * 128;  // [128 rows x 64] bf16 = 16 KB
+  static constexpr int kChunkQ = BQ * 128;    // [64 rows x 64] bf16 = 8 KB
+  static constexpr int kTileKV = (D / 64) * kChunkKV;
+  static constexpr int kTileQ = (D / 64) * kChunkQ;
+  static constexpr int kStages = 2;
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTileKV;
+  static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
+  static constexpr int kP = kQD + kStages * 2 * kTileQ;     // P^T  [128 keys x 64 q] bf16
+  static constexpr int kDS = kP + BKV * 128;                // dS^T [128 keys x 64 q] bf16
+  static constexpr int kStg = kDS + BKV * 128;              // dQ staging [64 q x D] fp32
+  static constexpr int kLse = kStg + BQ * D * 4;            // 2 x (64 lse + 64 delta) fp32
+  static constexpr int kBar = kLse + 2 * 2 * BQ * 4;
+  static constexpr int kNumBars = 2 + 2 * kStages + 2 + 2 + 2 + 2 + 1;
+  static constexpr int kBytes = kBar + kNumBars * 8 + 16;
+  static constexpr int kAlloc = kBytes + 1024;
+};
+
+struct Params {
+  const int64_t* off;
+  const int2* items;
+  const int64_t* n_items;
+  int64_t total_rows;
+  int H;
+  const float* lse;
+  const float* delta;
+  float* dq_acc;
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  float scale_log2;
+  float scale;
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    jfa_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                         Params p) {
+  using L = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* qd_full = bars + 2;
+  uint64_t* qd_empty = qd_full + L::kStages;
+  uint64_t* st_full = qd_empty + L::kStages;
+  uint64_t* st_empty = st_full + 1;
+  uint64_t* p_full = st_empty + 1;
+  uint64_t* pds_empty = p_full + 1;
+  uint64_t* dq_full = pds_empty + 1;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* dkv_full = dq_empty + 1;
+  uint64_t* dkv_empty = dkv_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(kv_full, 1);
+    tc::mbar_init(kv_empty, 1);
+    for (int s = 0; s < L::kStages; ++s) {
+      tc::mbar_init(qd_full + s, 1);
+      tc::mbar_init(qd_empty + s, 1);
+    }
+    tc::mbar_init(st_full, 1);
+    tc::mbar_init(st_empty, 4);
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(pds_empty, 1);
+    tc::mbar_init(dq_full, 1);
+    tc::mbar_init(dq_empty, 4);
+    tc::mbar_init(dkv_full, 1);
+    tc::mbar_init(dkv_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tm_q);
+    tc::tma_prefetch(&tm_k);
+    tc::tma_prefetch(&tm_v);
+    tc::tma_prefetch(&tm_do);
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int H = p.H;
+  const int64_t n_work = *p.n_items * H;
+
+  if (warp == 0) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      uint32_t item_cnt = 0, qd_cnt = 0;
+      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+        const int2 it = p.items[w / H];
+        const int h = (int)(w % H);
+        const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
+        const int nq = (int)((n + BQ - 1) / BQ);
+        const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
+        tc::mbar_wait(kv_empty, (item_cnt & 1) ^ 1);
+        tc::mbar_expect_tx(kv_full, 2 * L::kTileKV);
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, kv_full, c * 64, h, kv_row);
+          tc::tma_load_3d(smem + L::kV + c * L::kChunkKV, &tm_v, kv_full, c * 64, h, kv_row);
+        }
+        for (int j = 0; j < nq; ++j, ++qd_cnt) {
+          const uint32_t s = qd_cnt % L::kStages;
+          tc::mbar_wait(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1);
+          tc::mbar_expect_tx(qd_full + s, 2 * L::kTileQ);
+          uint8_t* qs = smem + L::kQD + s * 2 * L::kTileQ;
+          const int q_row = (int)(b0 + (int64_t)j * BQ);
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_load_3d(qs + c * L::kChunkQ, &tm_q, qd_full + s, c * 64, h, q_row);
+            tc::tma_load_3d(qs + L::kTileQ + c * L::kChunkQ, &tm_do, qd_full + s, c * 64, h, q_row);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t kIdS = tc::idesc_bf16_f32(BKV, BQ, false, false);  // S^T, dP^T
+      constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
+      constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
+      const uint32_t k_base = tc::smem_u32(smem + L::kK), v_base = tc::smem_u32(smem + L::kV);
+      const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
+      uint32_t item_cnt = 0, qd_cnt = 0, st_cnt = 0, p_cnt = 0, dq_cnt = 0;
+      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+        const int2 it = p.items[w / H];
+        const int64_t n = p.off[it.x + 1] - p.off[it.x];
+        const int nq = (int)((n + BQ - 1) / BQ);
+        tc::mbar_wait(kv_full, item_cnt & 1);
+        tc::mbar_wait(dkv_empty, (item_cnt & 1) ^ 1);
+        for (int j = 0; j < nq; ++j, ++qd_cnt) {
+          const uint32_t s = qd_cnt % L::kStages;
+          tc::mbar_wait(qd_full + s, (qd_cnt / L::kStages) & 1);
+          tc::mbar_wait(st_empty, (st_cnt & 1) ^ 1);
+          ++st_cnt;
+          tc::tc_fence_after();
+          const uint32_t q_base = tc::smem_u32(smem + L::kQD + s * 2 * L::kTileQ);
+          const uint32_t do_base = q_base + L::kTileQ;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
+            const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
+            tc::mma_bf16_ss(tmem + 0, tc::sw128_desc(k_base + ka, 16, 1024), tc::sw128_desc(q_base + kb, 16, 1024),
+                            kIdS, kk > 0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
+            const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
+            tc::mma_bf16_ss(tmem + 64, tc::sw128_desc(v_base + ka, 16, 1024), tc::sw128_desc(do_base + kb, 16, 1024),
+                            kIdS, kk > 0);
+          }
+          tc::mma_commit(st_full);
+          tc::mbar_wait(p_full, p_cnt & 1);
+          ++p_cnt;
+          tc::tc_fence_after();
+          // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk) {
+            tc::mma_bf16_ss(tmem + 256, tc::sw128_desc(p_base + kk * 32, 16, 1024),
+                            tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+          }
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk) {
+            tc::mma_bf16_ss(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
+                            tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+          }
+          // dQ_j^T = K^T dS^T  (A = K tile MN-major, M = head_dim; B = dS^T MN-major [128 keys x 64 q])
+          tc::mbar_wait(dq_empty, (dq_cnt & 1) ^ 1);
+          ++dq_cnt;
+          tc::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk) {
+            tc::mma_bf16_ss(tmem + 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
+                            tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
+          }
+          tc::mma_commit(dq_full);
+          tc::mma_commit(qd_empty + s);
+          tc::mma_commit(pds_empty);
+        }
+        tc::mma_commit(dkv_full);
+        tc::mma_commit(kv_empty);
+      }
+    }
+  } else if (warp >= kSmWarp0 && warp < kDqWarp0) {
+    // ===================================================== P^T / dS^T warpgroup (thread = key row)
+    const int tid = threadIdx.x - kSmWarp0 * 32;
+    const int wq = warp - kSmWarp0;
+    const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
+    const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
+    float* sm_ld = reinterpret_cast<float*>(smem + L::kLse);  // [2][lse 64 | delta 64]
+    uint32_t st_cnt = 0, pds_cnt = 0;
+    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int2 it = p.items[w / H];
+      const int h = (int)(w % H);
+      const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
+      const int nq = (int)((n + BQ - 1) / BQ);
+      const bool row_valid = (int64_t)it.y * BKV + tid < n;
+      for (int j = 0; j < nq; ++j) {
+        float* buf = sm_ld + (j & 1) * 2 * BQ;
+        {
+          const int64_t q = (int64_t)j * BQ + (tid & (BQ - 1));
+          const int64_t gi = (int64_t)h * p.total_rows + b0 + q;
+          if (tid < BQ) buf[tid] = q < n ? p.lse[gi] * kLog2e : INFINITY;
+          else buf[tid] = q < n ? p.delta[gi] : 0.f;
+        }
+        named_bar(1, 128);
+        tc::mbar_wait(st_full, st_cnt & 1);
+        ++st_cnt;
+        tc::tc_fence_after();
+        uint32_t pk[BQ / 2], dk2[BQ / 2];
+#pragma unroll
+        for (int c = 0; c < BQ / 32; ++c) {
+          uint32_t sr[32], dr[32];
+          tc::tmem_ld32(lane_addr + c * 32, sr);
+          tc::tmem_ld32(lane_addr + 64 + c * 32, dr);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int q0 = c * 32 + e;
+            float p0 = tc::ex2(__uint_as_float(sr[e]) * p.scale_log2 - buf[q0]);
+            float p1 = tc::ex2(__uint_as_float(sr[e + 1]) * p.scale_log2 - buf[q0 + 1]);
+            if (!row_valid) { p0 = 0.f; p1 = 0.f; }
+            const float d0 = p0 * (__uint_as_float(dr[e]) - buf[BQ + q0]);
+            const float d1 = p1 * (__uint_as_float(dr[e + 1]) - buf[BQ + q0 + 1]);
+            pk[q0 >> 1] = tc::pack_bf16(p0, p1);
+            dk2[q0 >> 1] = tc::pack_bf16(d0, d1);
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(st_empty);
+        tc::mbar_wait(pds_empty, (pds_cnt & 1) ^ 1);
+        ++pds_cnt;
+#pragma unroll
+        for (int u = 0; u < BQ / 8; ++u) {
+          const uint32_t o = tc::sw128_offset(tid, u);
+          tc::st_shared_v4(p_base + o, pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
+          tc::st_shared_v4(ds_base + o, dk2[u * 4], dk2[u * 4 + 1], dk2[u * 4 + 2], dk2[u * 4 + 3]);
+        }
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_full);
+      }
+    }
+  } else if (warp >= kDqWarp0) {
+    // ===================================================== dQ drain + dK/dV epilogue
+    const int tid = threadIdx.x - kDqWarp0 * 32;  // == TMEM lane: head-dim row of dQ^T, key row of dK/dV
+    const int wq = warp - kDqWarp0;
+    const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
+    float* stg = reinterpret_cast<float*>(smem + L::kStg);
+    const uint32_t stg_base = tc::smem_u32(stg);
+    uint32_t item_cnt = 0, dq_cnt = 0;
+    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+      const int2 it = p.items[w / H];
+      const int h = (int)(w % H);
+      const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
+      const int nq = (int)((n + BQ - 1) / BQ);
+      for (int j = 0; j < nq; ++j) {
+        tc::mbar_wait(dq_full, dq_cnt & 1);
+        ++dq_cnt;
+        tc::tc_fence_after();
+        uint32_t a[32], b[32];
+        tc::tmem_ld32(lane_addr + 128, a);
+        tc::tmem_ld32(lane_addr + 160, b);
+        tc::tmem_wait_ld();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(dq_empty);
+        if (tid < BQ) bulk_wait_read0();  // previous block's reductions have read the staging buffer
+        named_bar(2, 128);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) stg[q * D + tid] = __uint_as_float(a[q]) * p.scale;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) stg[(q + 32) * D + tid] = __uint_as_float(b[q]) * p.scale;
+        tc::fence_proxy_async_smem();
+        named_bar(2, 128);
+        if (tid < BQ) {
+          const int64_t q = (int64_t)j * BQ + tid;
+          if (q < n) {
+            bulk_reduce_add_f32(p.dq_acc + ((b0 + q) * H + h) * D, stg_base + tid * D * 4, D * 4);
+            bulk_commit();
+          }
+        }
+      }
+      // dK / dV for this key tile
+      tc::mbar_wait(dkv_full, item_cnt & 1);
+      tc::tc_fence_after();
+      const int64_t kv_local = (int64_t)it.y * BKV + tid;
+      const bool store = kv_local < n;
+      const int64_t gofs = ((b0 + kv_local) * H + h) * D;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        const uint32_t col = which == 0 ? 256 : 384;
+        const float sc = which == 0 ? 1.f : p.scale;
+        __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + gofs;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tc::tmem_ld32(lane_addr + col + c * 32, o);
+          tc::tmem_wait_ld();
+          if (store) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              uint4 v;
+              v.x = tc::pack_bf16(__uint_as_float(o[u * 8 + 0]) * sc, __uint_as_float(o[u * 8 + 1]) * sc);
+              v.y = tc::pack_bf16(__uint_as_float(o[u * 8 + 2]) * sc, __uint_as_float(o[u * 8 + 3]) * sc);
+              v.z = tc::pack_bf16(__uint_as_float(o[u * 8 + 4]) * sc, __uint_as_float(o[u * 8 + 5]) * sc);
+              v.w = tc::pack_bf16(__uint_as_float(o[u * 8 + 6]) * sc, __uint_as_float(o[u * 8 + 7]) * sc);
+              *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = v;
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(dkv_empty);
+    }
+    if (tid < BQ) bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
+// Delta = rowsum(dO * O) per (row, head) and zero the fp32 dQ accumulator (one warp per unit).
+template <int D>
+__global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* __restrict__ go,
+                                                           const __nv_bfloat16* __restrict__ o, int64_t units,
+                                                           int H, int64_t total_rows, float* __restrict__ delta,
+                                                           float* __restrict__ dq_acc) {
+  const int lane = threadIdx.x & 31;
+  constexpr int PER = D / 32;  // bf16 per lane
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < units;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t base = u * D + lane * PER;
+    float acc = 0.f;
+    if constexpr (PER == 4) {
+      const uint2 a = *reinterpret_cast<const uint2*>(go + base), b = *reinterpret_cast<const uint2*>(o + base);
+      const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
+        acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+      }
+      *reinterpret_cast<float4*>(dq_acc + base) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        acc = fmaf(__bfloat162float(go[base + e]), __bfloat162float(o[base + e]), acc);
+        dq_acc[base + e] = 0.f;
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const int64_t r = u / H;
+      delta[(u - r * H) * total_rows + r] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                                                         int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(acc)[i];
+    uint2 r;
+    r.x = tc::pack_bf16(v.x, v.y);
+    r.y = tc::pack_bf16(v.z, v.w);
+    reinterpret_cast<uint2*>(dq)[i] = r;
+  }
+}
+
+}  // namespace fb
+
+bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt) { return dt == JG_BF16 && head_dim == 128; }
+
+jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
+                                const void* k, const void* v, const void* go, const void* o, const float* lse,
+                                void* dq, void* dk, void* dv, float* delta, float* dq_acc, const int2* items,
+                                const int64_t* n_items, int64_t max_items, cudaStream_t st) {
+  (void)batch;
+  if (D != 128) return fail(JG_UNSUPPORTED, "tcgen05 attention backward: head_dim must be 128");
+  constexpr int kD = 128;
+  using L = fb::Smem<kD>;
+  const int sms = device_sm_count();
+  const int64_t units = total_rows * H;
+  fb::bwd_prologue_kernel<kD><<<(int)std::min<int64_t>((units + 7) / 8, 32 * sms), 256, 0, st>>>(
+      (const __nv_bfloat16*)go, (const __nv_bfloat16*)o, units, H, total_rows, delta, dq_acc);
+  JG_LAUNCHED("bwd_prologue_kernel");
+  CUtensorMap mq, mk, mv, mdo;
+  if (jg_status rc = make_map(&mq, q, total_rows, H, kD, fb::BQ)) return rc;
+  if (jg_status rc = make_map(&mk, k, total_rows, H, kD, fb::BKV)) return rc;
+  if (jg_status rc = make_map(&mv, v, total_rows, H, kD, fb::BKV)) return rc;
+  if (jg_status rc = make_map(&mdo, go, total_rows, H, kD, fb::BQ)) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    JG_CUDA(cudaFuncSetAttribute(fb::jfa_bwd_sm100_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
+    attr_set = true;
+  }
+  fb::Params p{off, items, n_items, total_rows, H, lse, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
+               1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD)};
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
+  fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, p);
+  JG_LAUNCHED("jfa_bwd_sm100_kernel");
+  const int64_t n4 = units * kD / 4;
+  fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,
+                                                                                          n4);
+  JG_LAUNCHED("dq_convert_kernel");
+  return JG_OK;
+}
+
+}  // namespace jg

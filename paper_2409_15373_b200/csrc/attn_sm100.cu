@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
+#include "tma_host.h"
 
 namespace jg {
 
@@ -325,34 +326,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace fa
 
 // ------------------------------------------------------------------ host side
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
-// 3-D map over a [rows, H, D] bf16 tensor: dims (D, H, rows), box (64, 1, 128), SWIZZLE_128B
-static jg_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int H, int D) {
-  auto enc = get_encode();
-  if (!enc) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)rows};
-  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2};
-  cuuint32_t box[3] = {64, 1, 128};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  return JG_OK;
-}
-
 bool attn_sm100_supported(int head_dim, jg_dtype dt) {
   return dt == JG_BF16 && (head_dim == 64 || head_dim == 128);
 }
@@ -363,9 +336,9 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
                             int64_t max_items, cudaStream_t st) {
   using L = fa::Smem<D>;
   CUtensorMap mq, mk, mv;
-  if (jg_status rc = make_map(&mq, q, total_rows, H, D)) return rc;
-  if (jg_status rc = make_map(&mk, k, total_rows, H, D)) return rc;
-  if (jg_status rc = make_map(&mv, v, total_rows, H, D)) return rc;
+  if (jg_status rc = make_map(&mq, q, total_rows, H, D, 128)) return rc;
+  if (jg_status rc = make_map(&mk, k, total_rows, H, D, 128)) return rc;
+  if (jg_status rc = make_map(&mv, v, total_rows, H, D, 128)) return rc;
   static bool attr_set = false;
   if (!attr_set) {
     JG_CUDA(cudaFuncSetAttribute(fa::jfa_fwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
@@ -388,12 +361,6 @@ jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total
   return fail(JG_UNSUPPORTED, "tcgen05 attention: head_dim must be 64 or 128");
 }
 
-jg_status launch_attn_bwd_sm100(const int64_t*, int64_t, int64_t, int, int, const void*, const void*, const void*,
-                                const void*, const void*, const float*, void*, void*, void*, float*, float*,
-                                const int2*, const int64_t*, int64_t, cudaStream_t) {
-  return fail(JG_UNSUPPORTED, "tcgen05 attention backward not built yet");
-}
 
-bool attn_sm100_bwd_supported(int, jg_dtype) { return false; }
 
 }  // namespace jg
