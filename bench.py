@@ -252,14 +252,16 @@ def run_ours(args, rank, world, local_rank):
             hoff.ctypes.data, len(hoff) - 1, H, D, hq.data_ptr(), hk.data_ptr(), hv.data_ptr(), hg.data_ptr(),
             ho.data_ptr(), hl.data_ptr(), hdq.data_ptr(), hdk.data_ptr(), hdv.data_ptr(), 1, stream.cuda_stream))
 
-    e2e_call()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t_e2e = time.perf_counter()
-    for _ in range(e2e_steps):
+    e2e_s = float("nan")
+    if not args.no_e2e:
         e2e_call()
-    e2e_s = (time.perf_counter() - t_e2e) / e2e_steps
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_e2e = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_call()
+        e2e_s = (time.perf_counter() - t_e2e) / e2e_steps
     h2d = 4 * hq.numel() * 2 + hoff.nbytes
     d2h = 4 * hq.numel() * 2 + hl.numel() * 4
 
@@ -324,6 +326,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))
