@@ -16,7 +16,9 @@
 //      bulk async reductions (cp.reduce.async.bulk .add.f32, one 512 B row per query).
 //   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
 // Warps: 0 TMA producer, 1 MMA issuer, 4-7 softmax/dS, 8-11 dQ drain + dK/dV epilogue.
-// TMEM columns: S^T [0,64), dP^T [64,128), dQ^T [128,192), dV [256,384), dK [384,512).
+// TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); dQ_j^T reuses the S^T slot
+// of buffer j&1 once its scores are consumed; dV [256,384), dK [384,512). S_{j+1} is issued before
+// dV_j/dK_j/dQ_j so the softmax warpgroup works on block j+1 while the tensor core finishes block j.
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
@@ -37,7 +39,7 @@ struct Smem {
   static constexpr int kChunkQ = BQ * 128;    // [64 rows x 64] bf16 = 8 KB
   static constexpr int kTileKV = (D / 64) * kChunkKV;
   static constexpr int kTileQ = (D / 64) * kChunkQ;
-  static constexpr int kStages = 2;
+  static constexpr int kStages = 3;
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTileKV;
   static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
@@ -46,9 +48,10 @@ struct Smem {
   static constexpr int kStg = kDS + BKV * 128;              // dQ staging [64 q x D] fp32
   static constexpr int kLse = kStg + BQ * D * 4;            // 2 x (64 lse + 64 delta) fp32
   static constexpr int kBar = kLse + 2 * 2 * BQ * 4;
-  static constexpr int kNumBars = 2 + 2 * kStages + 2 + 2 + 2 + 2 + 1;
+  static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 3 + 2 + 1;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes + 1024;
+  static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
 struct Params {
@@ -76,6 +79,14 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// lse (log2 units) or delta of query j*BQ + (tid % BQ) for the softmax warpgroup's smem staging
+__device__ __forceinline__ float lse_delta_value(const Params& p, int tid, int j, int h, int64_t b0, int64_t n) {
+  const int64_t q = (int64_t)j * BQ + (tid & (BQ - 1));
+  const int64_t gi = (int64_t)h * p.total_rows + b0 + q;
+  if (tid < BQ) return q < n ? p.lse[gi] * kLog2e : INFINITY;  // +inf -> P = 0 for padded queries
+  return q < n ? p.delta[gi] : 0.f;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     jfa_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -89,13 +100,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_empty = bars + 1;
   uint64_t* qd_full = bars + 2;
   uint64_t* qd_empty = qd_full + L::kStages;
-  uint64_t* st_full = qd_empty + L::kStages;
-  uint64_t* st_empty = st_full + 1;
-  uint64_t* p_full = st_empty + 1;
+  uint64_t* st_full = qd_empty + L::kStages;  // [2] per TMEM score buffer
+  uint64_t* st_empty = st_full + 2;           // [2]
+  uint64_t* p_full = st_empty + 2;
   uint64_t* pds_empty = p_full + 1;
   uint64_t* dq_full = pds_empty + 1;
-  uint64_t* dq_empty = dq_full + 1;
-  uint64_t* dkv_full = dq_empty + 1;
+  uint64_t* dq_empty = dq_full + 1;           // [2] dQ^T_j lives in score buffer j&1
+  uint64_t* dkv_full = dq_empty + 2;
   uint64_t* dkv_empty = dkv_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_empty + 1);
 
@@ -107,12 +118,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(qd_full + s, 1);
       tc::mbar_init(qd_empty + s, 1);
     }
-    tc::mbar_init(st_full, 1);
-    tc::mbar_init(st_empty, 4);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(st_full + b, 1);
+      tc::mbar_init(st_empty + b, 4);
+      tc::mbar_init(dq_empty + b, 4);
+    }
     tc::mbar_init(p_full, 4);
     tc::mbar_init(pds_empty, 1);
     tc::mbar_init(dq_full, 1);
-    tc::mbar_init(dq_empty, 4);
     tc::mbar_init(dkv_full, 1);
     tc::mbar_init(dkv_empty, 4);
     tc::fence_barrier_init();
@@ -162,45 +175,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================================================== MMA issuer
+    // Per item: S_0; then for each j: S_{j+1} (other TMEM buffer, overlaps softmax j), dV_j, dK_j, dQ_j.
     if (lane == 0) {
       constexpr uint32_t kIdS = tc::idesc_bf16_f32(BKV, BQ, false, false);  // S^T, dP^T
       constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
       constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
       const uint32_t k_base = tc::smem_u32(smem + L::kK), v_base = tc::smem_u32(smem + L::kV);
       const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
-      uint32_t item_cnt = 0, qd_cnt = 0, st_cnt = 0, p_cnt = 0, dq_cnt = 0;
+      const uint32_t qd_base = tc::smem_u32(smem + L::kQD);
+      uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill[2] = {0, 0};
+      auto stage_of = [&](uint32_t cnt) { return qd_base + (cnt % L::kStages) * 2 * L::kTileQ; };
+      auto issue_sdp = [&](uint32_t cnt, int b) {
+        const uint32_t s = cnt % L::kStages;
+        tc::mbar_wait(qd_full + s, (cnt / L::kStages) & 1);
+        tc::mbar_wait(st_empty + b, (fill[b] & 1) ^ 1);  // softmax done reading this buffer
+        tc::mbar_wait(dq_empty + b, (fill[b] & 1) ^ 1);  // dQ^T previously written here was drained
+        ++fill[b];
+        tc::tc_fence_after();
+        const uint32_t q_base = stage_of(cnt), do_base = q_base + L::kTileQ;
+        const uint32_t col = b * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
+          tc::mma_bf16_ss(tmem + col, tc::sw128_desc(k_base + ka, 16, 1024), tc::sw128_desc(q_base + kb, 16, 1024),
+                          kIdS, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
+          tc::mma_bf16_ss(tmem + col + 64, tc::sw128_desc(v_base + ka, 16, 1024),
+                          tc::sw128_desc(do_base + kb, 16, 1024), kIdS, kk > 0);
+        }
+        tc::mma_commit(st_full + b);
+      };
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
         tc::mbar_wait(kv_full, item_cnt & 1);
         tc::mbar_wait(dkv_empty, (item_cnt & 1) ^ 1);
+        issue_sdp(qd_cnt, 0);
         for (int j = 0; j < nq; ++j, ++qd_cnt) {
-          const uint32_t s = qd_cnt % L::kStages;
-          tc::mbar_wait(qd_full + s, (qd_cnt / L::kStages) & 1);
-          tc::mbar_wait(st_empty, (st_cnt & 1) ^ 1);
-          ++st_cnt;
-          tc::tc_fence_after();
-          const uint32_t q_base = tc::smem_u32(smem + L::kQD + s * 2 * L::kTileQ);
-          const uint32_t do_base = q_base + L::kTileQ;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
-            const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
-            tc::mma_bf16_ss(tmem + 0, tc::sw128_desc(k_base + ka, 16, 1024), tc::sw128_desc(q_base + kb, 16, 1024),
-                            kIdS, kk > 0);
-          }
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
-            const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
-            tc::mma_bf16_ss(tmem + 64, tc::sw128_desc(v_base + ka, 16, 1024), tc::sw128_desc(do_base + kb, 16, 1024),
-                            kIdS, kk > 0);
-          }
-          tc::mma_commit(st_full);
+          if (j + 1 < nq) issue_sdp(qd_cnt + 1, (j + 1) & 1);
           tc::mbar_wait(p_full, p_cnt & 1);
           ++p_cnt;
           tc::tc_fence_after();
+          const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
           // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk) {
@@ -212,17 +234,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_bf16_ss(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
                             tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
           }
-          // dQ_j^T = K^T dS^T  (A = K tile MN-major, M = head_dim; B = dS^T MN-major [128 keys x 64 q])
-          tc::mbar_wait(dq_empty, (dq_cnt & 1) ^ 1);
-          ++dq_cnt;
-          tc::tc_fence_after();
+          // dQ_j^T = K^T dS^T into the S^T slot of buffer j&1 (its scores were consumed: p_full)
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk) {
-            tc::mma_bf16_ss(tmem + 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
+            tc::mma_bf16_ss(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
                             tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
           }
           tc::mma_commit(dq_full);
-          tc::mma_commit(qd_empty + s);
+          tc::mma_commit(qd_empty + (qd_cnt % L::kStages));
           tc::mma_commit(pds_empty);
         }
         tc::mma_commit(dkv_full);
@@ -236,47 +255,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
     float* sm_ld = reinterpret_cast<float*>(smem + L::kLse);  // [2][lse 64 | delta 64]
-    uint32_t st_cnt = 0, pds_cnt = 0;
+    uint32_t cons[2] = {0, 0}, pds_cnt = 0;
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
       const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
       const int nq = (int)((n + BQ - 1) / BQ);
       const bool row_valid = (int64_t)it.y * BKV + tid < n;
+      float pf = lse_delta_value(p, tid, 0, h, b0, n);
       for (int j = 0; j < nq; ++j) {
-        float* buf = sm_ld + (j & 1) * 2 * BQ;
-        {
-          const int64_t q = (int64_t)j * BQ + (tid & (BQ - 1));
-          const int64_t gi = (int64_t)h * p.total_rows + b0 + q;
-          if (tid < BQ) buf[tid] = q < n ? p.lse[gi] * kLog2e : INFINITY;
-          else buf[tid] = q < n ? p.delta[gi] : 0.f;
-        }
+        const int b = j & 1;
+        float* buf = sm_ld + b * 2 * BQ;
+        buf[tid] = pf;
+        if (j + 1 < nq) pf = lse_delta_value(p, tid, j + 1, h, b0, n);  // prefetch: hidden behind block j
         named_bar(1, 128);
-        tc::mbar_wait(st_full, st_cnt & 1);
-        ++st_cnt;
+        tc::mbar_wait(st_full + b, cons[b] & 1);
+        ++cons[b];
         tc::tc_fence_after();
         uint32_t pk[BQ / 2], dk2[BQ / 2];
 #pragma unroll
         for (int c = 0; c < BQ / 32; ++c) {
           uint32_t sr[32], dr[32];
-          tc::tmem_ld32(lane_addr + c * 32, sr);
-          tc::tmem_ld32(lane_addr + 64 + c * 32, dr);
+          tc::tmem_ld32(lane_addr + b * 128 + c * 32, sr);
+          tc::tmem_ld32(lane_addr + b * 128 + 64 + c * 32, dr);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
+          for (int e = 0; e < 32; e += 4) {
             const int q0 = c * 32 + e;
-            float p0 = tc::ex2(__uint_as_float(sr[e]) * p.scale_log2 - buf[q0]);
-            float p1 = tc::ex2(__uint_as_float(sr[e + 1]) * p.scale_log2 - buf[q0 + 1]);
-            if (!row_valid) { p0 = 0.f; p1 = 0.f; }
-            const float d0 = p0 * (__uint_as_float(dr[e]) - buf[BQ + q0]);
-            const float d1 = p1 * (__uint_as_float(dr[e + 1]) - buf[BQ + q0 + 1]);
+            const float4 l4 = *reinterpret_cast<const float4*>(buf + q0);
+            const float4 d4 = *reinterpret_cast<const float4*>(buf + BQ + q0);
+            float p0 = tc::ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
+            float p1 = tc::ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
+            float p2 = tc::ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
+            float p3 = tc::ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w));
+            if (!row_valid) p0 = p1 = p2 = p3 = 0.f;
             pk[q0 >> 1] = tc::pack_bf16(p0, p1);
-            dk2[q0 >> 1] = tc::pack_bf16(d0, d1);
+            pk[(q0 >> 1) + 1] = tc::pack_bf16(p2, p3);
+            dk2[q0 >> 1] = tc::pack_bf16(p0 * (__uint_as_float(dr[e + 0]) - d4.x), p1 * (__uint_as_float(dr[e + 1]) - d4.y));
+            dk2[(q0 >> 1) + 1] =
+                tc::pack_bf16(p2 * (__uint_as_float(dr[e + 2]) - d4.z), p3 * (__uint_as_float(dr[e + 3]) - d4.w));
           }
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(st_empty);
+        if (lane == 0) tc::mbar_arrive(st_empty + b);
         tc::mbar_wait(pds_empty, (pds_cnt & 1) ^ 1);
         ++pds_cnt;
 #pragma unroll
@@ -305,22 +327,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
       const int nq = (int)((n + BQ - 1) / BQ);
       for (int j = 0; j < nq; ++j) {
+        const int b = j & 1;
         tc::mbar_wait(dq_full, dq_cnt & 1);
         ++dq_cnt;
         tc::tc_fence_after();
-        uint32_t a[32], b[32];
-        tc::tmem_ld32(lane_addr + 128, a);
-        tc::tmem_ld32(lane_addr + 160, b);
+        uint32_t a[32], c2[32];
+        tc::tmem_ld32(lane_addr + b * 128, a);
+        tc::tmem_ld32(lane_addr + b * 128 + 32, c2);
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(dq_empty);
+        if (lane == 0) tc::mbar_arrive(dq_empty + b);
         if (tid < BQ) bulk_wait_read0();  // previous block's reductions have read the staging buffer
         named_bar(2, 128);
 #pragma unroll
         for (int q = 0; q < 32; ++q) stg[q * D + tid] = __uint_as_float(a[q]) * p.scale;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stg[(q + 32) * D + tid] = __uint_as_float(b[q]) * p.scale;
+        for (int q = 0; q < 32; ++q) stg[(q + 32) * D + tid] = __uint_as_float(c2[q]) * p.scale;
         tc::fence_proxy_async_smem();
         named_bar(2, 128);
         if (tid < BQ) {

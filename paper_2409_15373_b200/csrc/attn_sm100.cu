@@ -234,12 +234,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t rem = n - (int64_t)j * BN;
         const int valid = rem < BN ? (int)rem : BN;
         float s[BN];
-        float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          s[c] = (c < valid) ? __uint_as_float(sr[c]) * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < BN; ++c) s[c] = __uint_as_float(sr[c]) * p.scale_log2;
+        if (valid < BN) {  // warp-uniform: only a segment's last key block is partial
+#pragma unroll
+          for (int c = 0; c < BN; ++c) s[c] = c < valid ? s[c] : -INFINITY;
         }
+        // 8 independent max chains (a single 128-long fmax chain costs ~512 cycles of latency)
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+        for (int c = 8; c < BN; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         float alpha = 1.f;
         bool rescale = false;
         if (mx > m + kRescaleThreshold || j == 0) {
@@ -247,12 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           rescale = j > 0;
           m = mx;
         }
-        float rs = 0.f;
+        float r8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
           s[c] = tc::ex2(s[c] - m);
-          rs += s[c];
+          r8[c & 7] += s[c];
         }
+        const float rs = ((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7]));
         l = l * alpha + rs;
         // PV_{j-1} must be complete before P is overwritten or O is rescaled
         if (j > 0) {
