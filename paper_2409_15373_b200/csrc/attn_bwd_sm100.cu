@@ -48,7 +48,7 @@ struct Smem {
   static constexpr int kStg = kDS + BKV * 128;              // dQ staging [64 q x D] fp32
   static constexpr int kLse = kStg + BQ * D * 4;            // 2 x (64 lse + 64 delta) fp32
   static constexpr int kBar = kLse + 2 * 2 * BQ * 4;
-  static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 3 + 2 + 1;
+  static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 4 + 2 + 1;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes + 1024;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -104,8 +104,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* st_empty = st_full + 2;           // [2]
   uint64_t* p_full = st_empty + 2;
   uint64_t* pds_empty = p_full + 1;
-  uint64_t* dq_full = pds_empty + 1;
-  uint64_t* dq_empty = dq_full + 1;           // [2] dQ^T_j lives in score buffer j&1
+  uint64_t* dq_full = pds_empty + 1;          // [2] one per score buffer: a single barrier could complete
+                                              // twice before the drain warps wait (no S fill between dQ_{n-2}, dQ_{n-1})
+  uint64_t* dq_empty = dq_full + 2;           // [2] dQ^T_j lives in score buffer j&1
   uint64_t* dkv_full = dq_empty + 2;
   uint64_t* dkv_empty = dkv_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_empty + 1);
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::mbar_init(p_full, 4);
     tc::mbar_init(pds_empty, 1);
     tc::mbar_init(dq_full, 1);
+    tc::mbar_init(dq_full + 1, 1);
     tc::mbar_init(dkv_full, 1);
     tc::mbar_init(dkv_empty, 4);
     tc::fence_barrier_init();
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_bf16_ss(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
                             tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
           }
-          tc::mma_commit(dq_full);
+          tc::mma_commit(dq_full + (j & 1));
           tc::mma_commit(qd_empty + (qd_cnt % L::kStages));
           tc::mma_commit(pds_empty);
         }
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     float* stg = reinterpret_cast<float*>(smem + L::kStg);
     const uint32_t stg_base = tc::smem_u32(stg);
-    uint32_t item_cnt = 0, dq_cnt = 0;
+    uint32_t item_cnt = 0, dqc[2] = {0, 0};
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
@@ -328,8 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nq = (int)((n + BQ - 1) / BQ);
       for (int j = 0; j < nq; ++j) {
         const int b = j & 1;
-        tc::mbar_wait(dq_full, dq_cnt & 1);
-        ++dq_cnt;
+        tc::mbar_wait(dq_full + b, dqc[b] & 1);
+        ++dqc[b];
         tc::tc_fence_after();
         uint32_t a[32], c2[32];
         tc::tmem_ld32(lane_addr + b * 128, a);
