@@ -67,6 +67,7 @@ struct Params {
   __nv_bfloat16* dv;
   float scale_log2;
   float scale;
+  unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23, drain 24-31)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -149,6 +150,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===================================================== TMA producer
     if (lane == 0) {
+      tc::WaitProf wp;
+      wp.init(p.prof, 0);
+      const long long t_role = clock64();
       uint32_t item_cnt = 0, qd_cnt = 0;
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
         const int2 it = p.items[w / H];
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
         const int nq = (int)((n + BQ - 1) / BQ);
         const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
-        tc::mbar_wait(kv_empty, (item_cnt & 1) ^ 1);
+        wp.wait(kv_empty, (item_cnt & 1) ^ 1, 0);
         tc::mbar_expect_tx(kv_full, 2 * L::kTileKV);
         for (int c = 0; c < D / 64; ++c) {
           tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, kv_full, c * 64, h, kv_row);
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int j = 0; j < nq; ++j, ++qd_cnt) {
           const uint32_t s = qd_cnt % L::kStages;
-          tc::mbar_wait(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1);
+          wp.wait(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1, 1);
           tc::mbar_expect_tx(qd_full + s, 2 * L::kTileQ);
           uint8_t* qs = smem + L::kQD + s * 2 * L::kTileQ;
           const int q_row = (int)(b0 + (int64_t)j * BQ);
@@ -174,11 +178,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      wp.add(7, clock64() - t_role);
+      wp.flush();
     }
   } else if (warp == 1) {
     // ===================================================== MMA issuer
     // Per item: S_0; then for each j: S_{j+1} (other TMEM buffer, overlaps softmax j), dV_j, dK_j, dQ_j.
     if (lane == 0) {
+      tc::WaitProf wp;
+      wp.init(p.prof, 8);
+      const long long t_role = clock64();
       constexpr uint32_t kIdS = tc::idesc_bf16_f32(BKV, BQ, false, false);  // S^T, dP^T
       constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
       constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
@@ -189,9 +198,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto stage_of = [&](uint32_t cnt) { return qd_base + (cnt % L::kStages) * 2 * L::kTileQ; };
       auto issue_sdp = [&](uint32_t cnt, int b) {
         const uint32_t s = cnt % L::kStages;
-        tc::mbar_wait(qd_full + s, (cnt / L::kStages) & 1);
-        tc::mbar_wait(st_empty + b, (fill[b] & 1) ^ 1);  // softmax done reading this buffer
-        tc::mbar_wait(dq_empty + b, (fill[b] & 1) ^ 1);  // dQ^T previously written here was drained
+        wp.wait(qd_full + s, (cnt / L::kStages) & 1, 2);
+        wp.wait(st_empty + b, (fill[b] & 1) ^ 1, 3);  // softmax done reading this buffer
+        wp.wait(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
         ++fill[b];
         tc::tc_fence_after();
         const uint32_t q_base = stage_of(cnt), do_base = q_base + L::kTileQ;
@@ -216,12 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
-        tc::mbar_wait(kv_full, item_cnt & 1);
-        tc::mbar_wait(dkv_empty, (item_cnt & 1) ^ 1);
+        wp.wait(kv_full, item_cnt & 1, 0);
+        wp.wait(dkv_empty, (item_cnt & 1) ^ 1, 1);
         issue_sdp(qd_cnt, 0);
         for (int j = 0; j < nq; ++j, ++qd_cnt) {
           if (j + 1 < nq) issue_sdp(qd_cnt + 1, (j + 1) & 1);
-          tc::mbar_wait(p_full, p_cnt & 1);
+          wp.wait(p_full, p_cnt & 1, 5);
           ++p_cnt;
           tc::tc_fence_after();
           const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
@@ -249,6 +258,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mma_commit(dkv_full);
         tc::mma_commit(kv_empty);
       }
+      wp.add(7, clock64() - t_role);
+      wp.flush();
     }
   } else if (warp >= kSmWarp0 && warp < kDqWarp0) {
     // ===================================================== P^T / dS^T warpgroup (thread = key row)
@@ -258,6 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
     float* sm_ld = reinterpret_cast<float*>(smem + L::kLse);  // [2][lse 64 | delta 64]
     uint32_t cons[2] = {0, 0}, pds_cnt = 0;
+    tc::WaitProf wp;
+    wp.init(tid == 0 ? p.prof : nullptr, 16);
+    const long long t_role = clock64();
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
@@ -270,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* buf = sm_ld + b * 2 * BQ;
         buf[tid] = pf;
         if (j + 1 < nq) pf = lse_delta_value(p, tid, j + 1, h, b0, n);  // prefetch: hidden behind block j
-        named_bar(1, 128);
-        tc::mbar_wait(st_full + b, cons[b] & 1);
+        { const long long t0 = clock64(); named_bar(1, 128); wp.add(0, clock64() - t0); }
+        wp.wait(st_full + b, cons[b] & 1, 1);
         ++cons[b];
         tc::tc_fence_after();
         uint32_t pk[BQ / 2], dk2[BQ / 2];
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(st_empty + b);
-        tc::mbar_wait(pds_empty, (pds_cnt & 1) ^ 1);
+        wp.wait(pds_empty, (pds_cnt & 1) ^ 1, 2);
         ++pds_cnt;
 #pragma unroll
         for (int u = 0; u < BQ / 8; ++u) {
@@ -315,6 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) tc::mbar_arrive(p_full);
       }
     }
+    wp.add(7, clock64() - t_role);
+    wp.flush();
   } else if (warp >= kDqWarp0) {
     // ===================================================== dQ drain + dK/dV epilogue
     const int tid = threadIdx.x - kDqWarp0 * 32;  // == TMEM lane: head-dim row of dQ^T, key row of dK/dV
@@ -323,6 +339,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* stg = reinterpret_cast<float*>(smem + L::kStg);
     const uint32_t stg_base = tc::smem_u32(stg);
     uint32_t item_cnt = 0, dqc[2] = {0, 0};
+    tc::WaitProf wp;
+    wp.init(tid == 0 ? p.prof : nullptr, 24);
+    const long long t_role = clock64();
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
@@ -330,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nq = (int)((n + BQ - 1) / BQ);
       for (int j = 0; j < nq; ++j) {
         const int b = j & 1;
-        tc::mbar_wait(dq_full + b, dqc[b] & 1);
+        wp.wait(dq_full + b, dqc[b] & 1, 0);
         ++dqc[b];
         tc::tc_fence_after();
         uint32_t a[32], c2[32];
@@ -340,8 +359,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(dq_empty + b);
+        const long long tb = clock64();
         if (tid < BQ) bulk_wait_read0();  // previous block's reductions have read the staging buffer
         named_bar(2, 128);
+        wp.add(1, clock64() - tb);
 #pragma unroll
         for (int q = 0; q < 32; ++q) stg[q * D + tid] = __uint_as_float(a[q]) * p.scale;
 #pragma unroll
@@ -357,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       // dK / dV for this key tile
-      tc::mbar_wait(dkv_full, item_cnt & 1);
+      wp.wait(dkv_full, item_cnt & 1, 2);
       tc::tc_fence_after();
       const int64_t kv_local = (int64_t)it.y * BKV + tid;
       const bool store = kv_local < n;
@@ -390,6 +411,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc::mbar_arrive(dkv_empty);
     }
     if (tid < BQ) bulk_wait0();
+    wp.add(7, clock64() - t_role);
+    wp.flush();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -475,10 +498,14 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
     attr_set = true;
   }
   fb::Params p{off, items, n_items, total_rows, H, lse, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
-               1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD)};
+               1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), wait_prof_begin(st)};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
   fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, p);
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
+  wait_prof_end(p.prof, st, "bwd",
+                {"P.kv_empty", "P.qd_empty", "", "", "", "", "", "P.total", "M.kv_full", "M.dkv_empty", "M.qd_full",
+                 "M.st_empty", "M.dq_empty", "M.p_full", "", "M.total", "S.lse_bar", "S.st_full", "S.pds_empty", "",
+                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total"});
   const int64_t n4 = units * kD / 4;
   fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,
                                                                                           n4);

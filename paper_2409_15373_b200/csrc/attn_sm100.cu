@@ -61,6 +61,7 @@ struct Params {
   __nv_bfloat16* out;
   float* lse;
   float scale_log2;
+  unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23)
 };
 
 template <int D>
@@ -117,20 +118,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================================================== TMA producer
     if (lane == 0) {
       uint32_t kv_cnt = 0, item_cnt = 0;
+      tc::WaitProf wp;
+      wp.init(p.prof, 0);
+      const long long t_role = clock64();
       for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++item_cnt) {
         const int2 it = p.items[w / H];
         const int h = (int)(w % H);
         const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
         const int nkv = (int)((n + BN - 1) / BN);
         const int q_row = (int)(b0 + (int64_t)it.y * BM);
-        tc::mbar_wait(q_empty, (item_cnt & 1) ^ 1);
+        wp.wait(q_empty, (item_cnt & 1) ^ 1, 0);
         tc::mbar_expect_tx(q_full, L::kTile);
         for (int c = 0; c < L::kChunks; ++c)
           tc::tma_load_3d(smem + L::kQ + c * L::kChunk, &tm_q, q_full, c * 64, h, q_row);
         // consumption order: K0, K1, V0, K2, V1, ..., K_{n-1}, V_{n-2}, V_{n-1}
         auto load = [&](const CUtensorMap* tm, int blk) {
           const uint32_t s = kv_cnt % L::kStages;
-          tc::mbar_wait(kv_empty + s, ((kv_cnt / L::kStages) & 1) ^ 1);
+          wp.wait(kv_empty + s, ((kv_cnt / L::kStages) & 1) ^ 1, 1);
           tc::mbar_expect_tx(kv_full + s, L::kTile);
           uint8_t* dst = smem + L::kKV + s * L::kTile;
           const int row = (int)(b0 + (int64_t)blk * BN);
@@ -144,6 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (j + 2 < nkv) load(&tm_k, j + 2);
         }
       }
+      wp.add(7, clock64() - t_role);
+      wp.flush();
     }
   } else if (warp == 1) {
     // ===================================================== MMA issuer
@@ -154,14 +160,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t p_base = tc::smem_u32(smem + L::kP);
       const uint32_t kv_base = tc::smem_u32(smem + L::kKV);
       uint32_t kv_cnt = 0, item_cnt = 0, s_use[2] = {0, 0}, p_cnt = 0;
+      tc::WaitProf wp;
+      wp.init(p.prof, 8);
+      const long long t_role = clock64();
       auto next_stage = [&]() {
         const uint32_t s = kv_cnt % L::kStages;
-        tc::mbar_wait(kv_full + s, (kv_cnt / L::kStages) & 1);
+        wp.wait(kv_full + s, (kv_cnt / L::kStages) & 1, 2);
         ++kv_cnt;
         return s;
       };
       auto issue_s = [&](int buf) {
-        tc::mbar_wait(s_empty + buf, (s_use[buf] & 1) ^ 1);
+        wp.wait(s_empty + buf, (s_use[buf] & 1) ^ 1, 1);
         ++s_use[buf];
         const uint32_t s = next_stage();
         tc::tc_fence_after();
@@ -179,12 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nkv = (int)((n + BN - 1) / BN);
-        tc::mbar_wait(q_full, item_cnt & 1);
+        wp.wait(q_full, item_cnt & 1, 0);
         issue_s(0);
         if (nkv > 1) issue_s(1);
-        tc::mbar_wait(o_empty, (item_cnt & 1) ^ 1);  // previous epilogue has drained O
+        wp.wait(o_empty, (item_cnt & 1) ^ 1, 3);  // previous epilogue has drained O
         for (int j = 0; j < nkv; ++j) {
-          tc::mbar_wait(p_full, p_cnt & 1);
+          wp.wait(p_full, p_cnt & 1, 4);
           ++p_cnt;
           const uint32_t s = next_stage();  // V_j
           tc::tc_fence_after();
@@ -203,6 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::mma_commit(q_empty);
       }
+      wp.add(7, clock64() - t_role);
+      wp.flush();
     }
   } else if (warp >= kSoftmaxWarp0) {
     // ===================================================== softmax / correction / epilogue
@@ -211,6 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     const uint32_t p_base = tc::smem_u32(smem + L::kP);
     uint32_t s_cons[2] = {0, 0}, pv_cnt = 0;
+    tc::WaitProf wp;
+    wp.init(row == 0 ? p.prof : nullptr, 16);
+    const long long t_role = clock64();
     for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
@@ -219,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         const int buf = j & 1;
-        tc::mbar_wait(s_full + buf, s_cons[buf] & 1);
+        wp.wait(s_full + buf, s_cons[buf] & 1, 0);
         ++s_cons[buf];
         tc::tc_fence_after();
         uint32_t sr[BN];
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         l = l * alpha + rs;
         // PV_{j-1} must be complete before P is overwritten or O is rescaled
         if (j > 0) {
-          tc::mbar_wait(o_done, pv_cnt & 1);
+          wp.wait(o_done, pv_cnt & 1, 1);
           ++pv_cnt;
           tc::tc_fence_after();
         }
@@ -294,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) tc::mbar_arrive(p_full);
       }
       // epilogue: wait for the last PV, normalise, store
-      tc::mbar_wait(o_done, pv_cnt & 1);
+      wp.wait(o_done, pv_cnt & 1, 2);
       ++pv_cnt;
       tc::tc_fence_after();
       const int64_t q_local = (int64_t)it.y * BM + row;
@@ -323,6 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc::mbar_arrive(o_empty);
       if (store) p.lse[(int64_t)h * p.total_rows + b0 + q_local] = (m + __log2f(l)) * 0.6931471805599453f;
     }
+    wp.add(7, clock64() - t_role);
+    wp.flush();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -354,11 +370,12 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
     attr_set = true;
   }
   fa::Params p{off, items, n_items, batch, total_rows, H, (__nv_bfloat16*)out, lse,
-               1.4426950408889634f / sqrtf((float)D)};
+               1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st)};
   const int64_t work = max_items * H;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sm_count(), work));
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
   JG_LAUNCHED("jfa_fwd_sm100_kernel");
+  wait_prof_end(p.prof, st, "fwd", {"P.q_empty", "P.kv_empty", "", "", "", "", "", "P.total", "M.q_full", "M.s_empty", "M.kv_full", "M.o_empty", "M.p_full", "", "", "M.total", "S.s_full", "S.o_done", "S.o_done_epi", "", "", "", "", "S.total"});
   return JG_OK;
 }
 

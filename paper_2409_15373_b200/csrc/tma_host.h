@@ -41,3 +41,35 @@ inline jg_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int H, 
 }
 
 }  // namespace jg
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+namespace jg {
+// JG_WAIT_PROF=1: per-role mbarrier wait accounting for the tcgen05 attention kernels (debug only;
+// synchronises the stream after the kernel and prints to stderr).
+inline unsigned long long* wait_prof_begin(cudaStream_t st) {
+  static unsigned long long* buf = nullptr;
+  const char* e = std::getenv("JG_WAIT_PROF");
+  if (!e || e[0] != '1') return nullptr;
+  if (!buf && cudaMalloc(&buf, 64 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(buf, 0, 64 * sizeof(unsigned long long), st);
+  return buf;
+}
+inline void wait_prof_end(unsigned long long* buf, cudaStream_t st, const char* tag, std::vector<const char*> names) {
+  if (!buf) return;
+  unsigned long long h[64] = {0};
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h, buf, sizeof(h), cudaMemcpyDeviceToHost);
+  std::fprintf(stderr, "[wait-prof %s]", tag);
+  for (size_t r = 0; r + 7 < names.size(); r += 8) {
+    const double tot = (double)h[r + 7];
+    if (tot <= 0) continue;
+    for (size_t i = r; i < r + 7; ++i)
+      if (names[i][0]) std::fprintf(stderr, " %s=%.1f%%", names[i], 100.0 * (double)h[i] / tot);
+    std::fprintf(stderr, " | %s=%.3g cyc;", names[r + 7], tot);
+  }
+  std::fprintf(stderr, "\n");
+}
+}  // namespace jg
