@@ -131,13 +131,17 @@ extern "C" jg_status jg_sq_offsets(const int64_t* offsets, int64_t batch, int64_
   return launch_scan(1, offsets, batch, sq_offsets, nullptr, as_stream(stream));
 }
 
+// Two LPT lists over the same offsets: (sample, 128-row tile) items for the key-stationary backward
+// and (sample, 256-row tile pair) items for the two-tile forward.
 struct jg_schedule_s {
   const int64_t* offsets;
-  int64_t batch, total_rows, max_items;
+  int64_t batch, total_rows, max_items, max_items2;
   int64_t* lengths;
   int64_t* sq;
   int2* items;
   int64_t* n_items;
+  int2* items2;
+  int64_t* n_items2;
   void* block;
 };
 
@@ -151,9 +155,10 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
   s->batch = batch;
   s->total_rows = total_rows;
   s->max_items = total_rows / 128 + batch + 1;
+  s->max_items2 = total_rows / 256 + batch + 1;
   const size_t b_len = sizeof(int64_t) * (batch + 1), b_sq = sizeof(int64_t) * (batch + 1),
-               b_items = sizeof(int2) * s->max_items;
-  const size_t bytes = b_len + b_sq + b_items + 64;
+               b_items = sizeof(int2) * s->max_items, b_items2 = sizeof(int2) * s->max_items2;
+  const size_t bytes = b_len + b_sq + 128 + b_items + b_items2;
   cudaError_t e = cudaMallocAsync(&s->block, bytes, st);
   if (e != cudaSuccess) {
     delete s;
@@ -163,14 +168,17 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
   s->lengths = (int64_t*)p; p += b_len;
   s->sq = (int64_t*)p; p += b_sq;
   s->n_items = (int64_t*)p; p += 64;
-  s->items = (int2*)p;
+  s->n_items2 = (int64_t*)p; p += 64;
+  s->items = (int2*)p; p += b_items;
+  s->items2 = (int2*)p;
   jg_status rc = JG_OK;
   if (batch > 0) {
     if ((rc = launch_lengths(offsets, batch, s->lengths, st))) goto err;
     if ((rc = launch_scan(1, offsets, batch, s->sq, nullptr, st))) goto err;
     if ((rc = launch_work_list(offsets, batch, 128, s->items, s->n_items, st))) goto err;
+    if ((rc = launch_work_list(offsets, batch, 256, s->items2, s->n_items2, st))) goto err;
   } else {
-    JG_CUDA(cudaMemsetAsync(s->n_items, 0, sizeof(int64_t), st));
+    JG_CUDA(cudaMemsetAsync(s->n_items, 0, 128, st));
     JG_CUDA(cudaMemsetAsync(s->sq, 0, sizeof(int64_t), st));
   }
   *out = s;
@@ -403,8 +411,8 @@ extern "C" jg_status jg_jagged_flash_attention_forward(const int64_t* off, int64
       if (jg_status rc = jg_schedule_create(off, batch, total_rows, stream, &own)) return rc;
       sched = own;
     }
-    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items,
-                                         sched->n_items, sched->max_items, st);
+    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
+                                         sched->n_items2, sched->max_items2, st);
     if (own) {
       cudaStreamSynchronize(st);
       jg_schedule_destroy(own);

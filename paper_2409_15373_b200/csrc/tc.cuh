@@ -45,15 +45,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Opt-in wait-site profiler (JG_WAIT_PROF=1): cycles each role spends blocked per barrier site are
 // accumulated per CTA and added to a global counter array at kernel exit. prof == nullptr -> no-op.
 struct WaitProf {
-  unsigned long long* g;  // global counters, or nullptr
-  unsigned long long acc[8];
-  int base;
-  __device__ __forceinline__ void init(unsigned long long* gp, int b) {
-    g = gp;
-    base = b;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0;
-  }
+  unsigned long long* g;  // global counters offset by the role base, or nullptr
+  __device__ __forceinline__ void init(unsigned long long* gp, int b) { g = gp ? gp + b : nullptr; }
   __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int site) {
     if (g == nullptr) {
       mbar_wait(bar, parity);
@@ -61,16 +54,12 @@ struct WaitProf {
     }
     const long long t0 = clock64();
     mbar_wait(bar, parity);
-    acc[site] += (unsigned long long)(clock64() - t0);
+    atomicAdd(g + site, (unsigned long long)(clock64() - t0));
   }
   __device__ __forceinline__ void add(int site, long long cycles) {
-    if (g) acc[site] += (unsigned long long)cycles;
+    if (g) atomicAdd(g + site, (unsigned long long)cycles);
   }
-  __device__ __forceinline__ void flush() {
-    if (g == nullptr) return;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) atomicAdd(g + base + i, acc[i]);
-  }
+  __device__ __forceinline__ void flush() {}
 };
 
 // ------------------------------------------------------------------ TMA
