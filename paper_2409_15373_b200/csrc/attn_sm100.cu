@@ -87,7 +87,7 @@ __device__ __forceinline__ Item load_item(const Params& p, int64_t w) {
 }
 
 template <int D>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kThreads, 1)
     jfa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, Params p) {
   using L = Smem<D>;
@@ -254,22 +254,19 @@ __global__ void __maxnreg__(200)
         wp.wait(s_full + t, s_cnt & 1, 0);
         ++s_cnt;
         tc::tc_fence_after();
-        uint32_t sr[BN];
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c)
-          tc::tmem_ld32(s_addr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-        tc::tmem_wait_ld();
         const int64_t rem = it.n - (int64_t)j * BN;
-        if (rem < BN) {  // warp-uniform: only a segment's last key block is partial
+        const bool partial = rem < BN;  // warp-uniform: only a segment's last key block is partial
+        // pass 1: raw-score row max over TMEM in 32-column chunks, 8 independent chains
+        float m8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int c = 0; c < BN; ++c) sr[c] = c < rem ? sr[c] : __float_as_uint(-INFINITY);
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld32(s_addr + c * 32, r);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!partial || c * 32 + e < rem) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e]));
         }
-        // raw-score row max in 8 independent chains; scale (> 0) applied once afterwards
-        float m8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) m8[k] = __uint_as_float(sr[k]);
-#pragma unroll
-        for (int c = 8; c < BN; ++c) m8[c & 7] = fmaxf(m8[c & 7], __uint_as_float(sr[c]));
         const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * p.scale_log2;
         float alpha = 1.f;
@@ -291,20 +288,29 @@ __global__ void __maxnreg__(200)
           }
           tc::tmem_wait_st();
         }
-        // P = exp2(S*scale - m) -> smem as bf16, SWIZZLE_128B K-major [128 rows x 128 keys] (two 64-key
-        // chunks), 8 keys (one 16-byte unit) at a time to keep register pressure low
+        // pass 2: P = exp2(S*scale - m) -> smem as bf16, SWIZZLE_128B K-major [128 rows x 128 keys]
+        // (two 64-key chunks), re-reading S from TMEM chunk by chunk
         float r8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int u = 0; u < BN / 8; ++u) {
-          float pv[8];
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld32(s_addr + c * 32, r);
+          tc::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            pv[e] = tc::ex2(fmaf(__uint_as_float(sr[u * 8 + e]), p.scale_log2, -m));
-            r8[e] += pv[e];
+          for (int u = 0; u < 4; ++u) {
+            float pv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = c * 32 + u * 8 + e;
+              pv[e] = tc::ex2(fmaf(__uint_as_float(r[u * 8 + e]), p.scale_log2, -m));
+              if (partial && col >= rem) pv[e] = 0.f;
+              r8[e] += pv[e];
+            }
+            const int unit = c * 4 + u;
+            const uint32_t addr = p_base + (unit >> 3) * L::kChunk + tc::sw128_offset(row, unit & 7);
+            tc::st_shared_v4(addr, tc::pack_bf16(pv[0], pv[1]), tc::pack_bf16(pv[2], pv[3]),
+                             tc::pack_bf16(pv[4], pv[5]), tc::pack_bf16(pv[6], pv[7]));
           }
-          const uint32_t addr = p_base + (u >> 3) * L::kChunk + tc::sw128_offset(row, u & 7);
-          tc::st_shared_v4(addr, tc::pack_bf16(pv[0], pv[1]), tc::pack_bf16(pv[2], pv[3]), tc::pack_bf16(pv[4], pv[5]),
-                           tc::pack_bf16(pv[6], pv[7]));
         }
         l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
         tc::fence_proxy_async_smem();
@@ -372,6 +378,11 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
   static bool attr_set = false;
   if (!attr_set) {
     JG_CUDA(cudaFuncSetAttribute(fa::jfa_fwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
+    cudaFuncAttributes fa_attr;
+    JG_CUDA(cudaFuncGetAttributes(&fa_attr, fa::jfa_fwd_sm100_kernel<D>));
+    if (fa_attr.maxThreadsPerBlock < fa::kThreads)
+      return fail(JG_CUDA_ERROR, "jfa_fwd_sm100_kernel: " + std::to_string(fa_attr.numRegs) + " registers allow only " +
+                                     std::to_string(fa_attr.maxThreadsPerBlock) + " threads per block");
     attr_set = true;
   }
   fa::Params p{off, items, n_items, batch, total_rows, H, (__nv_bfloat16*)out, lse,
