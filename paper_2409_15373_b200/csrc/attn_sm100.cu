@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         return s;
       };
       auto issue_s = [&](int t, uint32_t k_stage) {
+        const long long t0 = clock64();
         const uint32_t qa = q_base + t * L::kTile, ka = kv_base + k_stage * L::kTile;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -188,9 +189,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mma_bf16_ss(tmem + t * 256, tc::sw128_desc(qa + koff, 16, 1024), tc::sw128_desc(ka + koff, 16, 1024),
                           kIdescS, kk > 0);
         }
+        wp.add(5, clock64() - t0);
+        wp.add(6, D / 16);
         tc::mma_commit(s_full + t);
       };
       auto issue_pv = [&](int t, uint32_t v_stage, int j) {
+        const long long t0 = clock64();
         const uint32_t pa = p_base + t * 2 * L::kChunk, va = kv_base + v_stage * L::kTile;
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
@@ -199,10 +203,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mma_bf16_ss(tmem + t * 256 + 128, tc::sw128_desc(pa + aoff, 16, 1024),
                           tc::sw128_desc(va + kk * 16 * 128, L::kChunk, 1024), kIdescO, (j > 0 || kk > 0));
         }
+        wp.add(5, clock64() - t0);
+        wp.add(6, BN / 16);
       };
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+        const long long t_li = clock64();
         const Item it = load_item(p, w);
         const int nt = it.has_b ? 2 : 1;
+        wp.add(1, clock64() - t_li);
         wp.wait(q_full, item_cnt & 1, 0);
         uint32_t ks = next_stage();  // K_0
         for (int t = 0; t < nt; ++t) issue_s(t, ks);
@@ -258,14 +266,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool partial = rem < BN;  // warp-uniform: only a segment's last key block is partial
         // pass 1: raw-score row max over TMEM in 32-column chunks, 8 independent chains
         float m8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (!partial) {
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld32(s_addr + c * 32, r);
-          tc::tmem_wait_ld();
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tc::tmem_ld32(s_addr + c * 32, r);
+            tc::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (!partial || c * 32 + e < rem) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e]));
+            for (int e = 0; e < 32; ++e) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e]));
+          }
+        } else {
+          // last key block of the segment: write -inf over the keys of the next sample back into TMEM so
+          // the exp pass needs no masking (exp2(-inf) = 0)
+          const int remi = (int)rem;
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tc::tmem_ld32(s_addr + c * 32, r);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              r[e] = c * 32 + e < remi ? r[e] : __float_as_uint(-INFINITY);
+              m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e]));
+            }
+            tc::tmem_st32(s_addr + c * 32, r);
+          }
+          tc::tmem_wait_st();
         }
         const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * p.scale_log2;
@@ -301,9 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float pv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const int col = c * 32 + u * 8 + e;
               pv[e] = tc::ex2(fmaf(__uint_as_float(r[u * 8 + e]), p.scale_log2, -m));
-              if (partial && col >= rem) pv[e] = 0.f;
               r8[e] += pv[e];
             }
             const int unit = c * 4 + u;
@@ -392,8 +416,8 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
   JG_LAUNCHED("jfa_fwd_sm100_kernel");
   wait_prof_end(p.prof, st, "fwd",
-                {"P.q_empty", "P.kv_empty", "", "", "", "", "", "P.total", "M.q_full", "", "M.kv_full", "M.o_empty",
-                 "M.p_full", "", "", "M.total", "S.s_full", "", "S.o_done", "", "", "", "", "S.total"});
+                {"P.q_empty", "P.kv_empty", "", "", "", "", "", "P.total", "M.q_full", "M.load_item", "M.kv_full", "M.o_empty",
+                 "M.p_full", "M.issue_cyc", "M.n_mma(x1e-2%)", "M.total", "S.s_full", "", "S.o_done", "", "", "", "", "S.total"});
   return JG_OK;
 }
 
