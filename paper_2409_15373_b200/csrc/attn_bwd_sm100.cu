@@ -13,7 +13,7 @@
 //        dV += P^T dO_j, dK += dS^T Q_j                      (accumulated in TMEM across all j)
 //        dQ_j^T = K^T dS^T                                    (M = head_dim, N = 64 queries)
 //      dQ_j^T is drained by a second warpgroup through smem and added into the fp32 accumulator with
-//      bulk async reductions (cp.reduce.async.bulk .add.f32, one 512 B row per query).
+//      one TMA tensor reduce-add per block (cp.reduce.async.bulk.tensor .add, [64 q x D] fp32 box).
 //   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
 // Warps: 0 TMA producer, 1 MMA issuer, 4-7 softmax/dS, 8-11 dQ drain + dK/dV epilogue.
 // TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); dQ_j^T reuses the S^T slot
@@ -76,6 +76,12 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, uint32_t ssrc, 
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void tensor_reduce_add_3d(const CUtensorMap* map, uint32_t ssrc, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(ssrc), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -92,7 +98,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     jfa_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                         Params p) {
+                         const __grid_constant__ CUtensorMap tm_dq, Params p) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -138,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&tm_k);
     tc::tma_prefetch(&tm_v);
     tc::tma_prefetch(&tm_do);
+    tc::tma_prefetch(&tm_dq);
   }
   if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
@@ -360,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(dq_empty + b);
         const long long tb = clock64();
-        if (tid < BQ) bulk_wait_read0();  // previous block's reductions have read the staging buffer
+        if (tid == 0) bulk_wait_read0();  // the previous block's reduction has read the staging buffer
         named_bar(2, 128);
         wp.add(1, clock64() - tb);
 #pragma unroll
@@ -369,12 +376,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < 32; ++q) stg[(q + 32) * D + tid] = __uint_as_float(c2[q]) * p.scale;
         tc::fence_proxy_async_smem();
         named_bar(2, 128);
-        if (tid < BQ) {
-          const int64_t q = (int64_t)j * BQ + tid;
-          if (q < n) {
-            bulk_reduce_add_f32(p.dq_acc + ((b0 + q) * H + h) * D, stg_base + tid * D * 4, D * 4);
-            bulk_commit();
-          }
+        // one TMA tensor reduce-add of the whole [64 q x D] fp32 box into the accumulator; rows of padded
+        // queries are exactly zero (P = 0 there), so adding them into the next sample's rows is a no-op
+        if (tid == 0) {
+          tensor_reduce_add_3d(&tm_dq, stg_base, 0, h, (int)(b0 + (int64_t)j * BQ));
+          bulk_commit();
         }
       }
       // dK / dV for this key tile
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(dkv_empty);
     }
-    if (tid < BQ) bulk_wait0();
+    if (tid == 0) bulk_wait0();
     wp.add(7, clock64() - t_role);
     wp.flush();
   }
@@ -492,6 +498,8 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   if (jg_status rc = make_map(&mk, k, total_rows, H, kD, fb::BKV)) return rc;
   if (jg_status rc = make_map(&mv, v, total_rows, H, kD, fb::BKV)) return rc;
   if (jg_status rc = make_map(&mdo, go, total_rows, H, kD, fb::BQ)) return rc;
+  CUtensorMap mdq;
+  if (jg_status rc = make_map_f32(&mdq, dq_acc, total_rows, H, kD, fb::BQ)) return rc;
   static bool attr_set = false;
   if (!attr_set) {
     JG_CUDA(cudaFuncSetAttribute(fb::jfa_bwd_sm100_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
@@ -500,7 +508,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   fb::Params p{off, items, n_items, total_rows, H, lse, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), wait_prof_begin(st)};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
-  fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, p);
+  fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
   wait_prof_end(p.prof, st, "bwd",
                 {"P.kv_empty", "P.qd_empty", "", "", "", "", "", "P.total", "M.kv_full", "M.dkv_empty", "M.qd_full",

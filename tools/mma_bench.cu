@@ -21,10 +21,12 @@ template <int N, bool TWO_ACC, int CONT>
 __global__ void __launch_bounds__(256, 1) mma_bench(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
+  __shared__ uint64_t bar2;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     tc::mbar_init(&bar, 1);
+    tc::mbar_init(&bar2, 1);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc<512>(&slot);
@@ -66,6 +68,10 @@ __global__ void __launch_bounds__(256, 1) mma_bench(int iters, unsigned long lon
     for (int i = 0; i < iters; ++i) {
       const uint32_t d = TWO_ACC ? tmem + (i & 1) * 256 : tmem;
       tc::mma_bf16_ss(d, tc::sw128_desc(a + (i & 3) * 32, lbo, 1024), tc::sw128_desc(b + (i & 3) * 32, lbo, 1024), id, 1);
+      if ((CONT & 16) && (i & 7) == 7) {  // commit every 8 MMAs (to a barrier nobody waits on)
+        tc::mma_commit(&bar2);
+        tc::tc_fence_after();
+      }
     }
     const long long t1 = clock64();
     tc::mma_commit(&bar);
@@ -116,8 +122,7 @@ int main() {
   run<128, false, 1>(4096);
   run<128, false, 2>(4096);
   run<128, false, 3>(4096);
-  run<128, false, 4>(4096);
-  run<128, false, 12>(4096);
-  run<64, false, 12>(4096);
+  run<128, false, 16>(4096);
+  run<128, false, 17>(4096);
   return 0;
 }
