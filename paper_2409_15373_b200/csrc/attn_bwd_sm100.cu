@@ -12,8 +12,8 @@
 //        P^T, dS^T in registers -> smem (bf16, SWIZZLE_128B)  (softmax warpgroup, thread = key row)
 //        dV += P^T dO_j, dK += dS^T Q_j                      (accumulated in TMEM across all j)
 //        dQ_j^T = K^T dS^T                                    (M = head_dim, N = 64 queries)
-//      dQ_j^T is drained by a second warpgroup straight from TMEM into the fp32 accumulator with
-//      coalesced red.global.add.f32 (no smem staging: the freed 32 KB buys a 4th Q/dO stage).
+//      dQ_j^T is drained by a second warpgroup through smem and added into the fp32 accumulator with
+//      one TMA tensor reduce-add per block (cp.reduce.async.bulk.tensor .add, [64 q x D] fp32 box).
 //   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
 // Warps: 0 TMA producer, 1 MMA issuer, 4-7 softmax/dS, 8-11 dQ drain + dK/dV epilogue.
 // TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); dQ_j^T reuses the S^T slot
@@ -39,13 +39,14 @@ struct Smem {
   static constexpr int kChunkQ = BQ * 128;    // [64 rows x 64] bf16 = 8 KB
   static constexpr int kTileKV = (D / 64) * kChunkKV;
   static constexpr int kTileQ = (D / 64) * kChunkQ;
-  static constexpr int kStages = 4;
+  static constexpr int kStages = 3;
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTileKV;
   static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
   static constexpr int kP = kQD + kStages * 2 * kTileQ;     // P^T  [128 keys x 64 q] bf16
   static constexpr int kDS = kP + BKV * 128;                // dS^T [128 keys x 64 q] bf16
-  static constexpr int kLse = kDS + BKV * 128;              // 2 x (64 lse + 64 delta) fp32
+  static constexpr int kStg = kDS + BKV * 128;              // dQ staging [64 q x D] fp32
+  static constexpr int kLse = kStg + BQ * D * 4;            // 2 x (64 lse + 64 delta) fp32
   static constexpr int kBar = kLse + 2 * 2 * BQ * 4;
   static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 4 + 2 + 1;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
@@ -342,6 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = threadIdx.x - kDqWarp0 * 32;  // == TMEM lane: head-dim row of dQ^T, key row of dK/dV
     const int wq = warp - kDqWarp0;
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
+    float* stg = reinterpret_cast<float*>(smem + L::kStg);
+    const uint32_t stg_base = tc::smem_u32(stg);
     uint32_t item_cnt = 0, dqc[2] = {0, 0};
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 24);
@@ -363,18 +366,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(dq_empty + b);
-        // dQ_j rows += dQ^T_j columns: thread d adds its 64 values with coalesced fp32 reductions (a warp
-        // covers 32 consecutive floats of one query row); padded queries (q >= n) are skipped
-        const int64_t q0 = (int64_t)j * BQ;
-        float* dst = p.dq_acc + ((b0 + q0) * H + h) * D + tid;
-        const int64_t stride = (int64_t)H * D;
-        const int nv = n - q0 < BQ ? (int)(n - q0) : BQ;
+        const long long tb = clock64();
+        if (tid == 0) bulk_wait_read0();  // the previous block's reduction has read the staging buffer
+        named_bar(2, 128);
+        wp.add(1, clock64() - tb);
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q < nv) atomicAdd(dst + q * stride, __uint_as_float(a[q]) * p.scale);
+        for (int q = 0; q < 32; ++q) stg[q * D + tid] = __uint_as_float(a[q]) * p.scale;
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q + 32 < nv) atomicAdd(dst + (q + 32) * stride, __uint_as_float(c2[q]) * p.scale);
+        for (int q = 0; q < 32; ++q) stg[(q + 32) * D + tid] = __uint_as_float(c2[q]) * p.scale;
+        tc::fence_proxy_async_smem();
+        named_bar(2, 128);
+        // one TMA tensor reduce-add of the whole [64 q x D] fp32 box into the accumulator; rows of padded
+        // queries are exactly zero (P = 0 there), so adding them into the next sample's rows is a no-op
+        if (tid == 0) {
+          tensor_reduce_add_3d(&tm_dq, stg_base, 0, h, (int)(b0 + (int64_t)j * BQ));
+          bulk_commit();
+        }
       }
       // dK / dV for this key tile
       wp.wait(dkv_full, item_cnt & 1, 2);
@@ -409,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(dkv_empty);
     }
+    if (tid == 0) bulk_wait0();
     wp.add(7, clock64() - t_role);
     wp.flush();
   }
