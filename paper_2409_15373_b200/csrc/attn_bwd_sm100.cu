@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_bf16_ss(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
                             tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
           }
+          tc::mma_commit(qd_empty + (qd_cnt % L::kStages));  // Q_j, dO_j no longer needed
           // dQ_j^T = K^T dS^T into the S^T slot of buffer j&1 (its scores were consumed: p_full)
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk) {
@@ -259,7 +260,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
           }
           tc::mma_commit(dq_full + (j & 1));
-          tc::mma_commit(qd_empty + (qd_cnt % L::kStages));
           tc::mma_commit(pds_empty);
         }
         tc::mma_commit(dkv_full);
