@@ -1,0 +1,154 @@
+// dropin_test.cpp — the reference's own API, linked against the B200 drop-in instead of linalg.o /
+// attention.o. Written like the reference's tests (proj/tests/test_core.cpp style): build inputs with
+// jagged::make_jagged / jagged::Rng, call the jagged:: operators, compare with independent binary64
+// loops (cf. proj/tests/support/reference.hpp) and check the reference's exception texts.
+// Exit code 0 = all checks passed. Run by tests/test_gpu_cpp_dropin.py on the GPU box.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "jagged/attention.hpp"
+#include "jagged/linalg.hpp"
+#include "jagged/rng.hpp"
+#include "jagged/tensor.hpp"
+
+using namespace jagged;
+
+static int failures = 0;
+
+static void check(bool ok, const std::string& what) {
+  std::printf("%s %s\n", ok ? "OK  " : "FAIL", what.c_str());
+  if (!ok) ++failures;
+}
+
+// norm-wise relative error of a float result against a binary64 expectation
+static double rel(const std::vector<float>& got, const std::vector<double>& ref) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < ref.size(); ++i) {
+    num += (got[i] - ref[i]) * (got[i] - ref[i]);
+    den += ref[i] * ref[i];
+  }
+  return std::sqrt(num / (den > 0 ? den : 1));
+}
+
+template <typename F>
+static bool throws_with(F&& f, const std::string& text) {
+  try {
+    f();
+  } catch (const std::invalid_argument& e) {
+    return std::string(e.what()).find(text) != std::string::npos;
+  }
+  return false;
+}
+
+int main() {
+  const std::vector<int64_t> lengths = {0, 1, 2, 5, 7, 17, 33, 70, 130, 0, 257};
+  const int64_t D = 64, T = 16, B = (int64_t)lengths.size();
+  Rng rng(42);
+  int64_t S = 0;
+  for (auto n : lengths) S += n;
+  auto x = make_jagged<float>(lengths, uniform_values<float>(rng, S * D, -1, 1), D);
+  auto y = make_jagged<float>(lengths, uniform_values<float>(rng, S * D, -1, 1), D);
+  auto v = make_jagged<float>(lengths, uniform_values<float>(rng, S * D, -1, 1), D);
+  auto go = make_jagged<float>(lengths, uniform_values<float>(rng, S * D, -1, 1), D);
+  DenseTensor<float> w({B, D, T}, uniform_values<float>(rng, B * D * T, -1, 1));
+  const auto& off = x.offsets();
+
+  // --- jagged_dense_bmm (linalg.cpp:34-68)
+  {
+    auto o = jagged_dense_bmm(x, w);
+    std::vector<double> ref(S * T);
+    for (int64_t i = 0; i < B; ++i)
+      for (int64_t r = off[i]; r < off[i + 1]; ++r)
+        for (int64_t t = 0; t < T; ++t) {
+          double a = 0;
+          for (int64_t d = 0; d < D; ++d) a += (double)x.row(r)[d] * w.at(i, d, t);
+          ref[r * T + t] = a;
+        }
+    check(o.offsets() == off && rel(o.values(), ref) < 1e-5, "jagged_dense_bmm rel=" + std::to_string(rel(o.values(), ref)));
+  }
+  // --- jagged_softmax (linalg.cpp:98-120)
+  {
+    auto o = jagged_softmax(x);
+    std::vector<double> ref(S * D);
+    for (int64_t i = 0; i < B; ++i)
+      for (int64_t d = 0; d < D; ++d) {
+        double m = -INFINITY, s = 0;
+        for (int64_t r = off[i]; r < off[i + 1]; ++r) m = std::max(m, (double)x.row(r)[d]);
+        for (int64_t r = off[i]; r < off[i + 1]; ++r) s += std::exp(x.row(r)[d] - m);
+        for (int64_t r = off[i]; r < off[i + 1]; ++r) ref[r * D + d] = std::exp(x.row(r)[d] - m) / s;
+      }
+    check(rel(o.values(), ref) < 1e-5, "jagged_softmax rel=" + std::to_string(rel(o.values(), ref)));
+  }
+  // --- flash attention fwd / bwd vs unfused jagged_attention and a binary64 loop
+  {
+    auto saved = jagged_flash_attention_forward(x, y, v, 64, 64);
+    std::vector<double> ref(S * D), lse(S);
+    const double sc = 1.0 / std::sqrt((double)D);
+    for (int64_t i = 0; i < B; ++i)
+      for (int64_t a = off[i]; a < off[i + 1]; ++a) {
+        std::vector<double> s(off[i + 1] - off[i]);
+        double m = -INFINITY, z = 0;
+        for (int64_t c = off[i]; c < off[i + 1]; ++c) {
+          double acc = 0;
+          for (int64_t d = 0; d < D; ++d) acc += (double)x.row(a)[d] * y.row(c)[d];
+          s[c - off[i]] = acc * sc;
+          m = std::max(m, s[c - off[i]]);
+        }
+        for (auto& e : s) z += (e = std::exp(e - m));
+        for (int64_t d = 0; d < D; ++d) {
+          double acc = 0;
+          for (int64_t c = off[i]; c < off[i + 1]; ++c) acc += s[c - off[i]] * v.row(c)[d];
+          ref[a * D + d] = acc / z;
+        }
+        lse[a] = m + std::log(z);
+      }
+    check(rel(saved.output.values(), ref) < 1e-5,
+          "jagged_flash_attention_forward rel=" + std::to_string(rel(saved.output.values(), ref)));
+    check(rel(saved.logsumexp, lse) < 1e-6, "logsumexp rel=" + std::to_string(rel(saved.logsumexp, lse)));
+    auto un = jagged_attention(x, y, v);
+    check(rel(un.values(), ref) < 1e-5, "jagged_attention (unfused) rel=" + std::to_string(rel(un.values(), ref)));
+    auto g = jagged_flash_attention_backward(x, y, v, go, saved);
+    // dv = P^T dO check (attention.cpp:274-275)
+    std::vector<double> dv(S * D, 0.0);
+    for (int64_t i = 0; i < B; ++i)
+      for (int64_t a = off[i]; a < off[i + 1]; ++a)
+        for (int64_t c = off[i]; c < off[i + 1]; ++c) {
+          double acc = 0;
+          for (int64_t d = 0; d < D; ++d) acc += (double)x.row(a)[d] * y.row(c)[d];
+          const double p = std::exp(acc * sc - lse[a]);
+          for (int64_t d = 0; d < D; ++d) dv[c * D + d] += p * go.row(a)[d];
+        }
+    check(rel(g.dv.values(), dv) < 1e-5, "jagged_flash_attention_backward dv rel=" + std::to_string(rel(g.dv.values(), dv)));
+    check(g.dq.offsets() == off && g.dk.offsets() == off, "gradients keep the input offsets");
+  }
+  // --- feature_interaction composition (attention.cpp:291-309) runs end to end
+  {
+    DenseTensor<float> targets({B, 3, D}, uniform_values<float>(rng, B * 3 * D, -1, 1));
+    auto fi = feature_interaction(x, v, targets);
+    check(fi.shape() == std::vector<int64_t>({B, 3, D}), "feature_interaction shape");
+  }
+  // --- reference exception texts
+  check(throws_with([&] { jagged_dense_bmm(x, DenseTensor<float>({B, D}, std::vector<float>(B * D))); },
+                    "jagged_dense_bmm: w must be [B, D, T]"),
+        "error: w must be [B, D, T]");
+  check(throws_with([&] { jagged_flash_attention_forward(x, y, v, 0, 64); }, "block sizes must be >= 1"),
+        "error: block sizes must be >= 1");
+  {
+    std::vector<int64_t> l2 = lengths;
+    std::swap(l2[1], l2[2]);
+    auto z = make_jagged<float>(l2, std::vector<float>(S * D, 0.f), D);
+    check(throws_with([&] { jagged_jagged_bmm(x, z); }, "jagged_jagged_bmm: offsets differ first at sample 1"),
+          "error: offsets differ first at sample 1");
+    check(throws_with([&] { jagged_flash_attention_forward(x, z, v, 64, 64); }, "q, k, v must share offsets"),
+          "error: q, k, v must share offsets");
+  }
+  {
+    auto xd = make_jagged<double>(lengths, std::vector<double>(S * D, 0.0), D);
+    check(throws_with([&] { jagged_softmax(xd); }, "no B200 device path"), "binary64 reports no device path");
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
+  return failures ? 1 : 0;
+}
