@@ -318,15 +318,244 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ secondary BASELINE configs
+# `--config cfg1|cfg2|cfg4|cfg5|dense` prints one JSON line per measured operator group; cfg3 (the
+# headline) is the default mode above. Times are CUDA events on the launching stream after warm-up,
+# median over `--steps`; inputs are device-resident (cfg4/cfg5 inputs exceed L2).
+def _events_time(fn, steps, warmup):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def _cpu_ref_time(fn, reps=3):
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts))
+
+
+def run_configs(args):
+    import torch
+
+    from paper_2409_15373_b200 import _lib, synth
+    from paper_2409_15373_b200 import jagged as J
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    lib = _lib.lib()
+    pk_burst, _, hbm, src = peaks()
+    g = torch.Generator(device=dev).manual_seed(1)
+    rnd = lambda *s, dt=torch.bfloat16: (torch.rand(*s, device=dev, generator=g) * 2 - 1).to(dt)  # noqa: E731
+    kind, threads = _cpu_kind() if not args.no_cpu_baseline else ("none", 0)
+    out = []
+
+    def emit(line):
+        line.setdefault("data", "synthetic")
+        line.setdefault("n_gpus", 1)
+        print(json.dumps(line), flush=True)
+        out.append(line)
+
+    cfg = args.config
+    if cfg == "cfg1":
+        # jagged_dense_bmm + jagged_softmax, B=64 L=128 D=64 T=32 uniform lengths seed 0, fp32
+        ln = synth.gen_lengths("uniform", 128, 0, 64)
+        off = synth.offsets_of(ln)
+        S, B, D, T = int(off[-1]), 64, 64, 32
+        X = J.JaggedTensor(torch.from_numpy(off).to(dev), rnd(S, D, dt=torch.float32), off)
+        W = rnd(B, D, T, dt=torch.float32)
+
+        def step():
+            J.jagged_softmax(J.jagged_dense_bmm(X, W))
+
+        ms = _events_time(step, args.steps, args.warmup)
+        eb = 4
+        byts = (S * D + B * D * T + S * T) * eb + 2 * S * T * eb  # cost_model.cpp:153-155, :165-168
+        flops = 2 * S * D * T
+        cpu = None
+        if kind != "none":
+            from oracle import reference as F
+
+            xh, wh = X.values.cpu().numpy(), W.cpu().numpy()
+            t = _cpu_ref_time(lambda: F.jagged_softmax(off, F.jagged_dense_bmm(off, xh, wh, "f32", threads), "f32",
+                                                       threads))
+            cpu = {"value": byts / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+                   "sample": "full cfg1 (jagged_dense_bmm + jagged_softmax, fp32)", "us": t * 1e6}
+        emit({"metric": "jagged-op GB/s", "config": {"workload": "cfg1: jagged_dense_bmm + jagged_softmax B=64 "
+              "max_len=128 D=64 T=32 uniform seed 0", "sum_B": S}, "dtype": "f32", "value": byts / (ms * 1e-3) / 1e9,
+              "unit": "GB/s", "us_per_step": ms * 1e3, "tflops": flops / (ms * 1e-3) / 1e12,
+              "roofline": {"bound": "hbm", "achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                           "frac": byts / (ms * 1e-3) / 1e9 / hbm, "note": "~2.8 MB: launch-latency bound"},
+              "cpu_baseline": cpu})
+    elif cfg in ("cfg2", "cfg5"):
+        if cfg == "cfg2":
+            ln, D, H, fwd_only = synth.gen_lengths("zipf", 512, 0, 256, 1.1), 64, 1, True
+            wl = "cfg2: JFA fwd B=256 max_len=512 D=64 H=1 bf16 Zipf(1.1) seed 0"
+        else:
+            ln, D, H, fwd_only = synth.gen_lengths("zipf", 4096, 0, 4096, 0.8), 128, 1, False
+            wl = "cfg5: JFA fwd+bwd B=4096 max_len=4096 D=128 H=1 bf16 Zipf(0.8) seed 0"
+        off = synth.offsets_of(ln)
+        S = int(off[-1])
+        Q, K, V, G = (J.JaggedTensor(torch.from_numpy(off).to(dev), rnd(S, H, D), off) for _ in range(4))
+        sched = J.Schedule(Q)
+        fwd_fl, bwd_fl, sq = useful_flops(ln, H, D)
+        saved = J.jagged_flash_attention_forward(Q, K, V, schedule=sched)
+        ms_f = _events_time(lambda: J.jagged_flash_attention_forward(Q, K, V, schedule=sched), args.steps, args.warmup)
+        line = {"metric": "Jagged flash-attn " + ("fwd" if fwd_only else "fwd+bwd") + " TFLOP/s (useful FLOPs)",
+                "config": {"workload": wl, "sum_B": S, "sum_sq": sq}, "dtype": "bf16",
+                "fwd_ms": ms_f, "fwd_tflops": fwd_fl / (ms_f * 1e-3) / 1e12}
+        total_fl, total_ms = fwd_fl, ms_f
+        if not fwd_only:
+            ws = torch.empty(lib.jg_attention_backward_workspace_size(S, H, D), dtype=torch.uint8, device=dev)
+            ms_b = _events_time(lambda: J.jagged_flash_attention_backward(Q, K, V, G, saved, schedule=sched,
+                                                                          workspace=ws), args.steps, args.warmup)
+            line.update(bwd_ms=ms_b, bwd_tflops=bwd_fl / (ms_b * 1e-3) / 1e12)
+            total_fl, total_ms = fwd_fl + bwd_fl, ms_f + ms_b
+        line.update(value=total_fl / (total_ms * 1e-3) / 1e12, unit="TFLOP/s",
+                    roofline={"bound": "tensor", "achieved": total_fl / (total_ms * 1e-3) / 1e12, "peak": pk_burst,
+                              "unit": "TFLOP/s", "frac": total_fl / (total_ms * 1e-3) / 1e12 / pk_burst})
+        if kind != "none":
+            from oracle import reference as F
+
+            stride = 1 if cfg == "cfg2" else 64
+            sub = ln[::stride]
+            sub = sub[sub > 0]
+            so = synth.offsets_of(sub)
+            ss = int(so[-1])
+            r = np.random.default_rng(0)
+            qh, kh, vh, gh = (r.uniform(-1, 1, (ss, D)).astype(np.float32) for _ in range(4))
+
+            def cpu_run():
+                o, l_ = F.jfa_forward(so, qh, kh, vh, 64, 64, "f32", threads)
+                if not fwd_only:
+                    F.jfa_backward(so, qh, kh, vh, gh, o, l_, 64, 64, "f32", threads)
+
+            t = _cpu_ref_time(cpu_run, reps=1 if cfg == "cfg5" else 3)
+            fl = (4 if fwd_only else 14) * D * int((sub * sub).sum())
+            line["cpu_baseline"] = {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
+                                    "sample": f"every {stride}th sample ({len(sub)} samples), fp32, {t:.1f} s"}
+        emit(line)
+    elif cfg == "cfg4":
+        # jagged op suite at sum_B = 1,048,576 (half-mean B=2048 L=1024 seed 0), D=T=256, bf16 inputs
+        ln = synth.gen_lengths("half-mean", 1024, 0, 2048)
+        off = synth.offsets_of(ln)
+        S, B, D = int(off[-1]), len(ln), 256
+        sq = int((ln * ln).sum())
+        X, Y = (J.JaggedTensor(torch.from_numpy(off).to(dev), rnd(S, D), off) for _ in range(2))
+        A = J.Jagged2Tensor(X.offsets, rnd(sq), off)
+        eb = 2
+        ops = {
+            "jagged_jagged_bmm_jagged_out": (lambda: J.jagged_jagged_bmm_jagged_out(X, Y), 2 * sq * D,
+                                             (2 * S * D + sq) * eb),
+            "array_jagged_bmm_jagged_out": (lambda: J.array_jagged_bmm_jagged_out(A, X), 2 * sq * D,
+                                            (2 * S * D + sq) * eb),
+            "jagged_jagged_bmm": (lambda: J.jagged_jagged_bmm(X, Y), 2 * S * D * D, (2 * S * D + B * D * D) * eb),
+            "jagged_softmax": (lambda: J.jagged_softmax(X), 4 * S * D, 2 * S * D * eb),
+            "jagged2_softmax": (lambda: J.jagged2_softmax(A), 4 * sq, 2 * sq * eb),
+        }
+        for name, (fn, fl, byts) in ops.items():
+            ms = _events_time(fn, args.steps, args.warmup)
+            gbs, tfs = byts / (ms * 1e-3) / 1e9, fl / (ms * 1e-3) / 1e12
+            emit({"metric": "jagged-op GB/s", "op": name, "config": {"workload": "cfg4: half-mean B=2048 L=1024 "
+                  "seed 0 (sum_B=1,048,576), D=T=256, bf16 in / bf16 out", "sum_sq": sq}, "dtype": "bf16",
+                  "value": gbs, "unit": "GB/s", "ms": ms, "tflops": tfs,
+                  "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                               "tensor_frac": tfs / pk_burst}})
+    elif cfg == "dense":
+        # the paper's jagged-vs-padded comparison on cfg3: padded dense attention (materialised masked
+        # scores, PyTorch bf16 matmul + softmax, the paper's "PyTorch" column) and padded dense flash
+        # attention (torch SDPA with a key-padding mask) vs our jagged flash attention, fwd+bwd, with
+        # peak memory. These comparators are library code used only as baselines.
+        ln = synth.gen_lengths(CFG["dist"], CFG["max_len"], CFG["seed"], CFG["batch_per_gpu"])
+        off = synth.offsets_of(ln)
+        S, B, L, D, H = int(off[-1]), len(ln), CFG["max_len"], CFG["head_dim"], CFG["heads"]
+        fwd_fl, bwd_fl, _ = useful_flops(ln, H, D)
+        Q, K, V, G = (J.JaggedTensor(torch.from_numpy(off).to(dev), rnd(S, H, D), off) for _ in range(4))
+        sched = J.Schedule(Q)
+        ws = torch.empty(lib.jg_attention_backward_workspace_size(S, H, D), dtype=torch.uint8, device=dev)
+
+        def jagged_step():
+            s_ = J.jagged_flash_attention_forward(Q, K, V, schedule=sched)
+            J.jagged_flash_attention_backward(Q, K, V, G, s_, schedule=sched, workspace=ws)
+
+        def measure(fn):
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            ms = _events_time(fn, max(2, args.steps // 2), 2)
+            return ms, (torch.cuda.max_memory_allocated() - base) / 2**30
+
+        ms_j, mem_j = measure(jagged_step)
+        # padded inputs [B, H, L, D] built from the same jagged values (jagged_to_dense on device)
+        pad = lambda t: J.jagged_to_dense(J.JaggedTensor(t.offsets, t.values.reshape(S, H * D), off), L, 0.0) \
+            .reshape(B, L, H, D).transpose(1, 2).contiguous()  # noqa: E731
+        qp, kp, vp, gp = pad(Q), pad(K), pad(V), pad(G)
+        lens = torch.from_numpy(ln).to(dev)
+        keymask = torch.arange(L, device=dev)[None, :] < lens[:, None]  # [B, L]
+        addmask = torch.zeros(B, 1, 1, L, device=dev, dtype=torch.bfloat16).masked_fill(~keymask[:, None, None, :],
+                                                                                          float("-inf"))
+
+        def dense_step():
+            q_, k_, v_ = (t.detach().requires_grad_() for t in (qp, kp, vp))
+            s_ = torch.matmul(q_, k_.transpose(-1, -2)) * (D ** -0.5) + addmask
+            p_ = torch.softmax(s_.float(), dim=-1).nan_to_num_(0.0).to(torch.bfloat16)
+            o_ = torch.matmul(p_, v_)
+            o_.backward(gp)
+
+        def flash_step():
+            q_, k_, v_ = (t.detach().requires_grad_() for t in (qp, kp, vp))
+            o_ = torch.nn.functional.scaled_dot_product_attention(q_, k_, v_, attn_mask=keymask[:, None, None, :])
+            o_.backward(gp)
+
+        res = {"jagged_flash (ours)": (ms_j, mem_j)}
+        for name, fn in (("padded dense attention (torch matmul+softmax)", dense_step),
+                         ("padded dense flash (torch SDPA + mask)", flash_step)):
+            try:
+                res[name] = measure(fn)
+            except RuntimeError as e:  # OOM on the padded baselines is itself the memory claim
+                res[name] = (float("nan"), float("nan"))
+                print(f"{name}: {e}", file=sys.stderr)
+            torch.cuda.empty_cache()
+        emit({"metric": "jagged vs padded attention fwd+bwd (cfg3)", "config": {"workload": "cfg3 B=1024 L=1024 D=128 "
+              "H=4 bf16 half-mean seed 0", "padded_flops_ratio": float(B * L * L / (ln.astype(np.int64) ** 2).sum())},
+              "dtype": "bf16", "value": ms_j, "unit": "ms",
+              "results": {k2: {"ms": v2[0], "peak_GiB": v2[1], "useful_tflops": (fwd_fl + bwd_fl) / (v2[0] * 1e-3) / 1e12}
+                          for k2, v2 in res.items()},
+              "speedup_vs_dense": res["padded dense attention (torch matmul+softmax)"][0] / ms_j,
+              "speedup_vs_dense_flash": res["padded dense flash (torch SDPA + mask)"][0] / ms_j,
+              "memory_ratio_vs_dense": res["padded dense attention (torch matmul+softmax)"][1] / mem_j,
+              "memory_ratio_vs_dense_flash": res["padded dense flash (torch SDPA + mask)"][1] / mem_j})
+    if args.out:
+        with open(args.out, "a") as f:
+            for line in out:
+                f.write(json.dumps(line) + "\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "dense"],
+                    help="cfg3 = the headline JSON line; the others measure the secondary BASELINE configs")
+    ap.add_argument("--out", default=None, help="also append secondary-config lines to this file")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))
@@ -336,6 +565,9 @@ def main():
         world = 1  # single process
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+        return
+    if args.config != "cfg3":
+        run_configs(args)
         return
     if world > 1:
         import torch
