@@ -511,7 +511,7 @@ def run_configs(args):
         def dense_step():
             q_, k_, v_ = (t.detach().requires_grad_() for t in (qp, kp, vp))
             s_ = torch.matmul(q_, k_.transpose(-1, -2)) * (D ** -0.5) + addmask
-            p_ = torch.softmax(s_.float(), dim=-1).nan_to_num_(0.0).to(torch.bfloat16)
+            p_ = torch.nan_to_num(torch.softmax(s_.float(), dim=-1), 0.0).to(torch.bfloat16)  # empty samples
             o_ = torch.matmul(p_, v_)
             o_.backward(gp)
 

@@ -104,6 +104,20 @@ static jg_status check_out(const char* op, jg_dtype in, jg_dtype out) {
   return JG_OK;
 }
 
+static bool force_simt_gemm() {
+  const char* e = std::getenv("JG_GEMM_IMPL");
+  return e && std::strcmp(e, "simt") == 0;
+}
+
+// tcgen05 path for the forward bmm family (bf16 inputs); op codes as in internal.h
+static jg_status tc_gemm(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
+                         int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, cudaStream_t st) {
+  if (batch == 0) return JG_OK;
+  Scratch prefix(st);
+  if (jg_status rc = prefix.alloc(sizeof(int64_t) * (batch + 1))) return rc;
+  return launch_gemm_sm100(op, off, sq, batch, total_rows, D, T, a, b, out, out_dt, (int64_t*)prefix.p, st);
+}
+
 }  // namespace jg
 
 using namespace jg;
@@ -269,6 +283,8 @@ extern "C" jg_status jg_jagged_dense_bmm(const int64_t* off, int64_t batch, int6
   if (jg_status rc = check_out("jagged_dense_bmm", in_dt, out_dt)) return rc;
   REQUIRE(D > 0 && T > 0, JG_INVALID_ARGUMENT, "jagged_dense_bmm: w must be [B, D, T]");
   (void)total_rows;
+  if (!force_simt_gemm() && gemm_sm100_supported(3, D, T, in_dt))
+    return tc_gemm(3, off, nullptr, batch, total_rows, D, T, x, w, out, out_dt, as_stream(stream));
   GemmDesc g = desc(BI(), C_(T), C_(D), OFF(D), C_(D), C_(1), IDX(D * T), C_(T), C_(1), OFF(T), C_(T), C_(1));
   return gemm(g, off, nullptr, batch, x, w, out, in_dt, out_dt, as_stream(stream));
 }
@@ -279,6 +295,8 @@ extern "C" jg_status jg_jagged_jagged_bmm(const int64_t* off, int64_t batch, int
   if (jg_status rc = check_out("jagged_jagged_bmm", in_dt, out_dt)) return rc;
   REQUIRE(D > 0 && T > 0, JG_INVALID_ARGUMENT, "jagged_jagged_bmm: dims must be positive");
   (void)total_rows;
+  if (!force_simt_gemm() && gemm_sm100_supported(2, D, T, in_dt))
+    return tc_gemm(2, off, nullptr, batch, total_rows, D, T, x, y, out, out_dt, as_stream(stream));
   GemmDesc g = desc(C_(D), C_(T), BI(), OFF(D), C_(1), C_(D), OFF(T), C_(T), C_(1), IDX(D * T), C_(T), C_(1));
   return gemm(g, off, nullptr, batch, x, y, out, in_dt, out_dt, as_stream(stream));
 }
@@ -296,6 +314,8 @@ extern "C" jg_status jg_jagged_jagged_bmm_jagged_out(const int64_t* off, const i
   if (jg_status rc = check_out("jagged_jagged_bmm_jagged_out", in_dt, out_dt)) return rc;
   REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged_jagged_bmm_jagged_out: sq_offsets required");
   (void)total_rows;
+  if (!force_simt_gemm() && gemm_sm100_supported(0, D, D, in_dt))
+    return tc_gemm(0, off, sq, batch, total_rows, D, D, q, k, out, out_dt, as_stream(stream));
   GemmDesc g = desc(BI(), BI(), C_(D), OFF(D), C_(D), C_(1), OFF(D), C_(1), C_(D), SQ(), BI(), C_(1));
   return gemm(g, off, sq, batch, q, k, out, in_dt, out_dt, as_stream(stream));
 }
@@ -306,6 +326,8 @@ extern "C" jg_status jg_array_jagged_bmm_jagged_out(const int64_t* off, const in
   if (jg_status rc = check_out("array_jagged_bmm_jagged_out", in_dt, out_dt)) return rc;
   REQUIRE(sq, JG_INVALID_ARGUMENT, "array_jagged_bmm_jagged_out: sq_offsets required");
   (void)total_rows;
+  if (!force_simt_gemm() && gemm_sm100_supported(1, D, D, in_dt))
+    return tc_gemm(1, off, sq, batch, total_rows, D, D, a, v, out, out_dt, as_stream(stream));
   GemmDesc g = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
   return gemm(g, off, sq, batch, a, v, out, in_dt, out_dt, as_stream(stream));
 }

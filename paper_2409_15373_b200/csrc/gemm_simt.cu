@@ -15,15 +15,15 @@ namespace jg {
 constexpr int kBM = 64, kBN = 64, kBK = 16, kGemmThreads = 256;
 
 __global__ void __launch_bounds__(1024) gemm_prefix_kernel(GemmDesc g, const int64_t* __restrict__ off,
-                                                           const int64_t* __restrict__ sq, int64_t batch,
-                                                           int64_t* __restrict__ prefix) {
+                                                           const int64_t* __restrict__ sq, int64_t batch, int bm,
+                                                           int bn, int64_t* __restrict__ prefix) {
   const int64_t chunk = (batch + blockDim.x - 1) / blockDim.x;
   const int64_t b = (int64_t)threadIdx.x * chunk, e = min(batch, b + chunk);
   auto tiles = [&](int64_t i) -> int64_t {
     const int64_t Bi = off[i + 1] - off[i];
     const int64_t s = sq ? sq[i] : 0;
     const int64_t M = g.M.at(Bi, off[i], s, i), N = g.N.at(Bi, off[i], s, i);
-    return ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+    return ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
   };
   int64_t local = 0;
   for (int64_t i = b; i < e; ++i) local += tiles(i);
@@ -108,12 +108,18 @@ __global__ void __launch_bounds__(kGemmThreads) grouped_gemm_kernel(GemmDesc g, 
   }
 }
 
+jg_status launch_gemm_prefix(const GemmDesc& g, const int64_t* off, const int64_t* sq, int64_t batch, int bm, int bn,
+                             int64_t* tile_prefix, cudaStream_t st) {
+  gemm_prefix_kernel<<<1, 1024, 0, st>>>(g, off, sq, batch, bm, bn, tile_prefix);
+  JG_LAUNCHED("gemm_prefix_kernel");
+  return JG_OK;
+}
+
 jg_status launch_grouped_gemm(const GemmDesc& g, const int64_t* off, const int64_t* sq, int64_t batch,
                               const void* A, const void* B, void* C, jg_dtype in_dt, jg_dtype out_dt,
                               int64_t* tile_prefix, cudaStream_t st) {
   if (batch == 0) return JG_OK;
-  gemm_prefix_kernel<<<1, 1024, 0, st>>>(g, off, sq, batch, tile_prefix);
-  JG_LAUNCHED("gemm_prefix_kernel");
+  if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, kBM, kBN, tile_prefix, st)) return rc;
   const int grid = 8 * device_sm_count();
   using BF = __nv_bfloat16;
   if (in_dt == JG_F32 && out_dt == JG_F32)

@@ -57,6 +57,15 @@ jg_status launch_grouped_gemm(const GemmDesc& g, const int64_t* off, const int64
                               const void* A, const void* B, void* C, jg_dtype in_dt, jg_dtype out_dt,
                               int64_t* tile_prefix, cudaStream_t st);
 
+jg_status launch_gemm_prefix(const GemmDesc& g, const int64_t* off, const int64_t* sq, int64_t batch, int bm, int bn,
+                             int64_t* tile_prefix, cudaStream_t st);
+
+// tcgen05 bmm family (bf16 inputs): op 0 jjbmm_jout (q,k), 1 ajbmm_jout (a_j2,v), 2 jjbmm (x,y), 3 jdbmm (x,w)
+bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt);
+jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
+                            int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
+                            cudaStream_t st);
+
 // SIMT attention (fp32 mode, and any head_dim the tensor-core path does not cover)
 jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, void* out, float* lse,

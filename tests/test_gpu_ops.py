@@ -127,7 +127,8 @@ def _inputs(ln, D, T, seed, rnd):
                      go_dt=take(B * D * T, (B, D, T)), go_sq=take(SQ, (SQ,)))
 
 
-CASES = [("golden", 16, 8), ("uniform", 64, 32), ("long", 32, 48)]
+CASES = [("golden", 16, 8), ("uniform", 64, 32), ("long", 32, 48),
+         ("long", 128, 64), ("golden", 64, 128), ("uniform", 256, 256)]  # the last three hit tcgen05 (bf16)
 
 
 @pytest.mark.parametrize("lset,D,T", CASES)
