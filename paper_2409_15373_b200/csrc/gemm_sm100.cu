@@ -28,7 +28,8 @@ constexpr int kTileBytes = 16384;  // one operand stage: 128 x 64 bf16
 struct Smem {
   static constexpr int kA = 0;
   static constexpr int kB = kStages * kTileBytes;
-  static constexpr int kBar = 2 * kStages * kTileBytes;
+  static constexpr int kStg = 2 * kStages * kTileBytes;        // JJJ epilogue staging, 32 rows x 128 fp32 per warp
+  static constexpr int kBar = kStg + 4 * 32 * 128 * 4;
   static constexpr int kNumBars = 3 * kStages + 4 + 1;
   static constexpr int kAlloc = kBar + kNumBars * 8 + 16 + 1024;
 };
@@ -187,6 +188,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       else if (OP == JJ) base = tl.i * (int64_t)p.D * p.T + (int64_t)m * p.T + tl.n0;
       else base = (tl.b0 + m) * (int64_t)tl.N + tl.n0;
       const bool vec = OP != JJJ && ncols == BN;
+      if (OP == JJJ) {
+        // jagged^2 rows (stride Bi, arbitrary alignment): stage this warp's 32 rows in smem (row pitch 129
+        // floats, conflict-free) and write each row with the lanes along its columns (coalesced)
+        float* stg = reinterpret_cast<float*>(smem + Smem::kStg) + wq * 32 * 129;
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + c * 32, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) stg[lane * 129 + c * 32 + e] = __uint_as_float(v[e]);
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
+        const int nrows = tl.M - tl.m0 - wq * 32 < 32 ? tl.M - tl.m0 - wq * 32 : 32;
+        for (int rr = 0; rr < nrows; ++rr) {
+          const int64_t rb = tl.sqo + (int64_t)(tl.m0 + wq * 32 + rr) * tl.n + tl.n0;
+#pragma unroll
+          for (int h = 0; h < BN / 32; ++h) {
+            const int col = lane + 32 * h;
+            if (col < ncols) {
+              const float x = stg[rr * 129 + col];
+              if (p.out_f32) reinterpret_cast<float*>(p.out)[rb + col] = x;
+              else reinterpret_cast<__nv_bfloat16*>(p.out)[rb + col] = __float2bfloat16_rn(x);
+            }
+          }
+        }
+        __syncwarp();
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
@@ -242,18 +274,52 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         uint8_t* sa = smem + Smem::kA + s * kTileBytes;
         const int k0 = kb * BK;
         if (OP == AJ) {
-          // gather A[m0 + r][k0 + kk] (row stride Bi) into [128 rows x 64 k] SWIZZLE_128B K-major, zeros outside
+          // gather A[m0 + r][k0 .. k0+63] (row stride Bi, arbitrary 2-byte alignment) into the [128 rows x 64 k]
+          // SWIZZLE_128B K-major stage: 8 lanes per row, each producing one 16-byte unit from two aligned
+          // 16-byte loads realigned with funnel shifts; zeros past the sample (k >= Bi or m >= Bi).
           tc::mbar_wait(empty + s, ((cnt / kStages) & 1) ^ 1);
-          const __nv_bfloat16* blk = p.a_j2 + tl.sqo;
-          for (int rr = 0; rr < 32; ++rr) {
-            const int row = wq * 32 + rr, m = tl.m0 + row;
+          const char* base = reinterpret_cast<const char*>(p.a_j2);
+          const int u = lane & 7;
+          for (int it = 0; it < 8; ++it) {
+            const int row = wq * 32 + it * 4 + (lane >> 3), m = tl.m0 + row;
+            const int kb0 = k0 + u * 8;  // first element of this 16-byte unit
+            uint4 out = make_uint4(0, 0, 0, 0);
+            if (m < tl.M && kb0 < tl.K) {
+              const int64_t e0 = tl.sqo + (int64_t)m * tl.n + kb0;  // element index
+              const int64_t byte0 = e0 * 2;
+              const int64_t al = byte0 & ~int64_t(15);
+              const int sh = (int)(byte0 - al);  // 0..14, even
+              // an aligned 16-byte chunk holding at least one valid byte lies in the same page as that
+              // byte, so these over-reads never fault; hi is read only if valid elements reach into it
+              const int nvalid = tl.K - kb0 < 8 ? tl.K - kb0 : 8;
+              const uint4 lo = *reinterpret_cast<const uint4*>(base + al);
+              const uint4 hi = (sh != 0 && byte0 + 2 * nvalid > al + 16) ? *reinterpret_cast<const uint4*>(base + al + 16)
+                                                                        : make_uint4(0, 0, 0, 0);
+              const uint32_t w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w, w4 = hi.x, w5 = hi.y, w6 = hi.z, w7 = hi.w;
+              const int ws = sh >> 2;
+              const bool half = (sh & 2) != 0;
+              // x_k = word (ws + k) of the 32-byte window, k = 0..4 (register selects, no local memory)
+              const uint32_t x0 = ws == 0 ? w0 : ws == 1 ? w1 : ws == 2 ? w2 : w3;
+              const uint32_t x1 = ws == 0 ? w1 : ws == 1 ? w2 : ws == 2 ? w3 : w4;
+              const uint32_t x2 = ws == 0 ? w2 : ws == 1 ? w3 : ws == 2 ? w4 : w5;
+              const uint32_t x3 = ws == 0 ? w3 : ws == 1 ? w4 : ws == 2 ? w5 : w6;
+              const uint32_t x4 = ws == 0 ? w4 : ws == 1 ? w5 : ws == 2 ? w6 : w7;
+              uint32_t o[4];
+              o[0] = half ? __funnelshift_r(x0, x1, 16) : x0;
+              o[1] = half ? __funnelshift_r(x1, x2, 16) : x1;
+              o[2] = half ? __funnelshift_r(x2, x3, 16) : x2;
+              o[3] = half ? __funnelshift_r(x3, x4, 16) : x3;
+              const int valid = tl.K - kb0;  // elements of this unit inside the sample
+              if (valid < 8) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int kk = lane + 32 * h, k = k0 + kk;
-              __nv_bfloat16 x = __float2bfloat16_rn(0.f);
-              if (m < tl.M && k < tl.K) x = blk[(int64_t)m * tl.n + k];
-              *reinterpret_cast<__nv_bfloat16*>(sa + tc::sw128_offset(row, kk >> 3) + (kk & 7) * 2) = x;
+                for (int q = 0; q < 4; ++q) {
+                  if (2 * q >= valid) o[q] = 0;
+                  else if (2 * q + 1 >= valid) o[q] &= 0xFFFFu;
+                }
+              }
+              out = make_uint4(o[0], o[1], o[2], o[3]);
             }
+            *reinterpret_cast<uint4*>(sa + tc::sw128_offset(row, u)) = out;
           }
         } else {
           // JJ: zero the A (and B) rows of the K tail that belong to the next sample
