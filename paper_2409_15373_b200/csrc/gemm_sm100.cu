@@ -204,16 +204,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
         const int nrows = tl.M - tl.m0 - wq * 32 < 32 ? tl.M - tl.m0 - wq * 32 : 32;
+        // 8-byte stores: V elements per lane on V-aligned output addresses, scalar head/tail elements
+        const int V = p.out_f32 ? 2 : 4;
         for (int rr = 0; rr < nrows; ++rr) {
           const int64_t rb = tl.sqo + (int64_t)(tl.m0 + wq * 32 + rr) * tl.n + tl.n0;
-#pragma unroll
-          for (int h = 0; h < BN / 32; ++h) {
-            const int col = lane + 32 * h;
-            if (col < ncols) {
-              const float x = stg[rr * 129 + col];
-              if (p.out_f32) reinterpret_cast<float*>(p.out)[rb + col] = x;
-              else reinterpret_cast<__nv_bfloat16*>(p.out)[rb + col] = __float2bfloat16_rn(x);
+          const float* srow = stg + rr * 129;
+          int head = (int)(((rb + V - 1) & ~int64_t(V - 1)) - rb);
+          if (head > ncols) head = ncols;
+          const int ng = (ncols - head) / V, tail0 = head + ng * V;
+          for (int g2 = lane; g2 < ng; g2 += 32) {
+            const int col = head + g2 * V;
+            if (p.out_f32) {
+              *reinterpret_cast<float2*>(reinterpret_cast<float*>(p.out) + rb + col) = make_float2(srow[col], srow[col + 1]);
+            } else {
+              uint2 w;
+              w.x = tc::pack_bf16(srow[col], srow[col + 1]);
+              w.y = tc::pack_bf16(srow[col + 2], srow[col + 3]);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + rb + col) = w;
             }
+          }
+          const int ecol = lane < head ? lane : tail0 + (lane - head);
+          if (lane < head || (lane >= head && lane - head < ncols - tail0)) {
+            if (p.out_f32) reinterpret_cast<float*>(p.out)[rb + ecol] = srow[ecol];
+            else reinterpret_cast<__nv_bfloat16*>(p.out)[rb + ecol] = __float2bfloat16_rn(srow[ecol]);
           }
         }
         __syncwarp();
@@ -277,49 +290,56 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           // gather A[m0 + r][k0 .. k0+63] (row stride Bi, arbitrary 2-byte alignment) into the [128 rows x 64 k]
           // SWIZZLE_128B K-major stage: 8 lanes per row, each producing one 16-byte unit from two aligned
           // 16-byte loads realigned with funnel shifts; zeros past the sample (k >= Bi or m >= Bi).
-          tc::mbar_wait(empty + s, ((cnt / kStages) & 1) ^ 1);
+          // All 16 loads of a lane are issued before the stage is free and before any is consumed.
           const char* base = reinterpret_cast<const char*>(p.a_j2);
           const int u = lane & 7;
+          uint4 lo[8], hi[8];
+          int shv[8], nval[8];
+#pragma unroll
           for (int it = 0; it < 8; ++it) {
             const int row = wq * 32 + it * 4 + (lane >> 3), m = tl.m0 + row;
             const int kb0 = k0 + u * 8;  // first element of this 16-byte unit
-            uint4 out = make_uint4(0, 0, 0, 0);
-            if (m < tl.M && kb0 < tl.K) {
-              const int64_t e0 = tl.sqo + (int64_t)m * tl.n + kb0;  // element index
-              const int64_t byte0 = e0 * 2;
-              const int64_t al = byte0 & ~int64_t(15);
-              const int sh = (int)(byte0 - al);  // 0..14, even
+            nval[it] = (m < tl.M && kb0 < tl.K) ? (tl.K - kb0 < 8 ? tl.K - kb0 : 8) : 0;
+            lo[it] = hi[it] = make_uint4(0, 0, 0, 0);
+            shv[it] = 0;
+            if (nval[it] > 0) {
               // an aligned 16-byte chunk holding at least one valid byte lies in the same page as that
               // byte, so these over-reads never fault; hi is read only if valid elements reach into it
-              const int nvalid = tl.K - kb0 < 8 ? tl.K - kb0 : 8;
-              const uint4 lo = *reinterpret_cast<const uint4*>(base + al);
-              const uint4 hi = (sh != 0 && byte0 + 2 * nvalid > al + 16) ? *reinterpret_cast<const uint4*>(base + al + 16)
-                                                                        : make_uint4(0, 0, 0, 0);
-              const uint32_t w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w, w4 = hi.x, w5 = hi.y, w6 = hi.z, w7 = hi.w;
-              const int ws = sh >> 2;
-              const bool half = (sh & 2) != 0;
-              // x_k = word (ws + k) of the 32-byte window, k = 0..4 (register selects, no local memory)
-              const uint32_t x0 = ws == 0 ? w0 : ws == 1 ? w1 : ws == 2 ? w2 : w3;
-              const uint32_t x1 = ws == 0 ? w1 : ws == 1 ? w2 : ws == 2 ? w3 : w4;
-              const uint32_t x2 = ws == 0 ? w2 : ws == 1 ? w3 : ws == 2 ? w4 : w5;
-              const uint32_t x3 = ws == 0 ? w3 : ws == 1 ? w4 : ws == 2 ? w5 : w6;
-              const uint32_t x4 = ws == 0 ? w4 : ws == 1 ? w5 : ws == 2 ? w6 : w7;
-              uint32_t o[4];
-              o[0] = half ? __funnelshift_r(x0, x1, 16) : x0;
-              o[1] = half ? __funnelshift_r(x1, x2, 16) : x1;
-              o[2] = half ? __funnelshift_r(x2, x3, 16) : x2;
-              o[3] = half ? __funnelshift_r(x3, x4, 16) : x3;
-              const int valid = tl.K - kb0;  // elements of this unit inside the sample
-              if (valid < 8) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  if (2 * q >= valid) o[q] = 0;
-                  else if (2 * q + 1 >= valid) o[q] &= 0xFFFFu;
-                }
-              }
-              out = make_uint4(o[0], o[1], o[2], o[3]);
+              const int64_t byte0 = (tl.sqo + (int64_t)m * tl.n + kb0) * 2;
+              const int64_t al = byte0 & ~int64_t(15);
+              shv[it] = (int)(byte0 - al);
+              lo[it] = __ldg(reinterpret_cast<const uint4*>(base + al));
+              if (shv[it] != 0 && byte0 + 2 * nval[it] > al + 16) hi[it] = __ldg(reinterpret_cast<const uint4*>(base + al + 16));
             }
-            *reinterpret_cast<uint4*>(sa + tc::sw128_offset(row, u)) = out;
+          }
+          tc::mbar_wait(empty + s, ((cnt / kStages) & 1) ^ 1);
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int row = wq * 32 + it * 4 + (lane >> 3);
+            const int sh = shv[it], ws = sh >> 2;
+            const bool half = (sh & 2) != 0;
+            const uint32_t w0 = lo[it].x, w1 = lo[it].y, w2 = lo[it].z, w3 = lo[it].w;
+            const uint32_t w4 = hi[it].x, w5 = hi[it].y, w6 = hi[it].z, w7 = hi[it].w;
+            // x_k = word (ws + k) of the 32-byte window (register selects, no local memory)
+            const uint32_t x0 = ws == 0 ? w0 : ws == 1 ? w1 : ws == 2 ? w2 : w3;
+            const uint32_t x1 = ws == 0 ? w1 : ws == 1 ? w2 : ws == 2 ? w3 : w4;
+            const uint32_t x2 = ws == 0 ? w2 : ws == 1 ? w3 : ws == 2 ? w4 : w5;
+            const uint32_t x3 = ws == 0 ? w3 : ws == 1 ? w4 : ws == 2 ? w5 : w6;
+            const uint32_t x4 = ws == 0 ? w4 : ws == 1 ? w5 : ws == 2 ? w6 : w7;
+            uint32_t o[4];
+            o[0] = half ? __funnelshift_r(x0, x1, 16) : x0;
+            o[1] = half ? __funnelshift_r(x1, x2, 16) : x1;
+            o[2] = half ? __funnelshift_r(x2, x3, 16) : x2;
+            o[3] = half ? __funnelshift_r(x3, x4, 16) : x3;
+            const int valid = nval[it];
+            if (valid < 8) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (2 * q >= valid) o[q] = 0;
+                else if (2 * q + 1 >= valid) o[q] &= 0xFFFFu;
+              }
+            }
+            *reinterpret_cast<uint4*>(sa + tc::sw128_offset(row, u)) = make_uint4(o[0], o[1], o[2], o[3]);
           }
         } else {
           // JJ: zero the A (and B) rows of the K tail that belong to the next sample
