@@ -204,29 +204,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
         const int nrows = tl.M - tl.m0 - wq * 32 < 32 ? tl.M - tl.m0 - wq * 32 : 32;
-        // 8-byte stores: V elements per lane on V-aligned output addresses, scalar head/tail elements
-        const int V = p.out_f32 ? 2 : 4;
         for (int rr = 0; rr < nrows; ++rr) {
           const int64_t rb = tl.sqo + (int64_t)(tl.m0 + wq * 32 + rr) * tl.n + tl.n0;
-          const float* srow = stg + rr * 129;
-          int head = (int)(((rb + V - 1) & ~int64_t(V - 1)) - rb);
-          if (head > ncols) head = ncols;
-          const int ng = (ncols - head) / V, tail0 = head + ng * V;
-          for (int g2 = lane; g2 < ng; g2 += 32) {
-            const int col = head + g2 * V;
-            if (p.out_f32) {
-              *reinterpret_cast<float2*>(reinterpret_cast<float*>(p.out) + rb + col) = make_float2(srow[col], srow[col + 1]);
-            } else {
-              uint2 w;
-              w.x = tc::pack_bf16(srow[col], srow[col + 1]);
-              w.y = tc::pack_bf16(srow[col + 2], srow[col + 3]);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + rb + col) = w;
+#pragma unroll
+          for (int h = 0; h < BN / 32; ++h) {
+            const int col = lane + 32 * h;
+            if (col < ncols) {
+              const float x = stg[rr * 129 + col];
+              if (p.out_f32) reinterpret_cast<float*>(p.out)[rb + col] = x;
+              else reinterpret_cast<__nv_bfloat16*>(p.out)[rb + col] = __float2bfloat16_rn(x);
             }
-          }
-          const int ecol = lane < head ? lane : tail0 + (lane - head);
-          if (lane < head || (lane >= head && lane - head < ncols - tail0)) {
-            if (p.out_f32) reinterpret_cast<float*>(p.out)[rb + ecol] = srow[ecol];
-            else reinterpret_cast<__nv_bfloat16*>(p.out)[rb + ecol] = __float2bfloat16_rn(srow[ecol]);
           }
         }
         __syncwarp();
