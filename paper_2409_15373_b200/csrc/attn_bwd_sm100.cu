@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tc::mbar_init(kv_full, 1);
-    tc::mbar_init(kv_empty, 1);
+    tc::mbar_init(kv_empty, 2);  // both MMA issuers release K/V
     for (int s = 0; s < L::kStages; ++s) {
       tc::mbar_init(qd_full + s, 1);
       tc::mbar_init(qd_empty + s, 1);
@@ -188,82 +188,91 @@ __global__ void __launch_bounds__(kThreads, 1)
       wp.add(7, clock64() - t_role);
       wp.flush();
     }
-  } else if (warp == 1) {
-    // ===================================================== MMA issuer
-    // Per item: S_0; then for each j: S_{j+1} (other TMEM buffer, overlaps softmax j), dV_j, dK_j, dQ_j.
+  } else if (warp == 1 || warp == 2) {
+    // ===================================================== MMA issuers
+    // Two issuing threads feed the tensor core (each tcgen05.mma blocks its issuer for about one MMA
+    // duration, so a single issuer exposes every barrier wait as tensor idle time):
+    //   warp 1: S^T_j = K Q_j^T and dP^T_j = V dO_j^T into TMEM score buffer j&1, up to two blocks ahead
+    //   warp 2: dV += P^T_j dO_j, dK += dS^T_j Q_j, dQ^T_j = K^T dS^T_j once the softmax published block j
+    // They touch disjoint TMEM columns except dQ^T_j, which reuses buffer j&1 only after the softmax
+    // consumed it (p_full) and is drained before warp 1 refills that buffer (dq_empty).
     if (lane == 0) {
-      tc::WaitProf wp;
-      wp.init(p.prof, 8);
-      const long long t_role = clock64();
       constexpr uint32_t kIdS = tc::idesc_bf16_f32(BKV, BQ, false, false);  // S^T, dP^T
       constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
       constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
       const uint32_t k_base = tc::smem_u32(smem + L::kK), v_base = tc::smem_u32(smem + L::kV);
       const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
       const uint32_t qd_base = tc::smem_u32(smem + L::kQD);
-      uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill[2] = {0, 0};
       auto stage_of = [&](uint32_t cnt) { return qd_base + (cnt % L::kStages) * 2 * L::kTileQ; };
-      auto issue_sdp = [&](uint32_t cnt, int b) {
-        const uint32_t s = cnt % L::kStages;
-        wp.wait(qd_full + s, (cnt / L::kStages) & 1, 2);
-        wp.wait(st_empty + b, (fill[b] & 1) ^ 1, 3);  // softmax done reading this buffer
-        wp.wait(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
-        ++fill[b];
-        tc::tc_fence_after();
-        const uint32_t q_base = stage_of(cnt), do_base = q_base + L::kTileQ;
-        const uint32_t col = b * 128;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
-          const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
-          tc::mma_bf16_ss(tmem + col, tc::sw128_desc(k_base + ka, 16, 1024), tc::sw128_desc(q_base + kb, 16, 1024),
-                          kIdS, kk > 0);
-        }
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
-          const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
-          tc::mma_bf16_ss(tmem + col + 64, tc::sw128_desc(v_base + ka, 16, 1024),
-                          tc::sw128_desc(do_base + kb, 16, 1024), kIdS, kk > 0);
-        }
-        tc::mma_commit(st_full + b);
-      };
+      tc::WaitProf wp;
+      wp.init(p.prof, warp == 1 ? 8 : 32);
+      const long long t_role = clock64();
+      uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill[2] = {0, 0};
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
-        wp.wait(kv_full, item_cnt & 1, 0);
-        wp.wait(dkv_empty, (item_cnt & 1) ^ 1, 1);
-        issue_sdp(qd_cnt, 0);
-        for (int j = 0; j < nq; ++j, ++qd_cnt) {
-          if (j + 1 < nq) issue_sdp(qd_cnt + 1, (j + 1) & 1);
-          wp.wait(p_full, p_cnt & 1, 5);
-          ++p_cnt;
-          tc::tc_fence_after();
-          const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
-          // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
+        if (warp == 1) {
+          wp.wait(kv_full, item_cnt & 1, 0);
+          for (int j = 0; j < nq; ++j, ++qd_cnt) {
+            const int b = j & 1;
+            const uint32_t s = qd_cnt % L::kStages;
+            wp.wait(qd_full + s, (qd_cnt / L::kStages) & 1, 2);
+            wp.wait(st_empty + b, (fill[b] & 1) ^ 1, 3);  // softmax done reading this buffer
+            wp.wait(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
+            ++fill[b];
+            tc::tc_fence_after();
+            const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
+            const uint32_t col = b * 128;
 #pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk) {
-            tc::mma_bf16_ss(tmem + 256, tc::sw128_desc(p_base + kk * 32, 16, 1024),
-                            tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
-          }
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
+              const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
+              tc::mma_bf16_ss(tmem + col, tc::sw128_desc(k_base + ka, 16, 1024),
+                              tc::sw128_desc(q_base + kb, 16, 1024), kIdS, kk > 0);
+            }
 #pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk) {
-            tc::mma_bf16_ss(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
-                            tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
+              const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
+              tc::mma_bf16_ss(tmem + col + 64, tc::sw128_desc(v_base + ka, 16, 1024),
+                              tc::sw128_desc(do_base + kb, 16, 1024), kIdS, kk > 0);
+            }
+            tc::mma_commit(st_full + b);
           }
-          tc::mma_commit(qd_empty + (qd_cnt % L::kStages));  // Q_j, dO_j no longer needed
-          // dQ_j^T = K^T dS^T into the S^T slot of buffer j&1 (its scores were consumed: p_full)
+          tc::mma_commit(kv_empty);  // this issuer's reads of K and V are done
+        } else {
+          wp.wait(dkv_empty, (item_cnt & 1) ^ 1, 1);
+          for (int j = 0; j < nq; ++j, ++qd_cnt) {
+            wp.wait(p_full, p_cnt & 1, 5);
+            ++p_cnt;
+            tc::tc_fence_after();
+            const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
+            // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk) {
-            tc::mma_bf16_ss(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
-                            tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
+            for (int kk = 0; kk < BQ / 16; ++kk) {
+              tc::mma_bf16_ss(tmem + 256, tc::sw128_desc(p_base + kk * 32, 16, 1024),
+                              tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+            }
+#pragma unroll
+            for (int kk = 0; kk < BQ / 16; ++kk) {
+              tc::mma_bf16_ss(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
+                              tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+            }
+            // Q_j, dO_j are no longer needed (warp 1's S/dP_j completed before the softmax published P_j)
+            tc::mma_commit(qd_empty + (qd_cnt % L::kStages));
+            // dQ_j^T = K^T dS^T into the S^T slot of buffer j&1 (its scores were consumed: p_full)
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk) {
+              tc::mma_bf16_ss(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
+                              tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
+            }
+            tc::mma_commit(dq_full + (j & 1));
+            tc::mma_commit(pds_empty);
           }
-          tc::mma_commit(dq_full + (j & 1));
-          tc::mma_commit(pds_empty);
+          tc::mma_commit(dkv_full);
+          tc::mma_commit(kv_empty);
         }
-        tc::mma_commit(dkv_full);
-        tc::mma_commit(kv_empty);
       }
       wp.add(7, clock64() - t_role);
       wp.flush();
@@ -511,9 +520,9 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
   wait_prof_end(p.prof, st, "bwd",
-                {"P.kv_empty", "P.qd_empty", "", "", "", "", "", "P.total", "M.kv_full", "M.dkv_empty", "M.qd_full",
-                 "M.st_empty", "M.dq_empty", "M.p_full", "", "M.total", "S.lse_bar", "S.st_full", "S.pds_empty", "",
-                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total"});
+                {"P.kv_empty", "P.qd_empty", "", "", "", "", "", "P.total", "M.kv_full", "", "M.qd_full",
+                 "M.st_empty", "M.dq_empty", "", "", "M.total", "S.lse_bar", "S.st_full", "S.pds_empty", "",
+                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
   fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,
                                                                                           n4);
