@@ -32,6 +32,7 @@ constexpr int BQ = 64;    // query rows per streamed block
 constexpr int kThreads = 384;
 constexpr int kSmWarp0 = 4, kDqWarp0 = 8;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kPrefetch = 6;  // query blocks prefetched into L2 ahead of the producer
 
 template <int D>
 struct Smem {
@@ -167,6 +168,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
         const int nq = (int)((n + BQ - 1) / BQ);
         const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
+        // L2 prefetch of the first query blocks of this item before waiting for the K/V buffers
+        for (int j = 0; j < kPrefetch && j < nq; ++j)
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(b0 + (int64_t)j * BQ));
+            tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(b0 + (int64_t)j * BQ));
+          }
         wp.wait(kv_empty, (item_cnt & 1) ^ 1, 0);
         tc::mbar_expect_tx(kv_full, 2 * L::kTileKV);
         for (int c = 0; c < D / 64; ++c) {
@@ -175,6 +182,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int j = 0; j < nq; ++j, ++qd_cnt) {
           const uint32_t s = qd_cnt % L::kStages;
+          // keep kPrefetch query blocks ahead of the smem ring warm in L2 (the kv-tile CTAs of one sample
+          // stream the same Q/dO blocks in lockstep, so without this every block pays DRAM latency)
+          if (j + kPrefetch < nq)
+            for (int c = 0; c < D / 64; ++c) {
+              tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(b0 + (int64_t)(j + kPrefetch) * BQ));
+              tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(b0 + (int64_t)(j + kPrefetch) * BQ));
+            }
           wp.wait(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1, 1);
           tc::mbar_expect_tx(qd_full + s, 2 * L::kTileQ);
           uint8_t* qs = smem + L::kQD + s * 2 * L::kTileQ;
