@@ -15,7 +15,8 @@
 //      dQ_j^T is drained by a second warpgroup through smem and added into the fp32 accumulator with
 //      one TMA tensor reduce-add per block (cp.reduce.async.bulk.tensor .add, [64 q x D] fp32 box).
 //   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
-// Warps: 0 TMA producer, 1 MMA issuer, 4-7 softmax/dS, 8-11 dQ drain + dK/dV epilogue.
+// Warps: 0 TMA producer, 1-2 MMA issuers, 4-11 softmax/dS (two warps per TMEM lane
+// quarter, 32 query columns each), 12-15 dQ drain + dK/dV epilogue.
 // TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); dQ_j^T reuses the S^T slot
 // of buffer j&1 once its scores are consumed; dV [256,384), dK [384,512). S_{j+1} is issued before
 // dV_j/dK_j/dQ_j so the softmax warpgroup works on block j+1 while the tensor core finishes block j.
@@ -29,8 +30,9 @@ namespace fb {
 
 constexpr int BKV = 128;  // key rows per CTA tile
 constexpr int BQ = 64;    // query rows per streamed block
-constexpr int kThreads = 384;
-constexpr int kSmWarp0 = 4, kDqWarp0 = 8;
+constexpr int kThreads = 512;
+constexpr int kSmWarp0 = 4, kDqWarp0 = 12;
+constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 of the 64 query columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kPrefetch = 6;  // query blocks prefetched into L2 ahead of the producer
 
@@ -47,9 +49,10 @@ struct Smem {
   static constexpr int kP = kQD + kStages * 2 * kTileQ;     // P^T  [128 keys x 64 q] bf16
   static constexpr int kDS = kP + BKV * 128;                // dS^T [128 keys x 64 q] bf16
   static constexpr int kStg = kDS + BKV * 128;              // dQ staging [64 q x D] fp32
-  static constexpr int kLse = kStg + BQ * D * 4;            // 2 x (64 lse + 64 delta) fp32
-  static constexpr int kBar = kLse + 2 * 2 * BQ * 4;
-  static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 4 + 2 + 1;
+  static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 lse (log2 units) + 64 Delta, fp32
+  static constexpr int kLse = kStg + BQ * D * 4;            // kStages x kLsdBytes, loaded with (Q_j, dO_j)
+  static constexpr int kBar = kLse + kStages * kLsdBytes;
+  static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 4 + 2;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes + 1024;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -61,13 +64,14 @@ struct Params {
   const int64_t* n_items;
   int64_t total_rows;
   int H;
-  const float* lse;
-  const float* delta;
+  const float* lsd;  // [2][H][total_rows]: lse * log2(e), Delta (written by the prologue)
   float* dq_acc;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   float scale_log2;
   float scale;
+  int dbg;                   // JG_BWD_DBG diagnostic bits (results invalid when set): 1 skip the dQ reduce,
+                             // 4 skip the P/dS smem stores, 64 skip the main kernel, 128 sync + report after it
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23, drain 24-31)
 };
 
@@ -87,13 +91,6 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// lse (log2 units) or delta of query j*BQ + (tid % BQ) for the softmax warpgroup's smem staging
-__device__ __forceinline__ float lse_delta_value(const Params& p, int tid, int j, int h, int64_t b0, int64_t n) {
-  const int64_t q = (int64_t)j * BQ + (tid & (BQ - 1));
-  const int64_t gi = (int64_t)h * p.total_rows + b0 + q;
-  if (tid < BQ) return q < n ? p.lse[gi] * kLog2e : INFINITY;  // +inf -> P = 0 for padded queries
-  return q < n ? p.delta[gi] : 0.f;
-}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -124,15 +121,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::mbar_init(kv_full, 1);
     tc::mbar_init(kv_empty, 2);  // both MMA issuers release K/V
     for (int s = 0; s < L::kStages; ++s) {
-      tc::mbar_init(qd_full + s, 1);
+      tc::mbar_init(qd_full + s, 1 + 32);  // TMA expect_tx arrival + 32 cp.async (lse/Delta) arrivals
       tc::mbar_init(qd_empty + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(st_full + b, 1);
-      tc::mbar_init(st_empty + b, 4);
+      tc::mbar_init(st_empty + b, kSmWarps);
       tc::mbar_init(dq_empty + b, 4);
     }
-    tc::mbar_init(p_full, 4);
+    tc::mbar_init(p_full, kSmWarps);
     tc::mbar_init(pds_empty, 1);
     tc::mbar_init(dq_full, 1);
     tc::mbar_init(dq_full + 1, 1);
@@ -156,52 +153,73 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t n_work = *p.n_items * H;
 
   if (warp == 0) {
-    // ===================================================== TMA producer
-    if (lane == 0) {
-      tc::WaitProf wp;
-      wp.init(p.prof, 0);
-      const long long t_role = clock64();
-      uint32_t item_cnt = 0, qd_cnt = 0;
-      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
-        const int2 it = p.items[w / H];
-        const int h = (int)(w % H);
-        const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
-        const int nq = (int)((n + BQ - 1) / BQ);
-        const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
+    // ===================================================== producer warp
+    // Lane 0 issues the TMA loads; all 32 lanes stage the block's 64 lse and 64 Delta values with 4-byte
+    // cp.async copies (rows start anywhere, so a TMA tensor box is not aligned) that arrive on the same
+    // qd_full barrier as the (Q_j, dO_j) tiles.
+    tc::WaitProf wp;
+    wp.init(lane == 0 ? p.prof : nullptr, 0);
+    const long long t_role = clock64();
+    uint32_t item_cnt = 0, qd_cnt = 0;
+    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+      const int2 it = p.items[w / H];
+      const int h = (int)(w % H);
+      const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
+      const int nq = (int)((n + BQ - 1) / BQ);
+      const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
+      const float* lse_h = p.lsd + (int64_t)h * p.total_rows;
+      const float* del_h = p.lsd + ((int64_t)H + h) * p.total_rows;
+      if (lane == 0) {
         // L2 prefetch of the first query blocks of this item before waiting for the K/V buffers
         for (int j = 0; j < kPrefetch && j < nq; ++j)
           for (int c = 0; c < D / 64; ++c) {
             tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(b0 + (int64_t)j * BQ));
             tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(b0 + (int64_t)j * BQ));
           }
-        wp.wait(kv_empty, (item_cnt & 1) ^ 1, 0);
+      }
+      wp.wait_warp(kv_empty, (item_cnt & 1) ^ 1, 0);
+      if (lane == 0) {
         tc::mbar_expect_tx(kv_full, 2 * L::kTileKV);
         for (int c = 0; c < D / 64; ++c) {
           tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, kv_full, c * 64, h, kv_row);
           tc::tma_load_3d(smem + L::kV + c * L::kChunkKV, &tm_v, kv_full, c * 64, h, kv_row);
         }
-        for (int j = 0; j < nq; ++j, ++qd_cnt) {
-          const uint32_t s = qd_cnt % L::kStages;
-          // keep kPrefetch query blocks ahead of the smem ring warm in L2 (the kv-tile CTAs of one sample
-          // stream the same Q/dO blocks in lockstep, so without this every block pays DRAM latency)
-          if (j + kPrefetch < nq)
-            for (int c = 0; c < D / 64; ++c) {
-              tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(b0 + (int64_t)(j + kPrefetch) * BQ));
-              tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(b0 + (int64_t)(j + kPrefetch) * BQ));
-            }
-          wp.wait(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1, 1);
+        if (wp.g) wp.trace(50);
+      }
+      for (int j = 0; j < nq; ++j, ++qd_cnt) {
+        const uint32_t s = qd_cnt % L::kStages;
+        const int64_t q_row = b0 + (int64_t)j * BQ;
+        // keep kPrefetch query blocks ahead of the smem ring warm in L2 (the kv-tile CTAs of one sample
+        // stream the same Q/dO blocks in lockstep, so without this every block pays DRAM latency)
+        if (lane == 0 && j + kPrefetch < nq)
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(q_row + kPrefetch * BQ));
+            tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(q_row + kPrefetch * BQ));
+          }
+        wp.wait_warp(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1, 1);
+        // lse/Delta: rows past the sample are masked by the softmax; rows past the tensor are not copied
+        const uint32_t ls = tc::smem_u32(smem + L::kLse + s * L::kLsdBytes);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int t = lane + 32 * u;
+          if (q_row + t < p.total_rows) {
+            tc::cp_async_4(ls + t * 4, lse_h + q_row + t);
+            tc::cp_async_4(ls + (BQ + t) * 4, del_h + q_row + t);
+          }
+        }
+        tc::cp_async_arrive_noinc(qd_full + s);
+        if (lane == 0) {
           tc::mbar_expect_tx(qd_full + s, 2 * L::kTileQ);
           uint8_t* qs = smem + L::kQD + s * 2 * L::kTileQ;
-          const int q_row = (int)(b0 + (int64_t)j * BQ);
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_3d(qs + c * L::kChunkQ, &tm_q, qd_full + s, c * 64, h, q_row);
-            tc::tma_load_3d(qs + L::kTileQ + c * L::kChunkQ, &tm_do, qd_full + s, c * 64, h, q_row);
+            tc::tma_load_3d(qs + c * L::kChunkQ, &tm_q, qd_full + s, c * 64, h, (int)q_row);
+            tc::tma_load_3d(qs + L::kTileQ + c * L::kChunkQ, &tm_do, qd_full + s, c * 64, h, (int)q_row);
           }
         }
       }
-      wp.add(7, clock64() - t_role);
-      wp.flush();
     }
+    wp.add(7, clock64() - t_role);
+    wp.flush();
   } else if (warp == 1 || warp == 2) {
     // ===================================================== MMA issuers
     // Two issuing threads feed the tensor core (each tcgen05.mma blocks its issuer for about one MMA
@@ -210,7 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     //   warp 2: dV += P^T_j dO_j, dK += dS^T_j Q_j, dQ^T_j = K^T dS^T_j once the softmax published block j
     // They touch disjoint TMEM columns except dQ^T_j, which reuses buffer j&1 only after the softmax
     // consumed it (p_full) and is drained before warp 1 refills that buffer (dq_empty).
-    if (lane == 0) {
+    // The whole warp runs the issue loop with warp-uniform operands (they stay in uniform registers);
+    // one elected lane issues each MMA / commit. A single-lane loop needs R2UR moves per MMA, which the
+    // softmax warps' FFMA/MUFU traffic on the same SM sub-partition slows by ~25% (tools/mma_seq_bench.cu).
+    {
       constexpr uint32_t kIdS = tc::idesc_bf16_f32(BKV, BQ, false, false);  // S^T, dP^T
       constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
       constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
@@ -219,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t qd_base = tc::smem_u32(smem + L::kQD);
       auto stage_of = [&](uint32_t cnt) { return qd_base + (cnt % L::kStages) * 2 * L::kTileQ; };
       tc::WaitProf wp;
-      wp.init(p.prof, warp == 1 ? 8 : 32);
+      wp.init(lane == 0 ? p.prof : nullptr, warp == 1 ? 8 : 32);
       const long long t_role = clock64();
       uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill[2] = {0, 0};
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
@@ -227,129 +248,151 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
         if (warp == 1) {
-          wp.wait(kv_full, item_cnt & 1, 0);
+          wp.wait_warp(kv_full, item_cnt & 1, 0);
           for (int j = 0; j < nq; ++j, ++qd_cnt) {
             const int b = j & 1;
             const uint32_t s = qd_cnt % L::kStages;
-            wp.wait(qd_full + s, (qd_cnt / L::kStages) & 1, 2);
-            wp.wait(st_empty + b, (fill[b] & 1) ^ 1, 3);  // softmax done reading this buffer
-            wp.wait(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
+            wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 2);
+            wp.wait_warp(st_empty + b, (fill[b] & 1) ^ 1, 3);  // softmax done reading this buffer
+            wp.wait_warp(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
             ++fill[b];
             tc::tc_fence_after();
+            if (wp.g) wp.trace(56);
             const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
             const uint32_t col = b * 128;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
               const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
-              tc::mma_bf16_ss(tmem + col, tc::sw128_desc(k_base + ka, 16, 1024),
+              tc::mma_bf16_ss_warp(tmem + col, tc::sw128_desc(k_base + ka, 16, 1024),
                               tc::sw128_desc(q_base + kb, 16, 1024), kIdS, kk > 0);
             }
+            if (wp.g) wp.trace(57);
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t ka = (kk >> 2) * L::kChunkKV + (kk & 3) * 32;
               const uint32_t kb = (kk >> 2) * L::kChunkQ + (kk & 3) * 32;
-              tc::mma_bf16_ss(tmem + col + 64, tc::sw128_desc(v_base + ka, 16, 1024),
+              tc::mma_bf16_ss_warp(tmem + col + 64, tc::sw128_desc(v_base + ka, 16, 1024),
                               tc::sw128_desc(do_base + kb, 16, 1024), kIdS, kk > 0);
             }
-            tc::mma_commit(st_full + b);
+            tc::mma_commit_warp(st_full + b);
+            if (wp.g) wp.trace(58);
           }
-          tc::mma_commit(kv_empty);  // this issuer's reads of K and V are done
+          tc::mma_commit_warp(kv_empty);  // this issuer's reads of K and V are done
         } else {
-          wp.wait(dkv_empty, (item_cnt & 1) ^ 1, 1);
+          wp.wait_warp(dkv_empty, (item_cnt & 1) ^ 1, 1);
           for (int j = 0; j < nq; ++j, ++qd_cnt) {
-            wp.wait(p_full, p_cnt & 1, 5);
+            wp.wait_warp(p_full, p_cnt & 1, 5);
             ++p_cnt;
             tc::tc_fence_after();
             const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
+            if (wp.g) wp.trace(83);
+            // dQ_j^T = K^T dS^T first, into the S^T slot of buffer j&1 (its scores were consumed: p_full), so the
+            // drain frees that buffer for warp 1's S_{j+2} as early as possible
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk) {
+              tc::mma_bf16_ss_warp(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
+                              tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
+            }
+            tc::mma_commit_warp(dq_full + (j & 1));
+            if (wp.g) wp.trace(84);
             // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
 #pragma unroll
             for (int kk = 0; kk < BQ / 16; ++kk) {
-              tc::mma_bf16_ss(tmem + 256, tc::sw128_desc(p_base + kk * 32, 16, 1024),
+              tc::mma_bf16_ss_warp(tmem + 256, tc::sw128_desc(p_base + kk * 32, 16, 1024),
                               tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
             }
+            if (wp.g) wp.trace(85);
 #pragma unroll
             for (int kk = 0; kk < BQ / 16; ++kk) {
-              tc::mma_bf16_ss(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
+              tc::mma_bf16_ss_warp(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
                               tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
             }
             // Q_j, dO_j are no longer needed (warp 1's S/dP_j completed before the softmax published P_j)
-            tc::mma_commit(qd_empty + (qd_cnt % L::kStages));
-            // dQ_j^T = K^T dS^T into the S^T slot of buffer j&1 (its scores were consumed: p_full)
-#pragma unroll
-            for (int kk = 0; kk < BKV / 16; ++kk) {
-              tc::mma_bf16_ss(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
-                              tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
-            }
-            tc::mma_commit(dq_full + (j & 1));
-            tc::mma_commit(pds_empty);
+            tc::mma_commit_warp(qd_empty + (qd_cnt % L::kStages));
+            tc::mma_commit_warp(pds_empty);
+            if (wp.g) wp.trace(82);
           }
-          tc::mma_commit(dkv_full);
-          tc::mma_commit(kv_empty);
+          tc::mma_commit_warp(dkv_full);
+          tc::mma_commit_warp(kv_empty);
         }
       }
       wp.add(7, clock64() - t_role);
       wp.flush();
     }
-  } else if (warp >= kSmWarp0 && warp < kDqWarp0) {
-    // ===================================================== P^T / dS^T warpgroup (thread = key row)
+  } else if (warp >= kSmWarp0 && warp < kSmWarp0 + kSmWarps) {
+    // ===================================================== P^T / dS^T warps (thread = key row x 32 queries)
     const int tid = threadIdx.x - kSmWarp0 * 32;
-    const int wq = warp - kSmWarp0;
+    const int wq = warp & 3;                       // TMEM lane quarter
+    const int row = wq * 32 + lane;                // key row within the tile
+    const int half = (warp - kSmWarp0) >> 2;       // query columns [32 half, 32 half + 32)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
-    float* sm_ld = reinterpret_cast<float*>(smem + L::kLse);  // [2][lse 64 | delta 64]
-    uint32_t cons[2] = {0, 0}, pds_cnt = 0;
+    const float* lsd = reinterpret_cast<const float*>(smem + L::kLse);
+    uint32_t cons[2] = {0, 0}, pds_cnt = 0, qd_cnt = 0;
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int2 it = p.items[w / H];
-      const int h = (int)(w % H);
-      const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
+      const int64_t n = p.off[it.x + 1] - p.off[it.x];
       const int nq = (int)((n + BQ - 1) / BQ);
-      const bool row_valid = (int64_t)it.y * BKV + tid < n;
-      float pf = lse_delta_value(p, tid, 0, h, b0, n);
-      for (int j = 0; j < nq; ++j) {
+      const bool row_valid = (int64_t)it.y * BKV + row < n;
+      for (int j = 0; j < nq; ++j, ++qd_cnt) {
         const int b = j & 1;
-        float* buf = sm_ld + b * 2 * BQ;
-        buf[tid] = pf;
-        if (j + 1 < nq) pf = lse_delta_value(p, tid, j + 1, h, b0, n);  // prefetch: hidden behind block j
-        { const long long t0 = clock64(); named_bar(1, 128); wp.add(0, clock64() - t0); }
-        wp.wait(st_full + b, cons[b] & 1, 1);
+        const uint32_t s = qd_cnt % L::kStages;
+        wp.wait_warp(st_full + b, cons[b] & 1, 1);
         ++cons[b];
         tc::tc_fence_after();
-        uint32_t pk[BQ / 2], dk2[BQ / 2];
-#pragma unroll
-        for (int c = 0; c < BQ / 32; ++c) {
-          uint32_t sr[32], dr[32];
-          tc::tmem_ld32(lane_addr + b * 128 + c * 32, sr);
-          tc::tmem_ld32(lane_addr + b * 128 + 64 + c * 32, dr);
-          tc::tmem_wait_ld();
+        uint32_t sr[32], dr[32];
+        tc::tmem_ld32(lane_addr + b * 128 + half * 32, sr);
+        tc::tmem_ld32(lane_addr + b * 128 + 64 + half * 32, dr);
+        // lse/Delta of block j arrived with (Q_j, dO_j); the stage stays valid until p_full (the issuer's
+        // qd_empty commit follows the MMAs that consume P_j)
+        wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 0);
+        const float* lb = lsd + s * 2 * BQ + half * 32;
+        // queries past the sample end (rows of the next sample in the Q tile) and key rows past it get P = 0
+        const int64_t qrem = n - (int64_t)j * BQ - half * 32;
+        const int qlim = qrem < 32 ? (int)qrem : 32;
+        const bool full = __all_sync(0xffffffffu, row_valid && qlim == 32);
+        tc::tmem_wait_ld();
+        uint32_t pk[16], dk2[16];
+        auto body = [&](auto masked) {
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
-            const int q0 = c * 32 + e;
-            const float4 l4 = *reinterpret_cast<const float4*>(buf + q0);
-            const float4 d4 = *reinterpret_cast<const float4*>(buf + BQ + q0);
+            const float4 l4 = *reinterpret_cast<const float4*>(lb + e);
+            const float4 d4 = *reinterpret_cast<const float4*>(lb + BQ + e);
             float p0 = tc::ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
             float p1 = tc::ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
             float p2 = tc::ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
             float p3 = tc::ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w));
-            if (!row_valid) p0 = p1 = p2 = p3 = 0.f;
-            pk[q0 >> 1] = tc::pack_bf16(p0, p1);
-            pk[(q0 >> 1) + 1] = tc::pack_bf16(p2, p3);
-            dk2[q0 >> 1] = tc::pack_bf16(p0 * (__uint_as_float(dr[e + 0]) - d4.x), p1 * (__uint_as_float(dr[e + 1]) - d4.y));
-            dk2[(q0 >> 1) + 1] =
-                tc::pack_bf16(p2 * (__uint_as_float(dr[e + 2]) - d4.z), p3 * (__uint_as_float(dr[e + 3]) - d4.w));
+            float s0 = p0 * (__uint_as_float(dr[e + 0]) - d4.x), s1 = p1 * (__uint_as_float(dr[e + 1]) - d4.y);
+            float s2 = p2 * (__uint_as_float(dr[e + 2]) - d4.z), s3 = p3 * (__uint_as_float(dr[e + 3]) - d4.w);
+            if constexpr (decltype(masked)::value) {  // after the products: masked lanes may hold stale inf/nan
+              if (!row_valid || e + 0 >= qlim) p0 = s0 = 0.f;
+              if (!row_valid || e + 1 >= qlim) p1 = s1 = 0.f;
+              if (!row_valid || e + 2 >= qlim) p2 = s2 = 0.f;
+              if (!row_valid || e + 3 >= qlim) p3 = s3 = 0.f;
+            }
+            pk[e >> 1] = tc::pack_bf16(p0, p1);
+            pk[(e >> 1) + 1] = tc::pack_bf16(p2, p3);
+            dk2[e >> 1] = tc::pack_bf16(s0, s1);
+            dk2[(e >> 1) + 1] = tc::pack_bf16(s2, s3);
           }
-        }
+        };
+        if (full)
+          body(std::false_type{});
+        else
+          body(std::true_type{});
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(st_empty + b);
-        wp.wait(pds_empty, (pds_cnt & 1) ^ 1, 2);
+        wp.wait_warp(pds_empty, (pds_cnt & 1) ^ 1, 2);
         ++pds_cnt;
 #pragma unroll
-        for (int u = 0; u < BQ / 8; ++u) {
-          const uint32_t o = tc::sw128_offset(tid, u);
+        for (int u = 0; u < 4; ++u) {
+          if (p.dbg & 4) break;
+          const uint32_t o = tc::sw128_offset(row, half * 4 + u);
           tc::st_shared_v4(p_base + o, pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
           tc::st_shared_v4(ds_base + o, dk2[u * 4], dk2[u * 4 + 1], dk2[u * 4 + 2], dk2[u * 4 + 3]);
         }
@@ -357,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);
+        if (wp.g) wp.trace(66);
       }
     }
     wp.add(7, clock64() - t_role);
@@ -379,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nq = (int)((n + BQ - 1) / BQ);
       for (int j = 0; j < nq; ++j) {
         const int b = j & 1;
-        wp.wait(dq_full + b, dqc[b] & 1, 0);
+        wp.wait_warp(dq_full + b, dqc[b] & 1, 0);
         ++dqc[b];
         tc::tc_fence_after();
         uint32_t a[32], c2[32];
@@ -401,13 +445,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar(2, 128);
         // one TMA tensor reduce-add of the whole [64 q x D] fp32 box into the accumulator; rows of padded
         // queries are exactly zero (P = 0 there), so adding them into the next sample's rows is a no-op
-        if (tid == 0) {
+        if (tid == 0 && !(p.dbg & 1)) {
           tensor_reduce_add_3d(&tm_dq, stg_base, 0, h, (int)(b0 + (int64_t)j * BQ));
           bulk_commit();
         }
       }
       // dK / dV for this key tile
-      wp.wait(dkv_full, item_cnt & 1, 2);
+      wp.wait_warp(dkv_full, item_cnt & 1, 2);
       tc::tc_fence_after();
       const int64_t kv_local = (int64_t)it.y * BKV + tid;
       const bool store = kv_local < n;
@@ -438,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(dkv_empty);
+      if (wp.g) wp.trace(74);
     }
     if (tid == 0) bulk_wait0();
     wp.add(7, clock64() - t_role);
@@ -451,11 +496,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Delta = rowsum(dO * O) per (row, head) and zero the fp32 dQ accumulator (one warp per unit).
+// Delta = rowsum(dO * O) per (row, head), zero the fp32 dQ accumulator (one warp per unit), and write
+// lse (log2 units) and Delta into lsd[h][2][R] (R = total_rows rounded up to 4: a TMA-loadable layout whose
+// 64-row boxes land in the main kernel's (Q_j, dO_j) stages).
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* __restrict__ go,
                                                            const __nv_bfloat16* __restrict__ o, int64_t units,
-                                                           int H, int64_t total_rows, float* __restrict__ delta,
+                                                           int H, int64_t total_rows, const float* __restrict__ lse,
+                                                           float* __restrict__ lsd,
                                                            float* __restrict__ dq_acc) {
   const int lane = threadIdx.x & 31;
   constexpr int PER = D / 32;  // bf16 per lane
@@ -482,8 +530,9 @@ __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* 
     }
     acc = warp_sum(acc);
     if (lane == 0) {
-      const int64_t r = u / H;
-      delta[(u - r * H) * total_rows + r] = acc;
+      const int64_t r = u / H, h = u - r * H;
+      lsd[h * total_rows + r] = lse[h * total_rows + r] * kLog2e;
+      lsd[(H + h) * total_rows + r] = acc;
     }
   }
 }
@@ -514,7 +563,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   const int sms = device_sm_count();
   const int64_t units = total_rows * H;
   fb::bwd_prologue_kernel<kD><<<(int)std::min<int64_t>((units + 7) / 8, 32 * sms), 256, 0, st>>>(
-      (const __nv_bfloat16*)go, (const __nv_bfloat16*)o, units, H, total_rows, delta, dq_acc);
+      (const __nv_bfloat16*)go, (const __nv_bfloat16*)o, units, H, total_rows, lse, delta, dq_acc);
   JG_LAUNCHED("bwd_prologue_kernel");
   CUtensorMap mq, mk, mv, mdo;
   if (jg_status rc = make_map(&mq, q, total_rows, H, kD, fb::BQ)) return rc;
@@ -528,14 +577,19 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
     JG_CUDA(cudaFuncSetAttribute(fb::jfa_bwd_sm100_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
     attr_set = true;
   }
-  fb::Params p{off, items, n_items, total_rows, H, lse, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
-               1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), wait_prof_begin(st)};
+  fb::Params p{off, items, n_items, total_rows, H, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
+               1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), std::getenv("JG_BWD_DBG") ? std::atoi(std::getenv("JG_BWD_DBG")) : 0,
+               wait_prof_begin(st)};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
-  fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
+  if (!(p.dbg & 64)) fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
+  if (p.dbg & 128) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    std::fprintf(stderr, "[bwd dbg] main kernel: %s\n", cudaGetErrorString(e));
+  }
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
   wait_prof_end(p.prof, st, "bwd",
                 {"P.kv_empty", "P.qd_empty", "", "", "", "", "", "P.total", "M.kv_full", "", "M.qd_full",
-                 "M.st_empty", "M.dq_empty", "", "", "M.total", "S.lse_bar", "S.st_full", "S.pds_empty", "",
+                 "M.st_empty", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
                  "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
   fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,

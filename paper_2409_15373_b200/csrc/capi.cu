@@ -412,7 +412,7 @@ static bool force_simt() {
 }
 
 extern "C" int64_t jg_attention_backward_workspace_size(int64_t total_rows, int32_t num_heads, int32_t head_dim) {
-  const int64_t delta = ((total_rows * num_heads * 4 + 255) / 256) * 256;
+  const int64_t delta = attn_lsd_bytes(total_rows, num_heads);  // >= the SIMT path's [H, total_rows] Delta
   const int64_t acc = total_rows * num_heads * (int64_t)head_dim * 4;
   return delta + acc + 256;
 }
@@ -462,7 +462,7 @@ extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int6
     workspace = ws.p;
   }
   float* delta = (float*)workspace;
-  float* dq_acc = (float*)((char*)workspace + ((total_rows * H * 4 + 255) / 256) * 256);
+  float* dq_acc = (float*)((char*)workspace + attn_lsd_bytes(total_rows, H));
   if (!force_simt() && attn_sm100_bwd_supported(D, dtype)) {
     jg_schedule own = nullptr;
     if (!sched) {

@@ -75,6 +75,9 @@ jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
                                float* delta, jg_dtype dt, cudaStream_t st);
 
+// The backward workspace starts with lsd[2][H][total_rows] fp32: lse in log2 units, then Delta.
+inline int64_t attn_lsd_bytes(int64_t total_rows, int H) { return ((2 * (int64_t)H * total_rows * 4 + 255) / 256) * 256; }
+
 // tcgen05 attention (bf16, head_dim 64/128)
 bool attn_sm100_supported(int head_dim, jg_dtype dt);
 bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt);

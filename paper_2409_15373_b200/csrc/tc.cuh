@@ -46,21 +46,56 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // accumulated per CTA and added to a global counter array at kernel exit. prof == nullptr -> no-op.
 struct WaitProf {
   unsigned long long* g;  // global counters offset by the role base, or nullptr
-  __device__ __forceinline__ void init(unsigned long long* gp, int b) { g = gp ? gp + b : nullptr; }
+  // JG_WAIT_PROF=2 profiles CTA 0 only and records its timeline: gp[63] != 0 enables it; role r = base/8
+  // owns entries [r*kRoleCap, (r+1)*kRoleCap) of pairs gp[65 + 2i], gp[66 + 2i] = (clock64, code), with
+  // code = base + site (+1000 on wait exit). Plain stores with a per-thread index: no atomics on the path.
+  static constexpr unsigned kRoleCap = 12000;
+  int base = 0;
+  unsigned n_tr = 0;
+  bool tr = false;
+  __device__ __forceinline__ void init(unsigned long long* gp, int b) {
+    base = b;
+    const bool trace_mode = gp != nullptr && gp[63] != 0;
+    tr = trace_mode && blockIdx.x == 0;
+    g = (gp && (!trace_mode || blockIdx.x == 0)) ? gp + b : nullptr;
+  }
+  __device__ __forceinline__ void trace(int code) {
+    if (!tr || n_tr >= kRoleCap) return;
+    unsigned long long* e = g - base + 65 + 2ull * ((base / 8) * kRoleCap + n_tr++);
+    e[0] = (unsigned long long)clock64();
+    e[1] = (unsigned long long)code;
+  }
   __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int site) {
     if (g == nullptr) {
       mbar_wait(bar, parity);
       return;
     }
+    trace(base + site);
     const long long t0 = clock64();
     mbar_wait(bar, parity);
     atomicAdd(g + site, (unsigned long long)(clock64() - t0));
+    trace(1000 + base + site);
+  }
+  // warp-collective roles: reconverge after the spin so the .sync.aligned tcgen05 / elect.sync that
+  // follow see the whole warp
+  __device__ __forceinline__ void wait_warp(uint64_t* bar, uint32_t parity, int site) {
+    wait(bar, parity, site);
+    __syncwarp();
   }
   __device__ __forceinline__ void add(int site, long long cycles) {
     if (g) atomicAdd(g + site, (unsigned long long)cycles);
   }
   __device__ __forceinline__ void flush() {}
 };
+
+// ------------------------------------------------------------------ cp.async (4-byte) tracked by an mbarrier
+__device__ __forceinline__ void cp_async_4(uint32_t sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async copies land (counts against the init count)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -145,10 +180,36 @@ __device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, ui
       : "memory");
 }
 
+// Warp-collective form: every lane of the warp calls it with warp-uniform operands (so they live in
+// uniform registers) and one elected lane issues the MMA.
+__device__ __forceinline__ void mma_bf16_ss_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// warp-collective commit: the lane elected here is the one mma_bf16_ss_warp elected (lowest active lane)
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 // ------------------------------------------------------------------ TMEM <-> registers (32 lanes x 32 cols)

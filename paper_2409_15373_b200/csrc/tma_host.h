@@ -65,10 +65,16 @@ namespace jg {
 // synchronises the stream after the kernel and prints to stderr).
 inline unsigned long long* wait_prof_begin(cudaStream_t st) {
   static unsigned long long* buf = nullptr;
+  constexpr size_t kWords = 65 + 2 * 5 * 12000;
   const char* e = std::getenv("JG_WAIT_PROF");
-  if (!e || e[0] != '1') return nullptr;
-  if (!buf && cudaMalloc(&buf, 64 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-  cudaMemsetAsync(buf, 0, 64 * sizeof(unsigned long long), st);
+  if (!e || (e[0] != '1' && e[0] != '2')) return nullptr;
+  if (!buf && cudaMalloc(&buf, kWords * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(buf, 0, kWords * sizeof(unsigned long long), st);
+  if (e[0] == '2') {
+    const unsigned long long one = 1;
+    cudaMemcpyAsync(buf + 63, &one, sizeof(one), cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+  }
   return buf;
 }
 inline void wait_prof_end(unsigned long long* buf, cudaStream_t st, const char* tag, std::vector<const char*> names) {
@@ -85,5 +91,17 @@ inline void wait_prof_end(unsigned long long* buf, cudaStream_t st, const char* 
     std::fprintf(stderr, " | %s=%.3g cyc;", names[r + 7], tot);
   }
   std::fprintf(stderr, "\n");
+  const char* e = std::getenv("JG_WAIT_PROF");
+  if (e && e[0] == '2') {  // dump CTA 0's wait timeline
+    const size_t n = 5 * 12000;
+    std::vector<unsigned long long> t(2 * n);
+    cudaMemcpy(t.data(), buf + 65, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    const std::string path = std::string("gpurun_out/trace_") + tag + ".txt";
+    if (FILE* f = std::fopen(path.c_str(), "w")) {
+      for (size_t i = 0; i < n; ++i)
+        if (t[2 * i]) std::fprintf(f, "%llu %llu\n", t[2 * i], t[2 * i + 1]);
+      std::fclose(f);
+    }
+  }
 }
 }  // namespace jg

@@ -1,0 +1,40 @@
+"""Render CTA 0's barrier-wait timeline written by JG_WAIT_PROF=2 (gpurun_out/trace_<tag>.txt).
+
+    python tools/trace_view.py gpurun_out/trace_bwd.txt [first_item] [n_items]
+
+Each line: time in cycles since the first event, role column, event. A wait prints as
+"name ... +cycles" at its exit. Items are delimited by the producer's K/V issue (code 50).
+"""
+import sys
+
+NAMES = {0: "P.kv_empty", 1: "P.qd_empty", 8: "S.kv_full", 10: "S.qd_full", 11: "S.st_empty", 12: "S.dq_empty",
+         16: "X.lsd_full", 17: "X.st_full", 18: "X.pds_empty", 24: "D.dq_full", 26: "D.dkv_full", 33: "G.dkv_empty", 37: "G.p_full",
+         50: "P.KV-issued", 56: "S.issue-S", 57: "S.issue-dP", 83: "G.issue-dQ", 84: "G.issue-dV", 85: "G.issue-dK", 58: "S.commit-st", 82: "G.commit-dq", 66: "X.p_full-arrive", 74: "D.dkv-done"}
+COL = {"P": 0, "S": 1, "X": 2, "G": 3, "D": 4}
+
+
+def main():
+    path = sys.argv[1]
+    first = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    count = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    ev = sorted(tuple(map(int, ln.split())) for ln in open(path) if ln.strip())
+    t0 = ev[0][0]
+    starts = [t for t, c in ev if c == 50]
+    lo = starts[min(first, len(starts) - 1)]
+    hi = starts[min(first + count, len(starts) - 1)] if first + count < len(starts) else ev[-1][0]
+    open_w = {}
+    print(f"items {first}..{first + count - 1}: {hi - lo} cycles ({(hi - lo) / 1.9e3:.2f} us @1.9GHz)")
+    for t, c in ev:
+        if c < 1000 and c not in (50, 56, 57, 58, 82, 83, 84, 85, 66, 74):
+            open_w[c] = t
+            continue
+        if not (lo <= t <= hi):
+            continue
+        base = c - 1000 if c >= 1000 else c
+        name = NAMES.get(base, str(base))
+        extra = f" +{t - open_w.get(base, t)}" if c >= 1000 else ""
+        print(f"{t - lo:9d} " + " " * (22 * COL[name[0]]) + name + extra)
+
+
+if __name__ == "__main__":
+    main()
