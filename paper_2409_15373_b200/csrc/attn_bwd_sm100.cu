@@ -185,6 +185,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tma_load_3d(smem + L::kV + c * L::kChunkKV, &tm_v, kv_full, c * 64, h, kv_row);
         }
         if (wp.g) wp.trace(50);
+        // warm L2 with the next item's K/V: its loads wait for this item's last MMAs (kv_empty)
+        const int64_t wn = w + gridDim.x;
+        if (wn < n_work) {
+          const int2 itn = p.items[wn / H];
+          const int hn = (int)(wn % H);
+          const int kv_next = (int)(p.off[itn.x] + (int64_t)itn.y * BKV);
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_prefetch_l2_3d(&tm_k, c * 64, hn, kv_next);
+            tc::tma_prefetch_l2_3d(&tm_v, c * 64, hn, kv_next);
+          }
+        }
       }
       for (int j = 0; j < nq; ++j, ++qd_cnt) {
         const uint32_t s = qd_cnt % L::kStages;
