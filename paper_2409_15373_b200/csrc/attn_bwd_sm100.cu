@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - kSmWarp0) >> 2;       // query columns [32 half, 32 half + 32)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
-    const float* lsd = reinterpret_cast<const float*>(smem + L::kLse);
+    const uint32_t lsd = tc::smem_u32(smem + L::kLse);
     uint32_t cons[2] = {0, 0}, pds_cnt = 0, qd_cnt = 0;
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 16);
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // lse/Delta of block j arrived with (Q_j, dO_j); the stage stays valid until p_full (the issuer's
         // qd_empty commit follows the MMAs that consume P_j)
         wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 0);
-        const float* lb = lsd + s * 2 * BQ + half * 32;
+        const uint32_t lb = lsd + (s * 2 * BQ + half * 32) * 4;
         // queries past the sample end (rows of the next sample in the Q tile) and key rows past it get P = 0
         const int64_t qrem = n - (int64_t)j * BQ - half * 32;
         const int qlim = qrem < 32 ? (int)qrem : 32;
@@ -371,8 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto body = [&](auto masked) {
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
-            const float4 l4 = *reinterpret_cast<const float4*>(lb + e);
-            const float4 d4 = *reinterpret_cast<const float4*>(lb + BQ + e);
+            const float4 l4 = tc::ld_shared_f4(lb + e * 4);
+            const float4 d4 = tc::ld_shared_f4(lb + (BQ + e) * 4);
             float p0 = tc::ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
             float p1 = tc::ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
             float p2 = tc::ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
@@ -449,9 +449,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar(2, 128);
         wp.add(1, clock64() - tb);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stg[q * D + tid] = __uint_as_float(a[q]) * p.scale;
+        for (int q = 0; q < 32; ++q) tc::st_shared_f32(stg_base + (q * D + tid) * 4, __uint_as_float(a[q]) * p.scale);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stg[(q + 32) * D + tid] = __uint_as_float(c2[q]) * p.scale;
+        for (int q = 0; q < 32; ++q)
+          tc::st_shared_f32(stg_base + ((q + 32) * D + tid) * 4, __uint_as_float(c2[q]) * p.scale);
         tc::fence_proxy_async_smem();
         named_bar(2, 128);
         // one TMA tensor reduce-add of the whole [64 q x D] fp32 box into the accumulator; rows of padded

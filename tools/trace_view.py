@@ -7,9 +7,11 @@ Each line: time in cycles since the first event, role column, event. A wait prin
 """
 import sys
 
-NAMES = {0: "P.kv_empty", 1: "P.qd_empty", 8: "S.kv_full", 10: "S.qd_full", 11: "S.st_empty", 12: "S.dq_empty",
-         16: "X.lsd_full", 17: "X.st_full", 18: "X.pds_empty", 24: "D.dq_full", 26: "D.dkv_full", 33: "G.dkv_empty", 37: "G.p_full",
-         50: "P.KV-issued", 56: "S.issue-S", 57: "S.issue-dP", 83: "G.issue-dQ", 84: "G.issue-dV", 85: "G.issue-dK", 58: "S.commit-st", 82: "G.commit-dq", 66: "X.p_full-arrive", 74: "D.dkv-done"}
+NAMES = {0: "P.k_empty", 1: "P.qd_empty", 2: "P.v_empty", 8: "S.k_full", 9: "S.v_full", 10: "S.qd_full",
+         11: "S.buf_free", 12: "S.dq_empty", 16: "X.qd_full", 17: "X.st_full", 18: "X.ds_empty", 24: "D.dq_full",
+         26: "D.dkv_full", 32: "G.k_full", 33: "G.dv_empty", 34: "G.dk_empty", 37: "G.p_full",
+         50: "P.KV-issued", 58: "S.commit-st", 82: "G.commit-all", 83: "G.commit-dq", 66: "X.p_full-arrive",
+         74: "D.dkv-done"}
 COL = {"P": 0, "S": 1, "X": 2, "G": 3, "D": 4}
 
 
@@ -25,7 +27,7 @@ def main():
     open_w = {}
     print(f"items {first}..{first + count - 1}: {hi - lo} cycles ({(hi - lo) / 1.9e3:.2f} us @1.9GHz)")
     for t, c in ev:
-        if c < 1000 and c not in (50, 56, 57, 58, 82, 83, 84, 85, 66, 74):
+        if c < 1000 and c not in (50, 58, 82, 83, 66, 74):
             open_w[c] = t
             continue
         if not (lo <= t <= hi):
