@@ -52,7 +52,7 @@ struct Smem {
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 lse (log2 units) + 64 Delta, fp32
   static constexpr int kLse = kStg + BQ * D * 4;            // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
-  static constexpr int kNumBars = 2 + 2 * kStages + 4 + 2 + 4 + 2;
+  static constexpr int kNumBars = 4 + 2 * kStages + 4 + 2 + 4 + 2;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes + 1024;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -101,9 +101,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* kv_full = bars + 0;
-  uint64_t* kv_empty = bars + 1;
-  uint64_t* qd_full = bars + 2;
+  uint64_t* k_full = bars + 0;
+  uint64_t* k_empty = bars + 1;  // S issuer after its last S^T, G issuer after its last dQ^T
+  uint64_t* v_full = bars + 2;
+  uint64_t* v_empty = bars + 3;  // S issuer after its last dP^T: the next item's V loads while G finishes
+  uint64_t* qd_full = bars + 4;
   uint64_t* qd_empty = qd_full + L::kStages;
   uint64_t* st_full = qd_empty + L::kStages;  // [2] per TMEM score buffer
   uint64_t* st_empty = st_full + 2;           // [2]
@@ -118,8 +120,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    tc::mbar_init(kv_full, 1);
-    tc::mbar_init(kv_empty, 2);  // both MMA issuers release K/V
+    tc::mbar_init(k_full, 1);
+    tc::mbar_init(k_empty, 2);
+    tc::mbar_init(v_full, 1);
+    tc::mbar_init(v_empty, 1);
     for (int s = 0; s < L::kStages; ++s) {
       tc::mbar_init(qd_full + s, 1 + 32);  // TMA expect_tx arrival + 32 cp.async (lse/Delta) arrivals
       tc::mbar_init(qd_empty + s, 1);
@@ -177,13 +181,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(b0 + (int64_t)j * BQ));
           }
       }
-      wp.wait_warp(kv_empty, (item_cnt & 1) ^ 1, 0);
+      wp.wait_warp(v_empty, (item_cnt & 1) ^ 1, 2);
       if (lane == 0) {
-        tc::mbar_expect_tx(kv_full, 2 * L::kTileKV);
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, kv_full, c * 64, h, kv_row);
-          tc::tma_load_3d(smem + L::kV + c * L::kChunkKV, &tm_v, kv_full, c * 64, h, kv_row);
-        }
+        tc::mbar_expect_tx(v_full, L::kTileKV);
+        for (int c = 0; c < D / 64; ++c)
+          tc::tma_load_3d(smem + L::kV + c * L::kChunkKV, &tm_v, v_full, c * 64, h, kv_row);
+      }
+      wp.wait_warp(k_empty, (item_cnt & 1) ^ 1, 0);
+      if (lane == 0) {
+        tc::mbar_expect_tx(k_full, L::kTileKV);
+        for (int c = 0; c < D / 64; ++c)
+          tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, k_full, c * 64, h, kv_row);
         if (wp.g) wp.trace(50);
         // warm L2 with the next item's K/V: its loads wait for this item's last MMAs (kv_empty)
         const int64_t wn = w + gridDim.x;
@@ -259,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
         if (warp == 1) {
-          wp.wait_warp(kv_full, item_cnt & 1, 0);
+          wp.wait_warp(k_full, item_cnt & 1, 0);
+          wp.wait_warp(v_full, item_cnt & 1, 1);
           for (int j = 0; j < nq; ++j, ++qd_cnt) {
             const int b = j & 1;
             const uint32_t s = qd_cnt % L::kStages;
@@ -289,7 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_commit_warp(st_full + b);
             if (wp.g) wp.trace(58);
           }
-          tc::mma_commit_warp(kv_empty);  // this issuer's reads of K and V are done
+          tc::mma_commit_warp(v_empty);  // this issuer's reads of K and V are done
+          tc::mma_commit_warp(k_empty);
         } else {
           wp.wait_warp(dkv_empty, (item_cnt & 1) ^ 1, 1);
           for (int j = 0; j < nq; ++j, ++qd_cnt) {
@@ -306,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
             }
             tc::mma_commit_warp(dq_full + (j & 1));
+            if (j == nq - 1) tc::mma_commit_warp(k_empty);  // the item's last read of K: reload during dV/dK
             if (wp.g) wp.trace(84);
             // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
 #pragma unroll
@@ -325,7 +336,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (wp.g) wp.trace(82);
           }
           tc::mma_commit_warp(dkv_full);
-          tc::mma_commit_warp(kv_empty);
         }
       }
       wp.add(7, clock64() - t_role);
@@ -600,7 +610,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   }
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
   wait_prof_end(p.prof, st, "bwd",
-                {"P.kv_empty", "P.qd_empty", "", "", "", "", "", "P.total", "M.kv_full", "", "M.qd_full",
+                {"P.k_empty", "P.qd_empty", "P.v_empty", "", "", "", "", "P.total", "M.k_full", "M.v_full", "M.qd_full",
                  "M.st_empty", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
                  "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
