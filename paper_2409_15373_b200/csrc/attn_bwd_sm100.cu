@@ -34,7 +34,9 @@ constexpr int kThreads = 512;
 constexpr int kSmWarp0 = 4, kDqWarp0 = 12;
 constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 of the 64 query columns
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kPrefetch = 6;  // query blocks prefetched into L2 ahead of the producer
+constexpr int kPrefetch = 6;
+constexpr int kQdStages = 3;  // (Q_j, dO_j) smem ring depth (2 stages + 2 P/dS buffers measured slower)
+constexpr int kPdsBufs = 1;   // P^T/dS^T smem buffers (2 would let the softmax publish block j+1 while j is read)  // query blocks prefetched into L2 ahead of the producer
 
 template <int D>
 struct Smem {
@@ -42,17 +44,17 @@ struct Smem {
   static constexpr int kChunkQ = BQ * 128;    // [64 rows x 64] bf16 = 8 KB
   static constexpr int kTileKV = (D / 64) * kChunkKV;
   static constexpr int kTileQ = (D / 64) * kChunkQ;
-  static constexpr int kStages = 3;
+  static constexpr int kStages = kQdStages;
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTileKV;
   static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
-  static constexpr int kP = kQD + kStages * 2 * kTileQ;     // P^T  [128 keys x 64 q] bf16
-  static constexpr int kDS = kP + BKV * 128;                // dS^T [128 keys x 64 q] bf16
-  static constexpr int kStg = kDS + BKV * 128;              // dQ staging [64 q x D] fp32
+  static constexpr int kP = kQD + kStages * 2 * kTileQ;     // kPdsBufs x P^T  [128 keys x 64 q] bf16
+  static constexpr int kDS = kP + kPdsBufs * BKV * 128;     // kPdsBufs x dS^T [128 keys x 64 q] bf16
+  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging [64 q x D] fp32
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 lse (log2 units) + 64 Delta, fp32
   static constexpr int kLse = kStg + BQ * D * 4;            // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
-  static constexpr int kNumBars = 4 + 2 * kStages + 4 + 2 + 4 + 2;
+  static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes + 1024;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -110,8 +112,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* st_full = qd_empty + L::kStages;  // [2] per TMEM score buffer
   uint64_t* st_empty = st_full + 2;           // [2]
   uint64_t* p_full = st_empty + 2;
-  uint64_t* pds_empty = p_full + 1;
-  uint64_t* dq_full = pds_empty + 1;          // [2] one per score buffer: a single barrier could complete
+  uint64_t* pds_empty = p_full + 1;            // [kPdsBufs]
+  uint64_t* dq_full = pds_empty + kPdsBufs;          // [2] one per score buffer: a single barrier could complete
                                               // twice before the drain warps wait (no S fill between dQ_{n-2}, dQ_{n-1})
   uint64_t* dq_empty = dq_full + 2;           // [2] dQ^T_j lives in score buffer j&1
   uint64_t* dkv_full = dq_empty + 2;
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(dq_empty + b, 4);
     }
     tc::mbar_init(p_full, kSmWarps);
-    tc::mbar_init(pds_empty, 1);
+    for (int b = 0; b < kPdsBufs; ++b) tc::mbar_init(pds_empty + b, 1);
     tc::mbar_init(dq_full, 1);
     tc::mbar_init(dq_full + 1, 1);
     tc::mbar_init(dkv_full, 1);
@@ -304,6 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           wp.wait_warp(dkv_empty, (item_cnt & 1) ^ 1, 1);
           for (int j = 0; j < nq; ++j, ++qd_cnt) {
             wp.wait_warp(p_full, p_cnt & 1, 5);
+            const uint32_t pb = p_cnt % kPdsBufs;
+            const uint32_t p_cur = p_base + pb * (BKV * 128), ds_cur = ds_base + pb * (BKV * 128);
             ++p_cnt;
             tc::tc_fence_after();
             const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < BKV / 16; ++kk) {
               tc::mma_bf16_ss_warp(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
-                              tc::sw128_desc(ds_base + kk * 2048, 16, 1024), kIdQ, kk > 0);
+                              tc::sw128_desc(ds_cur + kk * 2048, 16, 1024), kIdQ, kk > 0);
             }
             tc::mma_commit_warp(dq_full + (j & 1));
             if (j == nq - 1) tc::mma_commit_warp(k_empty);  // the item's last read of K: reload during dV/dK
@@ -321,18 +325,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
 #pragma unroll
             for (int kk = 0; kk < BQ / 16; ++kk) {
-              tc::mma_bf16_ss_warp(tmem + 256, tc::sw128_desc(p_base + kk * 32, 16, 1024),
+              tc::mma_bf16_ss_warp(tmem + 256, tc::sw128_desc(p_cur + kk * 32, 16, 1024),
                               tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
             }
             if (wp.g) wp.trace(85);
 #pragma unroll
             for (int kk = 0; kk < BQ / 16; ++kk) {
-              tc::mma_bf16_ss_warp(tmem + 384, tc::sw128_desc(ds_base + kk * 32, 16, 1024),
+              tc::mma_bf16_ss_warp(tmem + 384, tc::sw128_desc(ds_cur + kk * 32, 16, 1024),
                               tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
             }
             // Q_j, dO_j are no longer needed (warp 1's S/dP_j completed before the softmax published P_j)
             tc::mma_commit_warp(qd_empty + (qd_cnt % L::kStages));
-            tc::mma_commit_warp(pds_empty);
+            tc::mma_commit_warp(pds_empty + pb);
             if (wp.g) wp.trace(82);
           }
           tc::mma_commit_warp(dkv_full);
@@ -408,14 +412,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(st_empty + b);
-        wp.wait_warp(pds_empty, (pds_cnt & 1) ^ 1, 2);
+        const uint32_t pb = pds_cnt % kPdsBufs;
+        wp.wait_warp(pds_empty + pb, ((pds_cnt / kPdsBufs) & 1) ^ 1, 2);
         ++pds_cnt;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (p.dbg & 4) break;
           const uint32_t o = tc::sw128_offset(row, half * 4 + u);
-          tc::st_shared_v4(p_base + o, pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
-          tc::st_shared_v4(ds_base + o, dk2[u * 4], dk2[u * 4 + 1], dk2[u * 4 + 2], dk2[u * 4 + 3]);
+          tc::st_shared_v4(p_base + pb * (BKV * 128) + o, pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
+          tc::st_shared_v4(ds_base + pb * (BKV * 128) + o, dk2[u * 4], dk2[u * 4 + 1], dk2[u * 4 + 2], dk2[u * 4 + 3]);
         }
         tc::fence_proxy_async_smem();
         tc::tc_fence_before();
