@@ -34,9 +34,9 @@ constexpr int kThreads = 512;
 constexpr int kSmWarp0 = 4, kDqWarp0 = 12;
 constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 of the 64 query columns
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kPrefetch = 6;
+constexpr int kPrefetch = 6;   // query blocks prefetched into L2 ahead of the producer
 constexpr int kQdStages = 3;  // (Q_j, dO_j) smem ring depth (2 stages + 2 P/dS buffers measured slower)
-constexpr int kPdsBufs = 1;   // P^T/dS^T smem buffers (2 would let the softmax publish block j+1 while j is read)  // query blocks prefetched into L2 ahead of the producer
+constexpr int kPdsBufs = 1;   // P^T/dS^T smem buffers (2 would let the softmax publish block j+1 while j is read)
 
 template <int D>
 struct Smem {
