@@ -163,19 +163,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ===================================================== MMA issuer
-    if (lane == 0) {
+    // warp-collective: operands stay warp-uniform (uniform registers) and one elected lane issues; a
+    // single-lane loop pays per-MMA R2UR moves that the softmax warps' traffic slows (tools/mma_seq_bench.cu)
+    {
       constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
       constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
       const uint32_t q_base = tc::smem_u32(smem + L::kQ);
       const uint32_t p_base = tc::smem_u32(smem + L::kP);
       const uint32_t kv_base = tc::smem_u32(smem + L::kKV);
       tc::WaitProf wp;
-      wp.init(p.prof, 8);
+      wp.init(lane == 0 ? p.prof : nullptr, 8);
       const long long t_role = clock64();
       uint32_t kv_cnt = 0, item_cnt = 0, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
       auto next_stage = [&]() {
         const uint32_t s = kv_cnt % L::kStages;
-        wp.wait(kv_full + s, (kv_cnt / L::kStages) & 1, 2);
+        wp.wait_warp(kv_full + s, (kv_cnt / L::kStages) & 1, 2);
         ++kv_cnt;
         tc::tc_fence_after();
         return s;
@@ -186,12 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t koff = (kk >> 2) * L::kChunk + (kk & 3) * 32;
-          tc::mma_bf16_ss(tmem + t * 256, tc::sw128_desc(qa + koff, 16, 1024), tc::sw128_desc(ka + koff, 16, 1024),
+          tc::mma_bf16_ss_warp(tmem + t * 256, tc::sw128_desc(qa + koff, 16, 1024), tc::sw128_desc(ka + koff, 16, 1024),
                           kIdescS, kk > 0);
         }
         wp.add(5, clock64() - t0);
         wp.add(6, D / 16);
-        tc::mma_commit(s_full + t);
+        tc::mma_commit_warp(s_full + t);
       };
       auto issue_pv = [&](int t, uint32_t v_stage, int j) {
         const long long t0 = clock64();
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < BN / 16; ++kk) {
           // A = P [128 x 128 keys] K-major; B = V [128 keys x D] MN-major (LBO = next 64-wide D chunk)
           const uint32_t aoff = (kk >> 2) * L::kChunk + (kk & 3) * 32;
-          tc::mma_bf16_ss(tmem + t * 256 + 128, tc::sw128_desc(pa + aoff, 16, 1024),
+          tc::mma_bf16_ss_warp(tmem + t * 256 + 128, tc::sw128_desc(pa + aoff, 16, 1024),
                           tc::sw128_desc(va + kk * 16 * 128, L::kChunk, 1024), kIdescO, (j > 0 || kk > 0));
         }
         wp.add(5, clock64() - t0);
@@ -211,33 +213,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Item it = load_item(p, w);
         const int nt = it.has_b ? 2 : 1;
         wp.add(1, clock64() - t_li);
-        wp.wait(q_full, item_cnt & 1, 0);
+        wp.wait_warp(q_full, item_cnt & 1, 0);
         uint32_t ks = next_stage();  // K_0
         for (int t = 0; t < nt; ++t) issue_s(t, ks);
-        tc::mma_commit(kv_empty + ks);
+        tc::mma_commit_warp(kv_empty + ks);
+        if (it.nkv == 1) tc::mma_commit_warp(q_empty);  // Q is only read by S MMAs: the next Q loads now
         for (int j = 0; j < it.nkv; ++j) {
           const uint32_t vs = next_stage();  // V_j
           const bool more = j + 1 < it.nkv;
           uint32_t kn = 0;
           for (int t = 0; t < nt; ++t) {
-            wp.wait(p_full + t, p_cnt[t] & 1, 4);  // softmax t wrote P_t(j) (and finished reading S_t(j))
+            wp.wait_warp(p_full + t, p_cnt[t] & 1, 4);  // softmax t wrote P_t(j) (and finished reading S_t(j))
             ++p_cnt[t];
             if (j == 0) {  // the previous item that used tile t has drained O_t
-              wp.wait(o_empty + t, (o_use[t] & 1) ^ 1, 3);
+              wp.wait_warp(o_empty + t, (o_use[t] & 1) ^ 1, 3);
               ++o_use[t];
             }
             tc::tc_fence_after();
             issue_pv(t, vs, j);
-            if (!more) tc::mma_commit(o_done + t);
+            if (!more) tc::mma_commit_warp(o_done + t);
             if (more) {
               if (t == 0) kn = next_stage();  // K_{j+1}
               issue_s(t, kn);
             }
           }
-          tc::mma_commit(kv_empty + vs);
-          if (more) tc::mma_commit(kv_empty + kn);
+          tc::mma_commit_warp(kv_empty + vs);
+          if (more) tc::mma_commit_warp(kv_empty + kn);
+          if (j + 2 == it.nkv) tc::mma_commit_warp(q_empty);  // after the item's last S MMAs
         }
-        tc::mma_commit(q_empty);
       }
       wp.add(7, clock64() - t_role);
       wp.flush();

@@ -13,7 +13,7 @@ sys.path.insert(0, '.')
 from paper_2409_15373_b200 import jagged as J, synth  # noqa: E402
 
 
-def run(name, ln, H=4, D=128, reps=10):
+def run(name, ln, H=4, D=128, reps=25):
     off = synth.offsets_of(ln)
     S = int(off[-1])
     mk = lambda: (torch.rand(S, H, D, device='cuda') * 2 - 1).bfloat16()  # noqa: E731
@@ -25,7 +25,7 @@ def run(name, ln, H=4, D=128, reps=10):
         J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    tf = tb = 0.0
+    tfs, tbs = [], []
     for _ in range(reps):
         ev[0].record()
         s = J.jagged_flash_attention_forward(Q, K, V, schedule=sch)
@@ -33,8 +33,9 @@ def run(name, ln, H=4, D=128, reps=10):
         J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch)
         ev[2].record()
         torch.cuda.synchronize()
-        tf += ev[0].elapsed_time(ev[1]) / reps
-        tb += ev[1].elapsed_time(ev[2]) / reps
+        tfs.append(ev[0].elapsed_time(ev[1]))
+        tbs.append(ev[1].elapsed_time(ev[2]))
+    tf, tb = float(np.median(tfs)), float(np.median(tbs))  # median: robust to clock/thermal noise
     sq = float((np.asarray(ln, np.float64) ** 2).sum())
     ff, fb = 4 * sq * H * D, 10 * sq * H * D
     print(f"{name:24s} sumB={S:8d} fwd {tf:7.3f} ms {ff / tf / 1e9:7.1f} TF/s   bwd {tb:7.3f} ms {fb / tb / 1e9:7.1f} TF/s",
