@@ -37,6 +37,7 @@ constexpr int BM = 128;          // query rows per tile (two tiles per work item
 constexpr int BN = 128;          // keys per block
 constexpr int kThreads = 320;    // 10 warps
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
+constexpr int kPolyExp = 2;               // of every 8 exponentials, this many run on the FMA pipe (ex2_poly)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
 
 template <int D>
@@ -44,10 +45,9 @@ struct Smem {
   static constexpr int kChunk = BM * 128;               // one [128 rows x 64] bf16 SW128 chunk = 16 KB
   static constexpr int kChunks = D / 64;
   static constexpr int kTile = kChunks * kChunk;        // 128 x D bf16
-  static constexpr int kStages = D == 128 ? 3 : 6;      // K/V ring
+  static constexpr int kStages = D == 128 ? 5 : 8;      // K/V ring (P lives in TMEM, not smem)
   static constexpr int kQ = 0;                           // Q_A, Q_B
-  static constexpr int kP = kQ + 2 * kTile;              // P_A, P_B: 128 x 128 bf16 = 32 KB each
-  static constexpr int kKV = kP + 2 * 2 * kChunk;
+  static constexpr int kKV = kQ + 2 * kTile;
   static constexpr int kBar = kKV + kStages * kTile;
   // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_done[2], o_empty[2], tmem slot
   static constexpr int kNumBars = 2 + 2 * kStages + 8 + 1;
@@ -66,6 +66,7 @@ struct Params {
   float* lse;
   float scale_log2;
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23)
+  int dbg;                   // JG_FWD_DBG (diagnostic, results invalid): 1 = softmax publishes P without computing
 };
 
 struct Item {
@@ -83,6 +84,14 @@ __device__ __forceinline__ Item load_item(const Params& p, int64_t w) {
   r.nkv = (int)((r.n + BN - 1) / BN);
   r.q_row = (int)(r.b0 + (int64_t)it.y * 2 * BM);
   r.has_b = (int64_t)it.y * 2 * BM + BM < r.n;
+  return r;
+}
+
+// the next work item's descriptor, loaded one item ahead by every role (its two dependent global loads
+// would otherwise sit at the start of every item); past the end: an empty item that is never used
+__device__ __forceinline__ Item load_item_or_empty(const Params& p, int64_t w, int64_t n_work) {
+  if (w < n_work) return load_item(p, w);
+  Item r{};
   return r;
 }
 
@@ -139,8 +148,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       wp.init(p.prof, 0);
       const long long t_role = clock64();
       uint32_t kv_cnt = 0, item_cnt = 0;
+      Item nxt = load_item_or_empty(p, blockIdx.x, n_work);
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
-        const Item it = load_item(p, w);
+        const Item it = nxt;
+        nxt = load_item_or_empty(p, w + gridDim.x, n_work);  // hidden behind this item
         wp.wait(q_empty, (item_cnt & 1) ^ 1, 0);
         tc::mbar_expect_tx(q_full, (it.has_b ? 2 : 1) * L::kTile);
         for (int t = 0; t < (it.has_b ? 2 : 1); ++t)
@@ -169,7 +180,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
       constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
       const uint32_t q_base = tc::smem_u32(smem + L::kQ);
-      const uint32_t p_base = tc::smem_u32(smem + L::kP);
       const uint32_t kv_base = tc::smem_u32(smem + L::kKV);
       tc::WaitProf wp;
       wp.init(lane == 0 ? p.prof : nullptr, 8);
@@ -197,20 +207,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto issue_pv = [&](int t, uint32_t v_stage, int j) {
         const long long t0 = clock64();
-        const uint32_t pa = p_base + t * 2 * L::kChunk, va = kv_base + v_stage * L::kTile;
+        const uint32_t va = kv_base + v_stage * L::kTile;
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          // A = P [128 x 128 keys] K-major; B = V [128 keys x D] MN-major (LBO = next 64-wide D chunk)
-          const uint32_t aoff = (kk >> 2) * L::kChunk + (kk & 3) * 32;
-          tc::mma_bf16_ss_warp(tmem + t * 256 + 128, tc::sw128_desc(pa + aoff, 16, 1024),
-                          tc::sw128_desc(va + kk * 16 * 128, L::kChunk, 1024), kIdescO, (j > 0 || kk > 0));
+          // A = P_t from TMEM (bf16 packed two per column over S_t's first 64 columns: keys 16kk.. at
+          // column 8kk); B = V [128 keys x D] MN-major (LBO = next 64-wide D chunk)
+          tc::mma_bf16_ts_warp(tmem + t * 256 + 128, tmem + t * 256 + kk * 8,
+                               tc::sw128_desc(va + kk * 16 * 128, L::kChunk, 1024), kIdescO, (j > 0 || kk > 0));
         }
         wp.add(5, clock64() - t0);
         wp.add(6, BN / 16);
       };
+      Item nxt = load_item_or_empty(p, blockIdx.x, n_work);
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
         const long long t_li = clock64();
-        const Item it = load_item(p, w);
+        const Item it = nxt;
+        nxt = load_item_or_empty(p, w + gridDim.x, n_work);
         const int nt = it.has_b ? 2 : 1;
         wp.add(1, clock64() - t_li);
         wp.wait_warp(q_full, item_cnt & 1, 0);
@@ -252,31 +264,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = wq * 32 + lane;             // query row within the tile == TMEM lane
     const uint32_t s_addr = tmem + ((uint32_t)(wq * 32) << 16) + t * 256;
     const uint32_t o_addr = s_addr + 128;
-    const uint32_t p_base = tc::smem_u32(smem + L::kP) + t * 2 * L::kChunk;
     uint32_t s_cnt = 0, done_cnt = 0;
     tc::WaitProf wp;
     wp.init(row == 0 && t == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
+    Item nxt = load_item_or_empty(p, blockIdx.x, n_work);
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-      const Item it = load_item(p, w);
+      const Item it = nxt;
+      nxt = load_item_or_empty(p, w + gridDim.x, n_work);
       if (t == 1 && !it.has_b) continue;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < it.nkv; ++j) {
         wp.wait(s_full + t, s_cnt & 1, 0);
         ++s_cnt;
         tc::tc_fence_after();
+        const long long t_sm = clock64();
+        if (p.dbg & 1) {
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(p_full + t);
+          continue;
+        }
         const int64_t rem = it.n - (int64_t)j * BN;
         const bool partial = rem < BN;  // warp-uniform: only a segment's last key block is partial
         // pass 1: raw-score row max over TMEM in 32-column chunks, 8 independent chains
         float m8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (!partial) {
+          // two 32-column loads in flight per wait
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tc::tmem_ld32(s_addr + c * 32, r);
+          for (int c = 0; c < BN / 32; c += 2) {
+            uint32_t r[2][32];
+            tc::tmem_ld32(s_addr + c * 32, r[0]);
+            tc::tmem_ld32(s_addr + c * 32 + 32, r[1]);
             tc::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e]));
+            for (int e = 0; e < 64; ++e) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e >> 5][e & 31]));
           }
         } else {
           // last key block of the segment: write -inf over the keys of the next sample back into TMEM so
@@ -317,33 +339,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc::tmem_wait_st();
         }
-        // pass 2: P = exp2(S*scale - m) -> smem as bf16, SWIZZLE_128B K-major [128 rows x 128 keys]
-        // (two 64-key chunks), re-reading S from TMEM chunk by chunk
+        // pass 2: P = exp2(S*scale - m) as bf16 back into TMEM over S_t's first 64 columns (the A operand of
+        // the PV MMA): chunk c (keys 32c..32c+31) packs into columns 16c..16c+15, which this thread has
+        // already read (they belong to chunks <= c)
         float r8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // software-pipelined: chunk c+1's TMEM load is in flight while chunk c is exponentiated
+        uint32_t r[2][32];
+        tc::tmem_ld32(s_addr, r[0]);
+        tc::tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld32(s_addr + c * 32, r);
-          tc::tmem_wait_ld();
+          if (c + 1 < BN / 32) tc::tmem_ld32(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
+          uint32_t pk[16];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             float pv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              pv[e] = tc::ex2(fmaf(__uint_as_float(r[u * 8 + e]), p.scale_log2, -m));
+              const float x = fmaf(__uint_as_float(r[c & 1][u * 8 + e]), p.scale_log2, -m);
+              pv[e] = e < 8 - kPolyExp ? tc::ex2(x) : tc::ex2_poly(x);
               r8[e] += pv[e];
             }
-            const int unit = c * 4 + u;
-            const uint32_t addr = p_base + (unit >> 3) * L::kChunk + tc::sw128_offset(row, unit & 7);
-            tc::st_shared_v4(addr, tc::pack_bf16(pv[0], pv[1]), tc::pack_bf16(pv[2], pv[3]),
-                             tc::pack_bf16(pv[4], pv[5]), tc::pack_bf16(pv[6], pv[7]));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk[u * 4 + e] = tc::pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
+          tc::tmem_st16(s_addr + c * 16, pk);
+          if (c + 1 < BN / 32) tc::tmem_wait_ld();
         }
         l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
-        tc::fence_proxy_async_smem();
+        tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full + t);
+        wp.add(3, clock64() - t_sm);
+        wp.add(4, 1);
       }
       // epilogue: last PV of the item, normalise, store
       wp.wait(o_done + t, done_cnt & 1, 2);
@@ -413,14 +442,15 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
     attr_set = true;
   }
   fa::Params p{off, items, n_items, batch, total_rows, H, (__nv_bfloat16*)out, lse,
-               1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st)};
+               1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st),
+               std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0};
   const int64_t work = max_items * H;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sm_count(), work));
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
   JG_LAUNCHED("jfa_fwd_sm100_kernel");
   wait_prof_end(p.prof, st, "fwd",
                 {"P.q_empty", "P.kv_empty", "", "", "", "", "", "P.total", "M.q_full", "M.load_item", "M.kv_full", "M.o_empty",
-                 "M.p_full", "M.issue_cyc", "M.n_mma(x1e-2%)", "M.total", "S.s_full", "", "S.o_done", "", "", "", "", "S.total"});
+                 "M.p_full", "M.issue_cyc", "M.n_mma(x1e-2%)", "M.total", "S.s_full", "", "S.o_done", "S.compute", "S.blocks(x1e-2%)", "", "", "S.total"});
   return JG_OK;
 }
 

@@ -259,6 +259,19 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ math
+// 2^x on the FMA pipe (x <= ~127): round-to-nearest split x = n + f, f in [-0.5, 0.5], degree-3 minimax
+// for 2^f (max relative error 7.5e-5, below half a bf16 ulp), n added into the exponent bits. Used for a
+// fraction of the softmax exponentials so the 16/clk/SM MUFU pipe stops being the bound.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: the rounded integer lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.05517132f, 0.24261054f);
+  p = fmaf(p, f, 0.69326099f);
+  p = fmaf(p, f, 0.99992811f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -55,6 +55,21 @@ __global__ void __launch_bounds__(512, 1) seq_bench(int blocks, unsigned long lo
       acc += r[0] + r[31];
     }
     if (acc == 12345) out[2] = acc;
+  } else if (warp >= 4 && warp < 12 && (CONT & 16)) {  // softmax-like: TMEM ld, exp, TMEM st (cols 128..255)
+    const uint32_t la = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 + ((warp >> 2) & 1) * 64;
+    float acc = 0.f;
+    while (!done) {
+      uint32_t r[32], pk[16];
+      tc::tmem_ld32(la, r);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pk[e] = tc::pack_bf16(tc::ex2(__uint_as_float(r[2 * e]) * 0.1f), tc::ex2(__uint_as_float(r[2 * e + 1]) * 0.1f));
+      tc::tmem_st16(la + 32, pk);
+      tc::tmem_wait_st();
+      acc += __uint_as_float(pk[3]);
+    }
+    if (acc == 12345.f) out[2] = 1;
   } else if (warp >= 4 && warp < 12 && (CONT & 4)) {  // softmax-like FFMA + MUFU stream
     float x[16];
 #pragma unroll
@@ -80,6 +95,23 @@ __global__ void __launch_bounds__(512, 1) seq_bench(int blocks, unsigned long lo
     const long long t0 = clock64();
     for (int j = 0; j < blocks; ++j) {
       const uint32_t col = (j & 1) * 128;
+      if (MODE & 16) {  // forward-like: S = Q K^T (SS) into cols 0..127, O += P V (TS, A = cols 0..63) into 256..383
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ka = (kk >> 2) * kChunkKV + (kk & 3) * 32;
+          MMA(tmem, tc::sw128_desc(k_base + ka, 16, 1024), tc::sw128_desc(v_base + ka, 16, 1024),
+              tc::idesc_bf16_f32(128, 128, false, false), kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          if (CONT & 8)
+            tc::mma_bf16_ts_warp(tmem + 256, tmem + kk * 8, tc::sw128_desc(v_base + kk * 2048, kChunkKV, 1024),
+                                 tc::idesc_bf16_f32(128, 128, false, true), 1);
+          else
+            MMA(tmem + 256, tc::sw128_desc(q_base + (kk >> 2) * kChunkKV + (kk & 3) * 32, 16, 1024),
+                tc::sw128_desc(v_base + kk * 2048, kChunkKV, 1024), tc::idesc_bf16_f32(128, 128, false, true), 1);
+        }
+      }
       if (MODE & 1) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -152,6 +184,11 @@ void run(int blocks, const char* what, double ideal) {
 }
 
 int main() {
+  run<16, 8>(512, "fwd S(SS)+PV(TS)", 1024);
+  run<16, 0>(512, "fwd S(SS)+PV(SS) 1-lane", 1024);
+  run<16, 8 | 16>(512, "fwd TS + softmax-like TMEM/exp", 1024);
+  run<16, 8 | 4>(512, "fwd TS + FFMA/MUFU", 1024);
+  run<16, 8 | 2>(512, "fwd TS + tmem ld", 1024);
   run<1>(512, "S^T + dP^T (16 x N=64)", 768);
   run<2>(512, "dQ^T (8 x N=64, MN-major A,B)", 384);
   run<4>(512, "dV + dK (8 x N=128, MN-major B)", 512);
