@@ -574,3 +574,133 @@ int or_dense_attention(const int64_t* lengths, int64_t B, int64_t L, int64_t D, 
   free(sc);
   return 0;
 }
+
+/* ---- feature interaction, attention.cpp:291-309 ----
+ * s = scale(jagged_dense_bmm(k_feat, transpose_per_sample(targets)), 1/sqrt(D))  (:302-303)
+ * p = jagged_softmax(s)  (softmax over each segment's rows, per target column)  (:305)
+ * out = jagged_jagged_bmm(p, v_feat)  (P_i^T V_i, zero for empty samples)  (:307) */
+int or_feature_interaction(const int64_t* off, int64_t B, int64_t D, int64_t Tq, const double* k_feat,
+                           const double* v_feat, const double* targets, int as_float, double* out) {
+  const int64_t S = off[B];
+  const double inv = as_float ? (double)(float)(1.0 / sqrt((double)D)) : 1.0 / sqrt((double)D);
+  double* s = (double*)malloc(sizeof(double) * (size_t)(S * Tq > 0 ? S * Tq : 1));
+  double* pr = (double*)malloc(sizeof(double) * (size_t)(S * Tq > 0 ? S * Tq : 1));
+  for (int64_t i = 0; i < B; ++i)
+    for (int64_t r = off[i]; r < off[i + 1]; ++r)
+      for (int64_t t = 0; t < Tq; ++t) {
+        double acc = 0.0;  /* jagged_dense_bmm against targets_i^T: w(d, t) = targets[i, t, d] */
+        for (int64_t d = 0; d < D; ++d) acc += k_feat[r * D + d] * targets[(i * Tq + t) * D + d];
+        if (as_float) acc = (double)(float)acc;
+        double sc = acc * inv;
+        s[r * Tq + t] = as_float ? (double)(float)sc : sc;
+      }
+  or_jagged_softmax(off, B, Tq, s, pr);
+  if (as_float)
+    for (int64_t e = 0; e < S * Tq; ++e) pr[e] = (double)(float)pr[e];
+  or_jagged_jagged_bmm(off, B, Tq, D, pr, v_feat, out);
+  free(s);
+  free(pr);
+  return 0;
+}
+
+/* ---- jagged MLP ---- */
+/* linalg.cpp:246-261: one affine layer in binary64, optional pre-activation capture */
+static void mlp_layer(int64_t rows, int64_t din, int64_t dout, const double* w, const double* b, int relu,
+                      const double* in, double* out, double* pre) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t o = 0; o < dout; ++o) {
+      double acc = b[o];
+      for (int64_t i = 0; i < din; ++i) acc += in[r * din + i] * w[i * dout + o];
+      if (pre) pre[r * dout + o] = acc;
+      out[r * dout + o] = relu ? fmax(acc, 0.0) : acc;
+    }
+}
+
+/* linalg.cpp:265-277 */
+int or_jagged_mlp(int64_t rows, int n_layers, const int64_t* dims, const double* w, const double* b,
+                  const int* relu, const double* x, double* out) {
+  if (n_layers < 1) return fail("jagged_mlp: at least one layer required");
+  int64_t maxd = 0;
+  for (int l = 0; l <= n_layers; ++l) maxd = dims[l] > maxd ? dims[l] : maxd;
+  double* a = (double*)malloc(sizeof(double) * (size_t)(rows * maxd > 0 ? rows * maxd : 1));
+  double* c = (double*)malloc(sizeof(double) * (size_t)(rows * maxd > 0 ? rows * maxd : 1));
+  memcpy(a, x, sizeof(double) * (size_t)(rows * dims[0]));
+  int64_t wo = 0, bo = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    mlp_layer(rows, dims[l], dims[l + 1], w + wo, b + bo, relu[l], a, c, NULL);
+    wo += dims[l] * dims[l + 1];
+    bo += dims[l + 1];
+    double* tmp = a;
+    a = c;
+    c = tmp;
+  }
+  memcpy(out, a, sizeof(double) * (size_t)(rows * dims[n_layers]));
+  free(a);
+  free(c);
+  return 0;
+}
+
+/* linalg.cpp:509-573: forward with retained activations / pre-activations, then per layer (last first):
+ * ReLU mask (pre <= 0 -> 0), db = column sums, dW = act^T delta, delta <- delta W^T */
+int or_jagged_mlp_vjp(int64_t rows, int n_layers, const int64_t* dims, const double* w, const double* b,
+                      const int* relu, const double* x, const double* grad_out, double* dx, double* dw,
+                      double* db) {
+  if (n_layers < 1) return fail("jagged_mlp: at least one layer required");
+  double** acts = (double**)malloc(sizeof(double*) * (size_t)(n_layers + 1));
+  double** pres = (double**)malloc(sizeof(double*) * (size_t)n_layers);
+  int64_t* wo = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_layers + 1));
+  int64_t* bo = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_layers + 1));
+  wo[0] = bo[0] = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    wo[l + 1] = wo[l] + dims[l] * dims[l + 1];
+    bo[l + 1] = bo[l] + dims[l + 1];
+  }
+  for (int l = 0; l <= n_layers; ++l)
+    acts[l] = (double*)malloc(sizeof(double) * (size_t)(rows * dims[l] > 0 ? rows * dims[l] : 1));
+  memcpy(acts[0], x, sizeof(double) * (size_t)(rows * dims[0]));
+  for (int l = 0; l < n_layers; ++l) {
+    pres[l] = (double*)malloc(sizeof(double) * (size_t)(rows * dims[l + 1] > 0 ? rows * dims[l + 1] : 1));
+    mlp_layer(rows, dims[l], dims[l + 1], w + wo[l], b + bo[l], relu[l], acts[l], acts[l + 1], pres[l]);
+  }
+  int64_t maxd = 0;
+  for (int l = 0; l <= n_layers; ++l) maxd = dims[l] > maxd ? dims[l] : maxd;
+  double* delta = (double*)malloc(sizeof(double) * (size_t)(rows * maxd > 0 ? rows * maxd : 1));
+  double* prev = (double*)malloc(sizeof(double) * (size_t)(rows * maxd > 0 ? rows * maxd : 1));
+  memcpy(delta, grad_out, sizeof(double) * (size_t)(rows * dims[n_layers]));
+  for (int l = n_layers - 1; l >= 0; --l) {
+    const int64_t din = dims[l], dout = dims[l + 1];
+    if (relu[l])
+      for (int64_t e = 0; e < rows * dout; ++e)
+        if (pres[l][e] <= 0.0) delta[e] = 0.0;
+    for (int64_t o = 0; o < dout; ++o) {
+      double acc = 0.0;
+      for (int64_t r = 0; r < rows; ++r) acc += delta[r * dout + o];
+      db[bo[l] + o] = acc;
+    }
+    for (int64_t i = 0; i < din; ++i)
+      for (int64_t o = 0; o < dout; ++o) {
+        double acc = 0.0;
+        for (int64_t r = 0; r < rows; ++r) acc += acts[l][r * din + i] * delta[r * dout + o];
+        dw[wo[l] + i * dout + o] = acc;
+      }
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t i = 0; i < din; ++i) {
+        double acc = 0.0;
+        for (int64_t o = 0; o < dout; ++o) acc += delta[r * dout + o] * w[wo[l] + i * dout + o];
+        prev[r * din + i] = acc;
+      }
+    double* tmp = delta;
+    delta = prev;
+    prev = tmp;
+  }
+  memcpy(dx, delta, sizeof(double) * (size_t)(rows * dims[0]));
+  for (int l = 0; l <= n_layers; ++l) free(acts[l]);
+  for (int l = 0; l < n_layers; ++l) free(pres[l]);
+  free(acts);
+  free(pres);
+  free(wo);
+  free(bo);
+  free(delta);
+  free(prev);
+  return 0;
+}

@@ -90,6 +90,22 @@ int or_jfa_backward(const int64_t* off, int64_t B, int64_t D, const double* q, c
 int or_dense_attention(const int64_t* lengths, int64_t B, int64_t L, int64_t D, const double* q,
                        const double* k, const double* v, double* out);
 
+/* ---- feature interaction (attention.cpp:291-309). targets [B, Tq, D] -> out [B, Tq, D].
+ * as_float != 0 rounds the scores to float after the 1/sqrt(D) scale and the softmax output to float, as
+ * the reference's float instantiation does between its composed operators (binary64 otherwise). */
+int or_feature_interaction(const int64_t* off, int64_t B, int64_t D, int64_t Tq, const double* k_feat,
+                           const double* v_feat, const double* targets, int as_float, double* out);
+
+/* ---- jagged MLP (linalg.cpp:224-277, VJP :509-573). Layer l maps dims[l] -> dims[l+1]
+ * with weights w + woff[l] ([dims[l], dims[l+1]] row-major), bias b + boff[l], relu[l] != 0 for ReLU.
+ * Activations stay binary64 between layers, as in the reference. */
+int or_jagged_mlp(int64_t rows, int n_layers, const int64_t* dims, const double* w, const double* b,
+                  const int* relu, const double* x, double* out);
+/* grads: dx [rows, dims[0]]; dw, db concatenated like w, b */
+int or_jagged_mlp_vjp(int64_t rows, int n_layers, const int64_t* dims, const double* w, const double* b,
+                      const int* relu, const double* x, const double* grad_out, double* dx, double* dw,
+                      double* db);
+
 /* ---- cost model (cost_model.cpp:94-189), used by bench/tests for algorithmic FLOPs/bytes ---- */
 int64_t or_sum_sq(const int64_t* off, int64_t B);
 

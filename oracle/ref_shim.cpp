@@ -196,6 +196,66 @@ extern "C" int ref_jagged2_softmax_vjp_f64(const int64_t* off, int64_t B, const 
   return guard([&] { put(jagged::jagged2_softmax_vjp(j2(off, B, s), j2(off, B, go)).values(), ds); });
 }
 
+// feature_interaction (attention.cpp:291-309) and jagged_mlp (linalg.cpp:265-277,
+// VJP :509-573) through the reference's own templates. MLP layers come in as dims[n+1], concatenated
+// row-major weights and biases, and relu flags.
+namespace {
+template <typename T>
+std::vector<jagged::MlpLayer<T>> mlp_layers(int n, const int64_t* dims, const T* w, const T* b, const int* relu) {
+  std::vector<jagged::MlpLayer<T>> layers;
+  int64_t wo = 0, bo = 0;
+  for (int l = 0; l < n; ++l) {
+    jagged::MlpLayer<T> L{jagged::DenseTensor<T>({dims[l], dims[l + 1]}, vec(w + wo, dims[l] * dims[l + 1])),
+                          vec(b + bo, dims[l + 1]), relu[l] ? jagged::Activation::relu : jagged::Activation::none};
+    layers.push_back(std::move(L));
+    wo += dims[l] * dims[l + 1];
+    bo += dims[l + 1];
+  }
+  return layers;
+}
+}  // namespace
+
+#define REF_FI_MLP(T, SUF)                                                                              \
+  extern "C" int ref_feature_interaction_##SUF(const int64_t* off, int64_t B, int64_t D, int64_t Tq,   \
+                                                const T* k, const T* v, const T* tg, T* out) {          \
+    return guard([&] {                                                                                  \
+      auto r = jagged::feature_interaction(jt(off, B, D, k), jt(off, B, D, v),                          \
+                                           jagged::DenseTensor<T>({B, Tq, D}, vec(tg, B * Tq * D)),     \
+                                           kopts(1, 64));                                               \
+      put(r.data(), out);                                                                               \
+    });                                                                                                 \
+  }                                                                                                     \
+  extern "C" int ref_jagged_mlp_##SUF(int64_t rows, int n, const int64_t* dims, const T* w, const T* b, \
+                                      const int* relu, const T* x, T* out) {                            \
+    return guard([&] {                                                                                  \
+      const int64_t off[2] = {0, rows};                                                                 \
+      auto layers = mlp_layers<T>(n, dims, w, b, relu);                                                 \
+      auto r = jagged::jagged_mlp(jt(off, 1, dims[0], x), std::span<const jagged::MlpLayer<T>>(layers)); \
+      put(r.values(), out);                                                                             \
+    });                                                                                                 \
+  }
+REF_FI_MLP(double, f64)
+REF_FI_MLP(float, f32)
+
+extern "C" int ref_jagged_mlp_vjp_f64(int64_t rows, int n, const int64_t* dims, const double* w, const double* b,
+                                      const int* relu, const double* x, const double* go, double* dx, double* dw,
+                                      double* db) {
+  return guard([&] {
+    const int64_t off[2] = {0, rows};
+    auto layers = mlp_layers<double>(n, dims, w, b, relu);
+    auto g = jagged::jagged_mlp_vjp(jt(off, 1, dims[0], x), std::span<const jagged::MlpLayer<double>>(layers),
+                                    jt(off, 1, dims[n], go));
+    put(g.dx.values(), dx);
+    int64_t wo = 0, bo = 0;
+    for (int l = 0; l < n; ++l) {
+      put(g.dlayers[l].dweights.data(), dw + wo);
+      put(g.dlayers[l].dbias, db + bo);
+      wo += dims[l] * dims[l + 1];
+      bo += dims[l + 1];
+    }
+  });
+}
+
 // Reference generators (rng.cpp) so the oracle's restated RNG can be pinned bit-exactly.
 extern "C" int ref_gen_lengths(int kind, int64_t max_len, uint64_t seed, int64_t batch,
                                int64_t* out) {

@@ -219,3 +219,48 @@ def jagged2_softmax_vjp(off, s, go):
     ds = np.empty_like(s)
     _chk(lib().ref_jagged2_softmax_vjp_f64(_p(off), _I(len(off) - 1), _p(s), _p(go), _p(ds)))
     return ds
+
+
+def feature_interaction(off, k_feat, v_feat, targets, prec="f64"):
+    """attention.cpp:291-309 through the compiled reference."""
+    dt = _DT[prec]
+    off, k_feat, v_feat, targets = _arr(off, np.int64), _arr(k_feat, dt), _arr(v_feat, dt), _arr(targets, dt)
+    B, Tq, D = targets.shape
+    out = np.empty((B, Tq, D), dt)
+    _chk(getattr(lib(), f"ref_feature_interaction_{prec}")(_p(off), _I(B), _I(D), _I(Tq), _p(k_feat), _p(v_feat),
+                                                           _p(targets), _p(out)))
+    return out
+
+
+def _mlp_pack(layers, dt):
+    dims = np.array([layers[0][0].shape[0]] + [w.shape[1] for w, _, _ in layers], np.int64)
+    w = np.ascontiguousarray(np.concatenate([np.asarray(w, dt).reshape(-1) for w, _, _ in layers]))
+    b = np.ascontiguousarray(np.concatenate([np.asarray(b, dt).reshape(-1) for _, b, _ in layers]))
+    relu = np.array([1 if r else 0 for _, _, r in layers], np.int32)
+    return dims, w, b, relu
+
+
+def jagged_mlp(x, layers, prec="f64"):
+    """linalg.cpp:265-277; layers = [(W [d_in, d_out], bias [d_out], relu)]."""
+    dt = _DT[prec]
+    x = _arr(x, dt)
+    dims, w, b, relu = _mlp_pack(layers, dt)
+    out = np.empty((x.shape[0], int(dims[-1])), dt)
+    _chk(getattr(lib(), f"ref_jagged_mlp_{prec}")(_I(x.shape[0]), C.c_int(len(layers)), _p(dims), _p(w), _p(b),
+                                                  _p(relu), _p(x), _p(out)))
+    return out
+
+
+def jagged_mlp_vjp(x, layers, go):
+    """linalg.cpp:509-573 (binary64 instantiation, the one the reference's callers import)."""
+    x, go = _arr(x, np.float64), _arr(go, np.float64)
+    dims, w, b, relu = _mlp_pack(layers, np.float64)
+    dx, dw, db = np.empty_like(x), np.empty_like(w), np.empty_like(b)
+    _chk(lib().ref_jagged_mlp_vjp_f64(_I(x.shape[0]), C.c_int(len(layers)), _p(dims), _p(w), _p(b), _p(relu),
+                                      _p(x), _p(go), _p(dx), _p(dw), _p(db)))
+    grads, wo, bo = [], 0, 0
+    for l in range(len(layers)):
+        di, do = int(dims[l]), int(dims[l + 1])
+        grads.append((dw[wo:wo + di * do].reshape(di, do), db[bo:bo + do].copy()))
+        wo, bo = wo + di * do, bo + do
+    return dx, grads

@@ -58,6 +58,10 @@ def lib():
             "or_jfa_backward": [_i64p, _I64, _I64, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, _I64,
                                 _f64p, _f64p, _f64p],
             "or_dense_attention": [_i64p, _I64, _I64, _I64, _f64p, _f64p, _f64p, _f64p],
+            "or_feature_interaction": [_i64p, _I64, _I64, _I64, _f64p, _f64p, _f64p, C.c_int, _f64p],
+            "or_jagged_mlp": [_I64, C.c_int, _i64p, _f64p, _f64p, C.POINTER(C.c_int), _f64p, _f64p],
+            "or_jagged_mlp_vjp": [_I64, C.c_int, _i64p, _f64p, _f64p, C.POINTER(C.c_int), _f64p, _f64p,
+                                  _f64p, _f64p, _f64p],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -300,3 +304,47 @@ def dense_attention(lengths, q, k, v):
     out = np.empty_like(q)
     _chk(lib().or_dense_attention(lengths, B, L, D, q.reshape(-1), k.reshape(-1), v.reshape(-1), out.reshape(-1)))
     return out
+
+
+def feature_interaction(off, k_feat, v_feat, targets, as_float=False):
+    """attention.cpp:291-309 -> [B, Tq, D] (jagged_oracle.c or_feature_interaction)."""
+    off, k_feat, v_feat, targets = _i64(off), _f64(k_feat), _f64(v_feat), _f64(targets)
+    B, Tq, D = targets.shape
+    out = np.zeros((B, Tq, D), np.float64)
+    _chk(lib().or_feature_interaction(off, B, D, Tq, k_feat.reshape(-1), v_feat.reshape(-1), targets.reshape(-1),
+                                      1 if as_float else 0, out.reshape(-1)))
+    return out
+
+
+def _mlp_pack(layers):
+    """layers: [(W [d_in, d_out], b [d_out], relu bool)] -> (dims, w, b, relu) flat arrays."""
+    dims = np.array([layers[0][0].shape[0]] + [w.shape[1] for w, _, _ in layers], np.int64)
+    w = np.concatenate([_f64(w).reshape(-1) for w, _, _ in layers])
+    b = np.concatenate([_f64(b).reshape(-1) for _, b, _ in layers])
+    relu = (C.c_int * len(layers))(*[1 if r else 0 for _, _, r in layers])
+    return dims, w, b, relu
+
+
+def jagged_mlp(x, layers):
+    """linalg.cpp:265-277 (activations in binary64 between layers)."""
+    x = _f64(x)
+    dims, w, b, relu = _mlp_pack(layers)
+    out = np.empty((x.shape[0], int(dims[-1])), np.float64)
+    _chk(lib().or_jagged_mlp(x.shape[0], len(layers), dims, w, b, relu, x.reshape(-1), out.reshape(-1)))
+    return out
+
+
+def jagged_mlp_vjp(x, layers, go):
+    """linalg.cpp:509-573 -> (dx, [(dW, db) per layer])."""
+    x, go = _f64(x), _f64(go)
+    dims, w, b, relu = _mlp_pack(layers)
+    dx = np.empty_like(x)
+    dw, db = np.empty_like(w), np.empty_like(b)
+    _chk(lib().or_jagged_mlp_vjp(x.shape[0], len(layers), dims, w, b, relu, x.reshape(-1), go.reshape(-1),
+                                 dx.reshape(-1), dw, db))
+    grads, wo, bo = [], 0, 0
+    for l in range(len(layers)):
+        di, do = int(dims[l]), int(dims[l + 1])
+        grads.append((dw[wo:wo + di * do].reshape(di, do), db[bo:bo + do].copy()))
+        wo, bo = wo + di * do, bo + do
+    return dx, grads

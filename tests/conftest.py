@@ -17,4 +17,4 @@ def golden():
     import numpy as np
 
     g = os.path.join(ROOT, "tests", "golden")
-    return {n: dict(np.load(os.path.join(g, n + ".npz"))) for n in ("kat", "ops", "attention", "lengths")}
+    return {n: dict(np.load(os.path.join(g, n + ".npz"))) for n in ("kat", "ops", "attention", "lengths", "next")}

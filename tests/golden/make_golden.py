@@ -12,6 +12,8 @@ Contents
   attention.npz  jagged_attention (unfused) + jagged_flash_attention fwd/bwd at blocks (3,3) and
                  (64,64) on lengths {0,1,2,5,7,17,33,70,130,257}, D=16, binary64 (attention.cpp:162-289).
   lengths.npz    gen_lengths outputs for the BASELINE configs (rng.cpp:35-57), for bit-exact checks.
+  next.npz       SURVEY §8f-1 feature_interaction (attention.cpp:291-309; f64 and f32) and §8f-2
+                 jagged_mlp forward (f64, f32) + VJP (f64) (linalg.cpp:265-277, :509-573).
 """
 from __future__ import annotations
 
@@ -107,6 +109,40 @@ def main() -> None:
     ln["uniform_B33_L50_s9"] = F.gen_lengths("uniform", 50, 9, 33)
     ln["halfmean_B33_L50_s9"] = F.gen_lengths("half-mean", 50, 9, 33)
     np.savez_compressed(os.path.join(HERE, "lengths.npz"), **ln)
+
+    # ---------------------------------------------------------------- §8f next rows
+    nx = {}
+    lens = np.array([0, 1, 2, 5, 7, 17, 33, 70], np.int64)
+    off = F.make_offsets(lens)
+    S, D, Tq = int(off[-1]), 16, 3
+    vals = F.uniform_values(11, 2 * S * D + len(lens) * Tq * D)
+    kf, vf = vals[:S * D].reshape(S, D), vals[S * D:2 * S * D].reshape(S, D)
+    tg = vals[2 * S * D:].reshape(len(lens), Tq, D)
+    nx["fi_off"], nx["fi_k"], nx["fi_v"], nx["fi_targets"] = off, kf, vf, tg
+    nx["fi_out_f64"] = F.feature_interaction(off, kf, vf, tg)
+    nx["fi_out_f32"] = F.feature_interaction(off, kf.astype(np.float32), vf.astype(np.float32),
+                                             tg.astype(np.float32), prec="f32")
+    rows, dims = 37, [16, 24, 8]
+    mv = F.uniform_values(12, rows * dims[0] + dims[0] * dims[1] + dims[1] + dims[1] * dims[2] + dims[2] + rows * dims[2])
+    c = 0
+
+    def take(n):
+        nonlocal c
+        c += n
+        return mv[c - n:c]
+
+    x = take(rows * dims[0]).reshape(rows, dims[0])
+    w0, b0 = take(dims[0] * dims[1]).reshape(dims[0], dims[1]), take(dims[1])
+    w1, b1 = take(dims[1] * dims[2]).reshape(dims[1], dims[2]), take(dims[2])
+    go = take(rows * dims[2]).reshape(rows, dims[2])
+    layers = [(w0, b0, True), (w1, b1, False)]
+    nx["mlp_x"], nx["mlp_w0"], nx["mlp_b0"], nx["mlp_w1"], nx["mlp_b1"], nx["mlp_go"] = x, w0, b0, w1, b1, go
+    nx["mlp_out_f64"] = F.jagged_mlp(x, layers)
+    nx["mlp_out_f32"] = F.jagged_mlp(x.astype(np.float32), [(w.astype(np.float32), b.astype(np.float32), r)
+                                                            for w, b, r in layers], prec="f32")
+    dx, g = F.jagged_mlp_vjp(x, layers, go)
+    nx["mlp_dx"], nx["mlp_dw0"], nx["mlp_db0"], nx["mlp_dw1"], nx["mlp_db1"] = dx, g[0][0], g[0][1], g[1][0], g[1][1]
+    np.savez_compressed(os.path.join(HERE, "next.npz"), **nx)
     print("wrote", sorted(os.listdir(HERE)))
 
 

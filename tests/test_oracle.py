@@ -150,3 +150,52 @@ def test_live_reference_random_shapes():
         for a_, b_ in zip(g1, g2):
             np.testing.assert_allclose(a_, b_, **EXACT)
         np.testing.assert_allclose(R.jagged_softmax(off, q), F.jagged_softmax(off, q), **EXACT)
+
+
+def _mlp_layers(nx):
+    return [(nx["mlp_w0"], nx["mlp_b0"], True), (nx["mlp_w1"], nx["mlp_b1"], False)]
+
+
+def test_next_rows_vs_reference_golden(golden):
+    """SURVEY §8f-1 feature_interaction and §8f-2 jagged_mlp (+VJP): oracle vs the reference's outputs."""
+    nx = golden["next"]
+    fi = R.feature_interaction(nx["fi_off"], nx["fi_k"], nx["fi_v"], nx["fi_targets"])
+    np.testing.assert_allclose(fi, nx["fi_out_f64"], rtol=1e-12, atol=1e-14)
+    # float instantiation: the oracle's as_float mode rounds where the reference's composed ops do
+    fi32 = R.feature_interaction(nx["fi_off"], nx["fi_k"].astype(np.float32), nx["fi_v"].astype(np.float32),
+                                 nx["fi_targets"].astype(np.float32), as_float=True)
+    np.testing.assert_allclose(fi32, nx["fi_out_f32"], rtol=2e-6, atol=1e-7)
+    layers = _mlp_layers(nx)
+    np.testing.assert_allclose(R.jagged_mlp(nx["mlp_x"], layers), nx["mlp_out_f64"], rtol=1e-12, atol=1e-13)
+    dx, g = R.jagged_mlp_vjp(nx["mlp_x"], layers, nx["mlp_go"])
+    np.testing.assert_allclose(dx, nx["mlp_dx"], rtol=1e-12, atol=1e-13)
+    for l, (dw, db) in enumerate(g):
+        np.testing.assert_allclose(dw, nx[f"mlp_dw{l}"], rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(db, nx[f"mlp_db{l}"], rtol=1e-12, atol=1e-13)
+    with pytest.raises(R.OracleError, match="at least one layer"):
+        R._chk(R.lib().or_jagged_mlp(1, 0, np.zeros(1, np.int64), np.zeros(1), np.zeros(1), None, np.zeros(1),
+                                     np.zeros(1)))
+
+
+@pytest.mark.skipif(not F.available(), reason="oracle/_ref not built")
+def test_next_rows_live_reference():
+    rng = np.random.default_rng(5)
+    for lens, D, Tq in (([3, 0, 9, 1], 8, 5), ([40, 2, 0, 17, 63], 32, 2)):
+        off = F.make_offsets(lens)
+        S = int(off[-1])
+        k, v = rng.uniform(-1, 1, (S, D)), rng.uniform(-1, 1, (S, D))
+        tg = rng.uniform(-1, 1, (len(lens), Tq, D))
+        np.testing.assert_allclose(R.feature_interaction(off, k, v, tg), F.feature_interaction(off, k, v, tg),
+                                   rtol=1e-12, atol=1e-14)
+    rows, dims = 19, [5, 7, 3, 4]
+    x = rng.uniform(-1, 1, (rows, dims[0]))
+    layers = [(rng.uniform(-1, 1, (dims[l], dims[l + 1])), rng.uniform(-1, 1, dims[l + 1]), l % 2 == 0)
+              for l in range(3)]
+    go = rng.uniform(-1, 1, (rows, dims[-1]))
+    np.testing.assert_allclose(R.jagged_mlp(x, layers), F.jagged_mlp(x, layers), rtol=1e-12, atol=1e-13)
+    dx, g = R.jagged_mlp_vjp(x, layers, go)
+    rdx, rg = F.jagged_mlp_vjp(x, layers, go)
+    np.testing.assert_allclose(dx, rdx, rtol=1e-12, atol=1e-13)
+    for (a, b), (c, d) in zip(g, rg):
+        np.testing.assert_allclose(a, c, rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(b, d, rtol=1e-12, atol=1e-13)
