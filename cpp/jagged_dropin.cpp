@@ -62,6 +62,15 @@ struct Dev {
     if (p) cudaFree(p);
   }
   Dev(Dev&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+  Dev& operator=(Dev&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+    }
+    return *this;
+  }
   Dev(const Dev&) = delete;
 };
 
@@ -181,9 +190,42 @@ Jagged2Tensor<T> jagged2_softmax(const Jagged2Tensor<T>& s, const KernelOptions&
   return Jagged2Tensor<T>(s.seq_lengths(), out.to<T>(s.values().size(), op));
 }
 
+// linalg.cpp:224-243 validation (same messages)
 template <typename T>
-JaggedTensor<T> jagged_mlp(const JaggedTensor<T>&, std::span<const MlpLayer<T>>, const KernelOptions&) {
-  no_device_path<T>("jagged_mlp");
+void validate_mlp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers) {
+  if (layers.empty()) throw std::invalid_argument("jagged_mlp: at least one layer required");
+  int64_t cur = x.dim();
+  for (size_t l = 0; l < layers.size(); ++l) {
+    const auto& w = layers[l].weights;
+    if (w.rank() != 2)
+      throw std::invalid_argument("jagged_mlp: layer " + std::to_string(l) + " weights must be rank 2");
+    if (w.shape()[0] != cur)
+      throw std::invalid_argument("jagged_mlp: layer " + std::to_string(l) + " input dim mismatch (" +
+                                  std::to_string(cur) + " vs " + std::to_string(w.shape()[0]) + ")");
+    if (static_cast<int64_t>(layers[l].bias.size()) != w.shape()[1])
+      throw std::invalid_argument("jagged_mlp: layer " + std::to_string(l) + " bias size " +
+                                  std::to_string(layers[l].bias.size()) + " != " + std::to_string(w.shape()[1]));
+    cur = w.shape()[1];
+  }
+}
+
+// linalg.cpp:265-277 via jg_mlp_layer_forward per layer (activations stay on the device between layers)
+template <typename T>
+JaggedTensor<T> jagged_mlp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers, const KernelOptions&) {
+  const char* op = "jagged_mlp";
+  validate_mlp(x, layers);
+  if constexpr (!is_f32<T>) no_device_path<T>(op);
+  const int64_t rows = x.total_rows();
+  Dev cur = Dev::from(x.values(), op);
+  for (const auto& L : layers) {
+    const int64_t di = L.weights.shape()[0], dout = L.weights.shape()[1];
+    Dev w = Dev::from(L.weights.data(), op), b = Dev::from(L.bias, op), out(sizeof(T) * rows * dout, op);
+    ck(op, jg_mlp_layer_forward(rows, di, dout, cur.p, w.p, b.p, L.activation == Activation::relu ? 1 : 0, out.p,
+                                nullptr, JG_F32, 0));
+    cur = std::move(out);
+  }
+  const int64_t dl = layers.back().weights.shape()[1];
+  return JaggedTensor<T>(x.offsets(), cur.to<T>(rows * dl, op), dl);
 }
 
 // ============================================================================ VJPs
@@ -284,10 +326,42 @@ Jagged2Tensor<T> jagged2_softmax_vjp(const Jagged2Tensor<T>& s, const Jagged2Ten
   return Jagged2Tensor<T>(s.seq_lengths(), ds.to<T>(s.values().size(), op));
 }
 
+// linalg.cpp:509-573: device forward keeping activations and pre-activations, then jg_mlp_layer_backward
 template <typename T>
-JaggedMlpGrads<T> jagged_mlp_vjp(const JaggedTensor<T>&, std::span<const MlpLayer<T>>, const JaggedTensor<T>&,
-                                 const KernelOptions&) {
-  no_device_path<T>("jagged_mlp_vjp");
+JaggedMlpGrads<T> jagged_mlp_vjp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers,
+                                 const JaggedTensor<T>& grad_out, const KernelOptions&) {
+  const char* op = "jagged_mlp_vjp";
+  validate_mlp(x, layers);
+  require_matching_offsets(x, grad_out, op);
+  if constexpr (!is_f32<T>) no_device_path<T>(op);
+  const int64_t rows = x.total_rows();
+  const size_t n = layers.size();
+  std::vector<Dev> acts, pres, ws;
+  acts.push_back(Dev::from(x.values(), op));
+  for (size_t l = 0; l < n; ++l) {
+    const auto& L = layers[l];
+    const int64_t di = L.weights.shape()[0], dout = L.weights.shape()[1];
+    ws.push_back(Dev::from(L.weights.data(), op));
+    Dev b = Dev::from(L.bias, op), out(sizeof(T) * rows * dout, op), pre(sizeof(T) * rows * dout, op);
+    ck(op, jg_mlp_layer_forward(rows, di, dout, acts.back().p, ws.back().p, b.p,
+                                L.activation == Activation::relu ? 1 : 0, out.p, pre.p, JG_F32, 0));
+    acts.push_back(std::move(out));
+    pres.push_back(std::move(pre));
+  }
+  JaggedMlpGrads<T> g{JaggedTensor<T>(x.offsets(), std::vector<T>(x.values().size()), x.dim()), {}};
+  g.dlayers.resize(n, MlpLayerGrads<T>{DenseTensor<T>::zeros({1, 1}), {}});
+  Dev delta = Dev::from(grad_out.values(), op);
+  for (size_t li = n; li-- > 0;) {
+    const auto& L = layers[li];
+    const int64_t di = L.weights.shape()[0], dout = L.weights.shape()[1];
+    Dev dw(sizeof(T) * di * dout, op), db(sizeof(T) * dout, op), dx(sizeof(T) * rows * di, op);
+    ck(op, jg_mlp_layer_backward(rows, di, dout, acts[li].p, ws[li].p, pres[li].p,
+                                 L.activation == Activation::relu ? 1 : 0, delta.p, dw.p, db.p, dx.p, JG_F32, 0));
+    g.dlayers[li] = MlpLayerGrads<T>{DenseTensor<T>({di, dout}, dw.to<T>(di * dout, op)), db.to<T>(dout, op)};
+    delta = std::move(dx);
+  }
+  g.dx = JaggedTensor<T>(x.offsets(), delta.to<T>(rows * x.dim(), op), x.dim());
+  return g;
 }
 
 // ============================================================================ attention
@@ -395,9 +469,15 @@ DenseTensor<T> feature_interaction(const JaggedTensor<T>& k_feat, const JaggedTe
     throw std::invalid_argument("feature_interaction: k_feat/v_feat layout mismatch");
   if (targets.rank() != 3 || targets.shape()[0] != k_feat.batch() || targets.shape()[2] != k_feat.dim())
     throw std::invalid_argument("feature_interaction: targets must be [B, Tq, D]");
-  const T inv_sqrt_d = static_cast<T>(1.0 / std::sqrt(static_cast<double>(k_feat.dim())));
-  const JaggedTensor<T> s = scale(jagged_dense_bmm(k_feat, transpose_per_sample(targets), opts), inv_sqrt_d);
-  return jagged_jagged_bmm(jagged_softmax(s, opts), v_feat, opts);
+  (void)opts;
+  const char* op = "feature_interaction";
+  if constexpr (!is_f32<T>) no_device_path<T>(op);
+  const int64_t b = k_feat.batch(), d = k_feat.dim(), tq = targets.shape()[1];
+  Dev off = Dev::from(k_feat.offsets(), op), k = Dev::from(k_feat.values(), op), v = Dev::from(v_feat.values(), op);
+  Dev tg = Dev::from(targets.data(), op), out(sizeof(T) * b * tq * d, op);
+  ck(op, jg_feature_interaction((const int64_t*)off.p, b, k_feat.total_rows(), d, tq, k.p, v.p, tg.p, out.p, JG_F32,
+                                nullptr, 0));
+  return DenseTensor<T>({b, tq, d}, out.to<T>(b * tq * d, op));
 }
 
 // ---------------------------------------------------------------------------- instantiations

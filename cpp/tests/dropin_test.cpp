@@ -130,6 +130,40 @@ int main() {
     auto fi = feature_interaction(x, v, targets);
     check(fi.shape() == std::vector<int64_t>({B, 3, D}), "feature_interaction shape");
   }
+  // --- jagged_mlp forward + VJP (linalg.cpp:246-277, :509-573) against a host binary64 restatement
+  {
+    const int64_t H1 = 24, O = 8;
+    MlpLayer<float> l0{DenseTensor<float>({D, H1}, uniform_values<float>(rng, D * H1, -0.3, 0.3)),
+                       uniform_values<float>(rng, H1, -0.1, 0.1), Activation::relu};
+    MlpLayer<float> l1{DenseTensor<float>({H1, O}, uniform_values<float>(rng, H1 * O, -0.3, 0.3)),
+                       uniform_values<float>(rng, O, -0.1, 0.1), Activation::none};
+    std::vector<MlpLayer<float>> layers{l0, l1};
+    auto y_mlp = jagged_mlp(x, std::span<const MlpLayer<float>>(layers));
+    std::vector<double> h(S * H1), pre(S * H1), outr(S * O);
+    for (int64_t r = 0; r < S; ++r) {
+      for (int64_t o = 0; o < H1; ++o) {
+        double acc = l0.bias[o];
+        for (int64_t i = 0; i < D; ++i) acc += (double)x.row(r)[i] * l0.weights.at(i, o);
+        pre[r * H1 + o] = acc;
+        h[r * H1 + o] = acc > 0 ? acc : 0;
+      }
+      for (int64_t o = 0; o < O; ++o) {
+        double acc = l1.bias[o];
+        for (int64_t i = 0; i < H1; ++i) acc += h[r * H1 + i] * l1.weights.at(i, o);
+        outr[r * O + o] = acc;
+      }
+    }
+    check(rel(y_mlp.values(), outr) < 1e-5, "jagged_mlp rel=" + std::to_string(rel(y_mlp.values(), outr)));
+    auto gout = make_jagged<float>(lengths, uniform_values<float>(rng, S * O, -1, 1), O);
+    auto g = jagged_mlp_vjp(x, std::span<const MlpLayer<float>>(layers), gout);
+    std::vector<double> db1(O, 0.0);
+    for (int64_t r = 0; r < S; ++r)
+      for (int64_t o = 0; o < O; ++o) db1[o] += gout.row(r)[o];
+    check(rel(g.dlayers[1].dbias, db1) < 1e-5, "jagged_mlp_vjp db rel=" + std::to_string(rel(g.dlayers[1].dbias, db1)));
+    check(g.dx.dim() == D && g.dlayers[0].dweights.shape() == std::vector<int64_t>({D, H1}), "jagged_mlp_vjp shapes");
+    check(throws_with([&] { jagged_mlp(x, std::span<const MlpLayer<float>>()); }, "at least one layer required"),
+          "error: at least one layer required");
+  }
   // --- reference exception texts
   check(throws_with([&] { jagged_dense_bmm(x, DenseTensor<float>({B, D}, std::vector<float>(B * D))); },
                     "jagged_dense_bmm: w must be [B, D, T]"),

@@ -183,6 +183,30 @@ jg_status jg_jagged_attention(const int64_t* offsets, const int64_t* sq_offsets,
                               int32_t head_dim, const void* q, const void* k, const void* v,
                               void* out, jg_dtype dtype, void* scores_workspace, void* stream);
 
+/* ---------------------------------------------------------------- SURVEY §8f "next" rows */
+/* attention.hpp:97 / attention.cpp:291-309 feature_interaction: targets [B, Tq, D] attend over each
+ * sample's jagged rows: out[i] = softmax_rows(K_i targets_i^T / sqrt(D))^T V_i, [B, Tq, D] (zeros for
+ * empty samples). Scores and weights are kept in fp32 for both dtypes (the reference's float
+ * instantiation rounds them to float). workspace: NULL or >= jg_feature_interaction_workspace_size()
+ * bytes. Errors as the reference: "feature_interaction: targets must be [B, Tq, D]". */
+int64_t jg_feature_interaction_workspace_size(int64_t total_rows, int64_t num_targets);
+jg_status jg_feature_interaction(const int64_t* offsets, int64_t batch, int64_t total_rows, int64_t dim,
+                                 int64_t num_targets, const void* k_feat, const void* v_feat,
+                                 const void* targets, void* out, jg_dtype dtype, void* workspace,
+                                 void* stream);
+/* linalg.hpp:59-68 / linalg.cpp:246-277 jagged_mlp, one layer: out[r] = act(x[r] W + bias) over all
+ * rows (weights shared across samples, no padding rows). W [d_in, d_out], bias [d_out]; relu != 0 for
+ * Activation::relu. preact: NULL or [rows, d_out] pre-activations (kept for the VJP). */
+jg_status jg_mlp_layer_forward(int64_t rows, int64_t d_in, int64_t d_out, const void* x, const void* w,
+                               const void* bias, int32_t relu, void* out, void* preact, jg_dtype dtype,
+                               void* stream);
+/* linalg.cpp:526-567 one layer of jagged_mlp_vjp: delta = grad_out masked by preact <= 0 (relu),
+ * db = column sums of delta, dW = x^T delta, dx = delta W^T. Any of dw/db/dx may be NULL.
+ * Under sample sharding dW/db are partial sums: all-reduce them across ranks. */
+jg_status jg_mlp_layer_backward(int64_t rows, int64_t d_in, int64_t d_out, const void* x, const void* w,
+                                const void* preact, int32_t relu, const void* grad_out, void* dw,
+                                void* db, void* dx, jg_dtype dtype, void* stream);
+
 /* Host-buffer convenience (what the reference API's by-value std::vector contract implies):
  * copies host q/k/v/grad_out in, runs forward + backward, copies out/lse/dq/dk/dv back.
  * Host pointers should be pinned for full PCIe bandwidth. offsets is a HOST array here. */

@@ -48,6 +48,9 @@ SIGNATURES = {
                                            P, P],
     "jg_jagged_attention": [P, P, I64, I64, I64, I32, I32, P, P, P, P, C.c_int, P, P],
     "jg_jagged_flash_attention_fwd_bwd_host": [P, I64, I32, I32, P, P, P, P, P, P, P, P, P, C.c_int, P],
+    "jg_feature_interaction": [P, I64, I64, I64, I64, P, P, P, P, C.c_int, P, P],
+    "jg_mlp_layer_forward": [I64, I64, I64, P, P, P, I32, P, P, C.c_int, P],
+    "jg_mlp_layer_backward": [I64, I64, I64, P, P, P, I32, P, P, P, P, C.c_int, P],
 }
 OTHER = {
     "jg_last_error": ([], C.c_char_p),
@@ -56,6 +59,7 @@ OTHER = {
     "jg_reset_launch_count": ([], None),
     "jg_schedule_sq_offsets": ([P], P),
     "jg_attention_backward_workspace_size": ([I64, I32, I32], C.c_int64),
+    "jg_feature_interaction_workspace_size": ([I64, I64], C.c_int64),
 }
 
 

@@ -567,3 +567,105 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   jg_schedule_destroy(sched);
   return rc;
 }
+
+// ============================================================================ SURVEY §8f next rows
+extern "C" int64_t jg_feature_interaction_workspace_size(int64_t total_rows, int64_t num_targets) {
+  const int64_t n = total_rows * num_targets;
+  return 2 * ((n * 4 + 255) / 256) * 256 + ((n * 2 + 255) / 256) * 256;
+}
+
+// attention.cpp:291-309: s = jdbmm(k, targets^T) (fp32 out), scale, jagged_softmax over rows, jjbmm(p, v)
+extern "C" jg_status jg_feature_interaction(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D,
+                                            int64_t Tq, const void* k_feat, const void* v_feat, const void* targets,
+                                            void* out, jg_dtype dtype, void* workspace, void* stream) {
+  CHECK_DT("feature_interaction", dtype);
+  REQUIRE(D >= 1 && Tq >= 1, JG_INVALID_ARGUMENT, "feature_interaction: targets must be [B, Tq, D]");
+  cudaStream_t st = as_stream(stream);
+  if (batch == 0) return JG_OK;
+  const int64_t n = total_rows * Tq;
+  Scratch ws(st);
+  if (!workspace) {
+    if (jg_status rc = ws.alloc(std::max<int64_t>(256, jg_feature_interaction_workspace_size(total_rows, Tq)))) return rc;
+    workspace = ws.p;
+  }
+  float* s = (float*)workspace;
+  float* pr = (float*)((char*)workspace + ((n * 4 + 255) / 256) * 256);
+  void* p16 = (char*)pr + ((n * 4 + 255) / 256) * 256;
+  // scores: M = Bi rows, N = Tq, K = D; B(d, t) = targets[i, t, d] (transpose_per_sample folded into strides)
+  GemmDesc gs = desc(BI(), C_(Tq), C_(D), OFF(D), C_(D), C_(1), IDX(Tq * D), C_(1), C_(D), OFF(Tq), C_(Tq), C_(1));
+  if (jg_status rc = gemm(gs, off, nullptr, batch, k_feat, targets, s, dtype, JG_F32, st)) return rc;
+  // scale by 1/sqrt(D) rounded to float (the reference's T(1/sqrt(d)), attention.cpp:300)
+  if (jg_status rc = launch_elementwise(3, s, nullptr, n, (double)(float)(1.0 / std::sqrt((double)D)), s, JG_F32, st))
+    return rc;
+  if (jg_status rc = launch_jagged_softmax(off, batch, Tq, s, nullptr, pr, JG_F32, false, st)) return rc;
+  // out_i = P_i^T V_i: M = Tq, N = D, K = Bi
+  GemmDesc gz = desc(C_(Tq), C_(D), BI(), OFF(Tq), C_(1), C_(Tq), OFF(D), C_(D), C_(1), IDX(Tq * D), C_(D), C_(1));
+  if (dtype == JG_F32) return gemm(gz, off, nullptr, batch, pr, v_feat, out, JG_F32, JG_F32, st);
+  if (jg_status rc = launch_cast_f32(pr, n, p16, JG_BF16, st)) return rc;
+  if (!force_simt_gemm() && gemm_sm100_supported(2, Tq, D, JG_BF16))
+    return tc_gemm(2, off, nullptr, batch, total_rows, Tq, D, p16, v_feat, out, JG_BF16, st);
+  return gemm(gz, off, nullptr, batch, p16, v_feat, out, JG_BF16, JG_BF16, st);
+}
+
+// linalg.cpp:246-261 one affine layer over all rows: fp32 accumulation, bias + activation epilogue
+extern "C" jg_status jg_mlp_layer_forward(int64_t rows, int64_t d_in, int64_t d_out, const void* x, const void* w,
+                                          const void* bias, int32_t relu, void* out, void* preact, jg_dtype dtype,
+                                          void* stream) {
+  CHECK_DT("jagged_mlp", dtype);
+  REQUIRE(d_in >= 1 && d_out >= 1, JG_INVALID_ARGUMENT, "jagged_mlp: layer dims must be positive");
+  cudaStream_t st = as_stream(stream);
+  if (rows == 0) return JG_OK;
+  Scratch sc(st);
+  if (jg_status rc = sc.alloc(256 + rows * d_out * 4)) return rc;
+  int64_t* off = (int64_t*)sc.p;
+  float* acc = (float*)((char*)sc.p + 256);
+  if (jg_status rc = launch_two_offsets(off, rows, st)) return rc;
+  if (!force_simt_gemm() && gemm_sm100_supported(3, d_in, d_out, dtype)) {
+    if (jg_status rc = tc_gemm(3, off, nullptr, 1, rows, d_in, d_out, x, w, acc, JG_F32, st)) return rc;
+  } else {
+    GemmDesc g = desc(BI(), C_(d_out), C_(d_in), C_(0), C_(d_in), C_(1), C_(0), C_(d_out), C_(1), C_(0), C_(d_out),
+                      C_(1));
+    if (jg_status rc = gemm(g, off, nullptr, 1, x, w, acc, dtype, JG_F32, st)) return rc;
+  }
+  return launch_bias_act(acc, bias, rows, d_out, relu, out, preact, dtype, st);
+}
+
+// linalg.cpp:526-567 one layer of the VJP
+extern "C" jg_status jg_mlp_layer_backward(int64_t rows, int64_t d_in, int64_t d_out, const void* x, const void* w,
+                                           const void* preact, int32_t relu, const void* grad_out, void* dw, void* db,
+                                           void* dx, jg_dtype dtype, void* stream) {
+  CHECK_DT("jagged_mlp_vjp", dtype);
+  REQUIRE(d_in >= 1 && d_out >= 1, JG_INVALID_ARGUMENT, "jagged_mlp_vjp: layer dims must be positive");
+  REQUIRE(!relu || preact || rows == 0, JG_INVALID_ARGUMENT, "jagged_mlp_vjp: relu layers need their pre-activations");
+  cudaStream_t st = as_stream(stream);
+  const size_t es = dsize(dtype);
+  const int64_t part = colsum_scratch_floats(rows, d_out);
+  Scratch sc(st);
+  if (jg_status rc = sc.alloc(256 + ((rows * d_out * es + 255) / 256) * 256 + part * 4 + 256)) return rc;
+  int64_t* off = (int64_t*)sc.p;
+  void* delta = (char*)sc.p + 256;
+  float* partial = (float*)((char*)delta + ((rows * d_out * es + 255) / 256) * 256);
+  if (jg_status rc = launch_two_offsets(off, rows, st)) return rc;
+  if (jg_status rc = launch_relu_mask(grad_out, preact, rows * d_out, relu, delta, dtype, st)) return rc;
+  if (db)
+    if (jg_status rc = launch_colsum(delta, rows, d_out, db, partial, dtype, st)) return rc;
+  if (dw) {  // dW = x^T delta: a one-segment jagged_jagged_bmm
+    if (!force_simt_gemm() && gemm_sm100_supported(2, d_in, d_out, dtype)) {
+      if (jg_status rc = tc_gemm(2, off, nullptr, 1, rows, d_in, d_out, x, delta, dw, dtype, st)) return rc;
+    } else {
+      GemmDesc g = desc(C_(d_in), C_(d_out), BI(), C_(0), C_(1), C_(d_in), C_(0), C_(d_out), C_(1), C_(0), C_(d_out),
+                        C_(1));
+      if (rows == 0) {
+        JG_CUDA(cudaMemsetAsync(dw, 0, d_in * d_out * es, st));
+      } else if (jg_status rc = gemm(g, off, nullptr, 1, x, delta, dw, dtype, dtype, st)) {
+        return rc;
+      }
+    }
+  }
+  if (dx && rows > 0) {  // dx = delta W^T: B(k = o, n = i) = W[i, o]
+    GemmDesc g = desc(BI(), C_(d_in), C_(d_out), C_(0), C_(d_out), C_(1), C_(0), C_(1), C_(d_out), C_(0), C_(d_in),
+                      C_(1));
+    if (jg_status rc = gemm(g, off, nullptr, 1, delta, w, dx, dtype, dtype, st)) return rc;
+  }
+  return JG_OK;
+}

@@ -66,6 +66,17 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
                             cudaStream_t st);
 
+// SURVEY §8f next rows (mlp_fi.cu)
+jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st);
+jg_status launch_bias_act(const float* acc, const void* bias, int64_t rows, int64_t d, int relu, void* out,
+                          void* preact, jg_dtype dt, cudaStream_t st);
+jg_status launch_relu_mask(const void* g, const void* preact, int64_t n, int relu, void* out, jg_dtype dt,
+                           cudaStream_t st);
+int64_t colsum_scratch_floats(int64_t rows, int64_t cols);
+jg_status launch_colsum(const void* x, int64_t rows, int64_t cols, void* out, float* partial, jg_dtype dt,
+                        cudaStream_t st);
+jg_status launch_cast_f32(const float* a, int64_t n, void* out, jg_dtype dt, cudaStream_t st);
+
 // SIMT attention (fp32 mode, and any head_dim the tensor-core path does not cover)
 jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, void* out, float* lse,

@@ -473,3 +473,106 @@ def scale(a, s: float):
     if isinstance(a, Jagged2Tensor):
         return Jagged2Tensor(a.offsets, out, a.host_offsets, a.sq_offsets)
     return a.with_values(out)
+
+
+# ---------------------------------------------------------------------------- SURVEY §8f "next" rows
+def feature_interaction(k_feat: JaggedTensor, v_feat: JaggedTensor, targets: torch.Tensor) -> torch.Tensor:
+    """attention.hpp:97 / attention.cpp:291-309: [B, Tq, D] targets attend over each sample's rows.
+
+    out[i] = softmax over rows(K_i targets_i^T / sqrt(D))^T V_i; empty samples give zeros.
+    """
+    if not (k_feat.same_offsets(v_feat) and k_feat.dim == v_feat.dim):
+        raise JaggedError("feature_interaction: k_feat/v_feat layout mismatch")
+    if targets.dim() != 3 or targets.shape[0] != k_feat.batch or targets.shape[2] != k_feat.dim:
+        raise JaggedError("feature_interaction: targets must be [B, Tq, D]")
+    targets = targets.contiguous().to(k_feat.values.dtype)
+    out = torch.zeros(k_feat.batch, targets.shape[1], k_feat.dim, dtype=k_feat.values.dtype,
+                      device=k_feat.values.device)
+    check(_lib.lib().jg_feature_interaction(_p(k_feat.offsets), k_feat.batch, k_feat.total_rows, k_feat.dim,
+                                            targets.shape[1], _p(k_feat.values), _p(v_feat.values), _p(targets),
+                                            _p(out), _dt(k_feat.values), None, _stream()))
+    return out
+
+
+RELU, NONE = "relu", "none"
+
+
+@dataclass
+class MlpLayer:
+    """linalg.hpp:59-63: weights [D_in, D_out] shared across samples, bias [D_out], activation."""
+    weights: torch.Tensor
+    bias: torch.Tensor
+    activation: str = NONE
+
+
+@dataclass
+class MlpLayerGrads:
+    dweights: torch.Tensor
+    dbias: torch.Tensor
+
+
+@dataclass
+class JaggedMlpGrads:
+    dx: JaggedTensor
+    dlayers: list
+
+
+def _validate_mlp(x: JaggedTensor, layers) -> None:
+    """linalg.cpp:224-243 (same messages)."""
+    if not layers:
+        raise JaggedError("jagged_mlp: at least one layer required")
+    cur = x.dim
+    for l, L in enumerate(layers):
+        w = L.weights
+        if w.dim() != 2:
+            raise JaggedError(f"jagged_mlp: layer {l} weights must be rank 2")
+        if w.shape[0] != cur:
+            raise JaggedError(f"jagged_mlp: layer {l} input dim mismatch ({cur} vs {w.shape[0]})")
+        if L.bias.numel() != w.shape[1]:
+            raise JaggedError(f"jagged_mlp: layer {l} bias size {L.bias.numel()} != {w.shape[1]}")
+        cur = w.shape[1]
+
+
+def _mlp_forward(x: JaggedTensor, layers, keep: bool):
+    acts, pres = [x.values], []
+    cur = x.values
+    for L in layers:
+        w = L.weights.contiguous().to(cur.dtype)
+        b = L.bias.contiguous().to(cur.dtype)
+        out = torch.empty(cur.shape[0], w.shape[1], dtype=cur.dtype, device=cur.device)
+        pre = torch.empty_like(out) if keep else None
+        check(_lib.lib().jg_mlp_layer_forward(cur.shape[0], w.shape[0], w.shape[1], _p(cur), _p(w), _p(b),
+                                              1 if L.activation == RELU else 0, _p(out), _p(pre) if keep else None,
+                                              _dt(cur), _stream()))
+        cur = out
+        acts.append(out)
+        pres.append(pre)
+    return acts, pres
+
+
+def jagged_mlp(x: JaggedTensor, layers) -> JaggedTensor:
+    """linalg.cpp:265-277: row-wise affine + activation chain (shared weights, no padding rows)."""
+    _validate_mlp(x, layers)
+    acts, _ = _mlp_forward(x, layers, keep=False)
+    return x.with_values(acts[-1])
+
+
+def jagged_mlp_vjp(x: JaggedTensor, layers, grad_out: JaggedTensor) -> JaggedMlpGrads:
+    """linalg.cpp:509-573: recomputes the forward, then per layer (last first) mask, db, dW, dx."""
+    _validate_mlp(x, layers)
+    _require_matching_offsets(x, grad_out, "jagged_mlp_vjp")
+    acts, pres = _mlp_forward(x, layers, keep=True)
+    delta = grad_out.values.contiguous().to(x.values.dtype)
+    dl = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        L = layers[l]
+        w = L.weights.contiguous().to(x.values.dtype)
+        dw = torch.empty_like(w)
+        db = torch.empty(w.shape[1], dtype=w.dtype, device=w.device)
+        dx = torch.empty(delta.shape[0], w.shape[0], dtype=delta.dtype, device=delta.device)
+        check(_lib.lib().jg_mlp_layer_backward(delta.shape[0], w.shape[0], w.shape[1], _p(acts[l]), _p(w),
+                                               _p(pres[l]), 1 if L.activation == RELU else 0, _p(delta), _p(dw),
+                                               _p(db), _p(dx), _dt(delta), _stream()))
+        dl[l] = MlpLayerGrads(dw, db)
+        delta = dx
+    return JaggedMlpGrads(x.with_values(delta), dl)

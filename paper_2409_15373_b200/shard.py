@@ -51,3 +51,15 @@ def make_shard(lengths, world: int, rank: int, cost: str = "sq") -> Shard:
     off = np.concatenate([[0], np.cumsum(ln)]).astype(np.int64)
     s0, s1 = int(b[rank]), int(b[rank + 1])
     return Shard(rank, s0, s1, int(off[s0]), int(off[s1]), off[s0:s1 + 1] - off[s0])
+
+
+def all_reduce_mlp_grads(dlayers, group=None) -> None:
+    """jagged_mlp_vjp under sample sharding: dW and db are sums over all rows
+    (linalg.cpp:540-554), so each rank's shard gives a partial sum; one in-place SUM all-reduce per
+    tensor (NCCL over NVLink for CUDA tensors, gloo on CPU) makes them the full-batch gradients.
+    dx stays per-rank (rows are not shared). `dlayers`: objects with .dweights/.dbias or (dW, db) pairs."""
+    import torch.distributed as dist
+
+    for g in dlayers:
+        for t in ((g.dweights, g.dbias) if hasattr(g, "dweights") else g):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)

@@ -79,3 +79,41 @@ def test_sharded_layout_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert all(ok and rb and tot for _, ok, rb, tot in res), res
+
+
+def _mlp_worker(rank, world, port, q):
+    """Each rank runs the (binary64) jagged_mlp_vjp on its sample shard; the all-reduced dW/db must equal the
+    single-process gradients (the one op with a collective on its compute path)."""
+    from oracle import restated as R
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ln = synth.gen_lengths("uniform", 40, 3, 16)
+    off = synth.offsets_of(ln)
+    rng = np.random.default_rng(7)
+    dims = [6, 9, 4]
+    layers = [(rng.uniform(-1, 1, (dims[l], dims[l + 1])), rng.uniform(-1, 1, dims[l + 1]), l == 0) for l in range(2)]
+    x = rng.uniform(-1, 1, (int(off[-1]), dims[0]))
+    go = rng.uniform(-1, 1, (int(off[-1]), dims[-1]))
+    sh = shard.make_shard(ln, world, rank, cost="linear")
+    _, g = R.jagged_mlp_vjp(x[sh.row_begin:sh.row_end], layers, go[sh.row_begin:sh.row_end])
+    tg = [(torch.from_numpy(dw.copy()), torch.from_numpy(db.copy())) for dw, db in g]
+    shard.all_reduce_mlp_grads(tg)
+    _, full = R.jagged_mlp_vjp(x, layers, go)
+    ok = all(np.allclose(a.numpy(), c, rtol=1e-12, atol=1e-12) and np.allclose(b.numpy(), d, rtol=1e-12, atol=1e-12)
+             for (a, b), (c, d) in zip(tg, full))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_sharded_mlp_grads_allreduce_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_mlp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
