@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -528,43 +529,105 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   for (int64_t i = 1; i <= batch; ++i)
     REQUIRE(host_offsets[i] >= host_offsets[i - 1], JG_INVALID_ARGUMENT,
             "JaggedTensor: offsets must be non-decreasing at index " + std::to_string(i));
-  cudaStream_t st = as_stream(stream);
+  cudaStream_t user = as_stream(stream);
   const int64_t S = host_offsets[batch];
-  const size_t tb = (size_t)S * H * D * dsize(dtype);
-  const size_t lb = (size_t)S * H * sizeof(float);
-  const size_t ob = sizeof(int64_t) * (batch + 1);
-  const size_t ws = (size_t)jg_attention_backward_workspace_size(S, H, D);
-  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  Scratch buf(st);
-  if (jg_status rc = buf.alloc(al(ob) + 8 * al(tb) + al(lb) + al(ws))) return rc;
-  char* p = (char*)buf.p;
-  int64_t* d_off = (int64_t*)p; p += al(ob);
-  char* t[8];
-  for (int j = 0; j < 8; ++j) { t[j] = p; p += al(tb); }
-  float* d_lse = (float*)p; p += al(lb);
-  void* d_ws = p;
-  JG_CUDA(cudaMemcpyAsync(d_off, host_offsets, ob, cudaMemcpyHostToDevice, st));
-  JG_CUDA(cudaMemcpyAsync(t[0], q, tb, cudaMemcpyHostToDevice, st));
-  JG_CUDA(cudaMemcpyAsync(t[1], k, tb, cudaMemcpyHostToDevice, st));
-  JG_CUDA(cudaMemcpyAsync(t[2], v, tb, cudaMemcpyHostToDevice, st));
-  JG_CUDA(cudaMemcpyAsync(t[3], go, tb, cudaMemcpyHostToDevice, st));
-  jg_schedule sched = nullptr;
-  if (jg_status rc = jg_schedule_create(d_off, batch, S, stream, &sched)) return rc;
-  jg_status rc = jg_jagged_flash_attention_forward(d_off, batch, S, H, D, t[0], t[1], t[2], 64, 64, t[4], d_lse,
-                                                   dtype, sched, stream);
-  if (!rc)
-    rc = jg_jagged_flash_attention_backward(d_off, batch, S, H, D, t[0], t[1], t[2], t[3], t[4], d_lse, 64, 64, t[5],
-                                            t[6], t[7], dtype, sched, d_ws, stream);
-  if (!rc) {
-    cudaMemcpyAsync(out, t[4], tb, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(lse, d_lse, lb, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(dq, t[5], tb, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(dk, t[6], tb, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(dv, t[7], tb, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) rc = cuda_status(e, "fwd_bwd_host");
+  if (S == 0) return JG_OK;
+  // Samples are independent, so the batch is cut into contiguous sample chunks of ~equal rows and run as a
+  // two-stream pipeline: chunk c+1's host->device copy and chunk c-1's device->host copy (separate copy
+  // engines) overlap chunk c's forward + backward. Host buffers should be pinned.
+  const int64_t n_chunks = std::max<int64_t>(1, std::min<int64_t>(8, batch));
+  std::vector<int64_t> cut{0};
+  for (int64_t c = 1; c < n_chunks; ++c) {
+    const int64_t target = S * c / n_chunks;
+    int64_t b = cut.back();
+    while (b < batch && host_offsets[b] < target) ++b;
+    if (b > cut.back() && b < batch) cut.push_back(b);
   }
-  jg_schedule_destroy(sched);
+  cut.push_back(batch);
+  const int64_t nc = (int64_t)cut.size() - 1;
+  int64_t max_rows = 0, max_b = 0;
+  std::vector<std::vector<int64_t>> offs(nc);
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t b0 = cut[c], b1 = cut[c + 1], r0 = host_offsets[b0];
+    max_rows = std::max(max_rows, host_offsets[b1] - r0);
+    max_b = std::max(max_b, b1 - b0);
+    offs[c].resize(b1 - b0 + 1);
+    for (int64_t i = b0; i <= b1; ++i) offs[c][i - b0] = host_offsets[i] - r0;
+  }
+  const size_t es = dsize(dtype);
+  const size_t row_b = (size_t)H * D * es;
+  const size_t tb = (size_t)max_rows * row_b, lb = (size_t)max_rows * H * sizeof(float);
+  const size_t ob = sizeof(int64_t) * (max_b + 1);
+  const size_t ws = (size_t)jg_attention_backward_workspace_size(max_rows, H, D);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t slot_bytes = al(ob) + 8 * al(tb) + al(lb) + al(ws);
+  cudaStream_t sx[2];
+  cudaEvent_t ev_start, ev_done[2];
+  for (int j = 0; j < 2; ++j) {
+    JG_CUDA(cudaStreamCreateWithFlags(&sx[j], cudaStreamNonBlocking));
+    JG_CUDA(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming));
+  }
+  JG_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  JG_CUDA(cudaEventRecord(ev_start, user));  // work already queued on the caller's stream comes first
+  Scratch buf(sx[0]);
+  jg_status rc = buf.alloc(2 * slot_bytes);
+  std::vector<jg_schedule> scheds;
+  for (int j = 0; j < 2 && !rc; ++j) JG_CUDA(cudaStreamWaitEvent(sx[j], ev_start, 0));
+  {
+    cudaEvent_t alloc_done;
+    JG_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
+    JG_CUDA(cudaEventRecord(alloc_done, sx[0]));  // the scratch allocation is ordered on sx[0]
+    JG_CUDA(cudaStreamWaitEvent(sx[1], alloc_done, 0));
+    cudaEventDestroy(alloc_done);
+  }
+  for (int64_t c = 0; c < nc && !rc; ++c) {
+    const int j = (int)(c & 1);
+    cudaStream_t st = sx[j];
+    char* p = (char*)buf.p + j * slot_bytes;
+    int64_t* d_off = (int64_t*)p; p += al(ob);
+    char* t[8];
+    for (int u = 0; u < 8; ++u) { t[u] = p; p += al(tb); }
+    float* d_lse = (float*)p; p += al(lb);
+    void* d_ws = p;
+    const int64_t b0 = cut[c], bc = cut[c + 1] - b0, r0 = host_offsets[b0], rows = offs[c].back();
+    const size_t cb = (size_t)rows * row_b, hoff = (size_t)r0 * row_b;
+    JG_CUDA(cudaMemcpyAsync(d_off, offs[c].data(), sizeof(int64_t) * (bc + 1), cudaMemcpyHostToDevice, st));
+    JG_CUDA(cudaMemcpyAsync(t[0], (const char*)q + hoff, cb, cudaMemcpyHostToDevice, st));
+    JG_CUDA(cudaMemcpyAsync(t[1], (const char*)k + hoff, cb, cudaMemcpyHostToDevice, st));
+    JG_CUDA(cudaMemcpyAsync(t[2], (const char*)v + hoff, cb, cudaMemcpyHostToDevice, st));
+    JG_CUDA(cudaMemcpyAsync(t[3], (const char*)go + hoff, cb, cudaMemcpyHostToDevice, st));
+    if (rows == 0) continue;
+    jg_schedule sched = nullptr;
+    if ((rc = jg_schedule_create(d_off, bc, rows, st, &sched))) break;
+    scheds.push_back(sched);
+    rc = jg_jagged_flash_attention_forward(d_off, bc, rows, H, D, t[0], t[1], t[2], 64, 64, t[4], d_lse, dtype, sched, st);
+    if (!rc)
+      rc = jg_jagged_flash_attention_backward(d_off, bc, rows, H, D, t[0], t[1], t[2], t[3], t[4], d_lse, 64, 64, t[5],
+                                              t[6], t[7], dtype, sched, d_ws, st);
+    if (rc) break;
+    JG_CUDA(cudaMemcpyAsync((char*)out + hoff, t[4], cb, cudaMemcpyDeviceToHost, st));
+    JG_CUDA(cudaMemcpy2DAsync(lse + r0, (size_t)S * sizeof(float), d_lse, (size_t)rows * sizeof(float),
+                              (size_t)rows * sizeof(float), (size_t)H, cudaMemcpyDeviceToHost, st));
+    JG_CUDA(cudaMemcpyAsync((char*)dq + hoff, t[5], cb, cudaMemcpyDeviceToHost, st));
+    JG_CUDA(cudaMemcpyAsync((char*)dk + hoff, t[6], cb, cudaMemcpyDeviceToHost, st));
+    JG_CUDA(cudaMemcpyAsync((char*)dv + hoff, t[7], cb, cudaMemcpyDeviceToHost, st));
+  }
+  // the scratch is released on sx[0] after both streams' work
+  JG_CUDA(cudaEventRecord(ev_done[1], sx[1]));
+  JG_CUDA(cudaStreamWaitEvent(sx[0], ev_done[1], 0));
+  for (int j = 0; j < 2; ++j) {
+    cudaError_t e = cudaStreamSynchronize(sx[j]);
+    if (e != cudaSuccess && !rc) rc = cuda_status(e, "fwd_bwd_host");
+  }
+  for (jg_schedule s : scheds) jg_schedule_destroy(s);
+  if (buf.p) cudaFreeAsync(buf.p, sx[0]);
+  buf.p = nullptr;
+  cudaStreamSynchronize(sx[0]);
+  for (int j = 0; j < 2; ++j) {
+    cudaStreamDestroy(sx[j]);
+    cudaEventDestroy(ev_done[j]);
+  }
+  cudaEventDestroy(ev_start);
   return rc;
 }
 
