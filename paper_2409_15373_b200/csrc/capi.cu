@@ -533,9 +533,10 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   const int64_t S = host_offsets[batch];
   if (S == 0) return JG_OK;
   // Samples are independent, so the batch is cut into contiguous sample chunks of ~equal rows and run as a
-  // two-stream pipeline: chunk c+1's host->device copy and chunk c-1's device->host copy (separate copy
-  // engines) overlap chunk c's forward + backward. Host buffers should be pinned.
-  const int64_t n_chunks = std::max<int64_t>(1, std::min<int64_t>(8, batch));
+  // kSlots-stream pipeline: later chunks' host->device copies and earlier chunks' device->host copies
+  // (separate copy engines) overlap a chunk's forward + backward. Host buffers should be pinned.
+  constexpr int kSlots = 3;
+  const int64_t n_chunks = std::max<int64_t>(1, std::min<int64_t>(16, batch));
   std::vector<int64_t> cut{0};
   for (int64_t c = 1; c < n_chunks; ++c) {
     const int64_t target = S * c / n_chunks;
@@ -561,27 +562,27 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   const size_t ws = (size_t)jg_attention_backward_workspace_size(max_rows, H, D);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t slot_bytes = al(ob) + 8 * al(tb) + al(lb) + al(ws);
-  cudaStream_t sx[2];
-  cudaEvent_t ev_start, ev_done[2];
-  for (int j = 0; j < 2; ++j) {
+  cudaStream_t sx[kSlots];
+  cudaEvent_t ev_start, ev_done[kSlots];
+  for (int j = 0; j < kSlots; ++j) {
     JG_CUDA(cudaStreamCreateWithFlags(&sx[j], cudaStreamNonBlocking));
     JG_CUDA(cudaEventCreateWithFlags(&ev_done[j], cudaEventDisableTiming));
   }
   JG_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
   JG_CUDA(cudaEventRecord(ev_start, user));  // work already queued on the caller's stream comes first
   Scratch buf(sx[0]);
-  jg_status rc = buf.alloc(2 * slot_bytes);
+  jg_status rc = buf.alloc(kSlots * slot_bytes);
   std::vector<jg_schedule> scheds;
-  for (int j = 0; j < 2 && !rc; ++j) JG_CUDA(cudaStreamWaitEvent(sx[j], ev_start, 0));
+  for (int j = 0; j < kSlots && !rc; ++j) JG_CUDA(cudaStreamWaitEvent(sx[j], ev_start, 0));
   {
     cudaEvent_t alloc_done;
     JG_CUDA(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming));
     JG_CUDA(cudaEventRecord(alloc_done, sx[0]));  // the scratch allocation is ordered on sx[0]
-    JG_CUDA(cudaStreamWaitEvent(sx[1], alloc_done, 0));
+    for (int j = 1; j < kSlots; ++j) JG_CUDA(cudaStreamWaitEvent(sx[j], alloc_done, 0));
     cudaEventDestroy(alloc_done);
   }
   for (int64_t c = 0; c < nc && !rc; ++c) {
-    const int j = (int)(c & 1);
+    const int j = (int)(c % kSlots);
     cudaStream_t st = sx[j];
     char* p = (char*)buf.p + j * slot_bytes;
     int64_t* d_off = (int64_t*)p; p += al(ob);
@@ -612,10 +613,12 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
     JG_CUDA(cudaMemcpyAsync((char*)dk + hoff, t[6], cb, cudaMemcpyDeviceToHost, st));
     JG_CUDA(cudaMemcpyAsync((char*)dv + hoff, t[7], cb, cudaMemcpyDeviceToHost, st));
   }
-  // the scratch is released on sx[0] after both streams' work
-  JG_CUDA(cudaEventRecord(ev_done[1], sx[1]));
-  JG_CUDA(cudaStreamWaitEvent(sx[0], ev_done[1], 0));
-  for (int j = 0; j < 2; ++j) {
+  // the scratch is released on sx[0] after every stream's work
+  for (int j = 1; j < kSlots; ++j) {
+    JG_CUDA(cudaEventRecord(ev_done[j], sx[j]));
+    JG_CUDA(cudaStreamWaitEvent(sx[0], ev_done[j], 0));
+  }
+  for (int j = 0; j < kSlots; ++j) {
     cudaError_t e = cudaStreamSynchronize(sx[j]);
     if (e != cudaSuccess && !rc) rc = cuda_status(e, "fwd_bwd_host");
   }
@@ -623,7 +626,7 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   if (buf.p) cudaFreeAsync(buf.p, sx[0]);
   buf.p = nullptr;
   cudaStreamSynchronize(sx[0]);
-  for (int j = 0; j < 2; ++j) {
+  for (int j = 0; j < kSlots; ++j) {
     cudaStreamDestroy(sx[j]);
     cudaEventDestroy(ev_done[j]);
   }
