@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libjagged_b200.so")
+# JG_LIB_PATH: load an alternative build (A/B timing of kernel variants in one process launch)
+LIB_PATH = os.environ.get("JG_LIB_PATH") or os.path.join(_PKG, "libjagged_b200.so")
 
 JG_F32, JG_BF16, JG_F64 = 0, 1, 2
 STATUS = {0: "JG_OK", 1: "JG_INVALID_ARGUMENT", 2: "JG_CUDA_ERROR", 3: "JG_OUT_OF_MEMORY", 4: "JG_UNSUPPORTED"}

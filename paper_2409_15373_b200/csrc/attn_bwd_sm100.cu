@@ -35,8 +35,8 @@ constexpr int kSmWarp0 = 4, kDqWarp0 = 12;
 constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 of the 64 query columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kPrefetch = 6;   // query blocks prefetched into L2 ahead of the producer
-constexpr int kQdStages = 3;  // (Q_j, dO_j) smem ring depth (2 stages + 2 P/dS buffers measured slower)
-constexpr int kPdsBufs = 1;   // P^T/dS^T smem buffers (2 would let the softmax publish block j+1 while j is read)
+constexpr int kQdStages = 4;  // (Q_j, dO_j) smem ring depth (4: better at item boundaries; 3 leaves room for one 64-row dQ reduce)
+constexpr int kPdsBufs = 1;   // dS^T smem buffers
 
 template <int D>
 struct Smem {
@@ -48,15 +48,16 @@ struct Smem {
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTileKV;
   static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
-  static constexpr int kP = kQD + kStages * 2 * kTileQ;     // kPdsBufs x P^T  [128 keys x 64 q] bf16
-  static constexpr int kDS = kP + kPdsBufs * BKV * 128;     // kPdsBufs x dS^T [128 keys x 64 q] bf16
-  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging [64 q x D] fp32
+  static constexpr int kDS = kQD + kStages * 2 * kTileQ;    // kPdsBufs x dS^T [128 keys x 64 q] bf16 (P^T is in TMEM)
+  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging [kStgRows q x D] fp32
+  static constexpr int kStgRows = kQdStages > 3 ? 32 : 64;  // dQ rows per TMA reduce (32: two per block)
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 lse (log2 units) + 64 Delta, fp32
-  static constexpr int kLse = kStg + BQ * D * 4;            // kStages x kLsdBytes, loaded with (Q_j, dO_j)
+  static constexpr int kLse = kStg + kStgRows * D * 4;      // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
   static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2;
   static constexpr int kBytes = kBar + kNumBars * 8 + 16;
-  static constexpr int kAlloc = kBytes + 1024;
+  // no alignment slack: the dynamic smem base is 1024-aligned (declared so; checked at kernel entry)
+  static constexpr int kAlloc = kBytes;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -100,8 +101,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_dq, Params p) {
   using L = Smem<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (tc::smem_u32(smem) & 1023) != 0) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* k_full = bars + 0;
   uint64_t* k_empty = bars + 1;  // S issuer after its last S^T, G issuer after its last dQ^T
@@ -110,8 +112,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* qd_full = bars + 4;
   uint64_t* qd_empty = qd_full + L::kStages;
   uint64_t* st_full = qd_empty + L::kStages;  // [2] per TMEM score buffer
-  uint64_t* st_empty = st_full + 2;           // [2]
-  uint64_t* p_full = st_empty + 2;
+  uint64_t* pt_free = st_full + 2;            // [2] dV finished reading P^T from TMEM buffer b
+  uint64_t* p_full = pt_free + 2;
   uint64_t* pds_empty = p_full + 1;            // [kPdsBufs]
   uint64_t* dq_full = pds_empty + kPdsBufs;          // [2] one per score buffer: a single barrier could complete
                                               // twice before the drain warps wait (no S fill between dQ_{n-2}, dQ_{n-1})
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(st_full + b, 1);
-      tc::mbar_init(st_empty + b, kSmWarps);
+      tc::mbar_init(pt_free + b, 1);
       tc::mbar_init(dq_empty + b, 4);
     }
     tc::mbar_init(p_full, kSmWarps);
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
       constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
       const uint32_t k_base = tc::smem_u32(smem + L::kK), v_base = tc::smem_u32(smem + L::kV);
-      const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
+      const uint32_t ds_base = tc::smem_u32(smem + L::kDS);
       const uint32_t qd_base = tc::smem_u32(smem + L::kQD);
       auto stage_of = [&](uint32_t cnt) { return qd_base + (cnt % L::kStages) * 2 * L::kTileQ; };
       tc::WaitProf wp;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int b = j & 1;
             const uint32_t s = qd_cnt % L::kStages;
             wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 2);
-            wp.wait_warp(st_empty + b, (fill[b] & 1) ^ 1, 3);  // softmax done reading this buffer
+            wp.wait_warp(pt_free + b, (fill[b] & 1) ^ 1, 3);  // dV of the block that used b read its P^T
             wp.wait_warp(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
             ++fill[b];
             tc::tc_fence_after();
@@ -307,33 +309,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < nq; ++j, ++qd_cnt) {
             wp.wait_warp(p_full, p_cnt & 1, 5);
             const uint32_t pb = p_cnt % kPdsBufs;
-            const uint32_t p_cur = p_base + pb * (BKV * 128), ds_cur = ds_base + pb * (BKV * 128);
+            const uint32_t ds_cur = ds_base + pb * (BKV * 128);
             ++p_cnt;
             tc::tc_fence_after();
             const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
+            const uint32_t col = (j & 1) * 128;
             if (wp.g) wp.trace(83);
-            // dQ_j^T = K^T dS^T first, into the S^T slot of buffer j&1 (its scores were consumed: p_full), so the
-            // drain frees that buffer for warp 1's S_{j+2} as early as possible
+            // dV += P^T dO_j first (TS: A = P^T from TMEM; K-step kk covers queries 16kk..16kk+15, which the
+            // softmax half kk/2 packed at columns col + 32(kk/2) + 8(kk&1)), so buffer j&1 frees early
 #pragma unroll
-            for (int kk = 0; kk < BKV / 16; ++kk) {
-              tc::mma_bf16_ss_warp(tmem + (j & 1) * 128, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
-                              tc::sw128_desc(ds_cur + kk * 2048, 16, 1024), kIdQ, kk > 0);
-            }
+            for (int kk = 0; kk < BQ / 16; ++kk)
+              tc::mma_bf16_ts_warp(tmem + 256, tmem + col + 32 * (kk >> 1) + 8 * (kk & 1),
+                                   tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+            tc::mma_commit_warp(pt_free + (j & 1));
+            // dQ_j^T = K^T dS^T into the consumed dP^T slot of buffer j&1
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk)
+              tc::mma_bf16_ss_warp(tmem + col + 64, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
+                                   tc::sw128_desc(ds_cur + kk * 2048, 16, 1024), kIdQ, kk > 0);
             tc::mma_commit_warp(dq_full + (j & 1));
-            if (j == nq - 1) tc::mma_commit_warp(k_empty);  // the item's last read of K: reload during dV/dK
+            if (j == nq - 1) tc::mma_commit_warp(k_empty);  // the item's last read of K: reload during dK
             if (wp.g) wp.trace(84);
-            // dV += P^T dO_j ; dK += dS^T Q_j   (A K-major [128 x 64 q]; B MN-major [64 q x D])
+            // dK += dS^T Q_j (A K-major [128 x 64 q] smem; B MN-major [64 q x D])
 #pragma unroll
-            for (int kk = 0; kk < BQ / 16; ++kk) {
-              tc::mma_bf16_ss_warp(tmem + 256, tc::sw128_desc(p_cur + kk * 32, 16, 1024),
-                              tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
-            }
-            if (wp.g) wp.trace(85);
-#pragma unroll
-            for (int kk = 0; kk < BQ / 16; ++kk) {
+            for (int kk = 0; kk < BQ / 16; ++kk)
               tc::mma_bf16_ss_warp(tmem + 384, tc::sw128_desc(ds_cur + kk * 32, 16, 1024),
-                              tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
-            }
+                                   tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
             // Q_j, dO_j are no longer needed (warp 1's S/dP_j completed before the softmax published P_j)
             tc::mma_commit_warp(qd_empty + (qd_cnt % L::kStages));
             tc::mma_commit_warp(pds_empty + pb);
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = wq * 32 + lane;                // key row within the tile
     const int half = (warp - kSmWarp0) >> 2;       // query columns [32 half, 32 half + 32)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
-    const uint32_t p_base = tc::smem_u32(smem + L::kP), ds_base = tc::smem_u32(smem + L::kDS);
+    const uint32_t ds_base = tc::smem_u32(smem + L::kDS);
     const uint32_t lsd = tc::smem_u32(smem + L::kLse);
     uint32_t cons[2] = {0, 0}, pds_cnt = 0, qd_cnt = 0;
     tc::WaitProf wp;
@@ -409,9 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           body(std::false_type{});
         else
           body(std::true_type{});
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(st_empty + b);
+        // P^T (bf16) back over the S^T columns this thread read: the A operand of the dV MMA
+        tc::tmem_st16(lane_addr + b * 128 + half * 32, pk);
         const uint32_t pb = pds_cnt % kPdsBufs;
         wp.wait_warp(pds_empty + pb, ((pds_cnt / kPdsBufs) & 1) ^ 1, 2);
         ++pds_cnt;
@@ -419,10 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = 0; u < 4; ++u) {
           if (p.dbg & 4) break;
           const uint32_t o = tc::sw128_offset(row, half * 4 + u);
-          tc::st_shared_v4(p_base + pb * (BKV * 128) + o, pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
           tc::st_shared_v4(ds_base + pb * (BKV * 128) + o, dk2[u * 4], dk2[u * 4 + 1], dk2[u * 4 + 2], dk2[u * 4 + 3]);
         }
         tc::fence_proxy_async_smem();
+        tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);
@@ -453,28 +453,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++dqc[b];
         tc::tc_fence_after();
         uint32_t a[32], c2[32];
-        tc::tmem_ld32(lane_addr + b * 128, a);
-        tc::tmem_ld32(lane_addr + b * 128 + 32, c2);
+        tc::tmem_ld32(lane_addr + b * 128 + 64, a);
+        tc::tmem_ld32(lane_addr + b * 128 + 96, c2);
         tc::tmem_wait_ld();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(dq_empty + b);
-        const long long tb = clock64();
-        if (tid == 0) bulk_wait_read0();  // the previous block's reduction has read the staging buffer
-        named_bar(2, 128);
-        wp.add(1, clock64() - tb);
-#pragma unroll
-        for (int q = 0; q < 32; ++q) tc::st_shared_f32(stg_base + (q * D + tid) * 4, __uint_as_float(a[q]) * p.scale);
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          tc::st_shared_f32(stg_base + ((q + 32) * D + tid) * 4, __uint_as_float(c2[q]) * p.scale);
-        tc::fence_proxy_async_smem();
-        named_bar(2, 128);
-        // one TMA tensor reduce-add of the whole [64 q x D] fp32 box into the accumulator; rows of padded
+        // two [32 q x D] fp32 boxes through the staging buffer, one TMA tensor reduce-add each; rows of padded
         // queries are exactly zero (P = 0 there), so adding them into the next sample's rows is a no-op
-        if (tid == 0 && !(p.dbg & 1)) {
-          tensor_reduce_add_3d(&tm_dq, stg_base, 0, h, (int)(b0 + (int64_t)j * BQ));
-          bulk_commit();
+#pragma unroll
+        for (int hh = 0; hh < BQ / L::kStgRows; ++hh) {
+          const long long tb = clock64();
+          if (tid == 0) bulk_wait_read0();  // the previous reduction has read the staging buffer
+          named_bar(2, 128);
+          wp.add(1, clock64() - tb);
+#pragma unroll
+          for (int q = 0; q < L::kStgRows; ++q) {
+            const int qq = hh * L::kStgRows + q;
+            tc::st_shared_f32(stg_base + (q * D + tid) * 4, __uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]) * p.scale);
+          }
+          tc::fence_proxy_async_smem();
+          named_bar(2, 128);
+          if (tid == 0 && !(p.dbg & 1)) {
+            tensor_reduce_add_3d(&tm_dq, stg_base, 0, h, (int)(b0 + (int64_t)j * BQ + L::kStgRows * hh));
+            bulk_commit();
+          }
         }
       }
       // dK / dV for this key tile
@@ -598,7 +601,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   if (jg_status rc = make_map(&mv, v, total_rows, H, kD, fb::BKV)) return rc;
   if (jg_status rc = make_map(&mdo, go, total_rows, H, kD, fb::BQ)) return rc;
   CUtensorMap mdq;
-  if (jg_status rc = make_map_f32(&mdq, dq_acc, total_rows, H, kD, fb::BQ)) return rc;
+  if (jg_status rc = make_map_f32(&mdq, dq_acc, total_rows, H, kD, L::kStgRows)) return rc;
   static bool attr_set = false;
   if (!attr_set) {
     JG_CUDA(cudaFuncSetAttribute(fb::jfa_bwd_sm100_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
@@ -616,7 +619,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
   wait_prof_end(p.prof, st, "bwd",
                 {"P.k_empty", "P.qd_empty", "P.v_empty", "", "", "", "", "P.total", "M.k_full", "M.v_full", "M.qd_full",
-                 "M.st_empty", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
+                 "M.pt_free", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
                  "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
   fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,
