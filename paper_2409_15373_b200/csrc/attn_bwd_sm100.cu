@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::WaitProf wp;
       wp.init(lane == 0 ? p.prof : nullptr, warp == 1 ? 8 : 32);
       const long long t_role = clock64();
-      uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill[2] = {0, 0};
+      // per-buffer phase parities live in bit b of a register (a runtime-indexed [2] array goes to local memory)
+      uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill_par = 0;
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
@@ -277,9 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int b = j & 1;
             const uint32_t s = qd_cnt % L::kStages;
             wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 2);
-            wp.wait_warp(pt_free + b, (fill[b] & 1) ^ 1, 3);  // dV of the block that used b read its P^T
-            wp.wait_warp(dq_empty + b, (fill[b] & 1) ^ 1, 4);  // dQ^T previously written here was drained
-            ++fill[b];
+            wp.wait_warp(pt_free + b, ((fill_par >> b) & 1) ^ 1, 3);  // dV of the block that used b read its P^T
+            wp.wait_warp(dq_empty + b, ((fill_par >> b) & 1) ^ 1, 4);  // dQ^T previously written here was drained
+            fill_par ^= 1u << b;
             tc::tc_fence_after();
             if (wp.g) wp.trace(56);
             const uint32_t q_base = stage_of(qd_cnt), do_base = q_base + L::kTileQ;
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     const uint32_t ds_base = tc::smem_u32(smem + L::kDS);
     const uint32_t lsd = tc::smem_u32(smem + L::kLse);
-    uint32_t cons[2] = {0, 0}, pds_cnt = 0, qd_cnt = 0;
+    uint32_t cons_par = 0, pds_cnt = 0, qd_cnt = 0;  // bit b: phase parity of st_full[b]
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
@@ -367,8 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nq; ++j, ++qd_cnt) {
         const int b = j & 1;
         const uint32_t s = qd_cnt % L::kStages;
-        wp.wait_warp(st_full + b, cons[b] & 1, 1);
-        ++cons[b];
+        wp.wait_warp(st_full + b, (cons_par >> b) & 1, 1);
+        cons_par ^= 1u << b;
         tc::tc_fence_after();
         uint32_t sr[32], dr[32];
         tc::tmem_ld32(lane_addr + b * 128 + half * 32, sr);
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(wq * 32) << 16);
     float* stg = reinterpret_cast<float*>(smem + L::kStg);
     const uint32_t stg_base = tc::smem_u32(stg);
-    uint32_t item_cnt = 0, dqc[2] = {0, 0};
+    uint32_t item_cnt = 0, dq_par = 0;  // bit b: phase parity of dq_full[b]
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 24);
     const long long t_role = clock64();
@@ -449,8 +450,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nq = (int)((n + BQ - 1) / BQ);
       for (int j = 0; j < nq; ++j) {
         const int b = j & 1;
-        wp.wait_warp(dq_full + b, dqc[b] & 1, 0);
-        ++dqc[b];
+        wp.wait_warp(dq_full + b, (dq_par >> b) & 1, 0);
+        dq_par ^= 1u << b;
         tc::tc_fence_after();
         uint32_t a[32], c2[32];
         tc::tmem_ld32(lane_addr + b * 128 + 64, a);
