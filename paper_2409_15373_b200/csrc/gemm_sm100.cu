@@ -10,9 +10,12 @@
 // so the epilogue of tile t overlaps the MMAs of tile t+1. TMA coordinates are global row indices
 // (offsets[i] + local row), so no padding is materialised; rows of the next sample that a tail tile
 // picks up are masked: never stored (M/N tails) or zeroed in smem before the MMA (K tails of JJ, where
-// the reduction runs over the jagged axis). Jagged^2 A operands (row stride Bi, not 16-byte aligned,
-// unusable by TMA) are gathered by a loader warpgroup into the swizzled layout with zeros past Bi.
-// Warps: 0 TMA producer, 1 MMA issuer, 4-7 epilogue (TMEM -> registers -> global), 8-11 loader.
+// the reduction runs over the jagged axis). Jagged^2 A operands (row stride Bi, arbitrary 2-byte
+// alignment, unusable by TMA) are first repacked by aj_repack_kernel into 16 KB tiles that are already
+// the smem image of one [128 m x 64 k] SWIZZLE_128B stage (zeros past Bi); the producer then moves each
+// stage with a single bulk copy (cp.async.bulk) — one pass of HBM traffic instead of a latency-bound
+// per-stage gather. Warps: 0 TMA producer, 1 MMA issuer, 4-7 epilogue (TMEM -> registers -> global),
+// 8-11 loader (JJ K-tail zeroing).
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
@@ -43,6 +46,8 @@ struct Params {
   const __nv_bfloat16* a_j2;  // AJ: jagged^2 A values
   void* out;
   int out_f32;
+  const uint8_t* a_tiles;     // AJ: repacked A stages (16 KB each)
+  const int64_t* a_prefix;    // AJ: A tiles per sample, exclusive prefix (ceil(Bi/128) * ceil(Bi/64))
 };
 
 struct Tile {
@@ -75,8 +80,73 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int64_t t) {
 template <int OP> struct Layout {
   static constexpr bool a_mn = OP == JJ;
   static constexpr bool b_mn = OP != JJJ;
-  static constexpr bool loader = OP == AJ || OP == JJ;  // stages pass through the loader warpgroup
+  static constexpr bool loader = OP == JJ;  // stages pass through the loader warpgroup (K-tail zeroing)
 };
+
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+// AJ A-operand repack: tile t of sample i (local index = m-block * nkb + k-block) becomes the exact smem
+// image of a [128 m x 64 k] SWIZZLE_128B K-major stage with zeros past Bi. One CTA per tile; thread u
+// builds 16-byte units from two aligned 16-byte loads realigned with funnel shifts (the jagged^2 rows
+// start at arbitrary 2-byte offsets). Reads the A values once, writes ~1.1x their bytes.
+__global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restrict__ off, const int64_t* __restrict__ sq,
+                                                        const int64_t* __restrict__ a_prefix, int64_t batch,
+                                                        const __nv_bfloat16* __restrict__ a, uint8_t* __restrict__ tiles) {
+  const int64_t n_tiles = a_prefix[batch];
+  const char* base = reinterpret_cast<const char*>(a);
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int64_t i = upper_index(a_prefix, batch, t);
+    const int Bi = (int)(off[i + 1] - off[i]);
+    const int64_t sqo = sq[i];
+    const int nkb = (Bi + BK - 1) / BK;
+    const int64_t local = t - a_prefix[i];
+    const int m0 = (int)(local / nkb) * BM, k0 = (int)(local % nkb) * BK;
+    uint8_t* dst = tiles + t * kTileBytes;
+#pragma unroll
+    for (int rep = 0; rep < 4; ++rep) {
+      const int u = rep * 256 + threadIdx.x;  // 16-byte unit: row u/8, column chunk u%8
+      const int row = u >> 3, c16 = u & 7;
+      const int m = m0 + row, kb0 = k0 + c16 * 8;
+      const int nval = (m < Bi && kb0 < Bi) ? (Bi - kb0 < 8 ? Bi - kb0 : 8) : 0;
+      uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+      int sh = 0;
+      if (nval > 0) {
+        // an aligned 16-byte chunk holding at least one valid byte lies in that byte's page: no fault
+        const int64_t byte0 = (sqo + (int64_t)m * Bi + kb0) * 2;
+        const int64_t al = byte0 & ~int64_t(15);
+        sh = (int)(byte0 - al);
+        lo = __ldg(reinterpret_cast<const uint4*>(base + al));
+        if (sh != 0 && byte0 + 2 * nval > al + 16) hi = __ldg(reinterpret_cast<const uint4*>(base + al + 16));
+      }
+      const int ws = sh >> 2;
+      const bool half = (sh & 2) != 0;
+      const uint32_t w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w, w4 = hi.x, w5 = hi.y, w6 = hi.z, w7 = hi.w;
+      const uint32_t x0 = ws == 0 ? w0 : ws == 1 ? w1 : ws == 2 ? w2 : w3;
+      const uint32_t x1 = ws == 0 ? w1 : ws == 1 ? w2 : ws == 2 ? w3 : w4;
+      const uint32_t x2 = ws == 0 ? w2 : ws == 1 ? w3 : ws == 2 ? w4 : w5;
+      const uint32_t x3 = ws == 0 ? w3 : ws == 1 ? w4 : ws == 2 ? w5 : w6;
+      const uint32_t x4 = ws == 0 ? w4 : ws == 1 ? w5 : ws == 2 ? w6 : w7;
+      uint32_t o[4];
+      o[0] = half ? __funnelshift_r(x0, x1, 16) : x0;
+      o[1] = half ? __funnelshift_r(x1, x2, 16) : x1;
+      o[2] = half ? __funnelshift_r(x2, x3, 16) : x2;
+      o[3] = half ? __funnelshift_r(x3, x4, 16) : x3;
+      if (nval < 8) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (2 * q >= nval) o[q] = 0;
+          else if (2 * q + 1 >= nval) o[q] &= 0xFFFFu;
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + tc::sw128_offset(row, c16)) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
 
 template <int OP>
 __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
@@ -126,8 +196,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           uint8_t* sa = smem + Smem::kA + s * kTileBytes;
           uint8_t* sb = smem + Smem::kB + s * kTileBytes;
           const int k0 = kb * BK;
-          const int bytes = (OP == AJ ? 1 : 2) * kTileBytes;
-          tc::mbar_expect_tx(full + s, bytes);
+          tc::mbar_expect_tx(full + s, 2 * kTileBytes);
+          if (OP == AJ) {
+            const int64_t at = p.a_prefix[tl.i] + (int64_t)(tl.m0 / BM) * tl.nk + kb;
+            bulk_load(sa, p.a_tiles + at * kTileBytes, kTileBytes, full + s);
+          }
           if (OP == JJJ || OP == JD)
             tc::tma_load_3d(sa, &tm_a, full + s, k0, 0, (int)(tl.b0 + tl.m0));
           if (OP == JJ)
@@ -273,62 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         const uint32_t s = cnt % kStages;
         uint8_t* sa = smem + Smem::kA + s * kTileBytes;
         const int k0 = kb * BK;
-        if (OP == AJ) {
-          // gather A[m0 + r][k0 .. k0+63] (row stride Bi, arbitrary 2-byte alignment) into the [128 rows x 64 k]
-          // SWIZZLE_128B K-major stage: 8 lanes per row, each producing one 16-byte unit from two aligned
-          // 16-byte loads realigned with funnel shifts; zeros past the sample (k >= Bi or m >= Bi).
-          // All 16 loads of a lane are issued before the stage is free and before any is consumed.
-          const char* base = reinterpret_cast<const char*>(p.a_j2);
-          const int u = lane & 7;
-          uint4 lo[8], hi[8];
-          int shv[8], nval[8];
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int row = wq * 32 + it * 4 + (lane >> 3), m = tl.m0 + row;
-            const int kb0 = k0 + u * 8;  // first element of this 16-byte unit
-            nval[it] = (m < tl.M && kb0 < tl.K) ? (tl.K - kb0 < 8 ? tl.K - kb0 : 8) : 0;
-            lo[it] = hi[it] = make_uint4(0, 0, 0, 0);
-            shv[it] = 0;
-            if (nval[it] > 0) {
-              // an aligned 16-byte chunk holding at least one valid byte lies in the same page as that
-              // byte, so these over-reads never fault; hi is read only if valid elements reach into it
-              const int64_t byte0 = (tl.sqo + (int64_t)m * tl.n + kb0) * 2;
-              const int64_t al = byte0 & ~int64_t(15);
-              shv[it] = (int)(byte0 - al);
-              lo[it] = __ldg(reinterpret_cast<const uint4*>(base + al));
-              if (shv[it] != 0 && byte0 + 2 * nval[it] > al + 16) hi[it] = __ldg(reinterpret_cast<const uint4*>(base + al + 16));
-            }
-          }
-          tc::mbar_wait(empty + s, ((cnt / kStages) & 1) ^ 1);
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int row = wq * 32 + it * 4 + (lane >> 3);
-            const int sh = shv[it], ws = sh >> 2;
-            const bool half = (sh & 2) != 0;
-            const uint32_t w0 = lo[it].x, w1 = lo[it].y, w2 = lo[it].z, w3 = lo[it].w;
-            const uint32_t w4 = hi[it].x, w5 = hi[it].y, w6 = hi[it].z, w7 = hi[it].w;
-            // x_k = word (ws + k) of the 32-byte window (register selects, no local memory)
-            const uint32_t x0 = ws == 0 ? w0 : ws == 1 ? w1 : ws == 2 ? w2 : w3;
-            const uint32_t x1 = ws == 0 ? w1 : ws == 1 ? w2 : ws == 2 ? w3 : w4;
-            const uint32_t x2 = ws == 0 ? w2 : ws == 1 ? w3 : ws == 2 ? w4 : w5;
-            const uint32_t x3 = ws == 0 ? w3 : ws == 1 ? w4 : ws == 2 ? w5 : w6;
-            const uint32_t x4 = ws == 0 ? w4 : ws == 1 ? w5 : ws == 2 ? w6 : w7;
-            uint32_t o[4];
-            o[0] = half ? __funnelshift_r(x0, x1, 16) : x0;
-            o[1] = half ? __funnelshift_r(x1, x2, 16) : x1;
-            o[2] = half ? __funnelshift_r(x2, x3, 16) : x2;
-            o[3] = half ? __funnelshift_r(x3, x4, 16) : x3;
-            const int valid = nval[it];
-            if (valid < 8) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (2 * q >= valid) o[q] = 0;
-                else if (2 * q + 1 >= valid) o[q] &= 0xFFFFu;
-              }
-            }
-            *reinterpret_cast<uint4*>(sa + tc::sw128_offset(row, u)) = make_uint4(o[0], o[1], o[2], o[3]);
-          }
-        } else {
+        {
           // JJ: zero the A (and B) rows of the K tail that belong to the next sample
           tc::mbar_wait(full + s, (cnt / kStages) & 1);
           const int rem = tl.K - k0;
@@ -399,7 +417,8 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
   if (op == gm::JJ) { g.M = L_const(D); g.N = L_const(T); }
   if (op == gm::JD) { g.M = bi; g.N = L_const(T); }
   if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, 128, tile_prefix, st)) return rc;
-  gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32};
+  gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32,
+               nullptr, nullptr};
   CUtensorMap ma{}, mb{};
   const int64_t rows = total_rows > 0 ? total_rows : 1;
   switch (op) {
@@ -407,9 +426,36 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       if (jg_status rc = gm::map2d(&ma, a, rows, D, 128)) return rc;
       if (jg_status rc = gm::map2d(&mb, b, rows, D, 128)) return rc;
       return gm::run<gm::JJJ>(p, ma, mb, st);
-    case gm::AJ:
+    case gm::AJ: {
       if (jg_status rc = gm::map2d(&mb, b, rows, D, 64)) return rc;
-      return gm::run<gm::AJ>(p, mb, mb, st);
+      // A tiles per sample: ceil(Bi/128) * ceil(Bi/64) (a prefix with M = N = Bi and 128 x 64 tiles)
+      int64_t* a_prefix = nullptr;
+      JG_CUDA(cudaMallocAsync(&a_prefix, sizeof(int64_t) * (batch + 1), st));
+      GemmDesc ga;
+      ga.M = bi;
+      ga.N = bi;
+      jg_status rc = launch_gemm_prefix(ga, off, sq, batch, 128, 64, a_prefix, st);
+      int64_t n_at = 0;
+      auto ok = [](cudaError_t e, const char* where) { return e == cudaSuccess ? JG_OK : cuda_status(e, where); };
+      // the tile count sizes the repack buffer: one 8-byte device->host read (stream-synchronising)
+      if (!rc) rc = ok(cudaMemcpyAsync(&n_at, a_prefix + batch, sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+                                "aj tile count");
+      if (!rc) rc = ok(cudaStreamSynchronize(st), "aj tile count");
+      uint8_t* tiles = nullptr;
+      if (!rc && n_at > 0) rc = ok(cudaMallocAsync(&tiles, (size_t)n_at * gm::kTileBytes, st), "aj tiles");
+      if (!rc && n_at > 0) {
+        gm::aj_repack_kernel<<<(unsigned)std::min<int64_t>(n_at, 16LL * device_sm_count()), 256, 0, st>>>(
+            off, sq, a_prefix, batch, (const __nv_bfloat16*)a, tiles);
+        rc = ok(cudaGetLastError(), "aj_repack_kernel");
+        count_launch();
+      }
+      p.a_tiles = tiles;
+      p.a_prefix = a_prefix;
+      if (!rc) rc = gm::run<gm::AJ>(p, mb, mb, st);
+      if (tiles) cudaFreeAsync(tiles, st);
+      cudaFreeAsync(a_prefix, st);
+      return rc;
+    }
     case gm::JJ:
       if (jg_status rc = gm::map2d(&ma, a, rows, D, 64)) return rc;
       if (jg_status rc = gm::map2d(&mb, b, rows, T, 64)) return rc;
