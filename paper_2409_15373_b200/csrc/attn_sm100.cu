@@ -298,7 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tmem_ld32(s_addr + c * 32 + 32, r[1]);
             tc::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 64; ++e) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e >> 5][e & 31]));
+            for (int e = 0; e < 64; e += 2)  // FMNMX3: two scores per instruction
+              m8[(e >> 1) & 7] = tc::fmax3(m8[(e >> 1) & 7], __uint_as_float(r[e >> 5][e & 31]),
+                                           __uint_as_float(r[e >> 5][(e & 31) + 1]));
           }
         } else {
           // last key block of the segment: write -inf over the keys of the next sample back into TMEM so
@@ -355,10 +357,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int u = 0; u < 4; ++u) {
             float pv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float x = fmaf(__uint_as_float(r[c & 1][u * 8 + e]), p.scale_log2, -m);
-              pv[e] = e < 8 - kPolyExp ? tc::ex2(x) : tc::ex2_poly(x);
-              r8[e] += pv[e];
+            for (int e = 0; e < 8; e += 2) {  // FFMA2 / FADD2: two scores per instruction
+              const float2 x = tc::ffma2(make_float2(__uint_as_float(r[c & 1][u * 8 + e]),
+                                                     __uint_as_float(r[c & 1][u * 8 + e + 1])),
+                                         make_float2(p.scale_log2, p.scale_log2), make_float2(-m, -m));
+              if (e + 2 <= 8 - kPolyExp) {
+                pv[e] = tc::ex2(x.x);
+                pv[e + 1] = tc::ex2(x.y);
+              } else {
+                const float2 y = tc::ex2_poly2(x);
+                pv[e] = y.x;
+                pv[e + 1] = y.y;
+              }
+              const float2 acc = tc::fadd2(make_float2(r8[e], r8[e + 1]), make_float2(pv[e], pv[e + 1]));
+              r8[e] = acc.x;
+              r8[e + 1] = acc.y;
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) pk[u * 4 + e] = tc::pack_bf16(pv[2 * e], pv[2 * e + 1]);

@@ -259,6 +259,48 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ math
+// sm_100 paired fp32 ALU ops (FFMA2 / FADD2 / FMUL2: two lanes of work per instruction) and the
+// 3-input max (FMNMX3); they halve the softmax's issue-slot count.
+__device__ __forceinline__ unsigned long long f2_as_u64(float2 v) {
+  return (unsigned long long)__float_as_uint(v.x) | ((unsigned long long)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ float2 u64_as_f2(unsigned long long u) {
+  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
+  return u64_as_f2(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(r);
+}
+// ex2_poly on a pair with paired ops (7 issue slots for two exponentials instead of 16)
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 f = fadd2(x, fadd2(magic, make_float2(-t.x, -t.y)));
+  float2 q = ffma2(f, make_float2(0.05517132f, 0.05517132f), make_float2(0.24261054f, 0.24261054f));
+  q = ffma2(q, f, make_float2(0.69326099f, 0.69326099f));
+  q = ffma2(q, f, make_float2(0.99992811f, 0.99992811f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // 2^x on the FMA pipe (x <= ~127): round-to-nearest split x = n + f, f in [-0.5, 0.5], degree-3 minimax
 // for 2^f (max relative error 7.5e-5, below half a bf16 ulp), n added into the exponent bits. Used for a
 // fraction of the softmax exponentials so the 16/clk/SM MUFU pipe stops being the bound.
