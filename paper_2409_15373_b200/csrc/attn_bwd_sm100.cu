@@ -51,7 +51,7 @@ struct Smem {
   static constexpr int kDS = kQD + kStages * 2 * kTileQ;    // kPdsBufs x dS^T [128 keys x 64 q] bf16 (P^T is in TMEM)
   static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging [kStgRows q x D] fp32
   static constexpr int kStgRows = kQdStages > 3 ? 32 : 64;  // dQ rows per TMA reduce (32: two per block)
-  static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 lse (log2 units) + 64 Delta, fp32
+  static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 -lse*log2(e) + 64 -Delta, fp32
   static constexpr int kLse = kStg + kStgRows * D * 4;      // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
   static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2;
@@ -389,12 +389,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 32; e += 4) {
             const float4 l4 = tc::ld_shared_f4(lb + e * 4);
             const float4 d4 = tc::ld_shared_f4(lb + (BQ + e) * 4);
-            float p0 = tc::ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
-            float p1 = tc::ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
-            float p2 = tc::ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
-            float p3 = tc::ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w));
-            float s0 = p0 * (__uint_as_float(dr[e + 0]) - d4.x), s1 = p1 * (__uint_as_float(dr[e + 1]) - d4.y);
-            float s2 = p2 * (__uint_as_float(dr[e + 2]) - d4.z), s3 = p3 * (__uint_as_float(dr[e + 3]) - d4.w);
+            // lsd holds -lse*log2(e) and -Delta, so each pair is one FFMA2 / FADD2 / FMUL2
+            const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+            const float2 x01 = tc::ffma2(make_float2(__uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1])), sc2,
+                                         make_float2(l4.x, l4.y));
+            const float2 x23 = tc::ffma2(make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])), sc2,
+                                         make_float2(l4.z, l4.w));
+            float p0 = tc::ex2(x01.x), p1 = tc::ex2(x01.y), p2 = tc::ex2(x23.x), p3 = tc::ex2(x23.y);
+            const float2 g01 = tc::fadd2(make_float2(__uint_as_float(dr[e + 0]), __uint_as_float(dr[e + 1])),
+                                         make_float2(d4.x, d4.y));
+            const float2 g23 = tc::fadd2(make_float2(__uint_as_float(dr[e + 2]), __uint_as_float(dr[e + 3])),
+                                         make_float2(d4.z, d4.w));
+            const float2 s01 = tc::fmul2(make_float2(p0, p1), g01), s23 = tc::fmul2(make_float2(p2, p3), g23);
+            float s0 = s01.x, s1 = s01.y, s2 = s23.x, s3 = s23.y;
             if constexpr (decltype(masked)::value) {  // after the products: masked lanes may hold stale inf/nan
               if (!row_valid || e + 0 >= qlim) p0 = s0 = 0.f;
               if (!row_valid || e + 1 >= qlim) p1 = s1 = 0.f;
@@ -528,8 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Delta = rowsum(dO * O) per (row, head), zero the fp32 dQ accumulator (one warp per unit), and write
-// lse (log2 units) and Delta into lsd[h][2][R] (R = total_rows rounded up to 4: a TMA-loadable layout whose
-// 64-row boxes land in the main kernel's (Q_j, dO_j) stages).
+// -lse*log2(e) and -Delta into lsd[2][H][total_rows] (staged per query block by the main kernel's producer
+// with cp.async; negated so the softmax needs one paired FFMA2 / FADD2 per two scores).
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* __restrict__ go,
                                                            const __nv_bfloat16* __restrict__ o, int64_t units,
@@ -562,8 +569,8 @@ __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* 
     acc = warp_sum(acc);
     if (lane == 0) {
       const int64_t r = u / H, h = u - r * H;
-      lsd[h * total_rows + r] = lse[h * total_rows + r] * kLog2e;
-      lsd[(H + h) * total_rows + r] = acc;
+      lsd[h * total_rows + r] = -lse[h * total_rows + r] * kLog2e;  // negated: one FFMA2 per pair downstream
+      lsd[(H + h) * total_rows + r] = -acc;
     }
   }
 }
