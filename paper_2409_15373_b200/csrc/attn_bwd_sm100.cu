@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&tm_do);
     tc::tma_prefetch(&tm_dq);
   }
+  tc::cta_time_mark(p.prof, 0);
   if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     wp.init(lane == 0 ? p.prof : nullptr, 0);
     const long long t_role = clock64();
     uint32_t item_cnt = 0, qd_cnt = 0;
-    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
       const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, k_full, c * 64, h, kv_row);
         if (wp.g) wp.trace(50);
         // warm L2 with the next item's K/V: its loads wait for this item's last MMAs (kv_empty)
-        const int64_t wn = w + gridDim.x;
+        const int64_t wn = tc::snake_work(k + 1);
         if (wn < n_work) {
           const int2 itn = p.items[wn / H];
           const int hn = (int)(wn % H);
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long t_role = clock64();
       // per-buffer phase parities live in bit b of a register (a runtime-indexed [2] array goes to local memory)
       uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill_par = 0;
-      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+      for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
-    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k)) {
       const int2 it = p.items[w / H];
       const int64_t n = p.off[it.x + 1] - p.off[it.x];
       const int nq = (int)((n + BQ - 1) / BQ);
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 24);
     const long long t_role = clock64();
-    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
       const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
@@ -532,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem);
   }
+  tc::cta_time_mark(p.prof, 1);
 }
 
 // Delta = rowsum(dO * O) per (row, head), zero the fp32 dQ accumulator (one warp per unit), and write

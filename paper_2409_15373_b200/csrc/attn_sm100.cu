@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&tm_k);
     tc::tma_prefetch(&tm_v);
   }
+  tc::cta_time_mark(p.prof, 0);
   if (warp == kMmaWarp) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
@@ -148,10 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       wp.init(p.prof, 0);
       const long long t_role = clock64();
       uint32_t kv_cnt = 0, item_cnt = 0;
-      Item nxt = load_item_or_empty(p, blockIdx.x, n_work);
-      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+      Item nxt = load_item_or_empty(p, tc::snake_work(0), n_work);
+      for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
         const Item it = nxt;
-        nxt = load_item_or_empty(p, w + gridDim.x, n_work);  // hidden behind this item
+        nxt = load_item_or_empty(p, tc::snake_work(k + 1), n_work);  // hidden behind this item
         wp.wait(q_empty, (item_cnt & 1) ^ 1, 0);
         tc::mbar_expect_tx(q_full, (it.has_b ? 2 : 1) * L::kTile);
         for (int t = 0; t < (it.has_b ? 2 : 1); ++t)
@@ -218,11 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         wp.add(5, clock64() - t0);
         wp.add(6, BN / 16);
       };
-      Item nxt = load_item_or_empty(p, blockIdx.x, n_work);
-      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item_cnt) {
+      Item nxt = load_item_or_empty(p, tc::snake_work(0), n_work);
+      for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
         const long long t_li = clock64();
         const Item it = nxt;
-        nxt = load_item_or_empty(p, w + gridDim.x, n_work);
+        nxt = load_item_or_empty(p, tc::snake_work(k + 1), n_work);
         const int nt = it.has_b ? 2 : 1;
         wp.add(1, clock64() - t_li);
         wp.wait_warp(q_full, item_cnt & 1, 0);
@@ -268,10 +269,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(row == 0 && t == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
-    Item nxt = load_item_or_empty(p, blockIdx.x, n_work);
-    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    Item nxt = load_item_or_empty(p, tc::snake_work(0), n_work);
+    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k)) {
       const Item it = nxt;
-      nxt = load_item_or_empty(p, w + gridDim.x, n_work);
+      nxt = load_item_or_empty(p, tc::snake_work(k + 1), n_work);
       if (t == 1 && !it.has_b) continue;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < it.nkv; ++j) {
@@ -426,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem);
   }
+  tc::cta_time_mark(p.prof, 1);
 }
 
 }  // namespace fa

@@ -55,9 +55,9 @@ struct WaitProf {
   bool tr = false;
   __device__ __forceinline__ void init(unsigned long long* gp, int b) {
     base = b;
-    const bool trace_mode = gp != nullptr && gp[63] != 0;
-    tr = trace_mode && blockIdx.x == 0;
-    g = (gp && (!trace_mode || blockIdx.x == 0)) ? gp + b : nullptr;
+    const bool cta0_mode = gp != nullptr && gp[63] != 0;   // 1: trace CTA 0; 3: per-CTA start/end times
+    tr = gp != nullptr && gp[63] == 1 && blockIdx.x == 0;
+    g = (gp && (!cta0_mode || blockIdx.x == 0)) ? gp + b : nullptr;
   }
   __device__ __forceinline__ void trace(int code) {
     if (!tr || n_tr >= kRoleCap) return;
@@ -95,6 +95,22 @@ __device__ __forceinline__ void cp_async_4(uint32_t sdst, const void* gsrc) {
 // arrive on `bar` once all of this thread's prior cp.async copies land (counts against the init count)
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Work order of the persistent kernels over an LPT-sorted list (cost descending): CTA b takes, in round k,
+// index k*G + b for even k and k*G + (G-1-b) for odd k ("snake" order). Plain round robin hands the
+// lowest-numbered CTAs the largest item of every round; alternating the direction cancels that bias.
+__device__ __forceinline__ int64_t snake_work(int64_t k) {
+  const int64_t G = gridDim.x;
+  return k * G + ((k & 1) ? (G - 1 - (int64_t)blockIdx.x) : (int64_t)blockIdx.x);
+}
+
+// JG_WAIT_PROF=3: each CTA's %globaltimer at entry and exit (load-balance / tail diagnostics)
+__device__ __forceinline__ void cta_time_mark(unsigned long long* gp, int slot) {
+  if (gp == nullptr || gp[63] != 3 || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  gp[65 + 2 * blockIdx.x + slot] = t;
 }
 
 // ------------------------------------------------------------------ TMA

@@ -56,6 +56,7 @@ inline jg_status make_map_f32(CUtensorMap* m, void* ptr, int64_t rows, int H, in
 
 }  // namespace jg
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -67,12 +68,13 @@ inline unsigned long long* wait_prof_begin(cudaStream_t st) {
   static unsigned long long* buf = nullptr;
   constexpr size_t kWords = 65 + 2 * 5 * 12000;
   const char* e = std::getenv("JG_WAIT_PROF");
-  if (!e || (e[0] != '1' && e[0] != '2')) return nullptr;
+  if (!e || (e[0] != '1' && e[0] != '2' && e[0] != '3')) return nullptr;
   if (!buf && cudaMalloc(&buf, kWords * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
   cudaMemsetAsync(buf, 0, kWords * sizeof(unsigned long long), st);
-  if (e[0] == '2') {
-    const unsigned long long one = 1;
-    cudaMemcpyAsync(buf + 63, &one, sizeof(one), cudaMemcpyHostToDevice, st);
+  if (e[0] == '2' || e[0] == '3') {
+    static const unsigned long long mode_trace = 1, mode_times = 3;
+    cudaMemcpyAsync(buf + 63, e[0] == '2' ? &mode_trace : &mode_times, sizeof(unsigned long long),
+                    cudaMemcpyHostToDevice, st);
     cudaStreamSynchronize(st);
   }
   return buf;
@@ -92,6 +94,27 @@ inline void wait_prof_end(unsigned long long* buf, cudaStream_t st, const char* 
   }
   std::fprintf(stderr, "\n");
   const char* e = std::getenv("JG_WAIT_PROF");
+  if (e && e[0] == '3') {  // per-CTA busy time and the spread of exit times (tail)
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    std::vector<unsigned long long> t(2 * sms);
+    cudaMemcpy(t.data(), buf + 65, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    unsigned long long s0 = ~0ull, e1 = 0, e0 = ~0ull;
+    double busy = 0;
+    int n = 0;
+    for (int b = 0; b < sms; ++b)
+      if (t[2 * b] && t[2 * b + 1]) {
+        s0 = std::min(s0, t[2 * b]);
+        e1 = std::max(e1, t[2 * b + 1]);
+        e0 = std::min(e0, t[2 * b + 1]);
+        busy += (double)(t[2 * b + 1] - t[2 * b]);
+        ++n;
+      }
+    if (n)
+      std::fprintf(stderr, "[cta-times %s] %d CTAs: makespan %.1f us, mean busy %.1f us, first exit %.1f us\n", tag, n,
+                   (e1 - s0) * 1e-3, busy / n * 1e-3, (e0 - s0) * 1e-3);
+  }
   if (e && e[0] == '2') {  // dump CTA 0's wait timeline
     const size_t n = 5 * 12000;
     std::vector<unsigned long long> t(2 * n);
