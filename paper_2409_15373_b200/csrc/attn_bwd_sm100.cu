@@ -34,7 +34,6 @@ constexpr int kThreads = 512;
 constexpr int kSmWarp0 = 4, kDqWarp0 = 12;
 constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 of the 64 query columns
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kPrefetch = 6;   // query blocks prefetched into L2 ahead of the producer
 constexpr int kQdStages = 4;  // (Q_j, dO_j) smem ring depth (4: better at item boundaries; 3 leaves room for one 64-row dQ reduce)
 constexpr int kPdsBufs = 1;   // dS^T smem buffers
 
@@ -178,14 +177,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
       const float* lse_h = p.lsd + (int64_t)h * p.total_rows;
       const float* del_h = p.lsd + ((int64_t)H + h) * p.total_rows;
-      if (lane == 0) {
-        // L2 prefetch of the first query blocks of this item before waiting for the K/V buffers
-        for (int j = 0; j < kPrefetch && j < nq; ++j)
-          for (int c = 0; c < D / 64; ++c) {
-            tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(b0 + (int64_t)j * BQ));
-            tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(b0 + (int64_t)j * BQ));
-          }
-      }
       wp.wait_warp(v_empty, (item_cnt & 1) ^ 1, 2);
       if (lane == 0) {
         tc::mbar_expect_tx(v_full, L::kTileKV);
@@ -198,28 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < D / 64; ++c)
           tc::tma_load_3d(smem + L::kK + c * L::kChunkKV, &tm_k, k_full, c * 64, h, kv_row);
         if (wp.g) wp.trace(50);
-        // warm L2 with the next item's K/V: its loads wait for this item's last MMAs (kv_empty)
-        const int64_t wn = tc::snake_work(k + 1);
-        if (wn < n_work) {
-          const int2 itn = p.items[wn / H];
-          const int hn = (int)(wn % H);
-          const int kv_next = (int)(p.off[itn.x] + (int64_t)itn.y * BKV);
-          for (int c = 0; c < D / 64; ++c) {
-            tc::tma_prefetch_l2_3d(&tm_k, c * 64, hn, kv_next);
-            tc::tma_prefetch_l2_3d(&tm_v, c * 64, hn, kv_next);
-          }
-        }
       }
       for (int j = 0; j < nq; ++j, ++qd_cnt) {
         const uint32_t s = qd_cnt % L::kStages;
         const int64_t q_row = b0 + (int64_t)j * BQ;
-        // keep kPrefetch query blocks ahead of the smem ring warm in L2 (the kv-tile CTAs of one sample
-        // stream the same Q/dO blocks in lockstep, so without this every block pays DRAM latency)
-        if (lane == 0 && j + kPrefetch < nq)
-          for (int c = 0; c < D / 64; ++c) {
-            tc::tma_prefetch_l2_3d(&tm_q, c * 64, h, (int)(q_row + kPrefetch * BQ));
-            tc::tma_prefetch_l2_3d(&tm_do, c * 64, h, (int)(q_row + kPrefetch * BQ));
-          }
         wp.wait_warp(qd_empty + s, ((qd_cnt / L::kStages) & 1) ^ 1, 1);
         // lse/Delta: rows past the sample are masked by the softmax; rows past the tensor are not copied
         const uint32_t ls = tc::smem_u32(smem + L::kLse + s * L::kLsdBytes);
