@@ -33,6 +33,10 @@ constexpr int BQ = 64;    // query rows per streamed block
 constexpr int kThreads = 512;
 constexpr int kSmWarp0 = 4, kDqWarp0 = 12;
 constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 of the 64 query columns
+// Dynamic work distribution: the producer takes items from a global counter (in LPT order) and hands
+// them to the other roles through a small smem ring; every other warp consumes each entry once.
+constexpr int kItemSlots = 4;
+constexpr int kItemConsumers = 2 + kSmWarps + 4;  // S and G issuers, softmax warps, drain warps
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kQdStages = 4;  // (Q_j, dO_j) smem ring depth (4: better at item boundaries; 3 leaves room for one 64-row dQ reduce)
 constexpr int kPdsBufs = 1;   // dS^T smem buffers
@@ -53,8 +57,9 @@ struct Smem {
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 -lse*log2(e) + 64 -Delta, fp32
   static constexpr int kLse = kStg + kStgRows * D * 4;      // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
-  static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2;
-  static constexpr int kBytes = kBar + kNumBars * 8 + 16;
+  static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2 + 2 * kItemSlots;
+  static constexpr int kItemRing = kBar + kNumBars * 8 + 16;  // kItemSlots work indices (int64)
+  static constexpr int kBytes = kBar + kNumBars * 8 + 16 + kItemSlots * 8;
   // no alignment slack: the dynamic smem base is 1024-aligned (declared so; checked at kernel entry)
   static constexpr int kAlloc = kBytes;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -74,6 +79,7 @@ struct Params {
   float scale;
   int dbg;                   // JG_BWD_DBG diagnostic bits (results invalid when set): 1 skip the dQ reduce,
                              // 4 skip the P/dS smem stores, 64 skip the main kernel, 128 sync + report after it
+  unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23, drain 24-31)
 };
 
@@ -119,7 +125,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dq_empty = dq_full + 2;           // [2] dQ^T_j lives in score buffer j&1
   uint64_t* dkv_full = dq_empty + 2;
   uint64_t* dkv_empty = dkv_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_empty + 1);
+  uint64_t* item_full = dkv_empty + 1;        // [kItemSlots]
+  uint64_t* item_empty = item_full + kItemSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_empty + kItemSlots);
+  volatile int64_t* item_ring = reinterpret_cast<volatile int64_t*>(smem + L::kItemRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -142,6 +151,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::mbar_init(dq_full + 1, 1);
     tc::mbar_init(dkv_full, 1);
     tc::mbar_init(dkv_empty, 4);
+    for (int s = 0; s < kItemSlots; ++s) {
+      tc::mbar_init(item_full + s, 1);
+      tc::mbar_init(item_empty + s, kItemConsumers);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -159,6 +172,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const int H = p.H;
   const int64_t n_work = *p.n_items * H;
+  // a consumer warp's next work index (the producer publishes n_work as the end marker)
+  auto take_item = [&](uint32_t ic) -> int64_t {
+    const uint32_t s = ic % kItemSlots;
+    tc::mbar_wait(item_full + s, (ic / kItemSlots) & 1);
+    const int64_t w = item_ring[s];
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(item_empty + s);
+    return w;
+  };
 
   if (warp == 0) {
     // ===================================================== producer warp
@@ -169,7 +191,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     wp.init(lane == 0 ? p.prof : nullptr, 0);
     const long long t_role = clock64();
     uint32_t item_cnt = 0, qd_cnt = 0;
-    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
+    int64_t w_next = blockIdx.x;  // first round static, then the global counter (LPT order)
+    for (;; ++item_cnt) {
+      const int64_t w = w_next < n_work ? w_next : n_work;
+      {  // publish to the consumer warps
+        const uint32_t s = item_cnt % kItemSlots;
+        wp.wait_warp(item_empty + s, ((item_cnt / kItemSlots) & 1) ^ 1, 3);
+        if (lane == 0) {
+          item_ring[s] = w;
+          tc::mbar_arrive(item_full + s);
+        }
+      }
+      if (w >= n_work) break;
+      if (lane == 0) w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
+      w_next = __shfl_sync(0xffffffffu, w_next, 0);
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
       const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
@@ -241,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long t_role = clock64();
       // per-buffer phase parities live in bit b of a register (a runtime-indexed [2] array goes to local memory)
       uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill_par = 0;
-      for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
+      for (int64_t w = take_item(item_cnt); w < n_work; w = take_item(++item_cnt)) {
         const int2 it = p.items[w / H];
         const int64_t n = p.off[it.x + 1] - p.off[it.x];
         const int nq = (int)((n + BQ - 1) / BQ);
@@ -334,7 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
-    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k)) {
+    uint32_t ic = 0;
+    for (int64_t w = take_item(ic); w < n_work; w = take_item(++ic)) {
       const int2 it = p.items[w / H];
       const int64_t n = p.off[it.x + 1] - p.off[it.x];
       const int nq = (int)((n + BQ - 1) / BQ);
@@ -424,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 24);
     const long long t_role = clock64();
-    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
+    for (int64_t w = take_item(item_cnt); w < n_work; w = take_item(++item_cnt)) {
       const int2 it = p.items[w / H];
       const int h = (int)(w % H);
       const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
@@ -590,9 +626,12 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
     JG_CUDA(cudaFuncSetAttribute(fb::jfa_bwd_sm100_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
     attr_set = true;
   }
+  // the work counter lives in the workspace's slack after the dQ accumulator
+  auto* counter = reinterpret_cast<unsigned long long*>(dq_acc + units * kD);
+  JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   fb::Params p{off, items, n_items, total_rows, H, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), std::getenv("JG_BWD_DBG") ? std::atoi(std::getenv("JG_BWD_DBG")) : 0,
-               wait_prof_begin(st)};
+               counter, wait_prof_begin(st)};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
   if (!(p.dbg & 64)) fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
   if (p.dbg & 128) {
@@ -601,7 +640,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   }
   JG_LAUNCHED("jfa_bwd_sm100_kernel");
   wait_prof_end(p.prof, st, "bwd",
-                {"P.k_empty", "P.qd_empty", "P.v_empty", "", "", "", "", "P.total", "M.k_full", "M.v_full", "M.qd_full",
+                {"P.k_empty", "P.qd_empty", "P.v_empty", "P.item_empty", "", "", "", "P.total", "M.k_full", "M.v_full", "M.qd_full",
                  "M.pt_free", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
                  "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
