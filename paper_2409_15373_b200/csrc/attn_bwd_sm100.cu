@@ -58,8 +58,8 @@ struct Smem {
   static constexpr int kLse = kStg + kStgRows * D * 4;      // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
   static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2 + 2 * kItemSlots;
-  static constexpr int kItemRing = kBar + kNumBars * 8 + 16;  // kItemSlots work indices (int64)
-  static constexpr int kBytes = kBar + kNumBars * 8 + 16 + kItemSlots * 8;
+  static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 32-byte descriptors
+  static constexpr int kBytes = kItemRing + kItemSlots * 32;
   // no alignment slack: the dynamic smem base is 1024-aligned (declared so; checked at kernel entry)
   static constexpr int kAlloc = kBytes;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -128,7 +128,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* item_full = dkv_empty + 1;        // [kItemSlots]
   uint64_t* item_empty = item_full + kItemSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_empty + kItemSlots);
-  volatile int64_t* item_ring = reinterpret_cast<volatile int64_t*>(smem + L::kItemRing);
+  // ring slot: (sample, key tile, head, end) (b0 lo, b0 hi, n lo, n hi) — the producer's decoded item, so
+  // the other roles never touch the work list or the offsets
+  const uint32_t item_ring = tc::smem_u32(smem + L::kItemRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -173,13 +175,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int H = p.H;
   const int64_t n_work = *p.n_items * H;
   // a consumer warp's next work index (the producer publishes n_work as the end marker)
-  auto take_item = [&](uint32_t ic) -> int64_t {
+  struct Work {
+    int2 it;
+    int h;
+    int64_t b0, n;
+  };
+  auto take_item = [&](uint32_t ic, Work& wk) -> bool {
     const uint32_t s = ic % kItemSlots;
     tc::mbar_wait(item_full + s, (ic / kItemSlots) & 1);
-    const int64_t w = item_ring[s];
+    const uint4 a = tc::ld_shared_v4u(item_ring + s * 32), c = tc::ld_shared_v4u(item_ring + s * 32 + 16);
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(item_empty + s);
-    return w;
+    wk.it = make_int2((int)a.x, (int)a.y);
+    wk.h = (int)a.z;
+    wk.b0 = (int64_t)(((uint64_t)c.y << 32) | c.x);
+    wk.n = (int64_t)(((uint64_t)c.w << 32) | c.z);
+    return a.w == 0;
   };
 
   if (warp == 0) {
@@ -194,20 +205,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t w_next = blockIdx.x;  // first round static, then the global counter (LPT order)
     for (;; ++item_cnt) {
       const int64_t w = w_next < n_work ? w_next : n_work;
-      {  // publish to the consumer warps
+      int2 it = make_int2(0, 0);
+      int64_t b0 = 0, n = 0;
+      if (w < n_work) {
+        it = p.items[w / H];
+        b0 = p.off[it.x];
+        n = p.off[it.x + 1] - b0;
+      }
+      const int h = (int)(w % H);
+      {  // publish the decoded item to the consumer warps
         const uint32_t s = item_cnt % kItemSlots;
         wp.wait_warp(item_empty + s, ((item_cnt / kItemSlots) & 1) ^ 1, 3);
         if (lane == 0) {
-          item_ring[s] = w;
+          tc::st_shared_v4(item_ring + s * 32, (uint32_t)it.x, (uint32_t)it.y, (uint32_t)h, w >= n_work ? 1u : 0u);
+          tc::st_shared_v4(item_ring + s * 32 + 16, (uint32_t)b0, (uint32_t)((uint64_t)b0 >> 32), (uint32_t)n,
+                           (uint32_t)((uint64_t)n >> 32));
           tc::mbar_arrive(item_full + s);
         }
       }
       if (w >= n_work) break;
       if (lane == 0) w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
       w_next = __shfl_sync(0xffffffffu, w_next, 0);
-      const int2 it = p.items[w / H];
-      const int h = (int)(w % H);
-      const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
       const int nq = (int)((n + BQ - 1) / BQ);
       const int kv_row = (int)(b0 + (int64_t)it.y * BKV);
       const float* lse_h = p.lsd + (int64_t)h * p.total_rows;
@@ -276,9 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long t_role = clock64();
       // per-buffer phase parities live in bit b of a register (a runtime-indexed [2] array goes to local memory)
       uint32_t item_cnt = 0, qd_cnt = 0, p_cnt = 0, fill_par = 0;
-      for (int64_t w = take_item(item_cnt); w < n_work; w = take_item(++item_cnt)) {
-        const int2 it = p.items[w / H];
-        const int64_t n = p.off[it.x + 1] - p.off[it.x];
+      Work wk;
+      for (bool more = take_item(item_cnt, wk); more; more = take_item(++item_cnt, wk)) {
+        const int2 it = wk.it;
+        const int64_t n = wk.n;
         const int nq = (int)((n + BQ - 1) / BQ);
         if (warp == 1) {
           wp.wait_warp(k_full, item_cnt & 1, 0);
@@ -370,9 +389,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     wp.init(tid == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
     uint32_t ic = 0;
-    for (int64_t w = take_item(ic); w < n_work; w = take_item(++ic)) {
-      const int2 it = p.items[w / H];
-      const int64_t n = p.off[it.x + 1] - p.off[it.x];
+    Work wk;
+    for (bool more = take_item(ic, wk); more; more = take_item(++ic, wk)) {
+      const int2 it = wk.it;
+      const int64_t n = wk.n;
       const int nq = (int)((n + BQ - 1) / BQ);
       const bool row_valid = (int64_t)it.y * BKV + row < n;
       for (int j = 0; j < nq; ++j, ++qd_cnt) {
@@ -460,10 +480,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(tid == 0 ? p.prof : nullptr, 24);
     const long long t_role = clock64();
-    for (int64_t w = take_item(item_cnt); w < n_work; w = take_item(++item_cnt)) {
-      const int2 it = p.items[w / H];
-      const int h = (int)(w % H);
-      const int64_t b0 = p.off[it.x], n = p.off[it.x + 1] - b0;
+    Work wk;
+    for (bool more = take_item(item_cnt, wk); more; more = take_item(++item_cnt, wk)) {
+      const int2 it = wk.it;
+      const int h = wk.h;
+      const int64_t b0 = wk.b0, n = wk.n;
       const int nq = (int)((n + BQ - 1) / BQ);
       for (int j = 0; j < nq; ++j) {
         const int b = j & 1;

@@ -37,6 +37,10 @@ constexpr int BM = 128;          // query rows per tile (two tiles per work item
 constexpr int BN = 128;          // keys per block
 constexpr int kThreads = 320;    // 10 warps
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
+// Dynamic work distribution: the producer takes items from a global counter (in LPT order) and hands them
+// to the MMA warp and the 8 softmax warps through a small smem ring.
+constexpr int kItemSlots = 4;
+constexpr int kItemConsumers = 1 + 8;
 constexpr int kPolyExp = 2;               // of every 8 exponentials, this many run on the FMA pipe (ex2_poly)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
 
@@ -50,8 +54,9 @@ struct Smem {
   static constexpr int kKV = kQ + 2 * kTile;
   static constexpr int kBar = kKV + kStages * kTile;
   // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_done[2], o_empty[2], tmem slot
-  static constexpr int kNumBars = 2 + 2 * kStages + 8 + 1;
-  static constexpr int kBytes = kBar + kNumBars * 8 + 16;
+  static constexpr int kNumBars = 2 + 2 * kStages + 8 + 1 + 2 * kItemSlots;
+  static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 32-byte descriptors
+  static constexpr int kBytes = kItemRing + kItemSlots * 32;
   static constexpr int kAlloc = kBytes + 1024;          // manual 1 KB alignment
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
@@ -66,6 +71,7 @@ struct Params {
   float* lse;
   float scale_log2;
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23)
+  unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
   int dbg;                   // JG_FWD_DBG (diagnostic, results invalid): 1 = softmax publishes P without computing
 };
 
@@ -87,14 +93,6 @@ __device__ __forceinline__ Item load_item(const Params& p, int64_t w) {
   return r;
 }
 
-// the next work item's descriptor, loaded one item ahead by every role (its two dependent global loads
-// would otherwise sit at the start of every item); past the end: an empty item that is never used
-__device__ __forceinline__ Item load_item_or_empty(const Params& p, int64_t w, int64_t n_work) {
-  if (w < n_work) return load_item(p, w);
-  Item r{};
-  return r;
-}
-
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     jfa_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -111,7 +109,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = s_full + 2;             // [2]
   uint64_t* o_done = p_full + 2;             // [2] last PV of an item
   uint64_t* o_empty = o_done + 2;            // [2] epilogue drained O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* item_full = o_empty + 2;  // [kItemSlots]
+  uint64_t* item_empty = item_full + kItemSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_empty + kItemSlots);
+  // ring slot: (b0 lo, b0 hi, n, q_row) (h, nkv, has_b, end) — the producer's decoded item, so the other
+  // roles never touch the work list or the offsets
+  const uint32_t item_ring = tc::smem_u32(smem + L::kItemRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -127,6 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(o_done + t, 1);
       tc::mbar_init(o_empty + t, 4);
     }
+    for (int s = 0; s < kItemSlots; ++s) {
+      tc::mbar_init(item_full + s, 1);
+      tc::mbar_init(item_empty + s, kItemConsumers);
+    }
     tc::fence_barrier_init();
   }
   if (warp == kProducerWarp && lane == 0) {
@@ -141,6 +148,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t n_work = *p.n_items * p.H;
+  // a consumer warp's next work index (the producer publishes n_work as the end marker)
+  auto take_item = [&](uint32_t ic, Item& it) -> bool {
+    const uint32_t s = ic % kItemSlots;
+    tc::mbar_wait(item_full + s, (ic / kItemSlots) & 1);
+    const uint4 a = tc::ld_shared_v4u(item_ring + s * 32), b = tc::ld_shared_v4u(item_ring + s * 32 + 16);
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(item_empty + s);
+    it.b0 = (int64_t)(((uint64_t)a.y << 32) | a.x);
+    it.n = (int)a.z;
+    it.q_row = (int)a.w;
+    it.h = (int)b.x;
+    it.nkv = (int)b.y;
+    it.has_b = b.z != 0;
+    return b.w == 0;
+  };
 
   if (warp == kProducerWarp) {
     // ===================================================== TMA producer
@@ -149,10 +171,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       wp.init(p.prof, 0);
       const long long t_role = clock64();
       uint32_t kv_cnt = 0, item_cnt = 0;
-      Item nxt = load_item_or_empty(p, tc::snake_work(0), n_work);
-      for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
-        const Item it = nxt;
-        nxt = load_item_or_empty(p, tc::snake_work(k + 1), n_work);  // hidden behind this item
+      int64_t w_next = blockIdx.x;  // first round static, then the global counter (LPT order)
+      for (;; ++item_cnt) {
+        const int64_t w = w_next < n_work ? w_next : n_work;
+        Item it{};
+        if (w < n_work) it = load_item(p, w);
+        const uint32_t slot = item_cnt % kItemSlots;
+        wp.wait(item_empty + slot, ((item_cnt / kItemSlots) & 1) ^ 1, 2);
+        tc::st_shared_v4(item_ring + slot * 32, (uint32_t)it.b0, (uint32_t)((uint64_t)it.b0 >> 32), (uint32_t)it.n,
+                         (uint32_t)it.q_row);
+        tc::st_shared_v4(item_ring + slot * 32 + 16, (uint32_t)it.h, (uint32_t)it.nkv, it.has_b ? 1u : 0u,
+                         w >= n_work ? 1u : 0u);
+        tc::mbar_arrive(item_full + slot);
+        if (w >= n_work) break;
+        w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
         wp.wait(q_empty, (item_cnt & 1) ^ 1, 0);
         tc::mbar_expect_tx(q_full, (it.has_b ? 2 : 1) * L::kTile);
         for (int t = 0; t < (it.has_b ? 2 : 1); ++t)
@@ -219,11 +251,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         wp.add(5, clock64() - t0);
         wp.add(6, BN / 16);
       };
-      Item nxt = load_item_or_empty(p, tc::snake_work(0), n_work);
-      for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k), ++item_cnt) {
+      Item it;
+      for (bool more = take_item(item_cnt, it); more; more = take_item(++item_cnt, it)) {
         const long long t_li = clock64();
-        const Item it = nxt;
-        nxt = load_item_or_empty(p, tc::snake_work(k + 1), n_work);
         const int nt = it.has_b ? 2 : 1;
         wp.add(1, clock64() - t_li);
         wp.wait_warp(q_full, item_cnt & 1, 0);
@@ -269,10 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::WaitProf wp;
     wp.init(row == 0 && t == 0 ? p.prof : nullptr, 16);
     const long long t_role = clock64();
-    Item nxt = load_item_or_empty(p, tc::snake_work(0), n_work);
-    for (int64_t k = 0, w = tc::snake_work(0); w < n_work; ++k, w = tc::snake_work(k)) {
-      const Item it = nxt;
-      nxt = load_item_or_empty(p, tc::snake_work(k + 1), n_work);
+    uint32_t ic = 0;
+    Item it;
+    for (bool more = take_item(ic, it); more; more = take_item(++ic, it)) {
       if (t == 1 && !it.has_b) continue;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < it.nkv; ++j) {
@@ -456,15 +485,21 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
                                      std::to_string(fa_attr.maxThreadsPerBlock) + " threads per block");
     attr_set = true;
   }
+  unsigned long long* counter = nullptr;  // stream-ordered 8-byte work counter for this launch
+  JG_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), st));
+  JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   fa::Params p{off, items, n_items, batch, total_rows, H, (__nv_bfloat16*)out, lse,
-               1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st),
+               1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st), counter,
                std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0};
   const int64_t work = max_items * H;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sm_count(), work));
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
-  JG_LAUNCHED("jfa_fwd_sm100_kernel");
+  const cudaError_t launch_err = cudaGetLastError();
+  cudaFreeAsync(counter, st);
+  if (launch_err != cudaSuccess) return cuda_status(launch_err, "jfa_fwd_sm100_kernel");
+  count_launch();
   wait_prof_end(p.prof, st, "fwd",
-                {"P.q_empty", "P.kv_empty", "", "", "", "", "", "P.total", "M.q_full", "M.load_item", "M.kv_full", "M.o_empty",
+                {"P.q_empty", "P.kv_empty", "P.item_empty", "", "", "", "", "P.total", "M.q_full", "M.load_item", "M.kv_full", "M.o_empty",
                  "M.p_full", "M.issue_cyc", "M.n_mma(x1e-2%)", "M.total", "S.s_full", "", "S.o_done", "S.compute", "S.blocks(x1e-2%)", "", "", "S.total"});
   return JG_OK;
 }

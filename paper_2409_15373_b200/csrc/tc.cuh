@@ -355,6 +355,12 @@ __device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
+__device__ __forceinline__ uint4 ld_shared_v4u(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
 // byte offset of element (row, col) inside a [rows x 64] bf16 SWIZZLE_128B K-major chunk
 __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t col16B) {
   return row * 128u + ((col16B ^ (row & 7u)) << 4);
