@@ -97,14 +97,6 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Work order of the persistent kernels over an LPT-sorted list (cost descending): CTA b takes, in round k,
-// index k*G + b for even k and k*G + (G-1-b) for odd k ("snake" order). Plain round robin hands the
-// lowest-numbered CTAs the largest item of every round; alternating the direction cancels that bias.
-__device__ __forceinline__ int64_t snake_work(int64_t k) {
-  const int64_t G = gridDim.x;
-  return k * G + ((k & 1) ? (G - 1 - (int64_t)blockIdx.x) : (int64_t)blockIdx.x);
-}
-
 // JG_WAIT_PROF=3: each CTA's %globaltimer at entry and exit (load-balance / tail diagnostics)
 __device__ __forceinline__ void cta_time_mark(unsigned long long* gp, int slot) {
   if (gp == nullptr || gp[63] != 3 || threadIdx.x != 0) return;
