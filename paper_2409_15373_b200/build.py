@@ -23,7 +23,8 @@ LIB = os.path.join(PKG, "libjagged_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-                "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+                "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC] + \
+    os.environ.get("JG_NVCC_DEFS", "").split()  # tuning variants for A/B runs, e.g. "-DJG_BWD_QD_STAGES=3"
 
 
 def _headers_mtime() -> float:

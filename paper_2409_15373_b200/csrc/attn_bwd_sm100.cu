@@ -38,7 +38,10 @@ constexpr int kSmWarps = 8;  // two warps per TMEM lane quarter, each owning 32 
 constexpr int kItemSlots = 4;
 constexpr int kItemConsumers = 2 + kSmWarps + 4;  // S and G issuers, softmax warps, drain warps
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kQdStages = 4;  // (Q_j, dO_j) smem ring depth (4: better at item boundaries; 3 leaves room for one 64-row dQ reduce)
+#ifndef JG_BWD_QD_STAGES
+#define JG_BWD_QD_STAGES 4
+#endif
+constexpr int kQdStages = JG_BWD_QD_STAGES;  // (Q_j, dO_j) smem ring depth (4: better at item boundaries; 3 leaves room for one 64-row dQ reduce)
 constexpr int kPdsBufs = 1;   // dS^T smem buffers
 
 template <int D>
@@ -52,10 +55,11 @@ struct Smem {
   static constexpr int kV = kK + kTileKV;
   static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
   static constexpr int kDS = kQD + kStages * 2 * kTileQ;    // kPdsBufs x dS^T [128 keys x 64 q] bf16 (P^T is in TMEM)
-  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging [kStgRows q x D] fp32
-  static constexpr int kStgRows = kQdStages > 3 ? 32 : 64;  // dQ rows per TMA reduce (32: two per block)
+  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging: kStgBufs x [kStgRows q x D] fp32
+  static constexpr int kStgRows = 16;                       // dQ rows per TMA reduce (four per block)
+  static constexpr int kStgBufs = kQdStages > 3 ? 2 : 4;    // fill one while the TMA reads the others
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 -lse*log2(e) + 64 -Delta, fp32
-  static constexpr int kLse = kStg + kStgRows * D * 4;      // kStages x kLsdBytes, loaded with (Q_j, dO_j)
+  static constexpr int kLse = kStg + kStgBufs * kStgRows * D * 4;  // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
   static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2 + 2 * kItemSlots;
   static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 32-byte descriptors
@@ -78,7 +82,7 @@ struct Params {
   float scale_log2;
   float scale;
   int dbg;                   // JG_BWD_DBG diagnostic bits (results invalid when set): 1 skip the dQ reduce,
-                             // 4 skip the P/dS smem stores, 64 skip the main kernel, 128 sync + report after it
+                             // 4 skip the P/dS smem stores, 8 skip the dK/dV stores, 64 skip the main kernel, 128 sync + report after it
   unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23, drain 24-31)
 };
@@ -97,6 +101,8 @@ __device__ __forceinline__ void tensor_reduce_add_3d(const CUtensorMap* map, uin
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 
@@ -498,54 +504,80 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(dq_empty + b);
-        // two [32 q x D] fp32 boxes through the staging buffer, one TMA tensor reduce-add each; rows of padded
-        // queries are exactly zero (P = 0 there), so adding them into the next sample's rows is a no-op
+        // four [16 q x D] fp32 boxes through two alternating staging buffers, one TMA tensor reduce-add each
+        // (the drain fills one buffer while the TMA unit reads the other); rows of padded queries are exactly
+        // zero (P = 0 there), so adding them into the next sample's rows is a no-op
+        static_assert((BQ / L::kStgRows) % L::kStgBufs == 0, "buffer index must be static per sub-block");
 #pragma unroll
         for (int hh = 0; hh < BQ / L::kStgRows; ++hh) {
+          const uint32_t sb = stg_base + (hh % L::kStgBufs) * (L::kStgRows * D * 4);
           const long long tb = clock64();
-          if (tid == 0) bulk_wait_read0();  // the previous reduction has read the staging buffer
+          if (tid == 0) bulk_wait_read<L::kStgBufs - 1>();  // the reduction issued from this buffer has read it
           named_bar(2, 128);
           wp.add(1, clock64() - tb);
 #pragma unroll
           for (int q = 0; q < L::kStgRows; ++q) {
             const int qq = hh * L::kStgRows + q;
-            tc::st_shared_f32(stg_base + (q * D + tid) * 4, __uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]) * p.scale);
+            tc::st_shared_f32(sb + (q * D + tid) * 4, __uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]) * p.scale);
           }
           tc::fence_proxy_async_smem();
           named_bar(2, 128);
           if (tid == 0 && !(p.dbg & 1)) {
-            tensor_reduce_add_3d(&tm_dq, stg_base, 0, h, (int)(b0 + (int64_t)j * BQ + L::kStgRows * hh));
+            tensor_reduce_add_3d(&tm_dq, sb, 0, h, (int)(b0 + (int64_t)j * BQ + L::kStgRows * hh));
             bulk_commit();
           }
         }
       }
-      // dK / dV for this key tile
+      // dK / dV for this key tile. A thread holds one key row; rows are 1 KB apart in HBM, so each warp
+      // transposes its 32 rows x 64 columns through a private 4 KB slice of the (now idle) dQ staging
+      // buffer and writes them back as whole 128-byte lines (four rows per instruction). Per-thread 16-byte
+      // row stores would leave every sector half-written and flood the SM's outbound path exactly when the
+      // next item's K/V/Q loads are issued.
       wp.wait_warp(dkv_full, item_cnt & 1, 2);
       tc::tc_fence_after();
-      const int64_t kv_local = (int64_t)it.y * BKV + tid;
-      const bool store = kv_local < n;
-      const int64_t gofs = ((b0 + kv_local) * H + h) * D;
-#pragma unroll
+      {
+        const long long tb = clock64();
+        if (tid == 0) bulk_wait_read0();  // the last dQ reductions have read the staging buffers
+        named_bar(2, 128);
+        wp.add(3, clock64() - tb);
+        if (wp.g) wp.trace(75);
+      }
+      const uint32_t xs = stg_base + wq * 4096;  // this warp's [32 rows x 128 B] slice, 16-byte chunks XOR row&7
+      const int64_t tile0 = (int64_t)it.y * BKV + wq * 32;  // first key row of this warp (sample-local)
+#pragma unroll 1
       for (int which = 0; which < 2; ++which) {
         const uint32_t col = which == 0 ? 256 : 384;
         const float sc = which == 0 ? 1.f : p.scale;
-        __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + gofs;
+        __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + ((b0 + tile0) * H + h) * D;  // this warp's first row
+#pragma unroll 1
+        for (int half = 0; half < D / 64; ++half) {
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          tc::tmem_ld32(lane_addr + col + c * 32, o);
-          tc::tmem_wait_ld();
-          if (store) {
+          for (int g = 0; g < 2; ++g) {  // 32 columns at a time (register budget)
+            uint32_t o[32];
+            const long long t4 = clock64();
+            tc::tmem_ld32(lane_addr + col + half * 64 + g * 32, o);
+            tc::tmem_wait_ld();
+            wp.add(4, clock64() - t4);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              uint4 v;
-              v.x = tc::pack_bf16(__uint_as_float(o[u * 8 + 0]) * sc, __uint_as_float(o[u * 8 + 1]) * sc);
-              v.y = tc::pack_bf16(__uint_as_float(o[u * 8 + 2]) * sc, __uint_as_float(o[u * 8 + 3]) * sc);
-              v.z = tc::pack_bf16(__uint_as_float(o[u * 8 + 4]) * sc, __uint_as_float(o[u * 8 + 5]) * sc);
-              v.w = tc::pack_bf16(__uint_as_float(o[u * 8 + 6]) * sc, __uint_as_float(o[u * 8 + 7]) * sc);
-              *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = v;
+            for (int uu = 0; uu < 4; ++uu) {
+              const int u = g * 4 + uu;
+#define JG_EPI(k) __uint_as_float(o[uu * 8 + (k)]) * sc
+              tc::st_shared_v4(xs + lane * 128 + ((u ^ (lane & 7)) << 4), tc::pack_bf16(JG_EPI(0), JG_EPI(1)),
+                               tc::pack_bf16(JG_EPI(2), JG_EPI(3)), tc::pack_bf16(JG_EPI(4), JG_EPI(5)),
+                               tc::pack_bf16(JG_EPI(6), JG_EPI(7)));
+#undef JG_EPI
             }
           }
+          __syncwarp();
+          const long long t5 = clock64();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), c = lane & 7;  // row within the warp's 32, 16-byte chunk
+            const uint4 v = tc::ld_shared_v4u(xs + r * 128 + ((c ^ (r & 7)) << 4));
+            if (tile0 + r < n && !(p.dbg & 8)) *reinterpret_cast<uint4*>(dst + (uint32_t)(r * H * D + half * 64 + c * 8)) = v;
+          }
+          __syncwarp();
+          wp.add(5, clock64() - t5);
         }
       }
       tc::tc_fence_before();
@@ -663,7 +695,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   wait_prof_end(p.prof, st, "bwd",
                 {"P.k_empty", "P.qd_empty", "P.v_empty", "P.item_empty", "", "", "", "P.total", "M.k_full", "M.v_full", "M.qd_full",
                  "M.pt_free", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
-                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "", "", "", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
+                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "D.epi_read0", "D.epi_tmem", "D.epi_out", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
   fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,
                                                                                           n4);

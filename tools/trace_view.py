@@ -8,11 +8,11 @@ Each line: time in cycles since the first event, role column, event. A wait prin
 """
 import sys
 
-NAMES = {0: "P.k_empty", 1: "P.qd_empty", 2: "P.v_empty", 8: "S.k_full", 9: "S.v_full", 10: "S.qd_full",
-         11: "S.st_empty", 12: "S.dq_empty", 16: "X.qd_full", 17: "X.st_full", 18: "X.pds_empty", 24: "D.dq_full",
-         26: "D.dkv_full", 32: "G.k_full", 33: "G.dkv_empty", 37: "G.p_full",
+NAMES = {0: "P.k_empty", 1: "P.qd_empty", 2: "P.v_empty", 3: "P.item_empty", 8: "S.k_full", 9: "S.v_full",
+         10: "S.qd_full", 11: "S.pt_free", 12: "S.dq_empty", 16: "X.qd_full", 17: "X.st_full", 18: "X.pds_empty",
+         24: "D.dq_full", 25: "D.stage_bar", 26: "D.dkv_full", 33: "G.dkv_empty", 37: "G.p_full",
          50: "P.KV-issued", 56: "S.start", 57: "S.S-issued", 58: "S.commit-st", 82: "G.commit-all", 83: "G.start", 84: "G.dq-issued", 85: "G.dv-issued", 66: "X.p_full-arrive",
-         74: "D.dkv-done"}
+         74: "D.dkv-done", 75: "D.epi-read0-done"}
 FWD_NAMES = {0: "P.q_empty", 1: "P.kv_empty", 8: "M.q_full", 10: "M.kv_full", 11: "M.o_empty", 12: "M.p_full",
              16: "X.s_full", 18: "X.o_done"}
 COL = {"P": 0, "S": 1, "M": 1, "X": 2, "G": 3, "D": 4}
@@ -33,7 +33,7 @@ def main():
     open_w = {}
     print(f"items {first}..{first + count - 1}: {hi - lo} cycles ({(hi - lo) / 1.9e3:.2f} us @1.9GHz)")
     for t, c in ev:
-        if c < 1000 and (fwd or c not in (50, 56, 57, 58, 82, 83, 84, 85, 66, 74)):
+        if c < 1000 and (fwd or c not in (50, 56, 57, 58, 82, 83, 84, 85, 66, 74, 75)):
             open_w[c] = t
             continue
         if not (lo <= t <= hi):
@@ -41,7 +41,7 @@ def main():
         base = c - 1000 if c >= 1000 else c
         name = NAMES.get(base, str(base))
         extra = f" +{t - open_w.get(base, t)}" if c >= 1000 else ""
-        print(f"{t - lo:9d} " + " " * (22 * COL[name[0]]) + name + extra)
+        print(f"{t - lo:9d} " + " " * (22 * COL.get(name[0], 5)) + name + extra)
 
 
 if __name__ == "__main__":

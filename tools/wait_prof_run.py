@@ -1,7 +1,7 @@
 import torch, numpy as np, sys
 sys.path.insert(0, '.')
 from paper_2409_15373_b200 import jagged as J, synth
-ln = synth.gen_lengths('half-mean', 1024, 0, 1024); off = synth.offsets_of(ln); S = int(off[-1]); H, D = 4, 128
+ln = (np.full(2048, int(sys.argv[1]), np.int64) if len(sys.argv) > 1 else synth.gen_lengths('half-mean', 1024, 0, 1024)); off = synth.offsets_of(ln); S = int(off[-1]); H, D = 4, 128
 mk = lambda: (torch.rand(S, H, D, device='cuda') * 2 - 1).bfloat16()
 T = lambda a: J.JaggedTensor(torch.from_numpy(off).cuda(), a, off)
 Q, K, V, G = T(mk()), T(mk()), T(mk()), T(mk())
