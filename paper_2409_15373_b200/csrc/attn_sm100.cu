@@ -431,15 +431,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tmem_ld32(o_addr + c * 32, o);
         tc::tmem_wait_ld();
         if (store) {
+          uint4 v[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            uint4 v;
-            v.x = tc::pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
-            v.y = tc::pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
-            v.z = tc::pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
-            v.w = tc::pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = v;
+            v[u].x = tc::pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
+            v[u].y = tc::pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
+            v[u].z = tc::pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
+            v[u].w = tc::pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
           }
+          tc::st_global_v8(orow + c * 32, v[0], v[1]);  // whole 32-byte sectors (rows are 1 KB apart)
+          tc::st_global_v8(orow + c * 32 + 16, v[2], v[3]);
         }
       }
       tc::tc_fence_before();
