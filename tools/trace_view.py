@@ -13,8 +13,8 @@ NAMES = {0: "P.k_empty", 1: "P.qd_empty", 2: "P.v_empty", 3: "P.item_empty", 8: 
          24: "D.dq_full", 25: "D.stage_bar", 26: "D.dkv_full", 33: "G.dkv_empty", 37: "G.p_full",
          50: "P.KV-issued", 56: "S.start", 57: "S.S-issued", 58: "S.commit-st", 82: "G.commit-all", 83: "G.start", 84: "G.dq-issued", 85: "G.dv-issued", 66: "X.p_full-arrive",
          74: "D.dkv-done", 75: "D.epi-read0-done"}
-FWD_NAMES = {0: "P.q_empty", 1: "P.kv_empty", 8: "M.q_full", 10: "M.kv_full", 11: "M.o_empty", 12: "M.p_full",
-             16: "X.s_full", 18: "X.o_done"}
+FWD_NAMES = {0: "P.q_empty", 1: "P.kv_empty", 2: "P.item_empty", 8: "M.q_full", 9: "M.load_item", 10: "M.kv_full",
+             11: "M.o_empty", 12: "M.p_full", 16: "X.s_full", 18: "X.o_done"}
 COL = {"P": 0, "S": 1, "M": 1, "X": 2, "G": 3, "D": 4}
 
 
