@@ -500,9 +500,10 @@ def run_configs(args):
 
         ms_j, mem_j = measure(jagged_step)
         # padded inputs [B, H, L, D] built from the same jagged values (jagged_to_dense on device)
-        pad = lambda t: J.jagged_to_dense(J.JaggedTensor(t.offsets, t.values.reshape(S, H * D), off), L, 0.0) \
-            .reshape(B, L, H, D).transpose(1, 2).contiguous()  # noqa: E731
-        qp, kp, vp, gp = pad(Q), pad(K), pad(V), pad(G)
+        pad_blhd = lambda t: J.jagged_to_dense(J.JaggedTensor(t.offsets, t.values.reshape(S, H * D), off), L,  # noqa
+                                               0.0).reshape(B, L, H, D)
+        qd, kd, vd, gd = pad_blhd(Q), pad_blhd(K), pad_blhd(V), pad_blhd(G)
+        qp, kp, vp, gp = (t.transpose(1, 2).contiguous() for t in (qd, kd, vd, gd))  # [B, H, L, D] for torch
         lens = torch.from_numpy(ln).to(dev)
         keymask = torch.arange(L, device=dev)[None, :] < lens[:, None]  # [B, L]
         addmask = torch.zeros(B, 1, 1, L, device=dev, dtype=torch.bfloat16).masked_fill(~keymask[:, None, None, :],
@@ -520,8 +521,14 @@ def run_configs(args):
             o_ = torch.nn.functional.scaled_dot_product_attention(q_, k_, v_, attn_mask=keymask[:, None, None, :])
             o_.backward(gp)
 
+        ws_p = torch.empty(lib.jg_attention_backward_workspace_size(B * L, H, D), dtype=torch.uint8, device=dev)
+
+        def padded_ours_step():  # the same kernels in padded mode (full L^2 work, masks)
+            s_ = J.dense_flash_attention(qd, kd, vd, ln)
+            J.dense_flash_attention_backward(qd, kd, vd, gd, s_, ln, workspace=ws_p)
+
         res = {"jagged_flash (ours)": (ms_j, mem_j)}
-        for name, fn in (("padded dense attention (torch matmul+softmax)", dense_step),
+        for name, fn in (("padded dense flash (ours: same kernels, padded mode)", padded_ours_step),("padded dense attention (torch matmul+softmax)", dense_step),
                          ("padded dense flash (torch SDPA + mask)", flash_step)):
             try:
                 res[name] = measure(fn)
@@ -536,6 +543,8 @@ def run_configs(args):
                           for k2, v2 in res.items()},
               "speedup_vs_dense": res["padded dense attention (torch matmul+softmax)"][0] / ms_j,
               "speedup_vs_dense_flash": res["padded dense flash (torch SDPA + mask)"][0] / ms_j,
+              "speedup_vs_padded_same_kernels": res["padded dense flash (ours: same kernels, padded mode)"][0] / ms_j,
+              "memory_ratio_vs_padded_same_kernels": res["padded dense flash (ours: same kernels, padded mode)"][1] / mem_j,
               "memory_ratio_vs_dense": res["padded dense attention (torch matmul+softmax)"][1] / mem_j,
               "memory_ratio_vs_dense_flash": res["padded dense flash (torch SDPA + mask)"][1] / mem_j})
     if args.out:

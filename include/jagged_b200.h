@@ -176,6 +176,26 @@ jg_status jg_jagged_flash_attention_backward(const int64_t* offsets, int64_t bat
                                              jg_schedule sched, void* workspace, void* stream);
 int64_t jg_attention_backward_workspace_size(int64_t total_rows, int32_t num_heads,
                                              int32_t head_dim);
+/* attention.hpp:55-58 dense_flash_attention (attention.cpp:106-160), GPU padded mode of the same tcgen05 /
+ * SIMT kernels: q/k/v/out are padded [batch, max_len, num_heads, head_dim]; `lengths` is a
+ * HOST array of batch entries, each in [0, max_len] (validated with the reference's messages). Keys past a
+ * sample's length are masked and its rows past the length are zero with lse = -inf (lse: float32
+ * [num_heads, batch * max_len]). The kernels run the full padded max_len^2 work per sample (segments at
+ * offsets i * max_len), which is what makes this the padded baseline of the jagged kernels. */
+jg_status jg_dense_flash_attention_forward(const int64_t* lengths, int64_t batch, int64_t max_len,
+                                           int32_t num_heads, int32_t head_dim, const void* q,
+                                           const void* k, const void* v, int64_t block_q,
+                                           int64_t block_k, void* out, float* lse, jg_dtype dtype,
+                                           void* stream);
+/* Backward of the padded mode (no reference counterpart; used for the padded-vs-jagged training-step
+ * comparison): rows past a sample's length get zero dq/dk/dv. workspace: NULL or
+ * >= jg_attention_backward_workspace_size(batch * max_len, num_heads, head_dim) bytes. */
+jg_status jg_dense_flash_attention_backward(const int64_t* lengths, int64_t batch, int64_t max_len,
+                                            int32_t num_heads, int32_t head_dim, const void* q,
+                                            const void* k, const void* v, const void* grad_out,
+                                            const void* out, const float* lse, int64_t block_q,
+                                            int64_t block_k, void* dq, void* dk, void* dv,
+                                            jg_dtype dtype, void* workspace, void* stream);
 /* attention.hpp:63-65 jagged_attention (unfused baseline): materializes sum Bi^2 scores per head
  * in `scores_workspace` (>= num_heads * sum Bi^2 elements of dtype, or NULL to allocate). */
 jg_status jg_jagged_attention(const int64_t* offsets, const int64_t* sq_offsets, int64_t batch,

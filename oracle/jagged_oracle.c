@@ -575,6 +575,56 @@ int or_dense_attention(const int64_t* lengths, int64_t B, int64_t L, int64_t D, 
   return 0;
 }
 
+/* attention.cpp:106-160: padded dense flash attention. Streams each padded row over key blocks of
+ * block_k with an online softmax; scores with a >= n or c >= n are -inf (:130), a block with no valid score
+ * yet is skipped (:134), rows with no valid key keep out = 0 and lse = -inf (:151-154). lse: B*L entries. */
+int or_dense_flash_attention(const int64_t* lengths, int64_t B, int64_t L, int64_t D, int64_t block_q,
+                             int64_t block_k, const double* q, const double* k, const double* v, double* out,
+                             double* lse) {
+  if (block_q < 1 || block_k < 1) return -1;
+  const double inv = 1.0 / sqrt((double)D);
+  const int64_t bk = block_k < L ? block_k : L;
+  double* row = (double*)malloc(sizeof(double) * (size_t)(bk > 0 ? bk : 1));
+  double* acc = (double*)malloc(sizeof(double) * (size_t)(D > 0 ? D : 1));
+  for (int64_t e = 0; e < B * L * D; ++e) out[e] = 0.0;
+  for (int64_t e = 0; e < B * L; ++e) lse[e] = -INFINITY;
+  for (int64_t i = 0; i < B; ++i) {
+    const int64_t n = lengths[i];
+    for (int64_t a = 0; a < L; ++a) {  /* the block_q loop of :124-125 visits every row once */
+      double m = -INFINITY, sum = 0.0;
+      for (int64_t d = 0; d < D; ++d) acc[d] = 0.0;
+      for (int64_t c0 = 0; c0 < L; c0 += block_k) {
+        const int64_t c1 = c0 + block_k < L ? c0 + block_k : L;
+        double bmax = -INFINITY;
+        for (int64_t c = c0; c < c1; ++c) {
+          const double sc = (a < n && c < n) ? dot_rows(q + (i * L + a) * D, k + (i * L + c) * D, D) * inv : -INFINITY;
+          row[c - c0] = sc;
+          bmax = fmax(bmax, sc);
+        }
+        const double m_new = fmax(m, bmax);
+        if (m_new == -INFINITY) continue;
+        const double rescale = m == -INFINITY ? 0.0 : exp(m - m_new);
+        sum *= rescale;
+        for (int64_t d = 0; d < D; ++d) acc[d] *= rescale;
+        for (int64_t c = c0; c < c1; ++c) {
+          if (row[c - c0] == -INFINITY) continue;
+          const double pr = exp(row[c - c0] - m_new);
+          sum += pr;
+          for (int64_t d = 0; d < D; ++d) acc[d] += pr * v[(i * L + c) * D + d];
+        }
+        m = m_new;
+      }
+      if (sum > 0.0) {
+        for (int64_t d = 0; d < D; ++d) out[(i * L + a) * D + d] = acc[d] / sum;
+        lse[i * L + a] = m + log(sum);
+      }
+    }
+  }
+  free(row);
+  free(acc);
+  return 0;
+}
+
 /* ---- feature interaction, attention.cpp:291-309 ----
  * s = scale(jagged_dense_bmm(k_feat, transpose_per_sample(targets)), 1/sqrt(D))  (:302-303)
  * p = jagged_softmax(s)  (softmax over each segment's rows, per target column)  (:305)

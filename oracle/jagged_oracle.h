@@ -89,6 +89,9 @@ int or_jfa_backward(const int64_t* off, int64_t B, int64_t D, const double* q, c
 /* padded-dense baseline semantics (attention.cpp:62-104) on [B,L,D] with lengths */
 int or_dense_attention(const int64_t* lengths, int64_t B, int64_t L, int64_t D, const double* q,
                        const double* k, const double* v, double* out);
+int or_dense_flash_attention(const int64_t* lengths, int64_t B, int64_t L, int64_t D, int64_t block_q,
+                             int64_t block_k, const double* q, const double* k, const double* v, double* out,
+                             double* lse);
 
 /* ---- feature interaction (attention.cpp:291-309). targets [B, Tq, D] -> out [B, Tq, D].
  * as_float != 0 rounds the scores to float after the 1/sqrt(D) scale and the softmax output to float, as

@@ -147,6 +147,23 @@ int guard(F&& f) {
 REF_T(float, f32)
 REF_T(double, f64)
 
+// the reference's padded dense_flash_attention (attention.cpp:106-160) on [B, L, D] inputs.
+#define REF_DENSE(T, SUF)                                                                                  \
+  extern "C" int ref_dense_flash_attention_##SUF(const int64_t* lengths, int64_t B, int64_t L, int64_t D,  \
+                                                 const T* q, const T* k, const T* v, int64_t bq,           \
+                                                 int64_t bk, int threads, T* out, T* lse) {                \
+    return guard([&] {                                                                                   \
+      auto dt = [&](const T* p) { return jagged::DenseTensor<T>({B, L, D}, vec(p, B * L * D)); };        \
+      const std::vector<int64_t> ln = vec(lengths, B);                                                   \
+      auto s = jagged::dense_flash_attention(dt(q), dt(k), dt(v), std::span<const int64_t>(ln), bq, bk,  \
+                                             kopts(threads, 64));                                        \
+      put(s.output.data(), out);                                                                         \
+      put(s.logsumexp, lse);                                                                             \
+    });                                                                                                  \
+  }
+REF_DENSE(float, f32)
+REF_DENSE(double, f64)
+
 // VJPs: the reference's registry and gradcheck use the double instantiation.
 extern "C" int ref_jagged_dense_bmm_vjp_f64(const int64_t* off, int64_t B, int64_t D, int64_t T,
                                             const double* x, const double* w, const double* go,

@@ -164,6 +164,19 @@ def jfa_forward(off, q, k, v, block_q=64, block_k=64, prec="f64", threads=1):
     return out, lse
 
 
+def dense_flash_attention(lengths, q, k, v, block_q=64, block_k=64, prec="f64", threads=1):
+    """The reference's attention.cpp:106-160 on [B, L, D] -> (out, lse [B*L])."""
+    dt = np.float64 if prec == "f64" else np.float32
+    lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+    q, k, v = (_arr(a, dt) for a in (q, k, v))
+    B, L, D = q.shape
+    out = np.empty_like(q)
+    lse = np.empty(B * L, dt)
+    _chk(getattr(lib(), f"ref_dense_flash_attention_{prec}")(_p(lengths), _I(B), _I(L), _I(D), _p(q), _p(k), _p(v),
+                                                              _I(block_q), _I(block_k), threads, _p(out), _p(lse)))
+    return out, lse
+
+
 def jfa_backward(off, q, k, v, go, out, lse, block_q=64, block_k=64, prec="f64", threads=1):
     dt = _DT[prec]
     off = _arr(off, np.int64)

@@ -58,6 +58,7 @@ def lib():
             "or_jfa_backward": [_i64p, _I64, _I64, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, _I64,
                                 _f64p, _f64p, _f64p],
             "or_dense_attention": [_i64p, _I64, _I64, _I64, _f64p, _f64p, _f64p, _f64p],
+            "or_dense_flash_attention": [_i64p, _I64, _I64, _I64, _I64, _I64, _f64p, _f64p, _f64p, _f64p, _f64p],
             "or_feature_interaction": [_i64p, _I64, _I64, _I64, _f64p, _f64p, _f64p, C.c_int, _f64p],
             "or_jagged_mlp": [_I64, C.c_int, _i64p, _f64p, _f64p, C.POINTER(C.c_int), _f64p, _f64p],
             "or_jagged_mlp_vjp": [_I64, C.c_int, _i64p, _f64p, _f64p, C.POINTER(C.c_int), _f64p, _f64p,
@@ -304,6 +305,18 @@ def dense_attention(lengths, q, k, v):
     out = np.empty_like(q)
     _chk(lib().or_dense_attention(lengths, B, L, D, q.reshape(-1), k.reshape(-1), v.reshape(-1), out.reshape(-1)))
     return out
+
+
+def dense_flash_attention(lengths, q, k, v, block_q=64, block_k=64):
+    """attention.cpp:106-160 -> (out [B, L, D], lse [B*L]) (jagged_oracle.c or_dense_flash_attention)."""
+    lengths = _i64(lengths)
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    B, L, D = q.shape
+    out = np.empty_like(q)
+    lse = np.empty(B * L)
+    _chk(lib().or_dense_flash_attention(lengths, B, L, D, block_q, block_k, q.reshape(-1), k.reshape(-1),
+                                        v.reshape(-1), out.reshape(-1), lse))
+    return out, lse
 
 
 def feature_interaction(off, k_feat, v_feat, targets, as_float=False):

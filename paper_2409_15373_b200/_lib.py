@@ -48,6 +48,8 @@ SIGNATURES = {
     "jg_jagged_flash_attention_backward": [P, I64, I64, I32, I32, P, P, P, P, P, P, I64, I64, P, P, P, C.c_int, P,
                                            P, P],
     "jg_jagged_attention": [P, P, I64, I64, I64, I32, I32, P, P, P, P, C.c_int, P, P],
+    "jg_dense_flash_attention_forward": [P, I64, I64, I32, I32, P, P, P, I64, I64, P, P, C.c_int, P],
+    "jg_dense_flash_attention_backward": [P, I64, I64, I32, I32, P, P, P, P, P, P, I64, I64, P, P, P, C.c_int, P, P],
     "jg_jagged_flash_attention_fwd_bwd_host": [P, I64, I32, I32, P, P, P, P, P, P, P, P, P, C.c_int, P],
     "jg_feature_interaction": [P, I64, I64, I64, I64, P, P, P, P, C.c_int, P, P],
     "jg_mlp_layer_forward": [I64, I64, I64, P, P, P, I32, P, P, C.c_int, P],

@@ -85,6 +85,8 @@ struct Params {
                              // 4 skip the P/dS smem stores, 8 skip the dK/dV stores, 64 skip the main kernel, 128 sync + report after it
   unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23, drain 24-31)
+  const int64_t* valid;      // padded mode: per-sample valid length <= segment length (nullptr: jagged). Keys and
+                             // queries past it get P = dS = 0, so their dQ/dK/dV rows come out zero.
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   struct Work {
     int2 it;
     int h;
-    int64_t b0, n;
+    int64_t b0, n, nv;  // nv: valid keys/queries (== n except in padded mode)
   };
   auto take_item = [&](uint32_t ic, Work& wk) -> bool {
     const uint32_t s = ic % kItemSlots;
@@ -195,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     wk.it = make_int2((int)a.x, (int)a.y);
     wk.h = (int)a.z;
     wk.b0 = (int64_t)(((uint64_t)c.y << 32) | c.x);
-    wk.n = (int64_t)(((uint64_t)c.w << 32) | c.z);
+    wk.n = (int64_t)c.z;
+    wk.nv = (int64_t)c.w;
     return a.w == 0;
   };
 
@@ -212,11 +215,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (;; ++item_cnt) {
       const int64_t w = w_next < n_work ? w_next : n_work;
       int2 it = make_int2(0, 0);
-      int64_t b0 = 0, n = 0;
+      int64_t b0 = 0, n = 0, nv = 0;
       if (w < n_work) {
         it = p.items[w / H];
         b0 = p.off[it.x];
         n = p.off[it.x + 1] - b0;
+        nv = p.valid ? (p.valid[it.x] < n ? p.valid[it.x] : n) : n;
       }
       const int h = (int)(w % H);
       {  // publish the decoded item to the consumer warps
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           tc::st_shared_v4(item_ring + s * 32, (uint32_t)it.x, (uint32_t)it.y, (uint32_t)h, w >= n_work ? 1u : 0u);
           tc::st_shared_v4(item_ring + s * 32 + 16, (uint32_t)b0, (uint32_t)((uint64_t)b0 >> 32), (uint32_t)n,
-                           (uint32_t)((uint64_t)n >> 32));
+                           (uint32_t)nv);
           tc::mbar_arrive(item_full + s);
         }
       }
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int2 it = wk.it;
       const int64_t n = wk.n;
       const int nq = (int)((n + BQ - 1) / BQ);
-      const bool row_valid = (int64_t)it.y * BKV + row < n;
+      const bool row_valid = (int64_t)it.y * BKV + row < wk.nv;
       for (int j = 0; j < nq; ++j, ++qd_cnt) {
         const int b = j & 1;
         const uint32_t s = qd_cnt % L::kStages;
@@ -415,8 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 0);
         const uint32_t lb = lsd + (s * 2 * BQ + half * 32) * 4;
         // queries past the sample end (rows of the next sample in the Q tile) and key rows past it get P = 0
-        const int64_t qrem = n - (int64_t)j * BQ - half * 32;
-        const int qlim = qrem < 32 ? (int)qrem : 32;
+        const int64_t qrem = wk.nv - (int64_t)j * BQ - half * 32;
+        const int qlim = qrem < 32 ? (qrem > 0 ? (int)qrem : 0) : 32;
         const bool full = __all_sync(0xffffffffu, row_valid && qlim == 32);
         tc::tmem_wait_ld();
         uint32_t pk[16], dk2[16];
@@ -657,7 +661,8 @@ bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt) { return dt == JG_BF16 
 jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                                 const void* k, const void* v, const void* go, const void* o, const float* lse,
                                 void* dq, void* dk, void* dv, float* delta, float* dq_acc, const int2* items,
-                                const int64_t* n_items, int64_t max_items, cudaStream_t st) {
+                                const int64_t* n_items, int64_t max_items, const int64_t* valid,
+                                cudaStream_t st) {
   (void)batch;
   if (D != 128) return fail(JG_UNSUPPORTED, "tcgen05 attention backward: head_dim must be 128");
   constexpr int kD = 128;
@@ -684,7 +689,7 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
   JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   fb::Params p{off, items, n_items, total_rows, H, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), std::getenv("JG_BWD_DBG") ? std::atoi(std::getenv("JG_BWD_DBG")) : 0,
-               counter, wait_prof_begin(st)};
+               counter, wait_prof_begin(st), valid};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
   if (!(p.dbg & 64)) fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
   if (p.dbg & 128) {

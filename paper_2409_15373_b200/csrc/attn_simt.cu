@@ -28,7 +28,7 @@ template <typename T>
 __global__ void __launch_bounds__(kAttnWarps * 32) attn_fwd_simt_kernel(
     const int64_t* __restrict__ off, int64_t batch, int64_t total_rows, int H, int D,
     const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v, T* __restrict__ out,
-    float* __restrict__ lse, float scale_log2) {
+    float* __restrict__ lse, float scale_log2, const int64_t* __restrict__ valid) {
   extern __shared__ float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* qs = smem + w * D;
@@ -37,8 +37,15 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_fwd_simt_kernel(
     const int64_t r = u / H;
     const int h = (int)(u - r * H);
     const int64_t i = sample_of_row(off, batch, r);
-    const int64_t b0 = off[i], n = off[i + 1] - b0;
+    const int64_t b0 = off[i], seg = off[i + 1] - b0;
     const int64_t rs = (int64_t)H * D;  // row stride
+    // padded mode: only the first `valid` keys attend; rows past it are zero with lse = -inf
+    const int64_t n = valid ? (valid[i] < seg ? valid[i] : seg) : seg;
+    if (r - b0 >= n) {
+      for (int d = lane; d < D; d += 32) st(out + r * rs + (int64_t)h * D + d, 0.f);
+      if (lane == 0) lse[(int64_t)h * total_rows + r] = -INFINITY;
+      continue;
+    }
     __syncwarp();
     for (int d = lane; d < D; d += 32) qs[d] = ld(q + r * rs + (int64_t)h * D + d);
     __syncwarp();
@@ -99,7 +106,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_bwd_simt_kernel(
     const int64_t* __restrict__ off, int64_t batch, int64_t total_rows, int H, int D,
     const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v, const T* __restrict__ go,
     const float* __restrict__ lse, const float* __restrict__ delta, T* __restrict__ o1,
-    T* __restrict__ o2, float scale_log2, float scale) {
+    T* __restrict__ o2, float scale_log2, float scale, const int64_t* __restrict__ valid) {
   extern __shared__ float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* xs = smem + w * 2 * D;  // MODE 0: q row | dO row ; MODE 1: k row | v row
@@ -110,8 +117,16 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_bwd_simt_kernel(
     const int64_t r = u / H;
     const int h = (int)(u - r * H);
     const int64_t i = sample_of_row(off, batch, r);
-    const int64_t b0 = off[i], n = off[i + 1] - b0;
+    const int64_t b0 = off[i], seg = off[i + 1] - b0;
     const int64_t hoff = (int64_t)h * D;
+    const int64_t n = valid ? (valid[i] < seg ? valid[i] : seg) : seg;  // padded mode: valid rows only
+    if (r - b0 >= n) {  // a padded row: no query/key interaction, zero gradient
+      for (int d = lane; d < D; d += 32) {
+        st(o1 + r * rs + hoff + d, 0.f);
+        if (MODE == 1) st(o2 + r * rs + hoff + d, 0.f);
+      }
+      continue;
+    }
     __syncwarp();
     if (MODE == 0) {
       for (int d = lane; d < D; d += 32) { xs[d] = ld(q + r * rs + hoff + d); ys[d] = ld(go + r * rs + hoff + d); }
@@ -174,13 +189,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_bwd_simt_kernel(
 
 template <typename T>
 static jg_status fwd_t(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
-                       const void* k, const void* v, void* out, float* lse, cudaStream_t st) {
+                       const void* k, const void* v, void* out, float* lse, const int64_t* valid, cudaStream_t st) {
   const int64_t units = total_rows * H;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + kAttnWarps - 1) / kAttnWarps,
                                                                16 * device_sm_count()));
   const float scale_log2 = kLog2eA / sqrtf((float)D);
   attn_fwd_simt_kernel<T><<<grid, kAttnWarps * 32, kAttnWarps * D * sizeof(float), st>>>(
-      off, batch, total_rows, H, D, (const T*)q, (const T*)k, (const T*)v, (T*)out, lse, scale_log2);
+      off, batch, total_rows, H, D, (const T*)q, (const T*)k, (const T*)v, (T*)out, lse, scale_log2, valid);
   JG_LAUNCHED("attn_fwd_simt_kernel");
   return JG_OK;
 }
@@ -188,7 +203,7 @@ static jg_status fwd_t(const int64_t* off, int64_t batch, int64_t total_rows, in
 template <typename T>
 static jg_status bwd_t(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                        const void* k, const void* v, const void* go, const void* o, const float* lse, void* dq,
-                       void* dk, void* dv, float* delta, cudaStream_t st) {
+                       void* dk, void* dv, float* delta, const int64_t* valid, cudaStream_t st) {
   const int64_t units = total_rows * H;
   const int sms = device_sm_count();
   attn_delta_kernel<T><<<(int)std::min<int64_t>((units + 7) / 8, 16 * sms), 256, 0, st>>>(
@@ -199,34 +214,35 @@ static jg_status bwd_t(const int64_t* off, int64_t batch, int64_t total_rows, in
   const size_t sm = kAttnWarps * 2 * D * sizeof(float);
   attn_bwd_simt_kernel<T, 0><<<grid, kAttnWarps * 32, sm, st>>>(off, batch, total_rows, H, D, (const T*)q,
                                                                (const T*)k, (const T*)v, (const T*)go, lse,
-                                                               delta, (T*)dq, nullptr, scale_log2, scale);
+                                                               delta, (T*)dq, nullptr, scale_log2, scale, valid);
   JG_LAUNCHED("attn_bwd_simt_kernel<dq>");
   attn_bwd_simt_kernel<T, 1><<<grid, kAttnWarps * 32, sm, st>>>(off, batch, total_rows, H, D, (const T*)q,
                                                                (const T*)k, (const T*)v, (const T*)go, lse,
-                                                               delta, (T*)dk, (T*)dv, scale_log2, scale);
+                                                               delta, (T*)dk, (T*)dv, scale_log2, scale, valid);
   JG_LAUNCHED("attn_bwd_simt_kernel<dkdv>");
   return JG_OK;
 }
 
 jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, void* out, float* lse,
-                               jg_dtype dt, cudaStream_t st) {
+                               jg_dtype dt, const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
   if (D > 32 * kMaxDPL) return fail(JG_UNSUPPORTED, "jagged_flash_attention_forward: head_dim > 256 unsupported");
-  if (dt == JG_F32) return fwd_t<float>(off, batch, total_rows, H, D, q, k, v, out, lse, st);
-  if (dt == JG_BF16) return fwd_t<__nv_bfloat16>(off, batch, total_rows, H, D, q, k, v, out, lse, st);
+  if (dt == JG_F32) return fwd_t<float>(off, batch, total_rows, H, D, q, k, v, out, lse, valid, st);
+  if (dt == JG_BF16) return fwd_t<__nv_bfloat16>(off, batch, total_rows, H, D, q, k, v, out, lse, valid, st);
   return fail(JG_UNSUPPORTED, "jagged_flash_attention_forward: dtype not supported on device (no CPU fallback)");
 }
 
 jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, const void* go,
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
-                               float* delta, jg_dtype dt, cudaStream_t st) {
+                               float* delta, jg_dtype dt, const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
   if (D > 32 * kMaxDPL) return fail(JG_UNSUPPORTED, "jagged_flash_attention_backward: head_dim > 256 unsupported");
-  if (dt == JG_F32) return bwd_t<float>(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, st);
+  if (dt == JG_F32)
+    return bwd_t<float>(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, valid, st);
   if (dt == JG_BF16)
-    return bwd_t<__nv_bfloat16>(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, st);
+    return bwd_t<__nv_bfloat16>(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, valid, st);
   return fail(JG_UNSUPPORTED, "jagged_flash_attention_backward: dtype not supported on device (no CPU fallback)");
 }
 

@@ -73,11 +73,14 @@ struct Params {
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23)
   unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
   int dbg;                   // JG_FWD_DBG (diagnostic, results invalid): 1 = softmax publishes P without computing
+  const int64_t* valid;      // padded mode (dense_flash_attention): per-sample valid length <= segment length, or
+                             // nullptr. Keys past it are masked, rows past it get zeros and lse = -inf.
 };
 
 struct Item {
   int64_t b0, n;
   int h, nkv, q_row;  // q_row: first row of tile A
+  int nv;             // valid rows/keys (== n except in padded mode)
   bool has_b;
 };
 
@@ -88,6 +91,7 @@ __device__ __forceinline__ Item load_item(const Params& p, int64_t w) {
   r.b0 = p.off[it.x];
   r.n = p.off[it.x + 1] - r.b0;
   r.nkv = (int)((r.n + BN - 1) / BN);
+  r.nv = (int)(p.valid ? (p.valid[it.x] < r.n ? p.valid[it.x] : r.n) : r.n);
   r.q_row = (int)(r.b0 + (int64_t)it.y * 2 * BM);
   r.has_b = (int64_t)it.y * 2 * BM + BM < r.n;
   return r;
@@ -160,8 +164,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     it.q_row = (int)a.w;
     it.h = (int)b.x;
     it.nkv = (int)b.y;
-    it.has_b = b.z != 0;
-    return b.w == 0;
+    it.has_b = (b.z & 1) != 0;
+    it.nv = (int)b.w;
+    return (b.z >> 1) == 0;
   };
 
   if (warp == kProducerWarp) {
@@ -180,8 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         wp.wait(item_empty + slot, ((item_cnt / kItemSlots) & 1) ^ 1, 2);
         tc::st_shared_v4(item_ring + slot * 32, (uint32_t)it.b0, (uint32_t)((uint64_t)it.b0 >> 32), (uint32_t)it.n,
                          (uint32_t)it.q_row);
-        tc::st_shared_v4(item_ring + slot * 32 + 16, (uint32_t)it.h, (uint32_t)it.nkv, it.has_b ? 1u : 0u,
-                         w >= n_work ? 1u : 0u);
+        tc::st_shared_v4(item_ring + slot * 32 + 16, (uint32_t)it.h, (uint32_t)it.nkv,
+                         (it.has_b ? 1u : 0u) | (w >= n_work ? 2u : 0u), (uint32_t)it.nv);
         tc::mbar_arrive(item_full + slot);
         if (w >= n_work) break;
         w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
@@ -315,8 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) tc::mbar_arrive(p_full + t);
           continue;
         }
-        const int64_t rem = it.n - (int64_t)j * BN;
-        const bool partial = rem < BN;  // warp-uniform: only a segment's last key block is partial
+        const int64_t rem = (int64_t)it.nv - (int64_t)j * BN;  // valid keys left (<= 0: block fully masked)
+        const bool partial = rem < BN;  // warp-uniform: a segment's last key block (or padded-mode masked blocks)
         // pass 1: raw-score row max over TMEM in 32-column chunks, 8 independent chains
         float m8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (!partial) {
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           // last key block of the segment: write -inf over the keys of the next sample back into TMEM so
           // the exp pass needs no masking (exp2(-inf) = 0)
-          const int remi = (int)rem;
+          const int remi = rem > 0 ? (int)rem : 0;
 #pragma unroll
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t r[32];
@@ -423,13 +428,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_after();
       const int64_t q_local = (int64_t)(it.q_row - it.b0) + t * BM + row;
       const bool store = q_local < it.n;
-      const float inv_l = 1.f / l;
+      const bool row_ok = q_local < it.nv;  // padded mode: rows past the valid length are zero, lse = -inf
+      const float inv_l = row_ok ? 1.f / l : 0.f;  // with o zeroed below: exact zeros even when l is NaN
       __nv_bfloat16* orow = p.out + ((it.b0 + q_local) * p.H + it.h) * D;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
         tc::tmem_ld32(o_addr + c * 32, o);
         tc::tmem_wait_ld();
+        if (!row_ok) {  // NaN-safe zeros (a segment with no valid key has m = -inf)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = 0u;
+        }
         if (store) {
           uint4 v[4];
 #pragma unroll
@@ -446,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(o_empty + t);
-      if (store) p.lse[(int64_t)it.h * p.total_rows + it.b0 + q_local] = (m + __log2f(l)) * 0.6931471805599453f;
+      if (store)
+        p.lse[(int64_t)it.h * p.total_rows + it.b0 + q_local] = row_ok ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
     }
     wp.add(7, clock64() - t_role);
     wp.flush();
@@ -470,7 +481,7 @@ bool attn_sm100_supported(int head_dim, jg_dtype dt) {
 template <int D>
 static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_rows, int H, const void* q, const void* k,
                             const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
-                            int64_t max_items, cudaStream_t st) {
+                            int64_t max_items, const int64_t* valid, cudaStream_t st) {
   using L = fa::Smem<D>;
   CUtensorMap mq, mk, mv;
   if (jg_status rc = make_map(&mq, q, total_rows, H, D, 128)) return rc;
@@ -491,7 +502,7 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
   JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   fa::Params p{off, items, n_items, batch, total_rows, H, (__nv_bfloat16*)out, lse,
                1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st), counter,
-               std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0};
+               std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0, valid};
   const int64_t work = max_items * H;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sm_count(), work));
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
@@ -508,9 +519,9 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
 // items: (sample, 256-row tile pair) LPT work list (schedule tile 256)
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                                 const void* k, const void* v, void* out, float* lse, const int2* items,
-                                const int64_t* n_items, int64_t max_items, cudaStream_t st) {
-  if (D == 128) return fwd_launch<128>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, st);
-  if (D == 64) return fwd_launch<64>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, st);
+                                const int64_t* n_items, int64_t max_items, const int64_t* valid, cudaStream_t st) {
+  if (D == 128) return fwd_launch<128>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
+  if (D == 64) return fwd_launch<64>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
   return fail(JG_UNSUPPORTED, "tcgen05 attention: head_dim must be 64 or 128");
 }
 

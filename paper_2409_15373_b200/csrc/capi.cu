@@ -418,6 +418,58 @@ extern "C" int64_t jg_attention_backward_workspace_size(int64_t total_rows, int3
   return delta + acc + 256;
 }
 
+// Shared by the jagged entry points (valid == nullptr) and the padded dense_flash_attention mode (valid =
+// per-sample lengths on device, offsets i*max_len): same kernels, masks from `valid`.
+static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_rows, int32_t H, int32_t D,
+                              const void* q, const void* k, const void* v, void* out, float* lse, jg_dtype dtype,
+                              jg_schedule sched, const int64_t* valid, cudaStream_t st) {
+  if (total_rows == 0) return JG_OK;
+  if (!force_simt() && attn_sm100_supported(D, dtype)) {
+    jg_schedule own = nullptr;
+    if (!sched) {
+      if (jg_status rc = jg_schedule_create(off, batch, total_rows, st, &own)) return rc;
+      sched = own;
+    }
+    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
+                                         sched->n_items2, sched->max_items2, valid, st);
+    if (own) {
+      cudaStreamSynchronize(st);
+      jg_schedule_destroy(own);
+    }
+    return rc;
+  }
+  return launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, valid, st);
+}
+
+static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_rows, int32_t H, int32_t D,
+                               const void* q, const void* k, const void* v, const void* go, const void* o,
+                               const float* lse, void* dq, void* dk, void* dv, jg_dtype dtype, jg_schedule sched,
+                               void* workspace, const int64_t* valid, cudaStream_t st) {
+  if (total_rows == 0) return JG_OK;
+  Scratch ws(st);
+  if (!workspace) {
+    if (jg_status rc = ws.alloc(jg_attention_backward_workspace_size(total_rows, H, D))) return rc;
+    workspace = ws.p;
+  }
+  float* delta = (float*)workspace;
+  float* dq_acc = (float*)((char*)workspace + attn_lsd_bytes(total_rows, H));
+  if (!force_simt() && attn_sm100_bwd_supported(D, dtype)) {
+    jg_schedule own = nullptr;
+    if (!sched) {
+      if (jg_status rc = jg_schedule_create(off, batch, total_rows, st, &own)) return rc;
+      sched = own;
+    }
+    jg_status rc = launch_attn_bwd_sm100(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta,
+                                         dq_acc, sched->items, sched->n_items, sched->max_items, valid, st);
+    if (own) {
+      cudaStreamSynchronize(st);
+      jg_schedule_destroy(own);
+    }
+    return rc;
+  }
+  return launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype, valid, st);
+}
+
 extern "C" jg_status jg_jagged_flash_attention_forward(const int64_t* off, int64_t batch, int64_t total_rows,
                                                        int32_t H, int32_t D, const void* q, const void* k,
                                                        const void* v, int64_t block_q, int64_t block_k, void* out,
@@ -426,23 +478,7 @@ extern "C" jg_status jg_jagged_flash_attention_forward(const int64_t* off, int64
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
           "jagged_flash_attention_forward: block sizes must be >= 1");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_forward: dim mismatch");
-  cudaStream_t st = as_stream(stream);
-  if (total_rows == 0) return JG_OK;
-  if (!force_simt() && attn_sm100_supported(D, dtype)) {
-    jg_schedule own = nullptr;
-    if (!sched) {
-      if (jg_status rc = jg_schedule_create(off, batch, total_rows, stream, &own)) return rc;
-      sched = own;
-    }
-    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
-                                         sched->n_items2, sched->max_items2, st);
-    if (own) {
-      cudaStreamSynchronize(st);
-      jg_schedule_destroy(own);
-    }
-    return rc;
-  }
-  return launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, st);
+  return attn_forward(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, sched, nullptr, as_stream(stream));
 }
 
 extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int64_t batch, int64_t total_rows,
@@ -455,30 +491,64 @@ extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int6
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
           "jagged_flash_attention_backward: saved state does not match inputs");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_backward: grad_out layout mismatch");
+  return attn_backward(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, sched, workspace,
+                       nullptr, as_stream(stream));
+}
+
+// Padded mode: validate lengths like attention.cpp:19-31 (require_self_attention_inputs), then upload
+// offsets i*max_len and the lengths into one stream-ordered scratch block.
+static jg_status padded_layout(const char* op, const int64_t* lengths, int64_t batch, int64_t max_len,
+                               Scratch& buf, const int64_t** d_off, const int64_t** d_valid) {
+  REQUIRE(batch >= 0 && max_len >= 0, JG_INVALID_ARGUMENT, std::string(op) + ": q, k, v must share a [B, L, D] shape");
+  REQUIRE(batch == 0 || lengths, JG_INVALID_ARGUMENT, std::string(op) + ": lengths size mismatch");
+  std::vector<int64_t> h(2 * batch + 1);
+  for (int64_t i = 0; i < batch; ++i) {
+    REQUIRE(lengths[i] >= 0 && lengths[i] <= max_len, JG_INVALID_ARGUMENT,
+            std::string(op) + ": sample " + std::to_string(i) + " length " + std::to_string(lengths[i]) +
+                " out of bounds for L=" + std::to_string(max_len));
+    h[i] = i * max_len;
+    h[batch + 1 + i] = lengths[i];
+  }
+  h[batch] = batch * max_len;
+  if (jg_status rc = buf.alloc(sizeof(int64_t) * h.size())) return rc;
+  JG_CUDA(cudaMemcpyAsync(buf.p, h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice, buf.s));
+  JG_CUDA(cudaStreamSynchronize(buf.s));  // `h` is pageable and goes out of scope
+  *d_off = (const int64_t*)buf.p;
+  *d_valid = (const int64_t*)buf.p + batch + 1;
+  return JG_OK;
+}
+
+extern "C" jg_status jg_dense_flash_attention_forward(const int64_t* lengths, int64_t batch, int64_t max_len,
+                                                      int32_t H, int32_t D, const void* q, const void* k,
+                                                      const void* v, int64_t block_q, int64_t block_k, void* out,
+                                                      float* lse, jg_dtype dtype, void* stream) {
+  CHECK_DT("dense_flash_attention", dtype);
+  REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT, "dense_flash_attention: block sizes must be >= 1");
+  REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "dense_flash_attention: q, k, v must share a [B, L, D] shape");
   cudaStream_t st = as_stream(stream);
-  if (total_rows == 0) return JG_OK;
-  Scratch ws(st);
-  if (!workspace) {
-    if (jg_status rc = ws.alloc(jg_attention_backward_workspace_size(total_rows, H, D))) return rc;
-    workspace = ws.p;
-  }
-  float* delta = (float*)workspace;
-  float* dq_acc = (float*)((char*)workspace + attn_lsd_bytes(total_rows, H));
-  if (!force_simt() && attn_sm100_bwd_supported(D, dtype)) {
-    jg_schedule own = nullptr;
-    if (!sched) {
-      if (jg_status rc = jg_schedule_create(off, batch, total_rows, stream, &own)) return rc;
-      sched = own;
-    }
-    jg_status rc = launch_attn_bwd_sm100(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta,
-                                         dq_acc, sched->items, sched->n_items, sched->max_items, st);
-    if (own) {
-      cudaStreamSynchronize(st);
-      jg_schedule_destroy(own);
-    }
+  Scratch buf(st);
+  const int64_t *d_off = nullptr, *d_valid = nullptr;
+  if (jg_status rc = padded_layout("dense_flash_attention", lengths, batch, max_len, buf, &d_off, &d_valid)) return rc;
+  return attn_forward(d_off, batch, batch * max_len, H, D, q, k, v, out, lse, dtype, nullptr, d_valid, st);
+}
+
+extern "C" jg_status jg_dense_flash_attention_backward(const int64_t* lengths, int64_t batch, int64_t max_len,
+                                                       int32_t H, int32_t D, const void* q, const void* k,
+                                                       const void* v, const void* go, const void* o,
+                                                       const float* lse, int64_t block_q, int64_t block_k, void* dq,
+                                                       void* dk, void* dv, jg_dtype dtype, void* workspace,
+                                                       void* stream) {
+  CHECK_DT("dense_flash_attention_backward", dtype);
+  REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
+          "dense_flash_attention_backward: block sizes must be >= 1");
+  REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "dense_flash_attention_backward: q, k, v must share a [B, L, D] shape");
+  cudaStream_t st = as_stream(stream);
+  Scratch buf(st);
+  const int64_t *d_off = nullptr, *d_valid = nullptr;
+  if (jg_status rc = padded_layout("dense_flash_attention_backward", lengths, batch, max_len, buf, &d_off, &d_valid))
     return rc;
-  }
-  return launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype, st);
+  return attn_backward(d_off, batch, batch * max_len, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, nullptr,
+                       workspace, d_valid, st);
 }
 
 extern "C" jg_status jg_jagged_attention(const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows,

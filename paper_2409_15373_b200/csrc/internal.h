@@ -77,14 +77,16 @@ jg_status launch_colsum(const void* x, int64_t rows, int64_t cols, void* out, fl
                         cudaStream_t st);
 jg_status launch_cast_f32(const float* a, int64_t n, void* out, jg_dtype dt, cudaStream_t st);
 
-// SIMT attention (fp32 mode, and any head_dim the tensor-core path does not cover)
+// SIMT attention (fp32 mode, and any head_dim the tensor-core path does not cover).
+// valid: nullptr (jagged), or per-sample valid lengths <= segment lengths (padded dense_flash_attention mode:
+// keys past the valid length are masked, rows past it produce zeros / lse = -inf / zero gradients).
 jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, void* out, float* lse,
-                               jg_dtype dt, cudaStream_t st);
+                               jg_dtype dt, const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, const void* go,
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
-                               float* delta, jg_dtype dt, cudaStream_t st);
+                               float* delta, jg_dtype dt, const int64_t* valid, cudaStream_t st);
 
 // The backward workspace starts with lsd[2][H][total_rows] fp32: lse in log2 units, then Delta.
 inline int64_t attn_lsd_bytes(int64_t total_rows, int H) { return ((2 * (int64_t)H * total_rows * 4 + 255) / 256) * 256; }
@@ -95,11 +97,12 @@ bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt);
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, void* out, float* lse,
                                 const int2* items, const int64_t* n_items, int64_t max_items,
-                                cudaStream_t st);
+                                const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, const void* go,
                                 const void* o, const float* lse, void* dq, void* dk, void* dv,
                                 float* delta, float* dq_accum, const int2* items,
-                                const int64_t* n_items, int64_t max_items, cudaStream_t st);
+                                const int64_t* n_items, int64_t max_items, const int64_t* valid,
+                                cudaStream_t st);
 
 }  // namespace jg

@@ -24,7 +24,8 @@ __all__ = [
     "array_jagged_bmm_jagged_out", "jagged2_softmax", "jagged_dense_bmm_vjp", "jagged_jagged_bmm_vjp",
     "jagged_softmax_vjp", "jagged_jagged_bmm_jagged_out_vjp", "array_jagged_bmm_jagged_out_vjp",
     "jagged2_softmax_vjp", "jagged_flash_attention_forward", "jagged_flash_attention_backward",
-    "jagged_attention", "jagged_to_dense", "dense_to_jagged", "jagged2_to_dense", "dense_to_jagged2",
+    "jagged_attention", "DenseAttentionSaved", "dense_flash_attention", "dense_flash_attention_backward",
+    "jagged_to_dense", "dense_to_jagged", "jagged2_to_dense", "dense_to_jagged2",
     "add", "sub", "mul", "scale", "JaggedError",
 ]
 
@@ -114,6 +115,16 @@ class Jagged2Tensor:
 class JaggedAttentionSaved:
     """attention.hpp:26-32: output + per-row logsumexp ([H, total_rows] float32) + block sizes."""
     output: JaggedTensor
+    logsumexp: torch.Tensor
+    block_q: int = 64
+    block_k: int = 64
+
+
+@dataclass
+class DenseAttentionSaved:
+    """attention.hpp:19-24: padded output [B, L, (H,) D], logsumexp ([H, B*L] float32, -inf past each
+    sample's length) and block sizes."""
+    output: torch.Tensor
     logsumexp: torch.Tensor
     block_q: int = 64
     block_k: int = 64
@@ -370,6 +381,50 @@ def jagged_flash_attention_backward(q: JaggedTensor, k: JaggedTensor, v: JaggedT
         _p(saved.output.values), _p(saved.logsumexp), saved.block_q, saved.block_k, _p(dq), _p(dk), _p(dv),
         _dt(q.values), schedule.handle if schedule else None, _p(workspace), _stream()))
     return AttentionGrads(q.with_values(dq), k.with_values(dk), v.with_values(dv))
+
+
+def _dense_attention_inputs(q, k, v, lengths, op):
+    # attention.cpp:19-31 (require_self_attention_inputs); q/k/v are [B, L, D] (one head, as the reference)
+    # or [B, L, H, D]
+    if q.dim() not in (3, 4) or q.shape != k.shape or q.shape != v.shape:
+        raise JaggedError(f"{op}: q, k, v must share a [B, L, D] shape")
+    ln = np.asarray(lengths, dtype=np.int64).reshape(-1)
+    if ln.shape[0] != q.shape[0]:
+        raise JaggedError(f"{op}: lengths size mismatch")
+    for i, n in enumerate(ln):
+        if n < 0 or n > q.shape[1]:
+            raise JaggedError(f"{op}: sample {i} length {int(n)} out of bounds for L={int(q.shape[1])}")
+    H = 1 if q.dim() == 3 else int(q.shape[2])
+    return np.ascontiguousarray(ln), int(q.shape[0]), int(q.shape[1]), H, int(q.shape[-1])
+
+
+def dense_flash_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, lengths, block_q: int = 64,
+                          block_k: int = 64) -> DenseAttentionSaved:
+    """attention.cpp:106-160 on the GPU: the jagged kernels in padded mode (segments of max_len rows, keys
+    and rows past each length masked), doing the full padded L^2 work — the padded baseline."""
+    ln, B, L, H, D = _dense_attention_inputs(q, k, v, lengths, "dense_flash_attention")
+    if block_q < 1 or block_k < 1:
+        raise JaggedError("dense_flash_attention: block sizes must be >= 1")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    out = torch.empty_like(q)
+    lse = torch.empty(H, B * L, dtype=torch.float32, device=q.device)
+    check(_lib.lib().jg_dense_flash_attention_forward(
+        ln.ctypes.data, B, L, H, D, _p(q), _p(k), _p(v), block_q, block_k, _p(out), _p(lse), _dt(q), _stream()))
+    return DenseAttentionSaved(out, lse, block_q, block_k)
+
+
+def dense_flash_attention_backward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grad_out: torch.Tensor,
+                                   saved: DenseAttentionSaved, lengths, workspace: torch.Tensor | None = None):
+    """Backward of the padded mode (no reference counterpart): returns (dq, dk, dv), zero past each length."""
+    ln, B, L, H, D = _dense_attention_inputs(q, k, v, lengths, "dense_flash_attention_backward")
+    if grad_out.shape != q.shape or saved.output.shape != q.shape or saved.logsumexp.numel() != B * L * H:
+        raise JaggedError("dense_flash_attention_backward: saved state does not match inputs")
+    q, k, v, grad_out = q.contiguous(), k.contiguous(), v.contiguous(), grad_out.contiguous()
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    check(_lib.lib().jg_dense_flash_attention_backward(
+        ln.ctypes.data, B, L, H, D, _p(q), _p(k), _p(v), _p(grad_out), _p(saved.output), _p(saved.logsumexp),
+        saved.block_q, saved.block_k, _p(dq), _p(dk), _p(dv), _dt(q), _p(workspace), _stream()))
+    return dq, dk, dv
 
 
 def jagged_attention(q: JaggedTensor, k: JaggedTensor, v: JaggedTensor) -> JaggedTensor:

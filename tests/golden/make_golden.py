@@ -12,7 +12,8 @@ Contents
   attention.npz  jagged_attention (unfused) + jagged_flash_attention fwd/bwd at blocks (3,3) and
                  (64,64) on lengths {0,1,2,5,7,17,33,70,130,257}, D=16, binary64 (attention.cpp:162-289).
   lengths.npz    gen_lengths outputs for the BASELINE configs (rng.cpp:35-57), for bit-exact checks.
-  next.npz       SURVEY §8f-1 feature_interaction (attention.cpp:291-309; f64 and f32) and §8f-2
+  next.npz       SURVEY §8f-1 feature_interaction (attention.cpp:291-309; f64 and f32), §8f-4
+                 dense_flash_attention (attention.cpp:106-160; f64 blocks (3,4)/(64,64) and f32) and §8f-2
                  jagged_mlp forward (f64, f32) + VJP (f64) (linalg.cpp:265-277, :509-573).
 """
 from __future__ import annotations
@@ -142,6 +143,17 @@ def main() -> None:
                                                             for w, b, r in layers], prec="f32")
     dx, g = F.jagged_mlp_vjp(x, layers, go)
     nx["mlp_dx"], nx["mlp_dw0"], nx["mlp_db0"], nx["mlp_dw1"], nx["mlp_db1"] = dx, g[0][0], g[0][1], g[1][0], g[1][1]
+    # §8f-4: the reference's padded dense_flash_attention (attention.cpp:106-160), f64 and f32, with
+    # lengths 0 (fully masked sample), L, and partial; blocks (3, 4) and (64, 64)
+    dl = np.array([5, 0, 9, 3, 1], np.int64)
+    Bd, Ld, Dd = len(dl), 9, 8
+    dv = F.uniform_values(41, 3 * Bd * Ld * Dd)
+    dq_, dk_, dv_ = (dv[i * Bd * Ld * Dd:(i + 1) * Bd * Ld * Dd].reshape(Bd, Ld, Dd) for i in range(3))
+    nx["df_len"], nx["df_q"], nx["df_k"], nx["df_v"] = dl, dq_, dk_, dv_
+    for bq, bk in ((3, 4), (64, 64)):
+        nx[f"df_out_f64_{bq}_{bk}"], nx[f"df_lse_f64_{bq}_{bk}"] = F.dense_flash_attention(dl, dq_, dk_, dv_, bq, bk)
+    nx["df_out_f32"], nx["df_lse_f32"] = F.dense_flash_attention(dl, dq_.astype(np.float32), dk_.astype(np.float32),
+                                                                 dv_.astype(np.float32), 64, 64, prec="f32")
     np.savez_compressed(os.path.join(HERE, "next.npz"), **nx)
     print("wrote", sorted(os.listdir(HERE)))
 

@@ -199,3 +199,38 @@ def test_next_rows_live_reference():
     for (a, b), (c, d) in zip(g, rg):
         np.testing.assert_allclose(a, c, rtol=1e-12, atol=1e-13)
         np.testing.assert_allclose(b, d, rtol=1e-12, atol=1e-13)
+
+
+def test_dense_flash_vs_reference_golden(golden):
+    """SURVEY §8f-4 padded dense_flash_attention: oracle vs the reference's outputs (incl. a zero-length sample:
+    zero rows and lse = -inf, attention.cpp:151-154)."""
+    nx = golden["next"]
+    ln, q, k, v = nx["df_len"], nx["df_q"], nx["df_k"], nx["df_v"]
+    for bq, bk in ((3, 4), (64, 64)):
+        o, lse = R.dense_flash_attention(ln, q, k, v, bq, bk)
+        np.testing.assert_allclose(o, nx[f"df_out_f64_{bq}_{bk}"], rtol=1e-12, atol=1e-14)
+        ref = nx[f"df_lse_f64_{bq}_{bk}"]
+        assert np.array_equal(np.isinf(lse), np.isinf(ref))
+        np.testing.assert_allclose(lse[np.isfinite(ref)], ref[np.isfinite(ref)], rtol=1e-12)
+    # the f32 instantiation accumulates in double and rounds the outputs
+    o32, l32 = R.dense_flash_attention(ln, *(a.astype(np.float32) for a in (q, k, v)))
+    np.testing.assert_allclose(o32, nx["df_out_f32"], rtol=2e-6, atol=1e-7)
+    fin = np.isfinite(nx["df_lse_f32"])
+    np.testing.assert_allclose(l32[fin], nx["df_lse_f32"][fin], rtol=2e-6)
+    # padded rows are zero; valid rows equal the unmasked dense attention
+    np.testing.assert_allclose(o, R.dense_attention(ln, q, k, v), rtol=1e-12, atol=1e-14)
+    with pytest.raises(R.OracleError):
+        R._chk(R.lib().or_dense_flash_attention(ln, len(ln), q.shape[1], q.shape[2], 0, 4, q.reshape(-1),
+                                                k.reshape(-1), v.reshape(-1), np.empty(q.size), np.empty(q.size)))
+
+
+@pytest.mark.skipif(not F.available(), reason="oracle/_ref not built")
+def test_dense_flash_live_reference():
+    rng = np.random.default_rng(9)
+    for ln, L, D, bq, bk in (([7, 0, 12, 12], 12, 16, 5, 3), ([1, 33, 20], 40, 8, 64, 64)):
+        q, k, v = (rng.uniform(-1, 1, (len(ln), L, D)) for _ in range(3))
+        o, lse = R.dense_flash_attention(ln, q, k, v, bq, bk)
+        ro, rl = F.dense_flash_attention(ln, q, k, v, bq, bk)
+        np.testing.assert_allclose(o, ro, rtol=1e-12, atol=1e-14)
+        assert np.array_equal(np.isinf(lse), np.isinf(rl))
+        np.testing.assert_allclose(lse[np.isfinite(rl)], rl[np.isfinite(rl)], rtol=1e-12)
