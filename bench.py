@@ -547,10 +547,138 @@ def run_configs(args):
               "memory_ratio_vs_padded_same_kernels": res["padded dense flash (ours: same kernels, padded mode)"][1] / mem_j,
               "memory_ratio_vs_dense": res["padded dense attention (torch matmul+softmax)"][1] / mem_j,
               "memory_ratio_vs_dense_flash": res["padded dense flash (torch SDPA + mask)"][1] / mem_j})
+    elif cfg == "table1":
+        run_table1(args, J, synth, dev, rnd, emit)
     if args.out:
         with open(args.out, "a") as f:
             for line in out:
                 f.write(json.dumps(line) + "\n")
+
+
+def run_table1(args, J, synth, dev, rnd, emit):
+    """the reference bench's records (bench.hpp:61-81, bench.cpp:200-372) for the GPU variants.
+    Per Table-1 op: variants[0] = "padded" (the same op on padded tensors with torch bf16 kernels — library
+    baseline), "jagged" = ours; the attention sweep point has the reference's four variants (dense_attention:
+    torch padded matmul+softmax; dense_flash_attention: our kernels in padded mode; jagged_attention /
+    jagged_flash_attention: ours). Outputs are cross-checked on the valid region before timing (bf16: max-abs
+    error <= 2e-2 x max|ref|), times are CUDA-event p10/p50/p90 over --steps, FLOPs/bytes come from the
+    reference's cost model (report.py), and the report is written in the reference's csv/json/md formats."""
+    import torch
+
+    from paper_2409_15373_b200 import report as RP
+
+    B, L, D, T, seed = 1024, 1024, 128, 128, 0
+    ln = synth.gen_lengths("half-mean", L, seed, B)
+    off = synth.offsets_of(ln)
+    S, sq = int(off[-1]), int((ln * ln).sum())
+    offd, lens = torch.from_numpy(off).to(dev), torch.from_numpy(ln).to(dev)
+    rowmask = torch.arange(L, device=dev)[None, :] < lens[:, None]  # [B, L]
+    sqmask = rowmask[:, :, None] & rowmask[:, None, :]              # [B, L, L]
+    jt = lambda v: J.JaggedTensor(offd, v, off)  # noqa: E731
+    X, K2, Y = jt(rnd(S, D)), jt(rnd(S, D)), jt(rnd(S, T))
+    A = J.Jagged2Tensor(offd, rnd(sq), off)
+    Wd = rnd(B, D, T)
+    W0, b0, W1, b1 = rnd(D, T) * D ** -0.5, rnd(T) * 0.1, rnd(T, D) * T ** -0.5, rnd(D) * 0.1
+    layers = [J.MlpLayer(W0, b0, J.RELU), J.MlpLayer(W1, b1, J.NONE)]
+    Xp, K2p, Yp, Ap = J.jagged_to_dense(X, L), J.jagged_to_dense(K2, L), J.jagged_to_dense(Y, L), J.jagged2_to_dense(A, L)
+    ninf = float("-inf")
+
+    def times_us(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        return ts
+
+    def crosscheck(op, got, ref):
+        g, r = got.float(), ref.float()
+        err = float((g - r).abs().max()) if r.numel() else 0.0
+        scale = max(float(r.abs().max()) if r.numel() else 0.0, 1e-30)
+        if not err <= 2e-2 * scale:
+            raise RuntimeError(f"{op}: jagged/padded outputs diverge before timing: max abs err {err:.3e} "
+                               f"vs 2e-2 x max|ref| {scale:.3e}")
+        return float(g.double().sum())
+
+    records = []
+
+    def record(op, variants, T_=T):
+        """variants: [(name, fn, valid_region_of_output)], [0] the padded baseline."""
+        ref_valid = variants[0][2](variants[0][1]())
+        rec = RP.BenchRecord(op, B, D, T_, L, "half_mean", seed, "bf16", 1)
+        for name, fn, valid in variants:
+            cs = crosscheck(op, valid(fn()), ref_valid)
+            rec.variants.append(RP.VariantStats.from_times(name, times_us(fn), cs))
+        rec.finalize(RP.OpConfig(op, D, T_, list(ln), 2, L))
+        records.append(rec)
+
+    rows = lambda t: t[rowmask]  # noqa: E731  padded [B, L, C] -> the jagged rows
+    vals = lambda t: t.values  # noqa: E731
+    record("jagged_dense_bmm", [("padded", lambda: torch.bmm(Xp, Wd), rows),
+                                ("jagged", lambda: J.jagged_dense_bmm(X, Wd), vals)])
+    record("jagged_jagged_bmm", [("padded", lambda: torch.bmm(Xp.transpose(1, 2), Yp), lambda t: t),
+                                 ("jagged", lambda: J.jagged_jagged_bmm(X, Y), lambda t: t)])
+    record("jagged_softmax", [("padded", lambda: torch.softmax(Xp.masked_fill(~rowmask[:, :, None], ninf), dim=1)
+                               .nan_to_num_(0.0), rows), ("jagged", lambda: J.jagged_softmax(X), vals)], T_=1)
+    record("jagged_jagged_bmm_jagged_out", [("padded", lambda: torch.bmm(Xp, K2p.transpose(1, 2)), lambda t: t[sqmask]),
+                                            ("jagged", lambda: J.jagged_jagged_bmm_jagged_out(X, K2), vals)], T_=1)
+    record("array_jagged_bmm_jagged_out", [("padded", lambda: torch.bmm(Ap, Xp), rows),
+                                           ("jagged", lambda: J.array_jagged_bmm_jagged_out(A, X), vals)], T_=1)
+    record("jagged2_softmax", [("padded", lambda: torch.softmax(Ap.masked_fill(~sqmask, ninf), dim=2).nan_to_num_(0.0),
+                                lambda t: t[sqmask]), ("jagged", lambda: J.jagged2_softmax(A), vals)], T_=1)
+
+    def mlp_padded():
+        h = torch.relu(torch.addmm(b0, Xp.reshape(B * L, D), W0))
+        return torch.addmm(b1, h, W1).reshape(B, L, D)
+
+    record("jagged_mlp", [("padded", mlp_padded, rows), ("jagged", lambda: J.jagged_mlp(X, layers), vals)])
+
+    # the attention sweep point (bench.cpp:317-372, 476-503): one record per variant, ratios vs dense_attention
+    Q1, K1, V1 = (jt(rnd(S, 1, D)) for _ in range(3))
+    Qp, Kp, Vp = (J.jagged_to_dense(J.JaggedTensor(offd, t.values.reshape(S, D), off), L) for t in (Q1, K1, V1))
+    keymask = sqmask
+
+    def dense_attention():
+        s_ = torch.bmm(Qp, Kp.transpose(1, 2)) * D ** -0.5
+        p_ = torch.softmax(s_.masked_fill(~keymask, ninf), dim=-1).nan_to_num_(0.0)
+        return torch.bmm(p_, Vp)
+
+    att = [("dense_attention", dense_attention, rows),
+           ("dense_flash_attention", lambda: J.dense_flash_attention(Qp, Kp, Vp, ln).output, rows),
+           ("jagged_attention", lambda: J.jagged_attention(Q1, K1, V1), lambda t: t.values.reshape(S, D)),
+           ("jagged_flash_attention", lambda: J.jagged_flash_attention_forward(Q1, K1, V1).output,
+            lambda t: t.values.reshape(S, D))]
+    ref_valid = rows(dense_attention())
+    stats = []
+    for name, fn, valid in att:
+        cs = crosscheck("attention", valid(fn()), ref_valid)
+        stats.append(RP.VariantStats.from_times(name, times_us(fn), cs))
+    cfg_a = RP.OpConfig("jagged_flash_attention", D, 1, list(ln), 2, L)
+    dense_bytes = RP.variant_bytes(cfg_a, "dense_attention")
+    for st_ in stats:
+        rec = RP.BenchRecord("attention", B, D, 1, L, "half_mean", seed, "bf16", 1)
+        c = RP.OpConfig(st_.variant, D, 1, list(ln), 2, L)
+        rec.flops_jagged, rec.flops_padded = RP.flops_of(c)
+        rec.bytes_jagged, rec.bytes_padded = RP.bytes_of(c)
+        st_.flops, st_.bytes = RP.variant_flops(c, st_.variant), RP.variant_bytes(c, st_.variant)
+        st_.speedup_vs_dense = stats[0].time_us_p50 / st_.time_us_p50
+        st_.bytes_ratio_vs_dense = st_.bytes / dense_bytes
+        rec.variants = [st_]
+        records.append(rec)
+    for r in records:
+        emit({"metric": "table1 record (reference bench schema)", "config": {"workload": f"half-mean B={B} L={L} "
+              f"seed {seed}, D={D}, T={T}, bf16, {args.steps} timed iterations"}, "dtype": "bf16",
+              "record": json.loads(RP.render_report([r], "json"))[0]})
+    if args.report:
+        for fmt in ("csv", "json", "md"):
+            with open(f"{args.report}.{fmt}", "w") as f:
+                f.write(RP.render_report(records, fmt))
 
 
 def main():
@@ -562,9 +690,11 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
-    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "dense"],
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "dense", "table1"],
                     help="cfg3 = the headline JSON line; the others measure the secondary BASELINE configs")
     ap.add_argument("--out", default=None, help="also append secondary-config lines to this file")
+    ap.add_argument("--report", default=None,
+                    help="--config table1: write the records as PATH.csv / PATH.json / PATH.md (reference formats)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))

@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "jagged/attention.hpp"
+#include "jagged/bench.hpp"
+#include "jagged/cost_model.hpp"
 #include "jagged/linalg.hpp"
 #include "jagged/rng.hpp"
 #include "jagged/tensor.hpp"
@@ -312,3 +314,32 @@ extern "C" int ref_hardware_threads(void) {
   return static_cast<int>(std::thread::hardware_concurrency());
 }
 extern "C" const char* ref_last_error(void) { return g_err.c_str(); }
+
+// the reference's analytic cost model (cost_model.cpp) and CSV header (bench.hpp:79-81), to pin
+// paper_2409_15373_b200/report.py. out: flops (jagged, padded), bytes (jagged, padded), intermediate elements
+// (jagged, padded), and — when `variant` is non-null — variant_flops, variant_bytes.
+extern "C" int ref_cost_model(const char* op, const char* variant, const int64_t* lengths, int64_t B, int64_t D,
+                              int64_t T, int64_t eb, int64_t padded_len, int64_t bq, int64_t bk, int64_t* out) {
+  return guard([&] {
+    jagged::OpConfig c;
+    c.op_id = op;
+    c.batch = B;
+    c.dim = D;
+    c.t = T;
+    c.lengths = vec(lengths, B);
+    c.element_bytes = eb;
+    if (padded_len >= 0) c.padded_len = padded_len;
+    c.block_q = bq;
+    c.block_k = bk;
+    const auto [fj, fp] = jagged::flops_of(c);
+    const auto [bj, bp] = jagged::bytes_of(c);
+    const auto [ij, ip] = jagged::intermediate_elements(c);
+    out[0] = fj, out[1] = fp, out[2] = bj, out[3] = bp, out[4] = ij, out[5] = ip;
+    if (variant) {
+      out[6] = jagged::variant_flops(c, variant);
+      out[7] = jagged::variant_bytes(c, variant);
+    }
+  });
+}
+
+extern "C" const char* ref_csv_header() { return jagged::bench::kCsvHeader.data(); }

@@ -277,3 +277,22 @@ def jagged_mlp_vjp(x, layers, go):
         grads.append((dw[wo:wo + di * do].reshape(di, do), db[bo:bo + do].copy()))
         wo, bo = wo + di * do, bo + do
     return dx, grads
+
+
+def cost_model(op, lengths, D, T, element_bytes=4, padded_len=None, block_q=64, block_k=64, variant=None):
+    """The reference's cost_model.cpp: dict of (jagged, padded) flops/bytes/intermediate (+ variant numbers)."""
+    ln = np.ascontiguousarray(lengths, dtype=np.int64)
+    out = np.zeros(8, np.int64)
+    _chk(lib().ref_cost_model(op.encode(), variant.encode() if variant else None, _p(ln), _I(len(ln)), _I(D), _I(T),
+                              _I(element_bytes), _I(-1 if padded_len is None else padded_len), _I(block_q),
+                              _I(block_k), _p(out)))
+    r = {"flops": (int(out[0]), int(out[1])), "bytes": (int(out[2]), int(out[3])),
+         "intermediate": (int(out[4]), int(out[5]))}
+    if variant:
+        r["variant"] = (int(out[6]), int(out[7]))
+    return r
+
+
+def csv_header() -> str:
+    lib().ref_csv_header.restype = C.c_char_p
+    return lib().ref_csv_header().decode()

@@ -31,8 +31,8 @@ constexpr int kTileBytes = 16384;  // one operand stage: 128 x 64 bf16
 struct Smem {
   static constexpr int kA = 0;
   static constexpr int kB = kStages * kTileBytes;
-  static constexpr int kStg = 2 * kStages * kTileBytes;        // JJJ epilogue staging, 32 rows x 128 fp32 per warp
-  static constexpr int kBar = kStg + 4 * 32 * 128 * 4;
+  static constexpr int kStg = 2 * kStages * kTileBytes;        // JJJ epilogue staging: 8 warps x 32 rows x 65 fp32
+  static constexpr int kBar = kStg + 8 * 32 * 65 * 4;
   static constexpr int kNumBars = 3 * kStages + 4 + 1;
   static constexpr int kAlloc = kBar + kNumBars * 8 + 16 + 1024;
 };
@@ -48,6 +48,7 @@ struct Params {
   int out_f32;
   const uint8_t* a_tiles;     // AJ: repacked A stages (16 KB each)
   const int64_t* a_prefix;    // AJ: A tiles per sample, exclusive prefix (ceil(Bi/128) * ceil(Bi/64))
+  int dbg;                    // JG_GEMM_DBG (diagnostic, results invalid): 1 = JJJ epilogue skips the stores
 };
 
 struct Tile {
@@ -55,10 +56,33 @@ struct Tile {
   int M, N, K, m0, n0, nk;
 };
 
+// Each CTA owns a contiguous range of tiles (equal counts; tiles of one op cost about the same), so the
+// owning sample advances monotonically: a cursor replaces the per-tile binary search over the prefix
+// (ten dependent L2 round trips per tile, which capped the producer's tile rate).
+struct TileCursor {
+  int64_t i = -1, lo = 0, hi = 0;  // current sample, its tile range [lo, hi)
+};
+
+__device__ __forceinline__ void tile_range(const Params& p, int64_t& t0, int64_t& t1) {
+  const int64_t n = p.prefix[p.batch];
+  t0 = n * blockIdx.x / gridDim.x;
+  t1 = n * (blockIdx.x + 1) / gridDim.x;
+}
+
 template <int OP>
-__device__ __forceinline__ Tile tile_of(const Params& p, int64_t t) {
+__device__ __forceinline__ Tile tile_of(const Params& p, int64_t t, TileCursor& c) {
+  if (c.i < 0) {
+    c.i = upper_index(p.prefix, p.batch, t);
+    c.lo = p.prefix[c.i];
+    c.hi = p.prefix[c.i + 1];
+  }
+  while (t >= c.hi) {  // skips empty samples (zero tiles)
+    ++c.i;
+    c.lo = c.hi;
+    c.hi = p.prefix[c.i + 1];
+  }
   Tile r;
-  r.i = upper_index(p.prefix, p.batch, t);
+  r.i = c.i;
   r.b0 = p.off[r.i];
   r.n = p.off[r.i + 1] - r.b0;
   r.sqo = p.sq ? p.sq[r.i] : 0;
@@ -68,7 +92,7 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int64_t t) {
   if (OP == JJ) { r.M = p.D; r.N = p.T; r.K = Bi; }
   if (OP == JD) { r.M = Bi; r.N = p.T; r.K = p.D; }
   const int tn = (r.N + BN - 1) / BN;
-  const int64_t local = t - p.prefix[r.i];
+  const int64_t local = t - c.lo;
   r.m0 = (int)(local / tn) * BM;
   r.n0 = (int)(local % tn) * BN;
   r.nk = (r.K + BK - 1) / BK;
@@ -169,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(acc_full + b, 1);
-      tc::mbar_init(acc_empty + b, 4);
+      tc::mbar_init(acc_empty + b, OP == JJJ ? 8 : 4);
     }
     tc::fence_barrier_init();
   }
@@ -182,14 +206,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t n_tiles = p.prefix[p.batch];
+  int64_t t_begin, t_end;
+  tile_range(p, t_begin, t_end);
 
   if (warp == 0) {
     // ============================================ TMA producer
     if (lane == 0) {
       uint32_t cnt = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const Tile tl = tile_of<OP>(p, t);
+      TileCursor cur;
+      for (int64_t t = t_begin; t < t_end; ++t) {
+        const Tile tl = tile_of<OP>(p, t, cur);
         for (int kb = 0; kb < tl.nk; ++kb, ++cnt) {
           const uint32_t s = cnt % kStages;
           tc::mbar_wait(empty + s, ((cnt / kStages) & 1) ^ 1);
@@ -221,8 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN, Ly::a_mn, Ly::b_mn);
       uint32_t cnt = 0, tcount = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tcount) {
-        const Tile tl = tile_of<OP>(p, t);
+      TileCursor cur;
+      for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
+        const Tile tl = tile_of<OP>(p, t, cur);
         const int ab = tcount & 1;
         tc::mbar_wait(acc_empty + ab, ((tcount >> 1) & 1) ^ 1);
         tc::tc_fence_after();
@@ -244,12 +271,78 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         tc::mma_commit(acc_full + ab);  // with no k blocks this arrives at once (epilogue writes zeros)
       }
     }
+  } else if (OP == JJJ && warp >= 4 && warp < 12) {
+    // ============================================ JJJ epilogue (8 warps: TMEM lane quarter x column half)
+    // jagged^2 output rows have stride Bi and arbitrary 2-byte alignment: each warp stages its 32 rows x 64
+    // columns in smem (row pitch 65 floats, conflict-free) and writes every row segment as 16-byte aligned
+    // chunks (one lane each) plus at most 7 leading / 7 trailing elements. (A per-row bulk-copy variant —
+    // realigned bf16 row images + cp.async.bulk global<-shared — measured slower: 690 vs 605 us on the table1
+    // shape.)
+    const int wq = warp & 3, hf = (warp - 4) >> 2;
+    // derived from smem_raw by pointer arithmetic so the compiler keeps the shared address space (LDS/STS)
+    float* stg = reinterpret_cast<float*>(smem_raw + (smem - smem_raw) + Smem::kStg) + (warp - 4) * 32 * 65;
+    uint32_t tcount = 0;
+    TileCursor cur;
+    for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
+      const Tile tl = tile_of<OP>(p, t, cur);
+      const int ab = tcount & 1;
+      tc::mbar_wait(acc_full + ab, (tcount >> 1) & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + hf * 64 + c * 32, v);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) stg[lane * 65 + c * 32 + e] = tl.nk == 0 ? 0.f : __uint_as_float(v[e]);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
+      const int ncols = tl.N - tl.n0 < BN ? tl.N - tl.n0 : BN;
+      const int nc = ncols - 64 * hf < 64 ? ncols - 64 * hf : 64;
+      const int nrows = tl.M - tl.m0 - wq * 32 < 32 ? tl.M - tl.m0 - wq * 32 : 32;
+      const int64_t row0 = tl.sqo + (int64_t)(tl.m0 + wq * 32) * tl.n + tl.n0 + 64 * hf;
+      auto store_rows = [&](auto tag) {
+        using E = decltype(tag);
+        constexpr int CE = 16 / sizeof(E);      // elements per 16-byte chunk
+        constexpr int LPR = 64 / CE;            // lanes per row
+        E* out = reinterpret_cast<E*>(p.out);
+        const int sub = lane / LPR, li = lane % LPR;
+#pragma unroll 2
+        for (int rr = sub; rr < nrows; rr += 32 / LPR) {
+          const int64_t s0 = row0 + (int64_t)rr * tl.n, e0 = s0 + nc;
+          const int64_t sa = (s0 + CE - 1) & ~(int64_t)(CE - 1), ea = e0 & ~(int64_t)(CE - 1);
+          const float* rs = stg + rr * 65;  // staging row rr: output element x is rs[x - s0]
+          auto src = [&](int64_t x) { return rs[(int)(x - s0)]; };
+          const int64_t c0 = sa + (int64_t)li * CE;
+          if (c0 + CE <= ea) {
+            if constexpr (sizeof(E) == 4) {
+              *reinterpret_cast<float4*>(out + c0) = make_float4(src(c0), src(c0 + 1), src(c0 + 2), src(c0 + 3));
+            } else {
+              *reinterpret_cast<uint4*>(out + c0) =
+                  make_uint4(tc::pack_bf16(src(c0), src(c0 + 1)), tc::pack_bf16(src(c0 + 2), src(c0 + 3)),
+                             tc::pack_bf16(src(c0 + 4), src(c0 + 5)), tc::pack_bf16(src(c0 + 6), src(c0 + 7)));
+            }
+          }
+          const int64_t nh = (sa < e0 ? sa : e0) - s0, t0 = ea > sa ? ea : sa;
+          if (li < nh) out[s0 + li] = E(src(s0 + li));
+          if (li < e0 - t0) out[t0 + li] = E(src(t0 + li));
+        }
+      };
+      if (nc > 0 && !(p.dbg & 1)) {
+        if (p.out_f32) store_rows(float{});
+        else store_rows(__nv_bfloat16{});
+      }
+      __syncwarp();
+    }
   } else if (warp >= 4 && warp < 8) {
     // ============================================ epilogue: thread = output row of the tile
     const int wq = warp - 4, r = wq * 32 + lane;
     uint32_t tcount = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tcount) {
-      const Tile tl = tile_of<OP>(p, t);
+    TileCursor cur;
+    for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
+      const Tile tl = tile_of<OP>(p, t, cur);
       const int ab = tcount & 1;
       tc::mbar_wait(acc_full + ab, (tcount >> 1) & 1);
       tc::tc_fence_after();
@@ -261,37 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       else if (OP == JJ) base = tl.i * (int64_t)p.D * p.T + (int64_t)m * p.T + tl.n0;
       else base = (tl.b0 + m) * (int64_t)tl.N + tl.n0;
       const bool vec = OP != JJJ && ncols == BN;
-      if (OP == JJJ) {
-        // jagged^2 rows (stride Bi, arbitrary alignment): stage this warp's 32 rows in smem (row pitch 129
-        // floats, conflict-free) and write each row with the lanes along its columns (coalesced)
-        float* stg = reinterpret_cast<float*>(smem + Smem::kStg) + wq * 32 * 129;
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v[32];
-          tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + c * 32, v);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) stg[lane * 129 + c * 32 + e] = __uint_as_float(v[e]);
-        }
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
-        const int nrows = tl.M - tl.m0 - wq * 32 < 32 ? tl.M - tl.m0 - wq * 32 : 32;
-        for (int rr = 0; rr < nrows; ++rr) {
-          const int64_t rb = tl.sqo + (int64_t)(tl.m0 + wq * 32 + rr) * tl.n + tl.n0;
-#pragma unroll
-          for (int h = 0; h < BN / 32; ++h) {
-            const int col = lane + 32 * h;
-            if (col < ncols) {
-              const float x = stg[rr * 129 + col];
-              if (p.out_f32) reinterpret_cast<float*>(p.out)[rb + col] = x;
-              else reinterpret_cast<__nv_bfloat16*>(p.out)[rb + col] = __float2bfloat16_rn(x);
-            }
-          }
-        }
-        __syncwarp();
-        continue;
-      }
+      // 32-byte alignment of every row start: N (or T) a multiple of 16 bf16 / 8 fp32 elements
+      const bool vec32 = vec && ((OP == JJ ? p.T : tl.N) % (p.out_f32 ? 8 : 16)) == 0;
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
@@ -304,7 +368,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         if (!row_ok) continue;
         if (p.out_f32) {
           float* o = reinterpret_cast<float*>(p.out) + base + c * 32;
-          if (vec) {
+          if (vec32) {
+#pragma unroll
+            for (int u = 0; u < 8; u += 2)  // 32-byte sectors (STG.256)
+              tc::st_global_v8(o + u * 4, make_uint4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]),
+                               make_uint4(v[u * 4 + 4], v[u * 4 + 5], v[u * 4 + 6], v[u * 4 + 7]));
+          } else if (vec) {
 #pragma unroll
             for (int u = 0; u < 8; ++u)
               *reinterpret_cast<uint4*>(o + u * 4) = make_uint4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
@@ -316,14 +385,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         } else {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + base + c * 32;
           if (vec) {
+            uint4 w[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              uint4 w;
-              w.x = tc::pack_bf16(__uint_as_float(v[u * 8 + 0]), __uint_as_float(v[u * 8 + 1]));
-              w.y = tc::pack_bf16(__uint_as_float(v[u * 8 + 2]), __uint_as_float(v[u * 8 + 3]));
-              w.z = tc::pack_bf16(__uint_as_float(v[u * 8 + 4]), __uint_as_float(v[u * 8 + 5]));
-              w.w = tc::pack_bf16(__uint_as_float(v[u * 8 + 6]), __uint_as_float(v[u * 8 + 7]));
-              *reinterpret_cast<uint4*>(o + u * 8) = w;
+              w[u].x = tc::pack_bf16(__uint_as_float(v[u * 8 + 0]), __uint_as_float(v[u * 8 + 1]));
+              w[u].y = tc::pack_bf16(__uint_as_float(v[u * 8 + 2]), __uint_as_float(v[u * 8 + 3]));
+              w[u].z = tc::pack_bf16(__uint_as_float(v[u * 8 + 4]), __uint_as_float(v[u * 8 + 5]));
+              w[u].w = tc::pack_bf16(__uint_as_float(v[u * 8 + 6]), __uint_as_float(v[u * 8 + 7]));
+            }
+            if (vec32) {  // 32-byte sectors (STG.256)
+              tc::st_global_v8(o, w[0], w[1]);
+              tc::st_global_v8(o + 16, w[2], w[3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(o + u * 8) = w[u];
             }
           } else {
 #pragma unroll
@@ -340,8 +415,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     // ============================================ loader warpgroup
     const int wq = warp - 8;
     uint32_t cnt = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile tl = tile_of<OP>(p, t);
+    TileCursor cur;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      const Tile tl = tile_of<OP>(p, t, cur);
       for (int kb = 0; kb < tl.nk; ++kb, ++cnt) {
         const uint32_t s = cnt % kStages;
         uint8_t* sa = smem + Smem::kA + s * kTileBytes;
@@ -418,7 +494,7 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
   if (op == gm::JD) { g.M = bi; g.N = L_const(T); }
   if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, 128, tile_prefix, st)) return rc;
   gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32,
-               nullptr, nullptr};
+               nullptr, nullptr, std::getenv("JG_GEMM_DBG") ? std::atoi(std::getenv("JG_GEMM_DBG")) : 0};
   CUtensorMap ma{}, mb{};
   const int64_t rows = total_rows > 0 ? total_rows : 1;
   switch (op) {
