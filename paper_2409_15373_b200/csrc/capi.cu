@@ -751,14 +751,16 @@ extern "C" jg_status jg_mlp_layer_forward(int64_t rows, int64_t d_in, int64_t d_
   REQUIRE(d_in >= 1 && d_out >= 1, JG_INVALID_ARGUMENT, "jagged_mlp: layer dims must be positive");
   cudaStream_t st = as_stream(stream);
   if (rows == 0) return JG_OK;
+  const bool tc = !force_simt_gemm() && gemm_sm100_supported(3, d_in, d_out, dtype);
   Scratch sc(st);
-  if (jg_status rc = sc.alloc(256 + rows * d_out * 4)) return rc;
+  if (jg_status rc = sc.alloc(512 + (tc ? 0 : rows * d_out * 4))) return rc;
   int64_t* off = (int64_t*)sc.p;
-  float* acc = (float*)((char*)sc.p + 256);
+  int64_t* prefix = (int64_t*)((char*)sc.p + 256);
+  float* acc = (float*)((char*)sc.p + 512);
   if (jg_status rc = launch_two_offsets(off, rows, st)) return rc;
-  if (!force_simt_gemm() && gemm_sm100_supported(3, d_in, d_out, dtype)) {
-    if (jg_status rc = tc_gemm(3, off, nullptr, 1, rows, d_in, d_out, x, w, acc, JG_F32, st)) return rc;
-  } else {
+  if (tc)  // bias + activation fused into the tcgen05 GEMM epilogue: no fp32 round trip through HBM
+    return launch_gemm_sm100(3, off, nullptr, 1, rows, d_in, d_out, x, w, out, JG_BF16, prefix, st, bias, relu, preact);
+  {
     GemmDesc g = desc(BI(), C_(d_out), C_(d_in), C_(0), C_(d_in), C_(1), C_(0), C_(d_out), C_(1), C_(0), C_(d_out),
                       C_(1));
     if (jg_status rc = gemm(g, off, nullptr, 1, x, w, acc, dtype, JG_F32, st)) return rc;

@@ -34,7 +34,8 @@ struct Smem {
   static constexpr int kStg = 2 * kStages * kTileBytes;        // JJJ epilogue staging: 8 warps x 32 rows x 65 fp32
   static constexpr int kBar = kStg + 8 * 32 * 65 * 4;
   static constexpr int kNumBars = 3 * kStages + 4 + 1;
-  static constexpr int kAlloc = kBar + kNumBars * 8 + 16 + 1024;
+  static constexpr int kKeys = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // producer's operand-block keys
+  static constexpr int kAlloc = kKeys + 2 * kStages * 8 + 1024;
 };
 
 struct Params {
@@ -49,6 +50,9 @@ struct Params {
   const uint8_t* a_tiles;     // AJ: repacked A stages (16 KB each)
   const int64_t* a_prefix;    // AJ: A tiles per sample, exclusive prefix (ceil(Bi/128) * ceil(Bi/64))
   int dbg;                    // JG_GEMM_DBG (diagnostic, results invalid): 1 = JJJ epilogue skips the stores
+  const __nv_bfloat16* bias;  // JD only (jagged_mlp layer, bf16 out): out = act(acc + bias[col]), preact = acc + bias
+  int relu;
+  __nv_bfloat16* preact;
 };
 
 struct Tile {
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(acc_full + b, 1);
-      tc::mbar_init(acc_empty + b, OP == JJJ ? 8 : 4);
+      tc::mbar_init(acc_empty + b, OP == JJ ? 4 : 8);
     }
     tc::fence_barrier_init();
   }
@@ -212,6 +216,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   if (warp == 0) {
     // ============================================ TMA producer
     if (lane == 0) {
+      // A stage whose A (or B) operand block is the one it already holds is not reloaded: one-segment JD (the
+      // jagged_mlp layers: every CTA would otherwise re-read the same weight block from one L2 slice), per-
+      // sample JD weights across a sample's row tiles, JJJ query panels across a row of tiles. Keys identify
+      // the operand block; JJ stages are rewritten by the loader (K-tail zeroing), so they always reload.
+      uint64_t* key = reinterpret_cast<uint64_t*>(smem + Smem::kKeys);  // [2][kStages], producer-private
+      for (int s = 0; s < 2 * kStages; ++s) key[s] = ~0ull;
       uint32_t cnt = 0;
       TileCursor cur;
       for (int64_t t = t_begin; t < t_end; ++t) {
@@ -222,21 +232,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           uint8_t* sa = smem + Smem::kA + s * kTileBytes;
           uint8_t* sb = smem + Smem::kB + s * kTileBytes;
           const int k0 = kb * BK;
-          tc::mbar_expect_tx(full + s, 2 * kTileBytes);
+          uint64_t ka = ~0ull, kbk = ~0ull;  // ~0: always load
+          if (OP == JJJ || OP == JD) ka = (uint64_t)(tl.b0 + tl.m0) * 65536u + (uint64_t)kb;
+          if (OP == JJJ) kbk = (uint64_t)(tl.b0 + tl.n0) * 65536u + (uint64_t)kb;
+          if (OP == JD) kbk = ((uint64_t)tl.i * p.D + k0) * 65536u + (uint64_t)(tl.n0 / BN);
+          if (OP == AJ) kbk = (uint64_t)(tl.b0 + k0) * 65536u + (uint64_t)(tl.n0 / BN);
+          const bool load_a = ka == ~0ull || key[s] != ka, load_b = kbk == ~0ull || key[kStages + s] != kbk;
+          key[s] = ka;
+          key[kStages + s] = kbk;
+          tc::mbar_expect_tx(full + s, (load_a || OP == AJ ? kTileBytes : 0) + (load_b ? kTileBytes : 0));
           if (OP == AJ) {
             const int64_t at = p.a_prefix[tl.i] + (int64_t)(tl.m0 / BM) * tl.nk + kb;
             bulk_load(sa, p.a_tiles + at * kTileBytes, kTileBytes, full + s);
           }
-          if (OP == JJJ || OP == JD)
+          if ((OP == JJJ || OP == JD) && load_a)
             tc::tma_load_3d(sa, &tm_a, full + s, k0, 0, (int)(tl.b0 + tl.m0));
           if (OP == JJ)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sa + c * 8192, &tm_a, full + s, tl.m0 + 64 * c, 0, (int)(tl.b0 + k0));
-          if (OP == JJJ) tc::tma_load_3d(sb, &tm_b, full + s, k0, 0, (int)(tl.b0 + tl.n0));
-          if (OP == AJ || OP == JJ)
+          if (OP == JJJ && load_b) tc::tma_load_3d(sb, &tm_b, full + s, k0, 0, (int)(tl.b0 + tl.n0));
+          if ((OP == AJ && load_b) || OP == JJ)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.b0 + k0));
-          if (OP == JD)
+          if (OP == JD && load_b)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.i * p.D + k0));
         }
@@ -336,9 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       }
       __syncwarp();
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < (Ly::loader ? 8 : 12)) {
     // ============================================ epilogue: thread = output row of the tile
-    const int wq = warp - 4, r = wq * 32 + lane;
+    // JD / AJ: 8 warps (TMEM lane quarter x column half, two 32-column chunks each); JJ: 4 warps (warps 8-11
+    // are its loader)
+    constexpr int kHalves = Ly::loader ? 1 : 2, kChunks = BN / 32 / kHalves;
+    const int wq = warp & 3, hf = (warp - 4) >> 2, r = wq * 32 + lane;
     uint32_t tcount = 0;
     TileCursor cur;
     for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
@@ -357,7 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       // 32-byte alignment of every row start: N (or T) a multiple of 16 bf16 / 8 fp32 elements
       const bool vec32 = vec && ((OP == JJ ? p.T : tl.N) % (p.out_f32 ? 8 : 16)) == 0;
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int cc = 0; cc < kChunks; ++cc) {
+        const int c = hf * kChunks + cc;
         uint32_t v[32];
         tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + c * 32, v);
         tc::tmem_wait_ld();
@@ -384,6 +406,35 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           }
         } else {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + base + c * 32;
+          if (OP == JD && p.bias && !(p.dbg & 2)) {  // fused jagged_mlp layer epilogue (= bias_act_kernel)
+            __nv_bfloat16* pre = p.preact ? p.preact + base + c * 32 : nullptr;
+            // the chunk's 32 bias values: four 16-byte loads (the same address in every lane: one broadcast
+            // transaction each) instead of 32 dependent 2-byte loads
+            uint32_t bw[16];
+            if (vec) {
+              const uint4* bp = reinterpret_cast<const uint4*>(p.bias + tl.n0 + c * 32);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint4 q = __ldg(bp + u);
+                bw[u * 4] = q.x, bw[u * 4 + 1] = q.y, bw[u * 4 + 2] = q.z, bw[u * 4 + 3] = q.w;
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int col = tl.n0 + c * 32 + 2 * u;
+                const uint32_t lo = col < tl.N ? __bfloat16_as_ushort(p.bias[col]) : 0u;
+                const uint32_t hi = col + 1 < tl.N ? __bfloat16_as_ushort(p.bias[col + 1]) : 0u;
+                bw[u] = lo | (hi << 16);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const float bv = __uint_as_float((e & 1) ? (bw[e >> 1] & 0xffff0000u) : (bw[e >> 1] << 16));
+              const float x = __uint_as_float(v[e]) + bv;
+              if (pre && c * 32 + e < ncols) pre[e] = __float2bfloat16_rn(x);
+              v[e] = __float_as_uint(p.relu ? fmaxf(x, 0.f) : x);
+            }
+          }
           if (vec) {
             uint4 w[4];
 #pragma unroll
@@ -483,7 +534,7 @@ bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt) {
 // A/B roles per op: JJJ (q, k), AJ (a_j2, v), JJ (x, y), JD (x, w)
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
-                            cudaStream_t st) {
+                            cudaStream_t st, const void* bias, int relu, void* preact) {
   // tile prefix over samples with the op's (M, N)
   GemmDesc g;
   Lin bi;
@@ -494,7 +545,9 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
   if (op == gm::JD) { g.M = bi; g.N = L_const(T); }
   if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, 128, tile_prefix, st)) return rc;
   gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32,
-               nullptr, nullptr, std::getenv("JG_GEMM_DBG") ? std::atoi(std::getenv("JG_GEMM_DBG")) : 0};
+               nullptr, nullptr, std::getenv("JG_GEMM_DBG") ? std::atoi(std::getenv("JG_GEMM_DBG")) : 0,
+               (const __nv_bfloat16*)bias, relu, (__nv_bfloat16*)preact};
+  if (bias && (op != gm::JD || out_dt != JG_BF16)) return fail(JG_UNSUPPORTED, "gemm_sm100: fused bias only for JD bf16");
   CUtensorMap ma{}, mb{};
   const int64_t rows = total_rows > 0 ? total_rows : 1;
   switch (op) {

@@ -62,9 +62,11 @@ jg_status launch_gemm_prefix(const GemmDesc& g, const int64_t* off, const int64_
 
 // tcgen05 bmm family (bf16 inputs): op 0 jjbmm_jout (q,k), 1 ajbmm_jout (a_j2,v), 2 jjbmm (x,y), 3 jdbmm (x,w)
 bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt);
+// JD only: optional fused epilogue out = act(acc + bias[col]) with preact = acc + bias (jagged_mlp layers)
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
-                            cudaStream_t st);
+                            cudaStream_t st,
+                            const void* bias = nullptr, int relu = 0, void* preact = nullptr);
 
 // SURVEY §8f next rows (mlp_fi.cu)
 jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st);
