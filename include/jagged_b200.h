@@ -197,7 +197,8 @@ jg_status jg_dense_flash_attention_backward(const int64_t* lengths, int64_t batc
                                             int64_t block_k, void* dq, void* dk, void* dv,
                                             jg_dtype dtype, void* workspace, void* stream);
 /* attention.hpp:63-65 jagged_attention (unfused baseline): materializes sum Bi^2 scores per head
- * in `scores_workspace` (>= num_heads * sum Bi^2 elements of dtype, or NULL to allocate). */
+ * in `scores_workspace` (scores and probabilities: >= 2 * round_up(num_heads * sum Bi^2 * sizeof(dtype), 256)
+ * bytes, or NULL to allocate). */
 jg_status jg_jagged_attention(const int64_t* offsets, const int64_t* sq_offsets, int64_t batch,
                               int64_t total_rows, int64_t sum_sq, int32_t num_heads,
                               int32_t head_dim, const void* q, const void* k, const void* v,

@@ -559,19 +559,31 @@ extern "C" jg_status jg_jagged_attention(const int64_t* off, const int64_t* sq, 
   cudaStream_t st = as_stream(stream);
   if (total_rows == 0) return JG_OK;
   const size_t es = dsize(dtype);
+  const size_t s_bytes = ((es * (size_t)sum_sq * H + 255) / 256) * 256;  // P starts 256-byte aligned
   Scratch ws(st);
   if (!scores_ws) {
-    if (jg_status rc = ws.alloc(2 * es * (size_t)sum_sq * H)) return rc;
+    if (jg_status rc = ws.alloc(2 * s_bytes)) return rc;
     scores_ws = ws.p;
   }
   char* S = (char*)scores_ws;
-  char* P = S + es * (size_t)sum_sq * H;
+  char* P = S + s_bytes;
   const int64_t RS = (int64_t)H * D;
+  // bf16: the two contractions run on the tcgen05 grouped GEMM, one head of the [rows, H, D] tensors at a time
+  // (TMA head coordinate); otherwise the SIMT grouped GEMM with strided descriptors
+  const bool tc = !force_simt_gemm() && gemm_sm100_supported(0, D, D, dtype) && gemm_sm100_supported(1, D, D, dtype);
+  Scratch prefix(st);
+  if (tc)
+    if (jg_status rc = prefix.alloc(sizeof(int64_t) * (batch + 1))) return rc;
   for (int h = 0; h < H; ++h) {
     const int64_t ho = (int64_t)h * D;
     char* Sh = S + es * (size_t)sum_sq * h;
-    char* Ph = P + es * (size_t)sum_sq * h;
     // jagged_jagged_bmm_jagged_out (attention.cpp:167) on head h
+    if (tc) {
+      if (jg_status rc = launch_gemm_sm100(0, off, sq, batch, total_rows, D, D, q, k, Sh, dtype, (int64_t*)prefix.p, st,
+                                           nullptr, 0, nullptr, H, h))
+        return rc;
+      continue;
+    }
     GemmDesc gs = desc(BI(), BI(), C_(D), OFF(RS, ho), C_(RS), C_(1), OFF(RS, ho), C_(1), C_(RS), SQ(), BI(), C_(1));
     if (jg_status rc = gemm(gs, off, sq, batch, q, k, Sh, dtype, dtype, st)) return rc;
   }
@@ -583,6 +595,12 @@ extern "C" jg_status jg_jagged_attention(const int64_t* off, const int64_t* sq, 
     char* Sh = S + es * (size_t)sum_sq * h;
     char* Ph = P + es * (size_t)sum_sq * h;
     if (jg_status rc = launch_jagged2_softmax(off, sq, batch, total_rows, Sh, nullptr, Ph, dtype, false, st)) return rc;
+    if (tc) {  // array_jagged_bmm_jagged_out (attention.cpp:169) on head h, into out[:, h, :]
+      if (jg_status rc = launch_gemm_sm100(1, off, sq, batch, total_rows, D, D, Ph, v, (char*)out + es * ho, dtype,
+                                           (int64_t*)prefix.p, st, nullptr, 0, nullptr, H, h))
+        return rc;
+      continue;
+    }
     GemmDesc go = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(RS, ho), C_(RS), C_(1), OFF(RS, ho), C_(RS), C_(1));
     if (jg_status rc = gemm(go, off, sq, batch, Ph, v, out, dtype, dtype, st)) return rc;
   }

@@ -53,6 +53,8 @@ struct Params {
   const __nv_bfloat16* bias;  // JD only (jagged_mlp layer, bf16 out): out = act(acc + bias[col]), preact = acc + bias
   int relu;
   __nv_bfloat16* preact;
+  int head;        // JJJ / AJ on one head of [rows, H, D] tensors (unfused jagged_attention): TMA head coordinate
+  int64_t out_ld;  // AJ / JD output row pitch in elements (0: N)
 };
 
 struct Tile {
@@ -145,11 +147,12 @@ __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restric
       int sh = 0;
       if (nval > 0) {
         // an aligned 16-byte chunk holding at least one valid byte lies in that byte's page: no fault
-        const int64_t byte0 = (sqo + (int64_t)m * Bi + kb0) * 2;
-        const int64_t al = byte0 & ~int64_t(15);
+        // absolute addresses: the A base itself need not be 16-byte aligned (e.g. a slice of a larger buffer)
+        const uintptr_t byte0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)((sqo + (int64_t)m * Bi + kb0) * 2);
+        const uintptr_t al = byte0 & ~uintptr_t(15);
         sh = (int)(byte0 - al);
-        lo = __ldg(reinterpret_cast<const uint4*>(base + al));
-        if (sh != 0 && byte0 + 2 * nval > al + 16) hi = __ldg(reinterpret_cast<const uint4*>(base + al + 16));
+        lo = __ldg(reinterpret_cast<const uint4*>(al));
+        if (sh != 0 && byte0 + 2 * nval > al + 16) hi = __ldg(reinterpret_cast<const uint4*>(al + 16));
       }
       const int ws = sh >> 2;
       const bool half = (sh & 2) != 0;
@@ -246,14 +249,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
             bulk_load(sa, p.a_tiles + at * kTileBytes, kTileBytes, full + s);
           }
           if ((OP == JJJ || OP == JD) && load_a)
-            tc::tma_load_3d(sa, &tm_a, full + s, k0, 0, (int)(tl.b0 + tl.m0));
+            tc::tma_load_3d(sa, &tm_a, full + s, k0, p.head, (int)(tl.b0 + tl.m0));
           if (OP == JJ)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sa + c * 8192, &tm_a, full + s, tl.m0 + 64 * c, 0, (int)(tl.b0 + k0));
-          if (OP == JJJ && load_b) tc::tma_load_3d(sb, &tm_b, full + s, k0, 0, (int)(tl.b0 + tl.n0));
+          if (OP == JJJ && load_b) tc::tma_load_3d(sb, &tm_b, full + s, k0, p.head, (int)(tl.b0 + tl.n0));
           if ((OP == AJ && load_b) || OP == JJ)
             for (int c = 0; c < 2; ++c)
-              tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.b0 + k0));
+              tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, OP == AJ ? p.head : 0, (int)(tl.b0 + k0));
           if (OP == JD && load_b)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.i * p.D + k0));
@@ -326,11 +329,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         constexpr int CE = 16 / sizeof(E);      // elements per 16-byte chunk
         constexpr int LPR = 64 / CE;            // lanes per row
         E* out = reinterpret_cast<E*>(p.out);
+        // chunk alignment is absolute (the output base need only be element-aligned)
+        const int64_t bo = (int64_t)((reinterpret_cast<uintptr_t>(p.out) / sizeof(E)) & (CE - 1));
         const int sub = lane / LPR, li = lane % LPR;
 #pragma unroll 2
         for (int rr = sub; rr < nrows; rr += 32 / LPR) {
           const int64_t s0 = row0 + (int64_t)rr * tl.n, e0 = s0 + nc;
-          const int64_t sa = (s0 + CE - 1) & ~(int64_t)(CE - 1), ea = e0 & ~(int64_t)(CE - 1);
+          const int64_t sa = ((s0 + bo + CE - 1) & ~(int64_t)(CE - 1)) - bo, ea = ((e0 + bo) & ~(int64_t)(CE - 1)) - bo;
           const float* rs = stg + rr * 65;  // staging row rr: output element x is rs[x - s0]
           auto src = [&](int64_t x) { return rs[(int)(x - s0)]; };
           const int64_t c0 = sa + (int64_t)li * CE;
@@ -373,10 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       int64_t base;  // element index of (m, n0) in the output
       if (OP == JJJ) base = tl.sqo + (int64_t)m * tl.n + tl.n0;
       else if (OP == JJ) base = tl.i * (int64_t)p.D * p.T + (int64_t)m * p.T + tl.n0;
-      else base = (tl.b0 + m) * (int64_t)tl.N + tl.n0;
+      else base = (tl.b0 + m) * (p.out_ld ? p.out_ld : (int64_t)tl.N) + tl.n0;
       const bool vec = OP != JJJ && ncols == BN;
       // 32-byte alignment of every row start: N (or T) a multiple of 16 bf16 / 8 fp32 elements
-      const bool vec32 = vec && ((OP == JJ ? p.T : tl.N) % (p.out_f32 ? 8 : 16)) == 0;
+      const bool vec32 = vec && ((OP == JJ ? p.T : (p.out_ld ? p.out_ld : tl.N)) % (p.out_f32 ? 8 : 16)) == 0 &&
+                         (reinterpret_cast<uintptr_t>(p.out) & 31) == 0;
 #pragma unroll
       for (int cc = 0; cc < kChunks; ++cc) {
         const int c = hf * kChunks + cc;
@@ -534,7 +540,7 @@ bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt) {
 // A/B roles per op: JJJ (q, k), AJ (a_j2, v), JJ (x, y), JD (x, w)
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
-                            cudaStream_t st, const void* bias, int relu, void* preact) {
+                            cudaStream_t st, const void* bias, int relu, void* preact, int heads, int head) {
   // tile prefix over samples with the op's (M, N)
   GemmDesc g;
   Lin bi;
@@ -546,17 +552,18 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
   if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, 128, tile_prefix, st)) return rc;
   gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32,
                nullptr, nullptr, std::getenv("JG_GEMM_DBG") ? std::atoi(std::getenv("JG_GEMM_DBG")) : 0,
-               (const __nv_bfloat16*)bias, relu, (__nv_bfloat16*)preact};
+               (const __nv_bfloat16*)bias, relu, (__nv_bfloat16*)preact, head,
+               heads > 1 && op == gm::AJ ? (int64_t)heads * D : 0};
   if (bias && (op != gm::JD || out_dt != JG_BF16)) return fail(JG_UNSUPPORTED, "gemm_sm100: fused bias only for JD bf16");
   CUtensorMap ma{}, mb{};
   const int64_t rows = total_rows > 0 ? total_rows : 1;
   switch (op) {
     case gm::JJJ:
-      if (jg_status rc = gm::map2d(&ma, a, rows, D, 128)) return rc;
-      if (jg_status rc = gm::map2d(&mb, b, rows, D, 128)) return rc;
+      if (jg_status rc = make_map(&ma, a, rows, heads, (int)D, 128)) return rc;
+      if (jg_status rc = make_map(&mb, b, rows, heads, (int)D, 128)) return rc;
       return gm::run<gm::JJJ>(p, ma, mb, st);
     case gm::AJ: {
-      if (jg_status rc = gm::map2d(&mb, b, rows, D, 64)) return rc;
+      if (jg_status rc = make_map(&mb, b, rows, heads, (int)D, 64)) return rc;
       // A tiles per sample: ceil(Bi/128) * ceil(Bi/64) (a prefix with M = N = Bi and 128 x 64 tiles)
       int64_t* a_prefix = nullptr;
       JG_CUDA(cudaMallocAsync(&a_prefix, sizeof(int64_t) * (batch + 1), st));

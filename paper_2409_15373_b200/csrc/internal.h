@@ -66,7 +66,10 @@ bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt);
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
                             cudaStream_t st,
-                            const void* bias = nullptr, int relu = 0, void* preact = nullptr);
+                            const void* bias = nullptr, int relu = 0, void* preact = nullptr,
+                            // JJJ / AJ on head `head` of [rows, heads, D] q/k (JJJ) or v (AJ); the AJ output
+                            // pointer is the head's column block of a [rows, heads, D] tensor
+                            int heads = 1, int head = 0);
 
 // SURVEY §8f next rows (mlp_fi.cu)
 jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st);

@@ -167,3 +167,11 @@ def test_fwd_bwd_host_entry_matches_device_api():
     np.testing.assert_allclose(lse.numpy(), saved.logsumexp.cpu().numpy(), rtol=1e-5, atol=1e-4)
     for got, ref, name in zip(outs[1:], (grads.dq, grads.dk, grads.dv), ("dq", "dk", "dv")):
         assert_bf16_close(got, ref.values.float().cpu().numpy(), tol=1e-2, what=name)
+
+
+def test_unfused_tensor_core_path_multihead():
+    """jagged_attention on the tcgen05 grouped GEMM (bf16, head_dim 128, two heads: TMA head coordinate, strided
+    output) and on a jagged^2 scratch whose size is not a multiple of 16 bytes."""
+    off, (q, k, v, go), (Q, K, V, G) = make([3, 129, 0, 70, 255], 2, 128, 8, torch.bfloat16)
+    ref = np.stack([R.jagged_attention(off, q[:, h], k[:, h], v[:, h]) for h in range(2)], 1)
+    assert_bf16_close(J.jagged_attention(Q, K, V).values, ref, tol=3e-2, what="unfused tcgen05 (2 heads)")
