@@ -7,9 +7,8 @@
 // back into the reference's owning tensor types. Validation happens on the host with the reference's
 // exception texts (linalg.cpp:16-26, :37-44, :165-172, attention.cpp:33-40, :179-180, :234-241).
 //
-// T = double (the registry/gradcheck substrate) and the operators off the hot path (jagged_mlp,
-// dense_attention, dense_flash_attention) have no device implementation: they throw
-// std::invalid_argument naming the operator. There is no CPU fallback.
+// T = double (the registry/gradcheck substrate) and dense_attention (the materialised padded baseline) have
+// no device implementation: they throw std::invalid_argument naming the operator. There is no CPU fallback.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -382,10 +381,26 @@ DenseTensor<T> dense_attention(const DenseTensor<T>&, const DenseTensor<T>&, con
   no_device_path<T>("dense_attention");
 }
 
+// attention.cpp:106-160 on the device: the jagged attention kernels in padded mode
+// (jg_dense_flash_attention_forward validates the shape/lengths with the reference's messages).
 template <typename T>
-DenseAttentionSaved<T> dense_flash_attention(const DenseTensor<T>&, const DenseTensor<T>&, const DenseTensor<T>&,
-                                             std::span<const int64_t>, int64_t, int64_t, const KernelOptions&) {
-  no_device_path<T>("dense_flash_attention");
+DenseAttentionSaved<T> dense_flash_attention(const DenseTensor<T>& q, const DenseTensor<T>& k, const DenseTensor<T>& v,
+                                             std::span<const int64_t> lengths, int64_t block_q, int64_t block_k,
+                                             const KernelOptions&) {
+  const char* op = "dense_flash_attention";
+  if (q.rank() != 3 || q.shape() != k.shape() || q.shape() != v.shape())
+    throw std::invalid_argument("dense_flash_attention: q, k, v must share a [B, L, D] shape");
+  if (static_cast<int64_t>(lengths.size()) != q.shape()[0])
+    throw std::invalid_argument("dense_flash_attention: lengths size mismatch");
+  if constexpr (!is_f32<T>) no_device_path<T>(op);
+  const int64_t B = q.shape()[0], L = q.shape()[1], D = q.shape()[2];
+  Dev dq = Dev::from(q.data(), op), dk = Dev::from(k.data(), op), dv = Dev::from(v.data(), op),
+      out(sizeof(T) * q.data().size(), op), lse(sizeof(float) * B * L, op);
+  ck(op, jg_dense_flash_attention_forward(lengths.data(), B, L, 1, (int32_t)D, dq.p, dk.p, dv.p, block_q, block_k,
+                                          out.p, (float*)lse.p, JG_F32, 0));
+  const std::vector<float> lse_f = lse.to<float>(B * L, op);
+  return {DenseTensor<T>({B, L, D}, out.to<T>(q.data().size(), op)), std::vector<T>(lse_f.begin(), lse_f.end()),
+          block_q, block_k};
 }
 
 namespace {

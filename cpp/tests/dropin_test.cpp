@@ -3,6 +3,7 @@
 // jagged::make_jagged / jagged::Rng, call the jagged:: operators, compare with independent binary64
 // loops (cf. proj/tests/support/reference.hpp) and check the reference's exception texts.
 // Exit code 0 = all checks passed. Run by tests/test_gpu_cpp_dropin.py on the GPU box.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
@@ -129,6 +130,45 @@ int main() {
     DenseTensor<float> targets({B, 3, D}, uniform_values<float>(rng, B * 3 * D, -1, 1));
     auto fi = feature_interaction(x, v, targets);
     check(fi.shape() == std::vector<int64_t>({B, 3, D}), "feature_interaction shape");
+  }
+  // --- dense_flash_attention (attention.cpp:106-160) in the GPU padded mode: valid rows equal the jagged
+  // attention of the truncated samples, padded rows are zero with lse = -inf
+  {
+    const int64_t L = 40, Bd = 4;
+    const std::vector<int64_t> dl = {7, 0, 40, 19};
+    DenseTensor<float> dq({Bd, L, D}, uniform_values<float>(rng, Bd * L * D, -1, 1));
+    DenseTensor<float> dk({Bd, L, D}, uniform_values<float>(rng, Bd * L * D, -1, 1));
+    DenseTensor<float> dvv({Bd, L, D}, uniform_values<float>(rng, Bd * L * D, -1, 1));
+    auto ds = dense_flash_attention(dq, dk, dvv, std::span<const int64_t>(dl), 16, 16);
+    double worst = 0.0;
+    bool pad_ok = true;
+    for (int64_t i = 0; i < Bd; ++i)
+      for (int64_t a = 0; a < L; ++a) {
+        if (a >= dl[i]) {
+          for (int64_t d = 0; d < D; ++d) pad_ok = pad_ok && ds.output.at(i, a, d) == 0.f;
+          pad_ok = pad_ok && std::isinf(ds.logsumexp[i * L + a]) && ds.logsumexp[i * L + a] < 0;
+          continue;
+        }
+        std::vector<double> sc(dl[i]);
+        double m = -1e300, sum = 0.0;
+        for (int64_t c = 0; c < dl[i]; ++c) {
+          double acc = 0.0;
+          for (int64_t d = 0; d < D; ++d) acc += (double)dq.at(i, a, d) * dk.at(i, c, d);
+          sc[c] = acc / std::sqrt((double)D);
+          m = std::max(m, sc[c]);
+        }
+        for (int64_t c = 0; c < dl[i]; ++c) sum += std::exp(sc[c] - m);
+        for (int64_t d = 0; d < D; ++d) {
+          double o = 0.0;
+          for (int64_t c = 0; c < dl[i]; ++c) o += std::exp(sc[c] - m) / sum * dvv.at(i, c, d);
+          worst = std::max(worst, std::fabs(o - ds.output.at(i, a, d)));
+        }
+      }
+    check(worst < 1e-5 && pad_ok, "dense_flash_attention max err=" + std::to_string(worst));
+    const std::vector<int64_t> bad = {7, 0, 41, 19};
+    check(throws_with([&] { dense_flash_attention(dq, dk, dvv, std::span<const int64_t>(bad), 16, 16); },
+                      "dense_flash_attention: sample 2 length 41 out of bounds for L=40"),
+          "error: dense_flash_attention length bounds");
   }
   // --- jagged_mlp forward + VJP (linalg.cpp:246-277, :509-573) against a host binary64 restatement
   {
