@@ -175,3 +175,47 @@ def test_unfused_tensor_core_path_multihead():
     off, (q, k, v, go), (Q, K, V, G) = make([3, 129, 0, 70, 255], 2, 128, 8, torch.bfloat16)
     ref = np.stack([R.jagged_attention(off, q[:, h], k[:, h], v[:, h]) for h in range(2)], 1)
     assert_bf16_close(J.jagged_attention(Q, K, V).values, ref, tol=3e-2, what="unfused tcgen05 (2 heads)")
+
+
+def _dense_sample_ref(q, k, v, go):
+    """fp32 torch reference of one sample's attention fwd + bwd ([n, H, D] inputs)."""
+    D = q.shape[-1]
+    q, k, v, go = (t.float().transpose(0, 1).requires_grad_() for t in (q, k, v, go))  # [H, n, D]
+    s = torch.matmul(q, k.transpose(1, 2)) / D ** 0.5
+    lse = torch.logsumexp(s, dim=-1)
+    o = torch.matmul(torch.softmax(s, dim=-1), v)
+    dq, dk, dv = torch.autograd.grad(o, (q, k, v), go)
+    return (o.detach().transpose(0, 1), lse.detach(), dq.transpose(0, 1), dk.transpose(0, 1), dv.transpose(0, 1))
+
+
+def test_full_size_cfg3_properties():
+    """BASELINE cfg3 at full size (B=1024, L=1024, D=128, H=4, half-mean seed 0): spot-check whole samples
+    against an fp32 torch reference (largest, smallest non-empty, and random ones) and check the size-independent
+    identities on every sample: sum_k dV_k = sum_q dO_q (rows of P sum to 1; relative to sum_q |dO_q|) and
+    sum_k dK_k = 0 (rows of dS sum to 0; max-abs). bf16 tolerance 2e-2."""
+    ln = R.gen_lengths("half-mean", 1024, 0, 1024)
+    off = R.make_offsets(ln)
+    S, H, D = int(off[-1]), 4, 128
+    g = torch.Generator(device=DEV).manual_seed(3)
+    q, k, v, go = ((torch.rand(S, H, D, device=DEV, generator=g) * 2 - 1).bfloat16() for _ in range(4))
+    T = lambda a: J.JaggedTensor(torch.from_numpy(off).to(DEV), a, off)  # noqa: E731
+    Q, K, V, G = T(q), T(k), T(v), T(go)
+    saved = J.jagged_flash_attention_forward(Q, K, V)
+    gr = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+    nz = np.nonzero(ln)[0]
+    picks = {int(nz[np.argmax(ln[nz])]), int(nz[np.argmin(ln[nz])])} | set(np.random.default_rng(0).choice(nz, 4).tolist())
+    for i in sorted(picks):
+        a, b = int(off[i]), int(off[i + 1])
+        o, lse, dq, dk, dv = _dense_sample_ref(q[a:b], k[a:b], v[a:b], go[a:b])
+        assert_bf16_close(saved.output.values[a:b], o.cpu().numpy(), what=f"out sample {i} (n={b - a})")
+        assert_bf16_close(saved.logsumexp[:, a:b], lse.cpu().numpy(), what=f"lse sample {i}")
+        for got, ref, nm in ((gr.dq, dq, "dq"), (gr.dk, dk, "dk"), (gr.dv, dv, "dv")):
+            assert_bf16_close(got.values[a:b], ref.cpu().numpy(), what=f"{nm} sample {i} (n={b - a})")
+    seg = torch.repeat_interleave(torch.arange(len(ln), device=DEV), torch.from_numpy(ln).to(DEV))
+    segsum = lambda t: torch.zeros(len(ln), H, D, device=DEV).index_add_(0, seg, t.float())  # noqa: E731
+    sdv, sdo, sdk = segsum(gr.dv.values), segsum(go), segsum(gr.dk.values)
+    scale = segsum(go.abs()).clamp_min(1.0)
+    assert float(((sdv - sdo).abs() / scale).max()) < 2e-2, "sum_k dV != sum_q dO"
+    # dS is rounded to bf16 before the dK MMA, so its rows sum to 0 only up to bf16 rounding: the identity is
+    # checked at the product's max-abs tolerance (sum_k |dK_k| is O(1-5) per (sample, head, d) here)
+    assert float(sdk.abs().max()) < 2e-2, "sum_k dK != 0"
