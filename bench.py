@@ -339,6 +339,28 @@ def _events_time(fn, steps, warmup):
     return float(np.median(ts))
 
 
+def _graph_time(fn, steps):
+    """Device time of `fn` replayed from a captured CUDA graph (no host/launch overhead; small configs are
+    launch-latency bound in eager mode). Returns ms, or None if capture is not possible."""
+    import torch
+
+    try:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()  # warm-up on the capture stream (one-time attribute setup happens outside the capture)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        return _events_time(g.replay, steps, 2)
+    except Exception as e:  # noqa: BLE001 — diagnostic leg only
+        print(f"graph capture failed: {e}", file=sys.stderr)
+        return None
+
+
 def _cpu_ref_time(fn, reps=3):
     ts = []
     for _ in range(reps):
@@ -382,6 +404,7 @@ def run_configs(args):
             J.jagged_softmax(J.jagged_dense_bmm(X, W))
 
         ms = _events_time(step, args.steps, args.warmup)
+        ms_graph = _graph_time(step, args.steps)
         eb = 4
         byts = (S * D + B * D * T + S * T) * eb + 2 * S * T * eb  # cost_model.cpp:153-155, :165-168
         flops = 2 * S * D * T
@@ -397,6 +420,7 @@ def run_configs(args):
         emit({"metric": "jagged-op GB/s", "config": {"workload": "cfg1: jagged_dense_bmm + jagged_softmax B=64 "
               "max_len=128 D=64 T=32 uniform seed 0", "sum_B": S}, "dtype": "f32", "value": byts / (ms * 1e-3) / 1e9,
               "unit": "GB/s", "us_per_step": ms * 1e3, "tflops": flops / (ms * 1e-3) / 1e12,
+              "graph_us_per_step": ms_graph * 1e3 if ms_graph else None,
               "roofline": {"bound": "hbm", "achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                            "frac": byts / (ms * 1e-3) / 1e9 / hbm, "note": "~2.8 MB: launch-latency bound"},
               "cpu_baseline": cpu})
@@ -414,9 +438,11 @@ def run_configs(args):
         fwd_fl, bwd_fl, sq = useful_flops(ln, H, D)
         saved = J.jagged_flash_attention_forward(Q, K, V, schedule=sched)
         ms_f = _events_time(lambda: J.jagged_flash_attention_forward(Q, K, V, schedule=sched), args.steps, args.warmup)
+        ms_fg = _graph_time(lambda: J.jagged_flash_attention_forward(Q, K, V, schedule=sched), args.steps)
         line = {"metric": "Jagged flash-attn " + ("fwd" if fwd_only else "fwd+bwd") + " TFLOP/s (useful FLOPs)",
                 "config": {"workload": wl, "sum_B": S, "sum_sq": sq}, "dtype": "bf16",
-                "fwd_ms": ms_f, "fwd_tflops": fwd_fl / (ms_f * 1e-3) / 1e12}
+                "fwd_ms": ms_f, "fwd_tflops": fwd_fl / (ms_f * 1e-3) / 1e12,
+                "fwd_graph_ms": ms_fg, "fwd_graph_tflops": fwd_fl / (ms_fg * 1e-3) / 1e12 if ms_fg else None}
         total_fl, total_ms = fwd_fl, ms_f
         if not fwd_only:
             ws = torch.empty(lib.jg_attention_backward_workspace_size(S, H, D), dtype=torch.uint8, device=dev)
