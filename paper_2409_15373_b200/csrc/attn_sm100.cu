@@ -41,7 +41,10 @@ constexpr int kProducerWarp = 8, kMmaWarp = 9;
 // to the MMA warp and the 8 softmax warps through a small smem ring.
 constexpr int kItemSlots = 4;
 constexpr int kItemConsumers = 1 + 8;
-constexpr int kPolyExp = 2;               // of every 8 exponentials, this many run on the FMA pipe (ex2_poly)
+#ifndef JG_FWD_POLY_EXP
+#define JG_FWD_POLY_EXP 2
+#endif
+constexpr int kPolyExp = JG_FWD_POLY_EXP;  // of every 8 exponentials, this many run on the FMA pipe (ex2_poly)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
 
 template <int D>
