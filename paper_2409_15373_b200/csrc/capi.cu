@@ -624,7 +624,10 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   // kSlots-stream pipeline: later chunks' host->device copies and earlier chunks' device->host copies
   // (separate copy engines) overlap a chunk's forward + backward. Host buffers should be pinned.
   constexpr int kSlots = 3;
-  const int64_t n_chunks = std::max<int64_t>(1, std::min<int64_t>(16, batch));
+#ifndef JG_HOST_CHUNKS
+#define JG_HOST_CHUNKS 32  // e2e on cfg3: 16 chunks 48.9 ms, 32 chunks 46.4-47.8 ms, 48 chunks 47.8 ms
+#endif
+  const int64_t n_chunks = std::max<int64_t>(1, std::min<int64_t>(JG_HOST_CHUNKS, batch));
   std::vector<int64_t> cut{0};
   for (int64_t c = 1; c < n_chunks; ++c) {
     const int64_t target = S * c / n_chunks;
