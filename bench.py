@@ -266,9 +266,12 @@ def run_ours(args, rank, world, local_rank):
     d2h = 4 * hq.numel() * 2 + hl.numel() * 4
 
     t = torch.tensor([elapsed_ms, e2e_s], dtype=torch.float64, device=dev)
+    nb = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)  # whole-job copy bytes per step
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nb, op=dist.ReduceOp.SUM)
     elapsed_ms, e2e_s = float(t[0]), float(t[1])
+    h2d, d2h = float(nb[0]), float(nb[1])
     if rank != 0:
         return
 
