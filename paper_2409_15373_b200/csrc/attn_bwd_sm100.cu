@@ -9,16 +9,17 @@
 //   2. main persistent kernel, key-stationary: a CTA owns 128 key rows of one (sample, head) and
 //      streams the sample's queries in 64-row blocks:
 //        S^T = K Q_j^T, dP^T = V dO_j^T                      (tcgen05, M=128 keys, N=64 queries)
-//        P^T, dS^T in registers -> smem (bf16, SWIZZLE_128B)  (softmax warpgroup, thread = key row)
-//        dV += P^T dO_j, dK += dS^T Q_j                      (accumulated in TMEM across all j)
+//        P^T (bf16) back into TMEM over S^T, dS^T -> smem      (softmax warps, thread = key row)
+//        dV += P^T dO_j (TS: A = P^T from TMEM), dK += dS^T Q_j   (accumulated in TMEM across all j)
 //        dQ_j^T = K^T dS^T                                    (M = head_dim, N = 64 queries)
 //      dQ_j^T is drained by a second warpgroup through smem and added into the fp32 accumulator with
-//      one TMA tensor reduce-add per block (cp.reduce.async.bulk.tensor .add, [64 q x D] fp32 box).
+//      four TMA tensor reduce-adds per block (cp.reduce.async.bulk.tensor .add, [16 q x D] fp32 boxes,
+//      two alternating staging buffers). Work items are taken dynamically in LPT order.
 //   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
 // Warps: 0 TMA producer, 1-2 MMA issuers, 4-11 softmax/dS (two warps per TMEM lane
 // quarter, 32 query columns each), 12-15 dQ drain + dK/dV epilogue.
-// TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); dQ_j^T reuses the S^T slot
-// of buffer j&1 once its scores are consumed; dV [256,384), dK [384,512). S_{j+1} is issued before
+// TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); P^T_j is written over the S^T
+// slot and dQ_j^T into the dP^T slot of buffer j&1 once its scores are consumed; dV [256,384), dK [384,512). S_{j+1} is issued before
 // dV_j/dK_j/dQ_j so the softmax warpgroup works on block j+1 while the tensor core finishes block j.
 #include "common.cuh"
 #include "internal.h"
@@ -41,7 +42,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef JG_BWD_QD_STAGES
 #define JG_BWD_QD_STAGES 4
 #endif
-constexpr int kQdStages = JG_BWD_QD_STAGES;  // (Q_j, dO_j) smem ring depth (4: better at item boundaries; 3 leaves room for one 64-row dQ reduce)
+constexpr int kQdStages = JG_BWD_QD_STAGES;  // (Q_j, dO_j) smem ring depth (4 on cfg3; 3 frees room for 4 dQ staging buffers)
 constexpr int kPdsBufs = 1;   // dS^T smem buffers
 
 template <int D>

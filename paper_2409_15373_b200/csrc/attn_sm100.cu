@@ -6,18 +6,21 @@
 // offsets[i] + 128*t of the flat [total_rows, H, D] buffers (3-D tensor map D x H x rows, SWIZZLE_128B);
 // rows past a segment end belong to the next sample and are masked (keys) or never stored (queries).
 //
-// Persistent kernel, one CTA per SM, walking the device LPT work list (layout.cu) of
-// (sample, 256-query tile pair) items x heads. A work item holds two 128-row query tiles A and B of
+// Persistent kernel, one CTA per SM, taking (sample, 256-query tile pair) x head items from the device LPT
+// work list (layout.cu) through a global counter (the first round is static). A work item holds two 128-row query tiles A and B of
 // the same sample (B absent when the sample has an odd number of 128-row tiles); they share every
 // K/V block, and their softmax warpgroups ping-pong with the tensor core (FlashAttention-4 style):
 //     tensor core:  PV_A(j) S_A(j+1) | PV_B(j) S_B(j+1) | PV_A(j+1) S_A(j+2) | ...
 //     softmax A  :          ^ works on S_A(j+1) while the tensor core runs PV_B(j), S_B(j+1)
 // Warp roles (10 warps):
 //   warps 0-3   softmax warpgroup A (thread = query row = TMEM lane), warps 4-7 warpgroup B:
-//               tcgen05.ld S, mask, running max, exp2, P -> smem (bf16, SWIZZLE_128B K-major),
-//               lazy O rescale in TMEM (only when the max grows by > 2^8), epilogue O / l -> global
-//   warp 8      TMA producer: Q tiles, then K_0, V_0, K_1, V_1, ... through a ring of smem stages
-//   warp 9      MMA issuer (one thread)
+//               tcgen05.ld S, mask, running max (FMNMX3), exp2 (MUFU + 2 of 8 on the FMA pipe, paired
+//               FFMA2/FADD2), P -> TMEM over S (bf16; the A operand of the TS-form PV MMA), lazy O rescale
+//               in TMEM (only when the max grows by > 2^8), epilogue O / l -> global (32-byte sector stores)
+//               (padded dense_flash_attention mode: keys/rows past each sample's valid length masked)
+//   warp 8      TMA producer: Q tiles, then K_0, V_0, K_1, V_1, ... through a ring of smem stages;
+//               claims work items and publishes decoded descriptors through an smem ring
+//   warp 9      MMA issuer (warp-collective, one elected lane issues)
 // TMEM (512 cols): S_A [0,128), O_A [128,256), S_B [256,384), O_B [384,512).
 // tcgen05 operations of one thread complete in issue order, so S_X(j+1) completing implies PV_X(j)
 // completed: the softmax needs no separate "PV done" barrier inside the key loop.
