@@ -6,16 +6,18 @@
 //   AJ   array_jagged_bmm_jagged_out  (:161)  O_i = A_i V_i        M=Bi N=D  K=Bi  A jagged^2 (manual), B MN-major
 //   JJ   jagged_jagged_bmm            (:70)   Z_i = X_i^T Y_i      M=D  N=T  K=Bi  A,B MN-major (TMA)
 //   JD   jagged_dense_bmm             (:34)   O_i = X_i W_i        M=Bi N=T  K=D   A K-major, B MN-major
-// 128x128 output tiles, 64-deep K stages through a 4-stage ring, accumulators double-buffered in TMEM
-// so the epilogue of tile t overlaps the MMAs of tile t+1. TMA coordinates are global row indices
+// 128x128 output tiles, 64-deep K stages through a 4-stage ring (a stage skips reloading an operand block
+// it already holds), accumulators double-buffered in TMEM so the epilogue of tile t overlaps the MMAs of
+// tile t+1; each CTA walks a contiguous tile range with a sample cursor. TMA coordinates are global row indices
 // (offsets[i] + local row), so no padding is materialised; rows of the next sample that a tail tile
 // picks up are masked: never stored (M/N tails) or zeroed in smem before the MMA (K tails of JJ, where
 // the reduction runs over the jagged axis). Jagged^2 A operands (row stride Bi, arbitrary 2-byte
 // alignment, unusable by TMA) are first repacked by aj_repack_kernel into 16 KB tiles that are already
 // the smem image of one [128 m x 64 k] SWIZZLE_128B stage (zeros past Bi); the producer then moves each
 // stage with a single bulk copy (cp.async.bulk) — one pass of HBM traffic instead of a latency-bound
-// per-stage gather. Warps: 0 TMA producer, 1 MMA issuer, 4-7 epilogue (TMEM -> registers -> global),
-// 8-11 loader (JJ K-tail zeroing).
+// per-stage gather. Warps: 0 TMA producer, 1 MMA issuer, 4-11 epilogue (TMEM -> registers -> global; lane
+// quarter x column half; JJJ stages through smem and writes aligned 16-byte chunks; JD can fuse the jagged_mlp
+// bias + ReLU), except JJ: 4-7 epilogue and 8-11 loader (K-tail zeroing).
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
