@@ -63,3 +63,72 @@ def all_reduce_mlp_grads(dlayers, group=None) -> None:
     for g in dlayers:
         for t in ((g.dweights, g.dbias) if hasattr(g, "dweights") else g):
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def scatter_jagged(offsets, values, world: int, rank: int, cost: str = "sq", src: int = 0, group=None):
+    """SURVEY §8e setup: `src` holds the full jagged batch (host offsets [B+1] int64, values [rows, ...]); every
+    rank receives its cost-balanced contiguous sample shard. Offsets go out by broadcast, each shard's rows by
+    one point-to-point send (batched isend/irecv: NCCL over NVLink for CUDA tensors, gloo on CPU). Returns
+    (Shard, local values). Non-src ranks pass values=None (CPU float32 receive buffers) or any tensor whose
+    dtype/device the receive buffer should take."""
+    import torch
+    import torch.distributed as dist
+
+    off_t = torch.as_tensor(np.asarray(offsets, np.int64)) if rank == src else None
+    n = torch.tensor([0 if off_t is None else off_t.numel()], dtype=torch.int64)
+    dist.broadcast(n, src, group=group)
+    if off_t is None:
+        off_t = torch.empty(int(n.item()), dtype=torch.int64)
+    dist.broadcast(off_t, src, group=group)
+    off = off_t.numpy()
+    sh = make_shard(np.diff(off), world, rank, cost)
+    # row shape / dtype travel with a small header from src
+    if rank == src:
+        meta = torch.tensor([values.dim()] + list(values.shape[1:]) + [0] * (4 - values.dim()), dtype=torch.int64)
+    else:
+        meta = torch.empty(4, dtype=torch.int64)
+    dist.broadcast(meta, src, group=group)
+    rest = [int(x) for x in meta[1:int(meta[0])].tolist()]
+    bounds = shard_bounds(np.diff(off), world, cost)
+    if rank == src:
+        ops = []
+        for r in range(world):
+            r0, r1 = int(off[bounds[r]]), int(off[bounds[r + 1]])
+            if r != src and r1 > r0:
+                ops.append(dist.P2POp(dist.isend, values[r0:r1].contiguous(), r, group=group))
+        for w in dist.batch_isend_irecv(ops) if ops else []:
+            w.wait()
+        local = values[sh.row_begin:sh.row_end].clone()
+    else:
+        local = torch.empty([sh.row_end - sh.row_begin] + rest, dtype=torch.float32 if values is None else values.dtype,
+                            device="cpu" if values is None else values.device)
+        if local.shape[0] > 0:
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.irecv, local, src, group=group)]):
+                w.wait()
+    return sh, local
+
+
+def gather_jagged(sh: Shard, local, offsets, world: int, rank: int, cost: str = "sq", dst: int = 0, group=None):
+    """SURVEY §8e verification: the inverse of `scatter_jagged` — every rank's shard rows (outputs, grads, or lse
+    rows) are sent to `dst`, which reassembles the full [rows, ...] tensor in sample order (None elsewhere)."""
+    import torch
+    import torch.distributed as dist
+
+    off = np.asarray(offsets, np.int64)
+    bounds = shard_bounds(np.diff(off), world, cost)
+    if rank != dst:
+        if local.shape[0] > 0:
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), dst, group=group)]):
+                w.wait()
+        return None
+    full = torch.empty([int(off[-1])] + list(local.shape[1:]), dtype=local.dtype, device=local.device)
+    ops = []
+    for r in range(world):
+        r0, r1 = int(off[bounds[r]]), int(off[bounds[r + 1]])
+        if r == dst:
+            full[r0:r1] = local
+        elif r1 > r0:
+            ops.append(dist.P2POp(dist.irecv, full[r0:r1], r, group=group))
+    for w in dist.batch_isend_irecv(ops) if ops else []:
+        w.wait()
+    return full
