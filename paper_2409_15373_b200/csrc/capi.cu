@@ -71,6 +71,15 @@ static size_t dsize(jg_dtype d) { return d == JG_F32 ? 4 : (d == JG_BF16 ? 2 : 8
     if (!(cond)) return ::jg::fail(code, msg); \
   } while (0)
 
+// device pointers a call dereferences must be non-null whenever there is data (checked before any CUDA call)
+#define REQUIRE_PTRS(op, nonempty, ...)                                                                   \
+  do {                                                                                                   \
+    const void* ptrs_[] = {__VA_ARGS__};                                                                 \
+    if (nonempty)                                                                                        \
+      for (const void* p_ : ptrs_)                                                                       \
+        REQUIRE(p_ != nullptr, JG_INVALID_ARGUMENT, std::string(op) + ": null device pointer");          \
+  } while (0)
+
 #define CHECK_DT(op, dt) \
   REQUIRE((dt) != JG_F64, JG_UNSUPPORTED, std::string(op) + ": f64 has no device path (no CPU fallback)"); \
   REQUIRE(dtype_ok(dt), JG_INVALID_ARGUMENT, std::string(op) + ": unknown dtype")
@@ -478,6 +487,7 @@ extern "C" jg_status jg_jagged_flash_attention_forward(const int64_t* off, int64
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
           "jagged_flash_attention_forward: block sizes must be >= 1");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_forward: dim mismatch");
+  REQUIRE_PTRS("jagged_flash_attention_forward", total_rows > 0, off, q, k, v, out, lse);
   return attn_forward(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, sched, nullptr, as_stream(stream));
 }
 
@@ -491,6 +501,7 @@ extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int6
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
           "jagged_flash_attention_backward: saved state does not match inputs");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_backward: grad_out layout mismatch");
+  REQUIRE_PTRS("jagged_flash_attention_backward", total_rows > 0, off, q, k, v, go, o, lse, dq, dk, dv);
   return attn_backward(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, sched, workspace,
                        nullptr, as_stream(stream));
 }
@@ -525,6 +536,7 @@ extern "C" jg_status jg_dense_flash_attention_forward(const int64_t* lengths, in
   CHECK_DT("dense_flash_attention", dtype);
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT, "dense_flash_attention: block sizes must be >= 1");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "dense_flash_attention: q, k, v must share a [B, L, D] shape");
+  REQUIRE_PTRS("dense_flash_attention", batch * max_len > 0, q, k, v, out, lse);
   cudaStream_t st = as_stream(stream);
   Scratch buf(st);
   const int64_t *d_off = nullptr, *d_valid = nullptr;
@@ -542,6 +554,7 @@ extern "C" jg_status jg_dense_flash_attention_backward(const int64_t* lengths, i
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
           "dense_flash_attention_backward: block sizes must be >= 1");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "dense_flash_attention_backward: q, k, v must share a [B, L, D] shape");
+  REQUIRE_PTRS("dense_flash_attention_backward", batch * max_len > 0, q, k, v, go, o, lse, dq, dk, dv);
   cudaStream_t st = as_stream(stream);
   Scratch buf(st);
   const int64_t *d_off = nullptr, *d_valid = nullptr;
@@ -556,6 +569,7 @@ extern "C" jg_status jg_jagged_attention(const int64_t* off, const int64_t* sq, 
                                          const void* v, void* out, jg_dtype dtype, void* scores_ws, void* stream) {
   CHECK_DT("jagged_attention", dtype);
   REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged_attention: sq_offsets required");
+  REQUIRE_PTRS("jagged_attention", total_rows > 0, off, q, k, v, out);
   cudaStream_t st = as_stream(stream);
   if (total_rows == 0) return JG_OK;
   const size_t es = dsize(dtype);

@@ -63,3 +63,20 @@ def test_no_oracle_in_product_package():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt and "libjagged_ref" not in txt, f
+
+
+def test_null_device_pointers_rejected_before_any_cuda_call(libpath):
+    """The attention entry points validate their device pointers on the host (no CUDA call is made, so this
+    runs without a GPU): a null pointer with data is JG_INVALID_ARGUMENT, not a device fault."""
+    import ctypes as C
+
+    lib = C.CDLL(libpath)
+    lib.jg_last_error.restype = C.c_char_p
+    P, I64, I32 = C.c_void_p, C.c_int64, C.c_int32
+    f = lib.jg_jagged_flash_attention_forward
+    f.argtypes = [P, I64, I64, I32, I32, P, P, P, I64, I64, P, P, C.c_int, P, P]
+    f.restype = C.c_int
+    rc = f(None, 2, 10, 1, 64, None, None, None, 64, 64, None, None, 1, None, None)
+    assert rc == 1 and b"null device pointer" in lib.jg_last_error()
+    rc = f(None, 0, 0, 1, 64, None, None, None, 64, 64, None, None, 1, None, None)  # no data: nothing to do
+    assert rc == 0
