@@ -61,8 +61,8 @@ struct Smem {
   static constexpr int kBar = kKV + kStages * kTile;
   // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_done[2], o_empty[2], tmem slot
   static constexpr int kNumBars = 2 + 2 * kStages + 8 + 1 + 2 * kItemSlots;
-  static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 32-byte descriptors
-  static constexpr int kBytes = kItemRing + kItemSlots * 32;
+  static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 48-byte descriptors
+  static constexpr int kBytes = kItemRing + kItemSlots * 48;
   static constexpr int kAlloc = kBytes + 1024;          // manual 1 KB alignment
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
@@ -81,12 +81,17 @@ struct Params {
   int dbg;                   // JG_FWD_DBG (diagnostic, results invalid): 1 = softmax publishes P without computing
   const int64_t* valid;      // padded mode (dense_flash_attention): per-sample valid length <= segment length, or
                              // nullptr. Keys past it are masked, rows past it get zeros and lse = -inf.
+  const int64_t* q_off;      // cross mode (fused feature_interaction): query segments [q_off[i], q_off[i+1]) over
+                             // the keys of sample i (`off`), or nullptr (self-attention). Samples without keys
+                             // produce zero rows. total_rows then counts query rows; lse may be nullptr.
 };
 
 struct Item {
-  int64_t b0, n;
+  int64_t b0, n;      // key segment
   int h, nkv, q_row;  // q_row: first row of tile A
-  int nv;             // valid rows/keys (== n except in padded mode)
+  int nv;             // valid keys (== n except in padded mode)
+  int store_end;      // query rows [q_row, store_end) are written ...
+  int valid_end;      // ... and those below valid_end hold attention (the others zero, lse = -inf)
   bool has_b;
 };
 
@@ -98,8 +103,18 @@ __device__ __forceinline__ Item load_item(const Params& p, int64_t w) {
   r.n = p.off[it.x + 1] - r.b0;
   r.nkv = (int)((r.n + BN - 1) / BN);
   r.nv = (int)(p.valid ? (p.valid[it.x] < r.n ? p.valid[it.x] : r.n) : r.n);
-  r.q_row = (int)(r.b0 + (int64_t)it.y * 2 * BM);
-  r.has_b = (int64_t)it.y * 2 * BM + BM < r.n;
+  if (p.q_off) {
+    const int64_t qb0 = p.q_off[it.x], nq = p.q_off[it.x + 1] - qb0;
+    r.q_row = (int)(qb0 + (int64_t)it.y * 2 * BM);
+    r.has_b = (int64_t)it.y * 2 * BM + BM < nq;
+    r.store_end = (int)(qb0 + nq);
+    r.valid_end = r.n > 0 ? r.store_end : 0;
+  } else {
+    r.q_row = (int)(r.b0 + (int64_t)it.y * 2 * BM);
+    r.has_b = (int64_t)it.y * 2 * BM + BM < r.n;
+    r.store_end = (int)(r.b0 + r.n);
+    r.valid_end = (int)(r.b0 + r.nv);
+  }
   return r;
 }
 
@@ -162,7 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto take_item = [&](uint32_t ic, Item& it) -> bool {
     const uint32_t s = ic % kItemSlots;
     tc::mbar_wait(item_full + s, (ic / kItemSlots) & 1);
-    const uint4 a = tc::ld_shared_v4u(item_ring + s * 32), b = tc::ld_shared_v4u(item_ring + s * 32 + 16);
+    const uint4 a = tc::ld_shared_v4u(item_ring + s * 48), b = tc::ld_shared_v4u(item_ring + s * 48 + 16),
+                c = tc::ld_shared_v4u(item_ring + s * 48 + 32);
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(item_empty + s);
     it.b0 = (int64_t)(((uint64_t)a.y << 32) | a.x);
@@ -172,6 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     it.nkv = (int)b.y;
     it.has_b = (b.z & 1) != 0;
     it.nv = (int)b.w;
+    it.store_end = (int)c.x;
+    it.valid_end = (int)c.y;
     return (b.z >> 1) == 0;
   };
 
@@ -181,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::WaitProf wp;
       wp.init(p.prof, 0);
       const long long t_role = clock64();
-      uint32_t kv_cnt = 0, item_cnt = 0;
+      uint32_t kv_cnt = 0, item_cnt = 0, q_cnt = 0;  // q_cnt: items with keys (cross mode may have none)
       int64_t w_next = blockIdx.x;  // first round static, then the global counter (LPT order)
       for (;; ++item_cnt) {
         const int64_t w = w_next < n_work ? w_next : n_work;
@@ -189,14 +207,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (w < n_work) it = load_item(p, w);
         const uint32_t slot = item_cnt % kItemSlots;
         wp.wait(item_empty + slot, ((item_cnt / kItemSlots) & 1) ^ 1, 2);
-        tc::st_shared_v4(item_ring + slot * 32, (uint32_t)it.b0, (uint32_t)((uint64_t)it.b0 >> 32), (uint32_t)it.n,
+        tc::st_shared_v4(item_ring + slot * 48, (uint32_t)it.b0, (uint32_t)((uint64_t)it.b0 >> 32), (uint32_t)it.n,
                          (uint32_t)it.q_row);
-        tc::st_shared_v4(item_ring + slot * 32 + 16, (uint32_t)it.h, (uint32_t)it.nkv,
+        tc::st_shared_v4(item_ring + slot * 48 + 16, (uint32_t)it.h, (uint32_t)it.nkv,
                          (it.has_b ? 1u : 0u) | (w >= n_work ? 2u : 0u), (uint32_t)it.nv);
+        tc::st_shared_v4(item_ring + slot * 48 + 32, (uint32_t)it.store_end, (uint32_t)it.valid_end, 0u, 0u);
         tc::mbar_arrive(item_full + slot);
         if (w >= n_work) break;
         w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
-        wp.wait(q_empty, (item_cnt & 1) ^ 1, 0);
+        if (it.nkv == 0) continue;  // cross mode, sample without keys: the softmax warps write zeros
+        wp.wait(q_empty, (q_cnt++ & 1) ^ 1, 0);
         tc::mbar_expect_tx(q_full, (it.has_b ? 2 : 1) * L::kTile);
         for (int t = 0; t < (it.has_b ? 2 : 1); ++t)
           for (int c = 0; c < L::kChunks; ++c)
@@ -228,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::WaitProf wp;
       wp.init(lane == 0 ? p.prof : nullptr, 8);
       const long long t_role = clock64();
-      uint32_t kv_cnt = 0, item_cnt = 0, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
+      uint32_t kv_cnt = 0, item_cnt = 0, q_cnt = 0, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
       auto next_stage = [&]() {
         const uint32_t s = kv_cnt % L::kStages;
         wp.wait_warp(kv_full + s, (kv_cnt / L::kStages) & 1, 2);
@@ -267,7 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long t_li = clock64();
         const int nt = it.has_b ? 2 : 1;
         wp.add(1, clock64() - t_li);
-        wp.wait_warp(q_full, item_cnt & 1, 0);
+        if (it.nkv == 0) continue;
+        wp.wait_warp(q_full, q_cnt++ & 1, 0);
         uint32_t ks = next_stage();  // K_0
         for (int t = 0; t < nt; ++t) issue_s(t, ks);
         tc::mma_commit_warp(kv_empty + ks);
@@ -314,6 +335,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     Item it;
     for (bool more = take_item(ic, it); more; more = take_item(++ic, it)) {
       if (t == 1 && !it.has_b) continue;
+      if (it.nkv == 0) {  // cross mode, sample without keys: zero rows (no TMEM or barrier traffic)
+        const int arow = it.q_row + t * BM + row;
+        if (arow < it.store_end) {
+          uint4* orow = reinterpret_cast<uint4*>(p.out + ((int64_t)arow * p.H + it.h) * D);
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) orow[c] = make_uint4(0u, 0u, 0u, 0u);
+          if (p.lse) p.lse[(int64_t)it.h * p.total_rows + arow] = -INFINITY;
+        }
+        continue;
+      }
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < it.nkv; ++j) {
         wp.wait(s_full + t, s_cnt & 1, 0);
@@ -432,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       wp.wait(o_done + t, done_cnt & 1, 2);
       ++done_cnt;
       tc::tc_fence_after();
-      const int64_t q_local = (int64_t)(it.q_row - it.b0) + t * BM + row;
-      const bool store = q_local < it.n;
-      const bool row_ok = q_local < it.nv;  // padded mode: rows past the valid length are zero, lse = -inf
+      const int64_t arow = (int64_t)it.q_row + t * BM + row;  // absolute query row
+      const bool store = arow < it.store_end;
+      const bool row_ok = arow < it.valid_end;  // padded mode: rows past the valid length are zero, lse = -inf
       const float inv_l = row_ok ? 1.f / l : 0.f;  // with o zeroed below: exact zeros even when l is NaN
-      __nv_bfloat16* orow = p.out + ((it.b0 + q_local) * p.H + it.h) * D;
+      __nv_bfloat16* orow = p.out + (arow * p.H + it.h) * D;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
@@ -462,8 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(o_empty + t);
-      if (store)
-        p.lse[(int64_t)it.h * p.total_rows + it.b0 + q_local] = row_ok ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      if (store && p.lse)
+        p.lse[(int64_t)it.h * p.total_rows + arow] = row_ok ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
     }
     wp.add(7, clock64() - t_role);
     wp.flush();
@@ -487,10 +518,11 @@ bool attn_sm100_supported(int head_dim, jg_dtype dt) {
 template <int D>
 static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_rows, int H, const void* q, const void* k,
                             const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
-                            int64_t max_items, const int64_t* valid, cudaStream_t st) {
+                            int64_t max_items, const int64_t* valid, const int64_t* q_off, int64_t q_rows,
+                            cudaStream_t st) {
   using L = fa::Smem<D>;
   CUtensorMap mq, mk, mv;
-  if (jg_status rc = make_map(&mq, q, total_rows, H, D, 128)) return rc;
+  if (jg_status rc = make_map(&mq, q, q_off ? q_rows : total_rows, H, D, 128)) return rc;
   if (jg_status rc = make_map(&mk, k, total_rows, H, D, 128)) return rc;
   if (jg_status rc = make_map(&mv, v, total_rows, H, D, 128)) return rc;
   static bool attr_set = false;
@@ -506,9 +538,9 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
   unsigned long long* counter = nullptr;  // stream-ordered 8-byte work counter for this launch
   JG_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), st));
   JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
-  fa::Params p{off, items, n_items, batch, total_rows, H, (__nv_bfloat16*)out, lse,
+  fa::Params p{off, items, n_items, batch, q_off ? q_rows : total_rows, H, (__nv_bfloat16*)out, lse,
                1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st), counter,
-               std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0, valid};
+               std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0, valid, q_off};
   const int64_t work = max_items * H;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sm_count(), work));
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
@@ -525,9 +557,12 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
 // items: (sample, 256-row tile pair) LPT work list (schedule tile 256)
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                                 const void* k, const void* v, void* out, float* lse, const int2* items,
-                                const int64_t* n_items, int64_t max_items, const int64_t* valid, cudaStream_t st) {
-  if (D == 128) return fwd_launch<128>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
-  if (D == 64) return fwd_launch<64>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
+                                const int64_t* n_items, int64_t max_items, const int64_t* valid, cudaStream_t st,
+                                const int64_t* q_off, int64_t q_rows) {
+  if (D == 128)
+    return fwd_launch<128>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, q_off, q_rows, st);
+  if (D == 64)
+    return fwd_launch<64>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, q_off, q_rows, st);
   return fail(JG_UNSUPPORTED, "tcgen05 attention: head_dim must be 64 or 128");
 }
 

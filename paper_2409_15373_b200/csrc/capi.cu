@@ -753,6 +753,22 @@ extern "C" jg_status jg_feature_interaction(const int64_t* off, int64_t batch, i
   REQUIRE(D >= 1 && Tq >= 1, JG_INVALID_ARGUMENT, "feature_interaction: targets must be [B, Tq, D]");
   cudaStream_t st = as_stream(stream);
   if (batch == 0) return JG_OK;
+  if (dtype == JG_BF16 && !force_simt() && attn_sm100_supported((int)D, dtype)) {
+    // fused: feature_interaction is attention with the Tq targets of sample i as queries over
+    // its k_feat rows (softmax over the segment axis per target) and v_feat as values — the forward JFA
+    // kernel in cross mode, one launch; samples without rows give zero outputs
+    Scratch qo(st);
+    if (jg_status rc = qo.alloc(sizeof(int64_t) * (batch + 1))) return rc;
+    if (jg_status rc = launch_uniform_offsets((int64_t*)qo.p, batch, Tq, st)) return rc;
+    jg_schedule qs = nullptr;  // (sample, 256-target pair) items over the query segments
+    if (jg_status rc = jg_schedule_create((const int64_t*)qo.p, batch, batch * Tq, st, &qs)) return rc;
+    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, 1, (int)D, targets, k_feat, v_feat, out, nullptr,
+                                         qs->items2, qs->n_items2, qs->max_items2, nullptr, st, (const int64_t*)qo.p,
+                                         batch * Tq);
+    cudaStreamSynchronize(st);
+    jg_schedule_destroy(qs);
+    return rc;
+  }
   const int64_t n = total_rows * Tq;
   Scratch ws(st);
   if (!workspace) {

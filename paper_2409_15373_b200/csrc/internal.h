@@ -73,6 +73,7 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
 
 // SURVEY §8f next rows (mlp_fi.cu)
 jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st);
+jg_status launch_uniform_offsets(int64_t* o, int64_t batch, int64_t step, cudaStream_t st);  // o[i] = i * step
 jg_status launch_bias_act(const float* acc, const void* bias, int64_t rows, int64_t d, int relu, void* out,
                           void* preact, jg_dtype dt, cudaStream_t st);
 jg_status launch_relu_mask(const void* g, const void* preact, int64_t n, int relu, void* out, jg_dtype dt,
@@ -102,7 +103,9 @@ bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt);
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, void* out, float* lse,
                                 const int2* items, const int64_t* n_items, int64_t max_items,
-                                const int64_t* valid, cudaStream_t st);
+                                const int64_t* valid, cudaStream_t st,
+                                // cross mode (fused feature_interaction): query segments over the key segments
+                                const int64_t* q_off = nullptr, int64_t q_rows = 0);
 jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, const void* go,
                                 const void* o, const float* lse, void* dq, void* dk, void* dv,

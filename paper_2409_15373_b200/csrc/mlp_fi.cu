@@ -84,6 +84,17 @@ static int grid_of(int64_t n) {
     else return fail(JG_UNSUPPORTED, "dtype not supported on device (no CPU fallback)"); \
   } while (0)
 
+__global__ void uniform_offsets_kernel(int64_t* o, int64_t batch, int64_t step) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= batch; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = i * step;
+}
+
+jg_status launch_uniform_offsets(int64_t* o, int64_t batch, int64_t step, cudaStream_t st) {
+  uniform_offsets_kernel<<<(unsigned)std::min<int64_t>((batch + 256) / 256, 1024), 256, 0, st>>>(o, batch, step);
+  JG_LAUNCHED("uniform_offsets_kernel");
+  return JG_OK;
+}
+
 jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st) {
   two_offsets_kernel<<<1, 1, 0, st>>>(o, rows);
   JG_LAUNCHED("two_offsets_kernel");

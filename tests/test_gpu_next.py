@@ -38,7 +38,8 @@ def test_feature_interaction_golden(golden):
 
 
 @pytest.mark.parametrize("lens,D,Tq", [([3, 0, 9, 1, 130, 64], 32, 5), ([257, 0, 70, 1, 128], 64, 64),
-                                       (list(R.gen_lengths("uniform", 128, 0, 64)), 64, 32)])
+                                       (list(R.gen_lengths("uniform", 128, 0, 64)), 64, 32),
+                                       ([5, 0, 300, 129, 0], 128, 300)])  # bf16 D=64/128: fused kernel
 @pytest.mark.parametrize("mode", ["fp32", "bf16"])
 def test_feature_interaction_random(lens, D, Tq, mode):
     off = R.make_offsets(lens)
