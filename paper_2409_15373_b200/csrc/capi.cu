@@ -221,6 +221,14 @@ extern "C" jg_status jg_schedule_destroy(jg_schedule s) {
   return JG_OK;
 }
 
+// A per-call schedule is released stream-ordered (no host synchronisation): its device block is freed after
+// the work queued on `st` that reads it.
+static void schedule_release(jg_schedule s, cudaStream_t st) {
+  if (!s) return;
+  cudaFreeAsync(s->block, st);
+  delete s;
+}
+
 extern "C" const int64_t* jg_schedule_sq_offsets(jg_schedule s) { return s ? s->sq : nullptr; }
 
 extern "C" jg_status jg_schedule_work_list(jg_schedule s, int32_t* host_items, int64_t capacity, int64_t* count) {
@@ -442,8 +450,7 @@ static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_r
     jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
                                          sched->n_items2, sched->max_items2, valid, st);
     if (own) {
-      cudaStreamSynchronize(st);
-      jg_schedule_destroy(own);
+      schedule_release(own, st);
     }
     return rc;
   }
@@ -471,8 +478,7 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
     jg_status rc = launch_attn_bwd_sm100(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta,
                                          dq_acc, sched->items, sched->n_items, sched->max_items, valid, st);
     if (own) {
-      cudaStreamSynchronize(st);
-      jg_schedule_destroy(own);
+      schedule_release(own, st);
     }
     return rc;
   }
@@ -765,8 +771,7 @@ extern "C" jg_status jg_feature_interaction(const int64_t* off, int64_t batch, i
     jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, 1, (int)D, targets, k_feat, v_feat, out, nullptr,
                                          qs->items2, qs->n_items2, qs->max_items2, nullptr, st, (const int64_t*)qo.p,
                                          batch * Tq);
-    cudaStreamSynchronize(st);
-    jg_schedule_destroy(qs);
+    schedule_release(qs, st);
     return rc;
   }
   const int64_t n = total_rows * Tq;
