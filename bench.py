@@ -239,6 +239,7 @@ def run_ours(args, rank, world, local_rank):
     elapsed_ms = t0.elapsed_time(t1)
     fwd_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     bwd_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]  # per-step spread (median with p10/p90)
 
     # e2e through the host-buffer C-ABI entry point (pinned host memory, H2D + compute + D2H)
     hq, hk, hv, hg = (t.cpu().pin_memory() for t in (q, k, v, go))
@@ -309,6 +310,7 @@ def run_ours(args, rank, world, local_rank):
                      "peak": pk_burst, "unit": "TFLOP/s", "frac": achieved / pk_burst, "traffic": traffic,
                      "peak_source": f"{src} burst bf16 (MEASURED_PEAKS.json); sustained {pk_sust}",
                      "flop_per_launch": dominant[1], "ms_per_launch": dominant[2]},
+        "step_ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
         "kernels": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
                     "fwd_tflops": fwd_fl / (fwd_ms * 1e-3) / 1e12, "bwd_tflops": bwd_fl / (bwd_ms * 1e-3) / 1e12},
         "cpu_baseline": cpu,
