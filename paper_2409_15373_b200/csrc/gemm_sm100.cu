@@ -28,7 +28,10 @@ namespace gm {
 
 enum Op { JJJ = 0, AJ = 1, JJ = 2, JD = 3 };
 
-constexpr int BM = 128, BN = 128, BK = 64, kStages = 4, kThreads = 384;
+#ifndef JG_GEMM_STAGES
+#define JG_GEMM_STAGES 4
+#endif
+constexpr int BM = 128, BN = 128, BK = 64, kStages = JG_GEMM_STAGES, kThreads = 384;
 constexpr int kTileBytes = 16384;  // one operand stage: 128 x 64 bf16
 struct Smem {
   static constexpr int kA = 0;
