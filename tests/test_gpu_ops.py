@@ -253,3 +253,45 @@ def test_empty_samples_zero_dense_outputs():
     del Z
     _, dw = J.jagged_dense_bmm_vjp(X, torch.ones(3, 4, 2, device=DEV), jt(off, np.ones((3, 2), np.float32)))
     assert bool((dw[0] == 0).all()) and bool((dw[2] == 0).all())
+
+
+def test_full_size_cfg4_properties():
+    """BASELINE cfg4 at full size (half-mean B=2048, L=1024 seed 0: sum_B = 1,048,576, SQ = 7.2461e8; D=T=256 bf16):
+    size-independent identities that tie the Table-1 ops together, plus whole-sample fp32 spot checks.
+      * per-sample associativity: (Q_i K_i^T) V_i == Q_i (K_i^T V_i), i.e.
+        array_jagged_bmm_jagged_out(jagged_jagged_bmm_jagged_out(Q, K), V) == jagged_dense_bmm(Q, jagged_jagged_bmm(K, V))
+      * softmax normalisation: jagged_softmax columns and jagged2_softmax rows sum to 1.
+    bf16 inputs; tolerances relative to the magnitudes involved (bf16 rounding of the intermediates)."""
+    ln = R.gen_lengths("half-mean", 1024, 0, 2048)
+    off = R.make_offsets(ln)
+    S, D = int(off[-1]), 256
+    assert S == 1_048_576
+    g = torch.Generator(device=DEV).manual_seed(5)
+    r = lambda *sh: ((torch.rand(*sh, device=DEV, generator=g) * 2 - 1) * 0.25).bfloat16()  # noqa: E731
+    offd = torch.from_numpy(off).to(DEV)
+    Q, K, V = (J.JaggedTensor(offd, r(S, D), off) for _ in range(3))
+    lhs = J.array_jagged_bmm_jagged_out(J.jagged_jagged_bmm_jagged_out(Q, K), V).values.float()
+    rhs = J.jagged_dense_bmm(Q, J.jagged_jagged_bmm(K, V)).values.float()
+    scale = float(rhs.abs().max())
+    err = float((lhs - rhs).abs().max())
+    assert err <= 2e-2 * scale, f"associativity: max |(QK^T)V - Q(K^T V)| = {err:.3e} vs max |.| = {scale:.3e}"
+    # whole-sample fp32 spot checks (largest and a few others)
+    nz = np.nonzero(ln)[0]
+    for i in {int(nz[np.argmax(ln[nz])]), int(nz[0]), int(nz[len(nz) // 2])}:
+        a, b = int(off[i]), int(off[i + 1])
+        q, k, v = (t.values[a:b].float() for t in (Q, K, V))
+        ref = (q @ k.T).bfloat16().float() @ v  # the jagged^2 intermediate is bf16, as in the device path
+        assert_bf16_close(lhs[a:b], ref.cpu().numpy(), what=f"ajbmm(jjbmm_jout) sample {i} (n={b - a})")
+    # softmax normalisation
+    X = J.JaggedTensor(offd, r(S, D) * 8, off)
+    P = J.jagged_softmax(X).values.float()
+    seg = torch.repeat_interleave(torch.arange(len(ln), device=DEV), torch.from_numpy(ln).to(DEV))
+    colsum = torch.zeros(len(ln), D, device=DEV).index_add_(0, seg, P)
+    ne = torch.from_numpy(ln > 0).to(DEV)
+    assert float((colsum[ne] - 1).abs().max()) < 2e-2 and bool((P >= 0).all())
+    A = J.jagged_jagged_bmm_jagged_out(Q, K)
+    P2 = J.jagged2_softmax(A)
+    rows = torch.repeat_interleave(torch.from_numpy(ln).to(DEV), torch.from_numpy(ln).to(DEV))  # Bi per row
+    row_id = torch.repeat_interleave(torch.arange(S, device=DEV), rows)
+    rowsum = torch.zeros(S, device=DEV).index_add_(0, row_id, P2.values.float())
+    assert float((rowsum - 1).abs().max()) < 2e-2
