@@ -60,7 +60,9 @@ struct Smem {
   static constexpr int kStgRows = 16;                       // dQ rows per TMA reduce (four per block)
   static constexpr int kStgBufs = kQdStages > 3 ? 2 : 4;    // fill one while the TMA reads the others
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 -lse*log2(e) + 64 -Delta, fp32
-  static constexpr int kLse = kStg + kStgBufs * kStgRows * D * 4;  // kStages x kLsdBytes, loaded with (Q_j, dO_j)
+  // the dK/dV epilogue reuses the staging region as four 4 KB warp slices (32 rows x 128 B)
+  static constexpr int kStgBytes = kStgBufs * kStgRows * D * 4 > 4 * 4096 ? kStgBufs * kStgRows * D * 4 : 4 * 4096;
+  static constexpr int kLse = kStg + kStgBytes;  // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
   static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2 + 2 * kItemSlots;
   static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 32-byte descriptors
@@ -295,7 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       constexpr uint32_t kIdS = tc::idesc_bf16_f32(BKV, BQ, false, false);  // S^T, dP^T
       constexpr uint32_t kIdKV = tc::idesc_bf16_f32(BKV, D, false, true);   // dV, dK
-      constexpr uint32_t kIdQ = tc::idesc_bf16_f32(D, BQ, true, true);      // dQ^T
+      // dQ^T: M = head_dim rows, run at M = 128 (for D = 64 the upper 64 rows read the next smem chunk and are
+      // never drained)
+      constexpr uint32_t kIdQ = tc::idesc_bf16_f32(128, BQ, true, true);
       const uint32_t k_base = tc::smem_u32(smem + L::kK), v_base = tc::smem_u32(smem + L::kV);
       const uint32_t ds_base = tc::smem_u32(smem + L::kDS);
       const uint32_t qd_base = tc::smem_u32(smem + L::kQD);
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int q = 0; q < L::kStgRows; ++q) {
             const int qq = hh * L::kStgRows + q;
-            tc::st_shared_f32(sb + (q * D + tid) * 4, __uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]) * p.scale);
+            if (tid < D) tc::st_shared_f32(sb + (q * D + tid) * 4, __uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]) * p.scale);
           }
           tc::fence_proxy_async_smem();
           named_bar(2, 128);
@@ -657,16 +661,13 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict
 
 }  // namespace fb
 
-bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt) { return dt == JG_BF16 && head_dim == 128; }
+bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt) { return dt == JG_BF16 && (head_dim == 128 || head_dim == 64); }
 
-jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
-                                const void* k, const void* v, const void* go, const void* o, const float* lse,
-                                void* dq, void* dk, void* dv, float* delta, float* dq_acc, const int2* items,
-                                const int64_t* n_items, int64_t max_items, const int64_t* valid,
-                                cudaStream_t st) {
-  (void)batch;
-  if (D != 128) return fail(JG_UNSUPPORTED, "tcgen05 attention backward: head_dim must be 128");
-  constexpr int kD = 128;
+template <int kD>
+static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
+                            const void* go, const void* o, const float* lse, void* dq, void* dk, void* dv,
+                            float* delta, float* dq_acc, const int2* items, const int64_t* n_items, int64_t max_items,
+                            const int64_t* valid, cudaStream_t st) {
   using L = fb::Smem<kD>;
   const int sms = device_sm_count();
   const int64_t units = total_rows * H;
@@ -707,6 +708,21 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
                                                                                           n4);
   JG_LAUNCHED("dq_convert_kernel");
   return JG_OK;
+}
+
+jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
+                                const void* k, const void* v, const void* go, const void* o, const float* lse,
+                                void* dq, void* dk, void* dv, float* delta, float* dq_acc, const int2* items,
+                                const int64_t* n_items, int64_t max_items, const int64_t* valid,
+                                cudaStream_t st) {
+  (void)batch;
+  if (D == 128)
+    return bwd_launch<128>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items, max_items,
+                           valid, st);
+  if (D == 64)
+    return bwd_launch<64>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items, max_items,
+                          valid, st);
+  return fail(JG_UNSUPPORTED, "tcgen05 attention backward: head_dim must be 64 or 128");
 }
 
 }  // namespace jg
