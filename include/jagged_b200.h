@@ -14,7 +14,10 @@
  *     at sq_offsets[i] = sum_{j<i} Bj^2 (tensor.hpp:42-62); jg_sq_offsets computes it on device;
  *   - errors return a jg_status; the reference's exception text is available from jg_last_error()
  *     (thread-local), e.g. "jagged_dense_bmm: dim mismatch (64 vs 32)" (linalg.cpp:42-44);
- *   - every call is stream-ordered on the caller's cudaStream_t (passed as void*); no host sync;
+ *   - every call is stream-ordered on the caller's cudaStream_t (passed as void*) without host
+ *     synchronisation, except: jg_dense_flash_attention_* (uploads the host `lengths`),
+ *     jg_array_jagged_bmm_jagged_out on the tcgen05 path (reads its repack tile count), and
+ *     jg_schedule_work_list (a host-side inspection helper);
  *   - KernelOptions{block, threads, meter} (linalg.hpp:16-20) have no device meaning and are not
  *     taken; block_q/block_k of the flash forward are validated (>= 1) exactly as the reference does
  *     and otherwise ignored (device tiles are fixed at 128x128).
@@ -23,6 +26,8 @@
  * fp32 accumulation). JG_F64 returns JG_UNSUPPORTED: there is no CPU fallback.
  * Attention tensors carry heads: [total_rows, num_heads, head_dim] row-major (token-major, the
  * reference's single-head layout when num_heads == 1); lse is float32 [num_heads, total_rows].
+ * Attention runs on tcgen05 for bf16 with head_dim 64 or 128 (forward and backward); fp32 and other
+ * head dims run SIMT kernels with the same semantics.
  */
 #ifndef JAGGED_B200_H
 #define JAGGED_B200_H
