@@ -616,34 +616,46 @@ __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* 
                                                            int H, int64_t total_rows, const float* __restrict__ lse,
                                                            float* __restrict__ lsd,
                                                            float* __restrict__ dq_acc) {
-  const int lane = threadIdx.x & 31;
-  constexpr int PER = D / 32;  // bf16 per lane
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < units;
-       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t base = u * D + lane * PER;
-    float acc = 0.f;
-    if constexpr (PER == 4) {
-      const uint2 a = *reinterpret_cast<const uint2*>(go + base), b = *reinterpret_cast<const uint2*>(o + base);
-      const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+  // LPU lanes per (row, head) unit, 16 bytes of dO and of O per lane; a warp covers UPW units per step and
+  // unrolls two steps with every load issued before the reductions (the streaming read is latency-bound
+  // with one dependent unit per warp)
+  constexpr int LPU = D / 8, UPW = 32 / LPU, kUnroll = 2;
+  const int lane = threadIdx.x & 31, sub = lane / LPU, li = lane % LPU;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (UPW * kUnroll); u0 < units;
+       u0 += warps * UPW * kUnroll) {
+    uint4 a[kUnroll], b[kUnroll];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
+    for (int k = 0; k < kUnroll; ++k) {
+      const int64_t u = u0 + k * UPW + sub;
+      a[k] = b[k] = make_uint4(0u, 0u, 0u, 0u);
+      if (u < units) {
+        a[k] = __ldcs(reinterpret_cast<const uint4*>(go + u * D) + li);  // streamed once: evict-first
+        b[k] = __ldcs(reinterpret_cast<const uint4*>(o + u * D) + li);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int64_t u = u0 + k * UPW + sub;
+      const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a[k]);
+      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b[k]);
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
         const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
         acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
       }
-      *reinterpret_cast<float4*>(dq_acc + base) = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
 #pragma unroll
-      for (int e = 0; e < PER; ++e) {
-        acc = fmaf(__bfloat162float(go[base + e]), __bfloat162float(o[base + e]), acc);
-        dq_acc[base + e] = 0.f;
+      for (int m = LPU / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+      if (u < units) {
+        // 8 fp32 zeros per lane: one 32-byte sector store
+        tc::st_global_v8(dq_acc + u * D + li * 8, make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u));
+        if (li == 0) {
+          const int64_t r = u / H, h = u - r * H;
+          lsd[h * total_rows + r] = -lse[h * total_rows + r] * kLog2e;  // negated: one FFMA2 per pair downstream
+          lsd[(H + h) * total_rows + r] = -acc;
+        }
       }
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const int64_t r = u / H, h = u - r * H;
-      lsd[h * total_rows + r] = -lse[h * total_rows + r] * kLog2e;  // negated: one FFMA2 per pair downstream
-      lsd[(H + h) * total_rows + r] = -acc;
     }
   }
 }
@@ -671,7 +683,7 @@ static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const
   using L = fb::Smem<kD>;
   const int sms = device_sm_count();
   const int64_t units = total_rows * H;
-  fb::bwd_prologue_kernel<kD><<<(int)std::min<int64_t>((units + 7) / 8, 32 * sms), 256, 0, st>>>(
+  fb::bwd_prologue_kernel<kD><<<(int)std::min<int64_t>((units + 8 * (256 / kD) * 2 - 1) / (8 * (256 / kD) * 2), 32 * sms), 256, 0, st>>>(
       (const __nv_bfloat16*)go, (const __nv_bfloat16*)o, units, H, total_rows, lse, delta, dq_acc);
   JG_LAUNCHED("bwd_prologue_kernel");
   CUtensorMap mq, mk, mv, mdo;
