@@ -610,6 +610,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Delta = rowsum(dO * O) per (row, head), zero the fp32 dQ accumulator (one warp per unit), and write
 // -lse*log2(e) and -Delta into lsd[2][H][total_rows] (staged per query block by the main kernel's producer
 // with cp.async; negated so the softmax needs one paired FFMA2 / FADD2 per two scores).
+#ifndef JG_PRO_LD
+#define JG_PRO_LD __ldcs
+#endif
 template <int D>
 __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* __restrict__ go,
                                                            const __nv_bfloat16* __restrict__ o, int64_t units,
@@ -630,8 +633,8 @@ __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* 
       const int64_t u = u0 + k * UPW + sub;
       a[k] = b[k] = make_uint4(0u, 0u, 0u, 0u);
       if (u < units) {
-        a[k] = __ldcs(reinterpret_cast<const uint4*>(go + u * D) + li);  // streamed once: evict-first
-        b[k] = __ldcs(reinterpret_cast<const uint4*>(o + u * D) + li);
+        a[k] = JG_PRO_LD(reinterpret_cast<const uint4*>(go + u * D) + li);  // streamed once
+        b[k] = JG_PRO_LD(reinterpret_cast<const uint4*>(o + u * D) + li);
       }
     }
 #pragma unroll
