@@ -70,13 +70,18 @@ struct VecIO {
   }
 };
 
+__device__ __forceinline__ float ex2a(float x) {  // MUFU.EX2 (ex2.approx.ftz; ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void online_update(float& m, float& s, float y) {
   // y already in log2 units
   if (y > m) {
-    s = s * exp2f(m - y) + 1.0f;
+    s = s * ex2a(m - y) + 1.0f;
     m = y;
   } else {
-    s += exp2f(y - m);
+    s += ex2a(y - m);
   }
 }
 
@@ -123,7 +128,23 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
 #pragma unroll
   for (int j = 0; j < VEC; ++j) { m[j] = -INFINITY; s[j] = 0.f; }
   if (active) {
-    for (int64_t r = b0 + w; r < b1; r += kSmWarps) {
+    // four rows per step: their loads in flight together, one branch-free running-max update per column
+    // (s = s * 2^(m - m') + sum_k 2^(y_k - m'), MUFU ex2) instead of a branchy update per element
+    int64_t r = b0 + w;
+    for (; r + 3 * kSmWarps < b1; r += 4 * kSmWarps) {
+      float v[4][VEC];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) VecIO<T, VEC>::load(x + (r + u * kSmWarps) * D + col, v[u]);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const float y0 = __fmul_rn(v[0][j], kLog2e), y1 = __fmul_rn(v[1][j], kLog2e);
+        const float y2 = __fmul_rn(v[2][j], kLog2e), y3 = __fmul_rn(v[3][j], kLog2e);
+        const float mn = fmaxf(m[j], fmaxf(fmaxf(y0, y1), fmaxf(y2, y3)));
+        s[j] = s[j] * ex2a(m[j] - mn) + ((ex2a(y0 - mn) + ex2a(y1 - mn)) + (ex2a(y2 - mn) + ex2a(y3 - mn)));
+        m[j] = mn;
+      }
+    }
+    for (; r < b1; r += kSmWarps) {
       float v[VEC];
       VecIO<T, VEC>::load(x + r * D + col, v);
 #pragma unroll
@@ -140,7 +161,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
       float v[VEC];
       VecIO<T, VEC>::load(x + r * D + col, v);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] = exp2f(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j];
+      for (int j = 0; j < VEC; ++j) v[j] = ex2a(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j];
       VecIO<T, VEC>::store(out + r * D + col, v);
     }
   } else {
@@ -154,7 +175,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
         VecIO<T, VEC>::load(x + r * D + col, v);
         VecIO<T, VEC>::load(g + r * D + col, gv);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) dot[j] += gv[j] * (exp2f(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j]);
+        for (int j = 0; j < VEC; ++j) dot[j] += gv[j] * (ex2a(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j]);
       }
     }
     __syncthreads();
@@ -173,7 +194,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
       VecIO<T, VEC>::load(x + r * D + col, v);
       VecIO<T, VEC>::load(g + r * D + col, gv);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] = exp2f(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j] * (gv[j] - dot[j]);
+      for (int j = 0; j < VEC; ++j) v[j] = ex2a(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j] * (gv[j] - dot[j]);
       VecIO<T, VEC>::store(out + r * D + col, v);
     }
   }
@@ -195,19 +216,27 @@ __global__ void __launch_bounds__(256) jagged2_softmax_kernel(const int64_t* __r
     const int64_t n = off[i + 1] - off[i], r = R - off[i];
     const int64_t base = sq[i] + r * n;
     float m = -INFINITY, sm = 0.f;
-    for (int64_t c = lane; c < n; c += 32) online_update(m, sm, __fmul_rn(ld(s + base + c), kLog2e));
+    int64_t c = lane;
+    for (; c + 96 < n; c += 128) {  // four elements per step: loads in flight together, one branch-free update
+      const float y0 = __fmul_rn(ld(s + base + c), kLog2e), y1 = __fmul_rn(ld(s + base + c + 32), kLog2e);
+      const float y2 = __fmul_rn(ld(s + base + c + 64), kLog2e), y3 = __fmul_rn(ld(s + base + c + 96), kLog2e);
+      const float mn = fmaxf(m, fmaxf(fmaxf(y0, y1), fmaxf(y2, y3)));
+      sm = sm * ex2a(m - mn) + ((ex2a(y0 - mn) + ex2a(y1 - mn)) + (ex2a(y2 - mn) + ex2a(y3 - mn)));
+      m = mn;
+    }
+    for (; c < n; c += 32) online_update(m, sm, __fmul_rn(ld(s + base + c), kLog2e));
     const float M = warp_max(m);
     const float S = warp_sum(m == -INFINITY ? 0.f : sm * exp2f(m - M));
     const float inv = 1.0f / S;
     if constexpr (MODE == 0) {
-      for (int64_t c = lane; c < n; c += 32) st(out + base + c, exp2f(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv);
+      for (int64_t c = lane; c < n; c += 32) st(out + base + c, ex2a(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv);
     } else {
       float dot = 0.f;
       for (int64_t c = lane; c < n; c += 32)
-        dot += ld(g + base + c) * (exp2f(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv);
+        dot += ld(g + base + c) * (ex2a(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv);
       dot = warp_sum(dot);
       for (int64_t c = lane; c < n; c += 32) {
-        const float p = exp2f(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv;
+        const float p = ex2a(__fmul_rn(ld(s + base + c), kLog2e) - M) * inv;
         st(out + base + c, p * (ld(g + base + c) - dot));
       }
     }
