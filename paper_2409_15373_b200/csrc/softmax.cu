@@ -209,10 +209,26 @@ __global__ void __launch_bounds__(256) jagged2_softmax_kernel(const int64_t* __r
                                                               const T* __restrict__ g,
                                                               T* __restrict__ out) {
   const int lane = threadIdx.x & 31;
+  // row -> sample: a 257-point coarse copy of the offsets in smem narrows each row's search to ~batch/256
+  // samples, so only ~log2(batch/256) dependent global loads remain per row
+  __shared__ int64_t coarse_off[257];
+  for (int k = threadIdx.x; k <= 256; k += blockDim.x) coarse_off[k] = off[(int64_t)k * batch / 256];
+  __syncthreads();
   if (total_rows < 0) total_rows = off[batch];  // device-resident row count (no host sync)
   for (int64_t R = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; R < total_rows;
        R += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t i = sample_of_row(off, batch, R);
+    int klo = 0, khi = 256;  // largest k with coarse_off[k] <= R
+    while (klo < khi) {
+      const int mid = (klo + khi + 1) >> 1;
+      if (coarse_off[mid] <= R) klo = mid; else khi = mid - 1;
+    }
+    int64_t lo = (int64_t)klo * batch / 256, hi = klo < 256 ? (int64_t)(klo + 1) * batch / 256 : batch;
+    if (hi > batch - 1) hi = batch - 1;
+    while (lo < hi) {  // sample_of_row restricted to [lo, hi]
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid + 1] <= R) lo = mid + 1; else hi = mid;
+    }
+    const int64_t i = lo;
     const int64_t n = off[i + 1] - off[i], r = R - off[i];
     const int64_t base = sq[i] + r * n;
     float m = -INFINITY, sm = 0.f;
