@@ -314,53 +314,155 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       const int ab = tcount & 1;
       tc::mbar_wait(acc_full + ab, (tcount >> 1) & 1);
       tc::tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + hf * 64 + c * 32, v);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) stg[lane * 65 + c * 32 + e] = tl.nk == 0 ? 0.f : __uint_as_float(v[e]);
-      }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
       const int ncols = tl.N - tl.n0 < BN ? tl.N - tl.n0 : BN;
       const int nc = ncols - 64 * hf < 64 ? ncols - 64 * hf : 64;
       const int nrows = tl.M - tl.m0 - wq * 32 < 32 ? tl.M - tl.m0 - wq * 32 : 32;
       const int64_t row0 = tl.sqo + (int64_t)(tl.m0 + wq * 32) * tl.n + tl.n0 + 64 * hf;
+      const int n32 = (int)tl.n;
+      uint32_t* img = reinterpret_cast<uint32_t*>(stg);
+      // bf16 output: absolute 16-byte alignment of the warp's first output element (the base need only be
+      // element-aligned); row r starts sh_r = (a0 + r * Bi) & 7 elements into its 16-byte chunk
+      const int a0 = (int)((reinterpret_cast<uintptr_t>(reinterpret_cast<__nv_bfloat16*>(p.out) + row0) >> 1) & 7);
+      {
+        uint32_t v0[32], v1[32];  // both column chunks in flight before one wait
+        tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + hf * 64, v0);
+        tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + hf * 64 + 32, v1);
+        tc::tmem_wait_ld();
+        if (p.out_f32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            stg[lane * 65 + e] = tl.nk == 0 ? 0.f : __uint_as_float(v0[e]);
+            stg[lane * 65 + 32 + e] = tl.nk == 0 ? 0.f : __uint_as_float(v1[e]);
+          }
+        } else {
+          // The lane's row becomes a bf16 image already in its output's 16-byte phase: image element sh + j
+          // holds column j, rows 36 words apart (16-byte aligned quads). Odd phases shift by one element
+          // (funnel shift of the packed pairs); the image then leaves as aligned 16-byte chunks.
+          const int sh = (a0 + lane * n32) & 7;
+          const uint32_t fs = (sh & 1) ? 16u : 32u;  // 32: funnelshift_rc returns the high word (no shift)
+          uint32_t* row = img + lane * 36 + (sh >> 1);
+          uint32_t prev = 0;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const uint32_t* v = k < 16 ? v0 : v1;
+            const int e = (k & 15) * 2;
+            const uint32_t w = tl.nk == 0 ? 0u : tc::pack_bf16(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+            row[k] = __funnelshift_rc(prev, w, fs);
+            prev = w;
+          }
+          row[32] = __funnelshift_rc(prev, 0u, fs);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + ab);  // TMEM drained; the stores below overlap the next tile
+      auto store_img = [&]() {
+        // 8 lanes per row (one 16-byte chunk each), 4 rows per step; all image reads before any store. The
+        // partial chunks at the row ends (at most 7 elements each) are 2-byte stores.
+        __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.out) + row0;
+        const uint16_t* img16 = reinterpret_cast<const uint16_t*>(img);
+        const int sub = lane >> 3, li = lane & 7;
+        uint4 body[8];
+        uint16_t lead[8], trail[8];
+        int cpos[8], lpos[8], tpos[8];
+        uint32_t okm = 0, lm = 0, tm = 0;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = sub + it * 4;
+          const int s0 = rr * n32, sh = (a0 + s0) & 7, end = sh + nc;
+          const bool live = rr < nrows;
+          const int qf = sh ? 1 : 0, ql = end >> 3;  // full chunks: image quads [qf, ql)
+          const int q = qf + li;
+          const bool okc = live && q < ql;
+          const int le = end < 8 ? end : 8, ts = 8 * ql > 8 * qf ? 8 * ql : 8 * qf;
+          const bool okl = live && sh > 0 && sh + li < le, okt = live && ts + li < end;
+          body[it] = *reinterpret_cast<const uint4*>(img + rr * 36 + 4 * (okc ? q : 0));
+          lead[it] = img16[rr * 72 + (okl ? sh + li : 0)];
+          trail[it] = img16[rr * 72 + (okt ? ts + li : 0)];
+          cpos[it] = s0 - sh + 8 * q;
+          lpos[it] = s0 + li;
+          tpos[it] = s0 - sh + ts + li;
+          okm |= (uint32_t)okc << it;
+          lm |= (uint32_t)okl << it;
+          tm |= (uint32_t)okt << it;
+        }
+        uint16_t* base16 = reinterpret_cast<uint16_t*>(base);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          if (okm >> it & 1) *reinterpret_cast<uint4*>(base + cpos[it]) = body[it];
+          if (lm >> it & 1) base16[lpos[it]] = lead[it];
+          if (tm >> it & 1) base16[tpos[it]] = trail[it];
+        }
+      };
       auto store_rows = [&](auto tag) {
         using E = decltype(tag);
         constexpr int CE = 16 / sizeof(E);      // elements per 16-byte chunk
         constexpr int LPR = 64 / CE;            // lanes per row
-        E* out = reinterpret_cast<E*>(p.out);
-        // chunk alignment is absolute (the output base need only be element-aligned)
-        const int64_t bo = (int64_t)((reinterpret_cast<uintptr_t>(p.out) / sizeof(E)) & (CE - 1));
-        const int sub = lane / LPR, li = lane % LPR;
-#pragma unroll 2
-        for (int rr = sub; rr < nrows; rr += 32 / LPR) {
-          const int64_t s0 = row0 + (int64_t)rr * tl.n, e0 = s0 + nc;
-          const int64_t sa = ((s0 + bo + CE - 1) & ~(int64_t)(CE - 1)) - bo, ea = ((e0 + bo) & ~(int64_t)(CE - 1)) - bo;
-          const float* rs = stg + rr * 65;  // staging row rr: output element x is rs[x - s0]
-          auto src = [&](int64_t x) { return rs[(int)(x - s0)]; };
-          const int64_t c0 = sa + (int64_t)li * CE;
-          if (c0 + CE <= ea) {
-            if constexpr (sizeof(E) == 4) {
-              *reinterpret_cast<float4*>(out + c0) = make_float4(src(c0), src(c0 + 1), src(c0 + 2), src(c0 + 3));
-            } else {
-              *reinterpret_cast<uint4*>(out + c0) =
-                  make_uint4(tc::pack_bf16(src(c0), src(c0 + 1)), tc::pack_bf16(src(c0 + 2), src(c0 + 3)),
-                             tc::pack_bf16(src(c0 + 4), src(c0 + 5)), tc::pack_bf16(src(c0 + 6), src(c0 + 7)));
-            }
+        constexpr int RPS = 32 / LPR;           // rows per step
+        constexpr int NIT = 32 / RPS;           // steps to cover the warp's 32 staged rows
+        constexpr int NE = (CE - 1 + LPR - 1) / LPR;  // edge elements per lane (at most CE - 1 per row end)
+        // Per-row positions are 32-bit offsets from the tile's first element (rr * Bi + 64 < 2^31); chunk
+        // alignment is absolute, so a0 = misalignment of that first element (the output base need only be
+        // element-aligned). All staging reads are issued before any global store (the generic output pointer
+        // could alias shared memory, so an interleaved loop serialises every LDS behind the previous STG), and
+        // the edge elements are predicated stores rather than divergent branches.
+        E* base = reinterpret_cast<E*>(p.out) + row0;
+        const int a0 = (int)((reinterpret_cast<uintptr_t>(base) / sizeof(E)) & (CE - 1));
+        const int sub = lane / LPR, li = lane % LPR, n32 = (int)tl.n;
+        uint4 body[NIT];
+        float lead[NIT][NE], trail[NIT][NE];
+        int cpos[NIT], s0s[NIT], t0s[NIT];
+        uint32_t okm = 0, lm = 0, tm = 0;  // bit it * NE + k: edge element li + k * LPR of step it
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int rr = sub + it * RPS;
+          const int s0 = rr * n32;                                  // row start (tile-relative)
+          const int hd = (CE - ((a0 + s0) & (CE - 1))) & (CE - 1);  // elements before the first aligned chunk
+          const int tl0 = (a0 + s0 + nc) & (CE - 1);                // elements after the last aligned chunk
+          const int nh = hd < nc ? hd : nc;
+          const int body_n = nc - nh - tl0;                        // aligned body length (may be < 0)
+          const int c = hd + li * CE;                               // row-relative chunk start
+          const bool live = rr < nrows;
+          const bool okc = live && c + CE <= hd + (body_n > 0 ? body_n : 0);
+          const int t0 = body_n > 0 ? nc - tl0 : nh;               // row-relative tail start
+          const float* rs = stg + rr * 65;
+          const int cb = okc ? c : 0;
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < CE; ++e) f[e] = rs[cb + e];
+          if constexpr (sizeof(E) == 4) {
+            body[it] = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+          } else {
+            body[it] = make_uint4(tc::pack_bf16(f[0], f[1]), tc::pack_bf16(f[2], f[3]), tc::pack_bf16(f[4], f[5]),
+                                  tc::pack_bf16(f[6], f[7]));
           }
-          const int64_t nh = (sa < e0 ? sa : e0) - s0, t0 = ea > sa ? ea : sa;
-          if (li < nh) out[s0 + li] = E(src(s0 + li));
-          if (li < e0 - t0) out[t0 + li] = E(src(t0 + li));
+#pragma unroll
+          for (int k = 0; k < NE; ++k) {
+            const int x = li + k * LPR;
+            const bool okl = live && x < nh, okt = live && x < nc - t0;
+            lead[it][k] = rs[okl ? x : 0];
+            trail[it][k] = rs[okt ? t0 + x : 0];
+            lm |= (uint32_t)okl << (it * NE + k);
+            tm |= (uint32_t)okt << (it * NE + k);
+          }
+          cpos[it] = s0 + c;
+          s0s[it] = s0;
+          t0s[it] = s0 + t0;
+          okm |= (uint32_t)okc << it;
+        }
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          if (okm >> it & 1) *reinterpret_cast<uint4*>(base + cpos[it]) = body[it];
+#pragma unroll
+          for (int k = 0; k < NE; ++k) {
+            if (lm >> (it * NE + k) & 1) base[s0s[it] + li + k * LPR] = E(lead[it][k]);
+            if (tm >> (it * NE + k) & 1) base[t0s[it] + li + k * LPR] = E(trail[it][k]);
+          }
         }
       };
       if (nc > 0 && !(p.dbg & 1)) {
         if (p.out_f32) store_rows(float{});
-        else store_rows(__nv_bfloat16{});
+        else store_img();
       }
       __syncwarp();
     }

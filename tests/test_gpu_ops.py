@@ -295,3 +295,24 @@ def test_full_size_cfg4_properties():
     row_id = torch.repeat_interleave(torch.arange(S, device=DEV), rows)
     rowsum = torch.zeros(S, device=DEV).index_add_(0, row_id, P2.values.float())
     assert float((rowsum - 1).abs().max()) < 2e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lens", [[1, 7, 129, 300, 0, 255, 513, 8, 9, 1000], list(range(1, 140, 3)), [1024] * 4 + [1023] * 3])
+def test_jjjout_bf16_output_matches_rounded_f32(lens):
+    """bf16-output jagged_jagged_bmm_jagged_out (tcgen05 epilogue writing realigned bf16 row images, every
+    row phase mod 8) equals the fp32-output run of the same kernel rounded to bf16 — bit for bit — and the
+    f64 oracle within the bf16 tolerance plus the bf16 storage rounding."""
+    ln = np.asarray(lens, np.int64)
+    D = 128
+    off, t = _inputs(ln, D, 8, 5, bf16_round)
+    X, K = jt(off, t["x"], torch.bfloat16), jt(off, t["k"], torch.bfloat16)
+    s32 = J.jagged_jagged_bmm_jagged_out(X, K, out_dtype=torch.float32).values
+    s16 = J.jagged_jagged_bmm_jagged_out(X, K).values
+    assert s16.dtype == torch.bfloat16 and s16.numel() == int((ln * ln).sum())
+    assert torch.equal(s16, s32.bfloat16())
+    ref = torch.from_numpy(np.asarray(R.jagged_jagged_bmm_jagged_out(off, t["x"], t["k"]), np.float64))
+    assert_bf16_close(s32, ref, what="jjbmm_jout f32 out")
+    # bf16 storage adds at most half an ulp (2^-9 relative) of the output's own magnitude
+    err = (s16.double().cpu() - ref).abs()
+    assert bool((err <= 2e-2 + ref.abs() * 2.0 ** -8).all()), float(err.max())
