@@ -166,14 +166,20 @@ REF_T(double, f64)
 REF_DENSE(float, f32)
 REF_DENSE(double, f64)
 
-// VJPs: the reference's registry and gradcheck use the double instantiation.
+// VJPs: the reference's registry and gradcheck use the double instantiation. KernelOptions.threads for them
+// (default 1, as the registry calls them) is set by ref_set_vjp_threads (scale parity tests run them threaded).
+namespace {
+int g_vjp_threads = 1;
+jagged::KernelOptions vjp_opts() { return kopts(g_vjp_threads, 64); }
+}  // namespace
+extern "C" void ref_set_vjp_threads(int threads) { g_vjp_threads = threads > 0 ? threads : 1; }
 extern "C" int ref_jagged_dense_bmm_vjp_f64(const int64_t* off, int64_t B, int64_t D, int64_t T,
                                             const double* x, const double* w, const double* go,
                                             double* dx, double* dw) {
   return guard([&] {
     auto g = jagged::jagged_dense_bmm_vjp(jt(off, B, D, x),
                                           jagged::DenseTensor<double>({B, D, T}, vec(w, B * D * T)),
-                                          jt(off, B, T, go));
+                                          jt(off, B, T, go), vjp_opts());
     put(g.dx.values(), dx);
     put(g.dw.data(), dw);
   });
@@ -183,20 +189,21 @@ extern "C" int ref_jagged_jagged_bmm_vjp_f64(const int64_t* off, int64_t B, int6
                                              double* dx, double* dy) {
   return guard([&] {
     auto g = jagged::jagged_jagged_bmm_vjp(jt(off, B, D, x), jt(off, B, T, y),
-                                           jagged::DenseTensor<double>({B, D, T}, vec(go, B * D * T)));
+                                           jagged::DenseTensor<double>({B, D, T}, vec(go, B * D * T)), vjp_opts());
     put(g.dx.values(), dx);
     put(g.dy.values(), dy);
   });
 }
 extern "C" int ref_jagged_softmax_vjp_f64(const int64_t* off, int64_t B, int64_t D,
                                           const double* x, const double* go, double* dx) {
-  return guard([&] { put(jagged::jagged_softmax_vjp(jt(off, B, D, x), jt(off, B, D, go)).values(), dx); });
+  return guard([&] { put(jagged::jagged_softmax_vjp(jt(off, B, D, x), jt(off, B, D, go), vjp_opts()).values(), dx); });
 }
 extern "C" int ref_jagged_jagged_bmm_jagged_out_vjp_f64(const int64_t* off, int64_t B, int64_t D,
                                                         const double* q, const double* k,
                                                         const double* go, double* dq, double* dk) {
   return guard([&] {
-    auto g = jagged::jagged_jagged_bmm_jagged_out_vjp(jt(off, B, D, q), jt(off, B, D, k), j2(off, B, go));
+    auto g = jagged::jagged_jagged_bmm_jagged_out_vjp(jt(off, B, D, q), jt(off, B, D, k), j2(off, B, go),
+                                                      vjp_opts());
     put(g.dq.values(), dq);
     put(g.dk.values(), dk);
   });
@@ -205,14 +212,15 @@ extern "C" int ref_array_jagged_bmm_jagged_out_vjp_f64(const int64_t* off, int64
                                                        const double* a, const double* v,
                                                        const double* go, double* da, double* dv) {
   return guard([&] {
-    auto g = jagged::array_jagged_bmm_jagged_out_vjp(j2(off, B, a), jt(off, B, D, v), jt(off, B, D, go));
+    auto g = jagged::array_jagged_bmm_jagged_out_vjp(j2(off, B, a), jt(off, B, D, v), jt(off, B, D, go),
+                                                     vjp_opts());
     put(g.da.values(), da);
     put(g.dv.values(), dv);
   });
 }
 extern "C" int ref_jagged2_softmax_vjp_f64(const int64_t* off, int64_t B, const double* s,
                                            const double* go, double* ds) {
-  return guard([&] { put(jagged::jagged2_softmax_vjp(j2(off, B, s), j2(off, B, go)).values(), ds); });
+  return guard([&] { put(jagged::jagged2_softmax_vjp(j2(off, B, s), j2(off, B, go), vjp_opts()).values(), ds); });
 }
 
 // feature_interaction (attention.cpp:291-309) and jagged_mlp (linalg.cpp:265-277,
@@ -297,6 +305,22 @@ extern "C" int ref_uniform_values_f32(uint64_t seed, int64_t n, double lo, doubl
   return guard([&] {
     jagged::Rng r(seed);
     put(jagged::uniform_values<float>(r, n, lo, hi), out);
+  });
+}
+// A stateful reference generator: successive draws continue one jagged::Rng stream, as bench.cpp draws q, k, v
+// (then grad_out) from Rng(seed + 1) one tensor after another (bench.cpp:323-329). Values are the reference's
+// uniform_values<float> (rng.cpp:59-64), produced in bounded chunks.
+extern "C" void* ref_rng_new(uint64_t seed) { return new jagged::Rng(seed); }
+extern "C" void ref_rng_free(void* r) { delete static_cast<jagged::Rng*>(r); }
+extern "C" int ref_rng_uniform_f32(void* r, int64_t n, double lo, double hi, float* out) {
+  return guard([&] {
+    auto& rng = *static_cast<jagged::Rng*>(r);
+    constexpr int64_t kChunk = int64_t(1) << 24;
+    for (int64_t i = 0; i < n; i += kChunk) {
+      const int64_t m = n - i < kChunk ? n - i : kChunk;
+      const auto v = jagged::uniform_values<float>(rng, m, lo, hi);
+      std::memcpy(out + i, v.data(), m * sizeof(float));
+    }
   });
 }
 extern "C" int ref_make_offsets(const int64_t* lengths, int64_t B, int64_t* offsets) {

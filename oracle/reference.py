@@ -71,6 +71,31 @@ def uniform_values(seed: int, n: int, lo=-1.0, hi=1.0, prec="f64") -> np.ndarray
     return out
 
 
+class RngStream:
+    """One jagged::Rng(seed) stream; successive uniform_f32 calls continue it (bench.cpp:323-329 draws q, k, v
+    and then grad_out from Rng(seed + 1) in that order)."""
+
+    def __init__(self, seed: int):
+        lib().ref_rng_new.restype = C.c_void_p
+        self._h = C.c_void_p(lib().ref_rng_new(C.c_uint64(seed)))
+
+    def uniform_f32(self, n: int, lo=-1.0, hi=1.0) -> np.ndarray:
+        out = np.empty(int(n), np.float32)
+        _chk(lib().ref_rng_uniform_f32(self._h, _I(int(n)), C.c_double(lo), C.c_double(hi), _p(out)))
+        return out
+
+    def __del__(self):
+        try:
+            lib().ref_rng_free(self._h)
+        except Exception:
+            pass
+
+
+def set_vjp_threads(threads: int) -> None:
+    """KernelOptions.threads for the reference VJPs (default 1, as the reference registry calls them)."""
+    lib().ref_set_vjp_threads(C.c_int(int(threads)))
+
+
 def make_offsets(lengths) -> np.ndarray:
     lengths = _arr(lengths, np.int64)
     off = np.empty(len(lengths) + 1, np.int64)

@@ -86,7 +86,7 @@ struct Params {
   float scale;
   int dbg;                   // JG_BWD_DBG diagnostic bits (results invalid when set): 1 skip the dQ reduce,
                              // 4 skip the P/dS smem stores, 8 skip the dK/dV stores, 64 skip the main kernel, 128 sync + report after it
-  unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
+  unsigned long long* work_counter;  // [2] self-resetting (internal.h work_counters_exit); items beyond the first round
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23, drain 24-31)
   const int64_t* valid;      // padded mode: per-sample valid length <= segment length (nullptr: jagged). Keys and
                              // queries past it get P = dS = 0, so their dQ/dK/dV rows come out zero.
@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem);
   }
+  if (threadIdx.x == 0) work_counters_exit(p.work_counter);
   tc::cta_time_mark(p.prof, 1);
 }
 
@@ -682,7 +683,7 @@ template <int kD>
 static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
                             const void* go, const void* o, const float* lse, void* dq, void* dk, void* dv,
                             float* delta, float* dq_acc, const int2* items, const int64_t* n_items, int64_t max_items,
-                            const int64_t* valid, cudaStream_t st) {
+                            const int64_t* valid, unsigned long long* counters, cudaStream_t st) {
   using L = fb::Smem<kD>;
   const int sms = device_sm_count();
   const int64_t units = total_rows * H;
@@ -696,17 +697,11 @@ static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const
   if (jg_status rc = make_map(&mdo, go, total_rows, H, kD, fb::BQ)) return rc;
   CUtensorMap mdq;
   if (jg_status rc = make_map_f32(&mdq, dq_acc, total_rows, H, kD, L::kStgRows)) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    JG_CUDA(cudaFuncSetAttribute(fb::jfa_bwd_sm100_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
-    attr_set = true;
-  }
-  // the work counter lives in the workspace's slack after the dQ accumulator
-  auto* counter = reinterpret_cast<unsigned long long*>(dq_acc + units * kD);
-  JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  if (jg_status rc = ensure_smem_attr((const void*)fb::jfa_bwd_sm100_kernel<kD>, L::kAlloc, "jfa_bwd_sm100_kernel"))
+    return rc;
   fb::Params p{off, items, n_items, total_rows, H, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), std::getenv("JG_BWD_DBG") ? std::atoi(std::getenv("JG_BWD_DBG")) : 0,
-               counter, wait_prof_begin(st), valid};
+               counters, wait_prof_begin(st), valid};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
   if (!(p.dbg & 64)) fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
   if (p.dbg & 128) {
@@ -729,14 +724,14 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
                                 const void* k, const void* v, const void* go, const void* o, const float* lse,
                                 void* dq, void* dk, void* dv, float* delta, float* dq_acc, const int2* items,
                                 const int64_t* n_items, int64_t max_items, const int64_t* valid,
-                                cudaStream_t st) {
+                                unsigned long long* counters, cudaStream_t st) {
   (void)batch;
   if (D == 128)
     return bwd_launch<128>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items, max_items,
-                           valid, st);
+                           valid, counters, st);
   if (D == 64)
     return bwd_launch<64>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items, max_items,
-                          valid, st);
+                          valid, counters, st);
   return fail(JG_UNSUPPORTED, "tcgen05 attention backward: head_dim must be 64 or 128");
 }
 

@@ -77,7 +77,7 @@ struct Params {
   float* lse;
   float scale_log2;
   unsigned long long* prof;  // JG_WAIT_PROF counters (producer 0-7, MMA 8-15, softmax 16-23)
-  unsigned long long* work_counter;  // zeroed before the launch; items beyond the first grid-wide round
+  unsigned long long* work_counter;  // [2] self-resetting (internal.h work_counters_exit); items beyond the first round
   int dbg;                   // JG_FWD_DBG (diagnostic, results invalid): 1 = softmax publishes P without computing
   const int64_t* valid;      // padded mode (dense_flash_attention): per-sample valid length <= segment length, or
                              // nullptr. Keys past it are masked, rows past it get zeros and lse = -inf.
@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem);
   }
+  if (threadIdx.x == 0) work_counters_exit(p.work_counter);
   tc::cta_time_mark(p.prof, 1);
 }
 
@@ -519,25 +520,14 @@ template <int D>
 static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_rows, int H, const void* q, const void* k,
                             const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
                             int64_t max_items, const int64_t* valid, const int64_t* q_off, int64_t q_rows,
-                            cudaStream_t st) {
+                            unsigned long long* counter, cudaStream_t st) {
   using L = fa::Smem<D>;
   CUtensorMap mq, mk, mv;
   if (jg_status rc = make_map(&mq, q, q_off ? q_rows : total_rows, H, D, 128)) return rc;
   if (jg_status rc = make_map(&mk, k, total_rows, H, D, 128)) return rc;
   if (jg_status rc = make_map(&mv, v, total_rows, H, D, 128)) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    JG_CUDA(cudaFuncSetAttribute(fa::jfa_fwd_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
-    cudaFuncAttributes fa_attr;
-    JG_CUDA(cudaFuncGetAttributes(&fa_attr, fa::jfa_fwd_sm100_kernel<D>));
-    if (fa_attr.maxThreadsPerBlock < fa::kThreads)
-      return fail(JG_CUDA_ERROR, "jfa_fwd_sm100_kernel: " + std::to_string(fa_attr.numRegs) + " registers allow only " +
-                                     std::to_string(fa_attr.maxThreadsPerBlock) + " threads per block");
-    attr_set = true;
-  }
-  unsigned long long* counter = nullptr;  // stream-ordered 8-byte work counter for this launch
-  JG_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), st));
-  JG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  if (jg_status rc = ensure_smem_attr((const void*)fa::jfa_fwd_sm100_kernel<D>, L::kAlloc, "jfa_fwd_sm100_kernel"))
+    return rc;
   fa::Params p{off, items, n_items, batch, q_off ? q_rows : total_rows, H, (__nv_bfloat16*)out, lse,
                1.4426950408889634f / sqrtf((float)D), wait_prof_begin(st), counter,
                std::getenv("JG_FWD_DBG") ? std::atoi(std::getenv("JG_FWD_DBG")) : 0, valid, q_off};
@@ -545,7 +535,6 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(device_sm_count(), work));
   fa::jfa_fwd_sm100_kernel<D><<<grid, fa::kThreads, L::kAlloc, st>>>(mq, mk, mv, p);
   const cudaError_t launch_err = cudaGetLastError();
-  cudaFreeAsync(counter, st);
   if (launch_err != cudaSuccess) return cuda_status(launch_err, "jfa_fwd_sm100_kernel");
   count_launch();
   wait_prof_end(p.prof, st, "fwd",
@@ -557,12 +546,14 @@ static jg_status fwd_launch(const int64_t* off, int64_t batch, int64_t total_row
 // items: (sample, 256-row tile pair) LPT work list (schedule tile 256)
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                                 const void* k, const void* v, void* out, float* lse, const int2* items,
-                                const int64_t* n_items, int64_t max_items, const int64_t* valid, cudaStream_t st,
-                                const int64_t* q_off, int64_t q_rows) {
+                                const int64_t* n_items, int64_t max_items, const int64_t* valid,
+                                unsigned long long* counters, cudaStream_t st, const int64_t* q_off, int64_t q_rows) {
   if (D == 128)
-    return fwd_launch<128>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, q_off, q_rows, st);
+    return fwd_launch<128>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, q_off, q_rows,
+                           counters, st);
   if (D == 64)
-    return fwd_launch<64>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, q_off, q_rows, st);
+    return fwd_launch<64>(off, batch, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, q_off, q_rows,
+                          counters, st);
   return fail(JG_UNSUPPORTED, "tcgen05 attention: head_dim must be 64 or 128");
 }
 

@@ -47,6 +47,20 @@ int device_sm_count() {
   return dev < 64 ? cached[dev] : kNumSMsB200;
 }
 
+jg_status ensure_smem_attr(const void* func, int bytes, const char* name) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, device) pairs already configured
+  int dev = 0;
+  JG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& d : done)
+    if (d.first == func && d.second == dev) return JG_OK;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_status(e, name);
+  done.emplace_back(func, dev);
+  return JG_OK;
+}
+
 // RAII stream-ordered scratch
 struct Scratch {
   void* p = nullptr;
@@ -166,6 +180,7 @@ struct jg_schedule_s {
   int64_t* n_items;
   int2* items2;
   int64_t* n_items2;
+  unsigned long long* counters;  // [4]: forward kernel (next item, exited CTAs), backward kernel (same)
   void* block;
 };
 
@@ -192,17 +207,19 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
   s->lengths = (int64_t*)p; p += b_len;
   s->sq = (int64_t*)p; p += b_sq;
   s->n_items = (int64_t*)p; p += 64;
-  s->n_items2 = (int64_t*)p; p += 64;
+  s->n_items2 = (int64_t*)p; p += 32;
+  s->counters = (unsigned long long*)p; p += 32;
   s->items = (int2*)p; p += b_items;
   s->items2 = (int2*)p;
   jg_status rc = JG_OK;
+  JG_CUDA(cudaMemsetAsync(s->counters, 0, 32, st));  // self-resetting afterwards (internal.h)
   if (batch > 0) {
     if ((rc = launch_lengths(offsets, batch, s->lengths, st))) goto err;
     if ((rc = launch_scan(1, offsets, batch, s->sq, nullptr, st))) goto err;
     if ((rc = launch_work_list(offsets, batch, 128, s->items, s->n_items, st))) goto err;
     if ((rc = launch_work_list(offsets, batch, 256, s->items2, s->n_items2, st))) goto err;
   } else {
-    JG_CUDA(cudaMemsetAsync(s->n_items, 0, 128, st));
+    JG_CUDA(cudaMemsetAsync(s->n_items, 0, 64, st));
     JG_CUDA(cudaMemsetAsync(s->sq, 0, sizeof(int64_t), st));
   }
   *out = s;
@@ -437,10 +454,21 @@ extern "C" int64_t jg_attention_backward_workspace_size(int64_t total_rows, int3
 
 // Shared by the jagged entry points (valid == nullptr) and the padded dense_flash_attention mode (valid =
 // per-sample lengths on device, offsets i*max_len): same kernels, masks from `valid`.
+// A caller-supplied schedule must be the one built for these offsets: the kernels index offsets[] with its
+// sample ids, so a schedule of another batch would read out of bounds and write rows of other samples.
+static jg_status check_schedule(const char* op, jg_schedule s, const int64_t* off, int64_t batch, int64_t total_rows) {
+  if (!s) return JG_OK;
+  REQUIRE(s->offsets == off && s->batch == batch && s->total_rows == total_rows, JG_INVALID_ARGUMENT,
+          std::string(op) + ": schedule was built for other offsets (batch " + std::to_string(s->batch) + ", rows " +
+              std::to_string(s->total_rows) + " vs " + std::to_string(batch) + ", " + std::to_string(total_rows) + ")");
+  return JG_OK;
+}
+
 static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_rows, int32_t H, int32_t D,
                               const void* q, const void* k, const void* v, void* out, float* lse, jg_dtype dtype,
                               jg_schedule sched, const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
+  if (jg_status rc = check_schedule("jagged_flash_attention_forward", sched, off, batch, total_rows)) return rc;
   if (!force_simt() && attn_sm100_supported(D, dtype)) {
     jg_schedule own = nullptr;
     if (!sched) {
@@ -448,7 +476,7 @@ static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_r
       sched = own;
     }
     jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
-                                         sched->n_items2, sched->max_items2, valid, st);
+                                         sched->n_items2, sched->max_items2, valid, sched->counters, st);
     if (own) {
       schedule_release(own, st);
     }
@@ -462,6 +490,7 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
                                const float* lse, void* dq, void* dk, void* dv, jg_dtype dtype, jg_schedule sched,
                                void* workspace, const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
+  if (jg_status rc = check_schedule("jagged_flash_attention_backward", sched, off, batch, total_rows)) return rc;
   Scratch ws(st);
   if (!workspace) {
     if (jg_status rc = ws.alloc(jg_attention_backward_workspace_size(total_rows, H, D))) return rc;
@@ -476,7 +505,8 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
       sched = own;
     }
     jg_status rc = launch_attn_bwd_sm100(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta,
-                                         dq_acc, sched->items, sched->n_items, sched->max_items, valid, st);
+                                         dq_acc, sched->items, sched->n_items, sched->max_items, valid,
+                                         sched->counters + 2, st);
     if (own) {
       schedule_release(own, st);
     }
@@ -518,18 +548,29 @@ static jg_status padded_layout(const char* op, const int64_t* lengths, int64_t b
                                Scratch& buf, const int64_t** d_off, const int64_t** d_valid) {
   REQUIRE(batch >= 0 && max_len >= 0, JG_INVALID_ARGUMENT, std::string(op) + ": q, k, v must share a [B, L, D] shape");
   REQUIRE(batch == 0 || lengths, JG_INVALID_ARGUMENT, std::string(op) + ": lengths size mismatch");
-  std::vector<int64_t> h(2 * batch + 1);
-  for (int64_t i = 0; i < batch; ++i) {
+  for (int64_t i = 0; i < batch; ++i)
     REQUIRE(lengths[i] >= 0 && lengths[i] <= max_len, JG_INVALID_ARGUMENT,
             std::string(op) + ": sample " + std::to_string(i) + " length " + std::to_string(lengths[i]) +
                 " out of bounds for L=" + std::to_string(max_len));
-    h[i] = i * max_len;
-    h[batch + 1 + i] = lengths[i];
+  // the staging vector lives until the stream has consumed it (released by a host callback, no host sync)
+  auto* h = new std::vector<int64_t>(2 * batch + 1);
+  for (int64_t i = 0; i < batch; ++i) {
+    (*h)[i] = i * max_len;
+    (*h)[batch + 1 + i] = lengths[i];
   }
-  h[batch] = batch * max_len;
-  if (jg_status rc = buf.alloc(sizeof(int64_t) * h.size())) return rc;
-  JG_CUDA(cudaMemcpyAsync(buf.p, h.data(), sizeof(int64_t) * h.size(), cudaMemcpyHostToDevice, buf.s));
-  JG_CUDA(cudaStreamSynchronize(buf.s));  // `h` is pageable and goes out of scope
+  (*h)[batch] = batch * max_len;
+  if (jg_status rc = buf.alloc(sizeof(int64_t) * h->size())) {
+    delete h;
+    return rc;
+  }
+  cudaError_t e = cudaMemcpyAsync(buf.p, h->data(), sizeof(int64_t) * h->size(), cudaMemcpyHostToDevice, buf.s);
+  if (e == cudaSuccess)
+    e = cudaLaunchHostFunc(buf.s, [](void* v) { delete static_cast<std::vector<int64_t>*>(v); }, h);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(buf.s);
+    delete h;
+    return cuda_status(e, "padded layout upload");
+  }
   *d_off = (const int64_t*)buf.p;
   *d_valid = (const int64_t*)buf.p + batch + 1;
   return JG_OK;
@@ -759,6 +800,11 @@ extern "C" jg_status jg_feature_interaction(const int64_t* off, int64_t batch, i
   REQUIRE(D >= 1 && Tq >= 1, JG_INVALID_ARGUMENT, "feature_interaction: targets must be [B, Tq, D]");
   cudaStream_t st = as_stream(stream);
   if (batch == 0) return JG_OK;
+  REQUIRE_PTRS("feature_interaction", true, off, targets, out);
+  if (total_rows == 0) {  // every sample empty: the reference returns [B, Tq, D] zeros
+    JG_CUDA(cudaMemsetAsync(out, 0, (size_t)batch * Tq * D * dsize(dtype), st));
+    return JG_OK;
+  }
   if (dtype == JG_BF16 && !force_simt() && attn_sm100_supported((int)D, dtype)) {
     // fused: feature_interaction is attention with the Tq targets of sample i as queries over
     // its k_feat rows (softmax over the segment axis per target) and v_feat as values — the forward JFA
@@ -769,8 +815,8 @@ extern "C" jg_status jg_feature_interaction(const int64_t* off, int64_t batch, i
     jg_schedule qs = nullptr;  // (sample, 256-target pair) items over the query segments
     if (jg_status rc = jg_schedule_create((const int64_t*)qo.p, batch, batch * Tq, st, &qs)) return rc;
     jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, 1, (int)D, targets, k_feat, v_feat, out, nullptr,
-                                         qs->items2, qs->n_items2, qs->max_items2, nullptr, st, (const int64_t*)qo.p,
-                                         batch * Tq);
+                                         qs->items2, qs->n_items2, qs->max_items2, nullptr, qs->counters, st,
+                                         (const int64_t*)qo.p, batch * Tq);
     schedule_release(qs, st);
     return rc;
   }

@@ -621,11 +621,7 @@ static jg_status map2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t co
 
 template <int OP>
 static jg_status run(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    JG_CUDA(cudaFuncSetAttribute(gemm_sm100_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::kAlloc));
-    attr = true;
-  }
+  if (jg_status rc = ensure_smem_attr((const void*)gemm_sm100_kernel<OP>, Smem::kAlloc, "gemm_sm100_kernel")) return rc;
   gemm_sm100_kernel<OP><<<device_sm_count(), kThreads, Smem::kAlloc, st>>>(ma, mb, p);
   JG_LAUNCHED("gemm_sm100_kernel");
   return JG_OK;

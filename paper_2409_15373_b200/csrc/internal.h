@@ -28,6 +28,26 @@ struct GemmDesc {
   Lin c0, scm, scn;  // C(m,n) = C[c0 + m*scm + n*scn]
 };
 
+// Per-device, mutex-guarded, lazily-set kernel attribute: the opt-in dynamic shared memory size of `func`
+// (cudaFuncSetAttribute is per device; a process driving several devices sets it once on each).
+jg_status ensure_smem_attr(const void* func, int bytes, const char* name);
+
+// Self-resetting work counters for the persistent kernels: counters[0] = next dynamic item, counters[1] = CTAs
+// exited. Zeroed once when allocated (schedule creation); the last CTA of a launch to exit zeroes both, so
+// consecutive launches on one stream need no memset. A schedule's counters serialise the launches that use
+// it: one schedule must not drive two concurrently running kernels.
+#ifdef __CUDACC__
+__device__ __forceinline__ void work_counters_exit(unsigned long long* counters) {
+  if (counters == nullptr) return;
+  __threadfence();
+  if (atomicAdd(counters + 1, 1ull) == gridDim.x - 1) {
+    counters[0] = 0;
+    counters[1] = 0;
+    __threadfence();
+  }
+}
+#endif
+
 jg_status launch_scan(int mode, const int64_t* in, int64_t n, int64_t* out, int64_t* bad, cudaStream_t s);
 jg_status launch_lengths(const int64_t* off, int64_t n, int64_t* len, cudaStream_t s);
 jg_status launch_work_list(const int64_t* off, int64_t batch, int tile, int2* items, int64_t* count,
@@ -103,7 +123,7 @@ bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt);
 jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, void* out, float* lse,
                                 const int2* items, const int64_t* n_items, int64_t max_items,
-                                const int64_t* valid, cudaStream_t st,
+                                const int64_t* valid, unsigned long long* counters, cudaStream_t st,
                                 // cross mode (fused feature_interaction): query segments over the key segments
                                 const int64_t* q_off = nullptr, int64_t q_rows = 0);
 jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
@@ -111,6 +131,6 @@ jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total
                                 const void* o, const float* lse, void* dq, void* dk, void* dv,
                                 float* delta, float* dq_accum, const int2* items,
                                 const int64_t* n_items, int64_t max_items, const int64_t* valid,
-                                cudaStream_t st);
+                                unsigned long long* counters, cudaStream_t st);
 
 }  // namespace jg

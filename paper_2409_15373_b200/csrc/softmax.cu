@@ -80,7 +80,7 @@ __device__ __forceinline__ void online_update(float& m, float& s, float y) {
   if (y > m) {
     s = s * ex2a(m - y) + 1.0f;
     m = y;
-  } else {
+  } else if (m != -INFINITY) {  // y <= m = -inf means y = -inf: weight 0 (ex2(-inf - -inf) would be NaN)
     s += ex2a(y - m);
   }
 }
@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
         const float y0 = __fmul_rn(v[0][j], kLog2e), y1 = __fmul_rn(v[1][j], kLog2e);
         const float y2 = __fmul_rn(v[2][j], kLog2e), y3 = __fmul_rn(v[3][j], kLog2e);
         const float mn = fmaxf(m[j], fmaxf(fmaxf(y0, y1), fmaxf(y2, y3)));
-        s[j] = s[j] * ex2a(m[j] - mn) + ((ex2a(y0 - mn) + ex2a(y1 - mn)) + (ex2a(y2 - mn) + ex2a(y3 - mn)));
+        const float ms = mn == -INFINITY ? 0.f : mn;  // safe max: all -inf so far gives weights 0, not NaN
+        s[j] = s[j] * ex2a(m[j] - ms) + ((ex2a(y0 - ms) + ex2a(y1 - ms)) + (ex2a(y2 - ms) + ex2a(y3 - ms)));
         m[j] = mn;
       }
     }
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(256) jagged2_softmax_kernel(const int64_t* __r
       const float y0 = __fmul_rn(ld(s + base + c), kLog2e), y1 = __fmul_rn(ld(s + base + c + 32), kLog2e);
       const float y2 = __fmul_rn(ld(s + base + c + 64), kLog2e), y3 = __fmul_rn(ld(s + base + c + 96), kLog2e);
       const float mn = fmaxf(m, fmaxf(fmaxf(y0, y1), fmaxf(y2, y3)));
-      sm = sm * ex2a(m - mn) + ((ex2a(y0 - mn) + ex2a(y1 - mn)) + (ex2a(y2 - mn) + ex2a(y3 - mn)));
+      const float ms = mn == -INFINITY ? 0.f : mn;  // safe max (see online_update)
+      sm = sm * ex2a(m - ms) + ((ex2a(y0 - ms) + ex2a(y1 - ms)) + (ex2a(y2 - ms) + ex2a(y3 - ms)));
       m = mn;
     }
     for (; c < n; c += 32) online_update(m, sm, __fmul_rn(ld(s + base + c), kLog2e));

@@ -192,6 +192,20 @@ def _require_matching_offsets(a: JaggedTensor, b: JaggedTensor, op: str) -> None
         raise JaggedError(f"{op}: offsets differ first at sample {int(diff[0])}")
 
 
+def _operands(op: str, ref: torch.Tensor, *others) -> None:
+    """Paired operands share the reference operand's dtype and live on its CUDA device: the C-ABI takes one
+    dtype per call, so a mismatch would make a kernel read past a buffer (or dereference a host pointer)."""
+    for t in (ref,) + others:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise JaggedError(f"{op}: operands must be CUDA tensors")
+        if t.device != ref.device:
+            raise JaggedError(f"{op}: operands must be on one device ({ref.device} vs {t.device})")
+        if t.dtype != ref.dtype:
+            raise JaggedError(f"{op}: dtype mismatch ({ref.dtype} vs {t.dtype})")
+
+
 def _out_dtype(x: torch.Tensor, out_dtype):
     return x.dtype if out_dtype is None else out_dtype
 
@@ -205,6 +219,7 @@ def jagged_dense_bmm(x: JaggedTensor, w: torch.Tensor, out_dtype=None) -> Jagged
         raise JaggedError(f"jagged_dense_bmm: batch mismatch ({x.batch} vs {B})")
     if D != x.dim:
         raise JaggedError(f"jagged_dense_bmm: dim mismatch ({x.dim} vs {D})")
+    _operands("jagged_dense_bmm", x.values, w)
     out = torch.empty(x.total_rows, T, dtype=_out_dtype(x.values, out_dtype), device=x.values.device)
     check(_lib.lib().jg_jagged_dense_bmm(_p(x.offsets), x.batch, x.total_rows, D, T, _p(x.values),
                                          _p(w.contiguous()), _p(out), _dt(x.values), _dt(out), _stream()))
@@ -213,6 +228,7 @@ def jagged_dense_bmm(x: JaggedTensor, w: torch.Tensor, out_dtype=None) -> Jagged
 
 def jagged_jagged_bmm(x: JaggedTensor, y: JaggedTensor, out_dtype=None) -> torch.Tensor:
     _require_matching_offsets(x, y, "jagged_jagged_bmm")
+    _operands("jagged_jagged_bmm", x.values, y.values)
     out = torch.empty(x.batch, x.dim, y.dim, dtype=_out_dtype(x.values, out_dtype), device=x.values.device)
     check(_lib.lib().jg_jagged_jagged_bmm(_p(x.offsets), x.batch, x.total_rows, x.dim, y.dim, _p(x.values),
                                           _p(y.values), _p(out), _dt(x.values), _dt(out), _stream()))
@@ -220,6 +236,7 @@ def jagged_jagged_bmm(x: JaggedTensor, y: JaggedTensor, out_dtype=None) -> torch
 
 
 def jagged_softmax(x: JaggedTensor) -> JaggedTensor:
+    _operands("jagged_softmax", x.values)
     out = torch.empty_like(x.values)
     check(_lib.lib().jg_jagged_softmax(_p(x.offsets), x.batch, x.total_rows, x.dim, _p(x.values), _p(out),
                                        _dt(x.values), _stream()))
@@ -230,6 +247,7 @@ def jagged_jagged_bmm_jagged_out(q: JaggedTensor, k: JaggedTensor, out_dtype=Non
     _require_matching_offsets(q, k, "jagged_jagged_bmm_jagged_out")
     if q.dim != k.dim:
         raise JaggedError(f"jagged_jagged_bmm_jagged_out: dim mismatch ({q.dim} vs {k.dim})")
+    _operands("jagged_jagged_bmm_jagged_out", q.values, k.values)
     ln = q.lengths()
     sq = torch.empty(q.batch + 1, dtype=torch.int64, device=q.values.device)
     check(_lib.lib().jg_sq_offsets(_p(q.offsets), q.batch, _p(sq), _stream()))
@@ -246,6 +264,7 @@ def array_jagged_bmm_jagged_out(a: Jagged2Tensor, v: JaggedTensor, out_dtype=Non
     diff = np.nonzero(a.seq_lengths() != v.lengths())[0]
     if diff.size:
         raise JaggedError(f"array_jagged_bmm_jagged_out: length mismatch at sample {int(diff[0])}")
+    _operands("array_jagged_bmm_jagged_out", v.values, a.values)
     out = torch.empty(v.values.shape, dtype=_out_dtype(v.values, out_dtype), device=v.values.device)
     check(_lib.lib().jg_array_jagged_bmm_jagged_out(_p(v.offsets), _p(a.sq_offsets), v.batch, v.total_rows, v.dim,
                                                     _p(a.values), _p(v.values), _p(out), _dt(v.values), _dt(out),
@@ -254,6 +273,7 @@ def array_jagged_bmm_jagged_out(a: Jagged2Tensor, v: JaggedTensor, out_dtype=Non
 
 
 def jagged2_softmax(s: Jagged2Tensor) -> Jagged2Tensor:
+    _operands("jagged2_softmax", s.values)
     out = torch.empty_like(s.values)
     check(_lib.lib().jg_jagged2_softmax(_p(s.offsets), _p(s.sq_offsets), s.batch, _p(s.values), _p(out),
                                         _dt(s.values), _stream()))
@@ -268,6 +288,7 @@ def jagged_dense_bmm_vjp(x: JaggedTensor, w: torch.Tensor, grad_out: JaggedTenso
     B, D, T = w.shape
     if grad_out.dim != T:
         raise JaggedError("jagged_dense_bmm_vjp: grad_out dim mismatch")
+    _operands("jagged_dense_bmm_vjp", x.values, w, grad_out.values)
     od = _out_dtype(x.values, out_dtype)
     dx = torch.empty(x.values.shape, dtype=od, device=x.values.device)
     dw = torch.empty(w.shape, dtype=od, device=x.values.device)
@@ -281,6 +302,7 @@ def jagged_jagged_bmm_vjp(x: JaggedTensor, y: JaggedTensor, grad_out: torch.Tens
     _require_matching_offsets(x, y, "jagged_jagged_bmm_vjp")
     if grad_out.dim() != 3 or tuple(grad_out.shape) != (x.batch, x.dim, y.dim):
         raise JaggedError("jagged_jagged_bmm_vjp: grad_out must be [B, D, T]")
+    _operands("jagged_jagged_bmm_vjp", x.values, y.values, grad_out)
     od = _out_dtype(x.values, out_dtype)
     dx = torch.empty(x.values.shape, dtype=od, device=x.values.device)
     dy = torch.empty(y.values.shape, dtype=od, device=x.values.device)
@@ -294,6 +316,7 @@ def jagged_softmax_vjp(x: JaggedTensor, grad_out: JaggedTensor) -> JaggedTensor:
     _require_matching_offsets(x, grad_out, "jagged_softmax_vjp")
     if x.dim != grad_out.dim:
         raise JaggedError("jagged_softmax_vjp: dim mismatch")
+    _operands("jagged_softmax_vjp", x.values, grad_out.values)
     dx = torch.empty_like(x.values)
     check(_lib.lib().jg_jagged_softmax_vjp(_p(x.offsets), x.batch, x.total_rows, x.dim, _p(x.values),
                                            _p(grad_out.values), _p(dx), _dt(x.values), _stream()))
@@ -305,6 +328,7 @@ def jagged_jagged_bmm_jagged_out_vjp(q: JaggedTensor, k: JaggedTensor, grad_out:
     diff = np.nonzero(grad_out.seq_lengths() != q.lengths())[0]
     if diff.size:
         raise JaggedError(f"jagged_jagged_bmm_jagged_out_vjp: grad_out length mismatch at sample {int(diff[0])}")
+    _operands("jagged_jagged_bmm_jagged_out_vjp", q.values, k.values, grad_out.values)
     od = _out_dtype(q.values, out_dtype)
     dq = torch.empty(q.values.shape, dtype=od, device=q.values.device)
     dk = torch.empty(k.values.shape, dtype=od, device=q.values.device)
@@ -319,6 +343,7 @@ def array_jagged_bmm_jagged_out_vjp(a: Jagged2Tensor, v: JaggedTensor, grad_out:
     diff = np.nonzero(a.seq_lengths() != v.lengths())[0]
     if diff.size:
         raise JaggedError(f"array_jagged_bmm_jagged_out_vjp: length mismatch at sample {int(diff[0])}")
+    _operands("array_jagged_bmm_jagged_out_vjp", v.values, a.values, grad_out.values)
     od = _out_dtype(v.values, out_dtype)
     da = torch.empty(a.values.shape, dtype=od, device=v.values.device)
     dv = torch.empty(v.values.shape, dtype=od, device=v.values.device)
@@ -331,6 +356,7 @@ def array_jagged_bmm_jagged_out_vjp(a: Jagged2Tensor, v: JaggedTensor, grad_out:
 def jagged2_softmax_vjp(s: Jagged2Tensor, grad_out: Jagged2Tensor) -> Jagged2Tensor:
     if s.batch != grad_out.batch or not np.array_equal(s.seq_lengths(), grad_out.seq_lengths()):
         raise JaggedError("jagged2_softmax_vjp: layout mismatch")
+    _operands("jagged2_softmax_vjp", s.values, grad_out.values)
     ds = torch.empty_like(s.values)
     check(_lib.lib().jg_jagged2_softmax_vjp(_p(s.offsets), _p(s.sq_offsets), s.batch, _p(s.values),
                                             _p(grad_out.values), _p(ds), _dt(s.values), _stream()))
@@ -349,6 +375,7 @@ def _require_attention_inputs(q, k, v, op):
         raise JaggedError(f"{op}: dim mismatch")
     if not q.same_offsets(k) or not q.same_offsets(v):
         raise JaggedError(f"{op}: q, k, v must share offsets")
+    _operands(op, q.values, k.values, v.values)
 
 
 def jagged_flash_attention_forward(q: JaggedTensor, k: JaggedTensor, v: JaggedTensor, block_q: int = 64,
@@ -375,6 +402,16 @@ def jagged_flash_attention_backward(q: JaggedTensor, k: JaggedTensor, v: JaggedT
     if (not saved.output.same_offsets(q) or saved.output.values.shape != q.values.shape
             or saved.logsumexp.numel() != q.total_rows * H or saved.block_q < 1 or saved.block_k < 1):
         raise JaggedError("jagged_flash_attention_backward: saved state does not match inputs")
+    _operands("jagged_flash_attention_backward", q.values, grad_out.values, saved.output.values)
+    lse = saved.logsumexp
+    if lse.dtype != torch.float32 or not lse.is_cuda or lse.device != q.values.device or not lse.is_contiguous():
+        raise JaggedError("jagged_flash_attention_backward: logsumexp must be a contiguous float32 CUDA tensor")
+    if workspace is not None:
+        if not workspace.is_cuda or workspace.device != q.values.device:
+            raise JaggedError("jagged_flash_attention_backward: workspace must be on the inputs' CUDA device")
+        need = int(_lib.lib().jg_attention_backward_workspace_size(q.total_rows, H, D))
+        if workspace.numel() * workspace.element_size() < need or not workspace.is_contiguous():
+            raise JaggedError(f"jagged_flash_attention_backward: workspace needs {need} contiguous bytes")
     dq, dk, dv = (torch.empty_like(q.values) for _ in range(3))
     check(_lib.lib().jg_jagged_flash_attention_backward(
         _p(q.offsets), q.batch, q.total_rows, H, D, _p(q.values), _p(k.values), _p(v.values), _p(grad_out.values),
@@ -538,6 +575,9 @@ def feature_interaction(k_feat: JaggedTensor, v_feat: JaggedTensor, targets: tor
     """
     if not (k_feat.same_offsets(v_feat) and k_feat.dim == v_feat.dim):
         raise JaggedError("feature_interaction: k_feat/v_feat layout mismatch")
+    _operands("feature_interaction", k_feat.values, v_feat.values)
+    if not targets.is_cuda or targets.device != k_feat.values.device:
+        raise JaggedError("feature_interaction: operands must be CUDA tensors on one device")
     if targets.dim() != 3 or targets.shape[0] != k_feat.batch or targets.shape[2] != k_feat.dim:
         raise JaggedError("feature_interaction: targets must be [B, Tq, D]")
     targets = targets.contiguous().to(k_feat.values.dtype)
@@ -589,6 +629,9 @@ def _validate_mlp(x: JaggedTensor, layers) -> None:
 
 
 def _mlp_forward(x: JaggedTensor, layers, keep: bool):
+    for L in layers:
+        if not (L.weights.is_cuda and L.bias.is_cuda) or L.weights.device != x.values.device:
+            raise JaggedError("jagged_mlp: weights and bias must be CUDA tensors on the input's device")
     acts, pres = [x.values], []
     cur = x.values
     for L in layers:
