@@ -200,7 +200,7 @@ def run_ours(args, rank, world, local_rank):
     Q, K, V, G = T(q), T(k), T(v), T(go)
     sched = J.Schedule(Q)
     lib = _lib.lib()
-    ws = torch.empty(lib.jg_attention_backward_workspace_size(S, H, D), dtype=torch.uint8, device=dev)
+    ws = torch.empty(J.backward_workspace_size(Q), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
     def step(evs=None):
@@ -450,7 +450,7 @@ def run_configs(args):
                 "fwd_graph_ms": ms_fg, "fwd_graph_tflops": fwd_fl / (ms_fg * 1e-3) / 1e12 if ms_fg else None}
         total_fl, total_ms = fwd_fl, ms_f
         if not fwd_only:
-            ws = torch.empty(lib.jg_attention_backward_workspace_size(S, H, D), dtype=torch.uint8, device=dev)
+            ws = torch.empty(J.backward_workspace_size(Q), dtype=torch.uint8, device=dev)
             ms_b = _events_time(lambda: J.jagged_flash_attention_backward(Q, K, V, G, saved, schedule=sched,
                                                                           workspace=ws), args.steps, args.warmup)
             line.update(bwd_ms=ms_b, bwd_tflops=bwd_fl / (ms_b * 1e-3) / 1e12)
@@ -516,7 +516,7 @@ def run_configs(args):
         fwd_fl, bwd_fl, _ = useful_flops(ln, H, D)
         Q, K, V, G = (J.JaggedTensor(torch.from_numpy(off).to(dev), rnd(S, H, D), off) for _ in range(4))
         sched = J.Schedule(Q)
-        ws = torch.empty(lib.jg_attention_backward_workspace_size(S, H, D), dtype=torch.uint8, device=dev)
+        ws = torch.empty(J.backward_workspace_size(Q), dtype=torch.uint8, device=dev)
 
         def jagged_step():
             s_ = J.jagged_flash_attention_forward(Q, K, V, schedule=sched)
@@ -552,7 +552,7 @@ def run_configs(args):
             o_ = torch.nn.functional.scaled_dot_product_attention(q_, k_, v_, attn_mask=keymask[:, None, None, :])
             o_.backward(gp)
 
-        ws_p = torch.empty(lib.jg_attention_backward_workspace_size(B * L, H, D), dtype=torch.uint8, device=dev)
+        ws_p = torch.empty(lib.jg_attention_backward_workspace_size(B * L, B, H, D), dtype=torch.uint8, device=dev)
 
         def padded_ours_step():  # the same kernels in padded mode (full L^2 work, masks)
             s_ = J.dense_flash_attention(qd, kd, vd, ln)

@@ -470,7 +470,7 @@ AttentionGrads<T> jagged_flash_attention_backward(const JaggedTensor<T>& q, cons
       dk(sizeof(T) * k.values().size(), op), dv(sizeof(T) * v.values().size(), op);
   ck(op, jg_jagged_flash_attention_backward((const int64_t*)off.p, q.batch(), S, 1, (int32_t)q.dim(), dq_in.p, dk_in.p,
                                             dv_in.p, dgo.p, dout.p, (const float*)dlse.p, saved.block_q, saved.block_k,
-                                            dq.p, dk.p, dv.p, JG_F32, nullptr, nullptr, 0));
+                                            dq.p, dk.p, dv.p, JG_F32, 1, nullptr, nullptr, 0));
   return {JaggedTensor<T>(q.offsets(), dq.to<T>(q.values().size(), op), q.dim()),
           JaggedTensor<T>(k.offsets(), dk.to<T>(k.values().size(), op), k.dim()),
           JaggedTensor<T>(v.offsets(), dv.to<T>(v.values().size(), op), v.dim())};

@@ -171,15 +171,22 @@ jg_status jg_jagged_flash_attention_forward(const int64_t* offsets, int64_t batc
                                             void* out, float* lse, jg_dtype dtype,
                                             jg_schedule sched, void* stream);
 /* attention.hpp:82-88 jagged_flash_attention_backward: recompute from (q, k, lse).
- * workspace: NULL or >= jg_attention_backward_workspace_size() bytes of device memory. */
+ * deterministic != 0 (the default of every wrapper): bit-identical gradients across runs, grid sizes and
+ * schedules (the reference's fixed summation order, attention.cpp:252-254). The
+ * tcgen05 kernel then accumulates the key tiles' partial dQ in 64-bit fixed point (2^-32 units; integer
+ * adds are order-independent); 0 selects fp32 accumulation, whose last bits depend on the order in which
+ * key tiles finish. The SIMT path is sequential per key and deterministic either way.
+ * workspace: NULL or >= jg_attention_backward_workspace_size(total_rows, batch, ...) bytes of device
+ * memory. A schedule (and a workspace) must not be shared by two concurrently running calls. */
 jg_status jg_jagged_flash_attention_backward(const int64_t* offsets, int64_t batch,
                                              int64_t total_rows, int32_t num_heads,
                                              int32_t head_dim, const void* q, const void* k,
                                              const void* v, const void* grad_out, const void* out,
                                              const float* lse, int64_t block_q, int64_t block_k,
                                              void* dq, void* dk, void* dv, jg_dtype dtype,
-                                             jg_schedule sched, void* workspace, void* stream);
-int64_t jg_attention_backward_workspace_size(int64_t total_rows, int32_t num_heads,
+                                             int32_t deterministic, jg_schedule sched,
+                                             void* workspace, void* stream);
+int64_t jg_attention_backward_workspace_size(int64_t total_rows, int64_t batch, int32_t num_heads,
                                              int32_t head_dim);
 /* attention.hpp:55-58 dense_flash_attention (attention.cpp:106-160), GPU padded mode of the same tcgen05 /
  * SIMT kernels: q/k/v/out are padded [batch, max_len, num_heads, head_dim]; `lengths` is a
@@ -194,7 +201,7 @@ jg_status jg_dense_flash_attention_forward(const int64_t* lengths, int64_t batch
                                            void* stream);
 /* Backward of the padded mode (no reference counterpart; used for the padded-vs-jagged training-step
  * comparison): rows past a sample's length get zero dq/dk/dv. workspace: NULL or
- * >= jg_attention_backward_workspace_size(batch * max_len, num_heads, head_dim) bytes. */
+ * >= jg_attention_backward_workspace_size(batch * max_len, batch, num_heads, head_dim) bytes. */
 jg_status jg_dense_flash_attention_backward(const int64_t* lengths, int64_t batch, int64_t max_len,
                                             int32_t num_heads, int32_t head_dim, const void* q,
                                             const void* k, const void* v, const void* grad_out,

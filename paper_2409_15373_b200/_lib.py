@@ -45,8 +45,8 @@ SIGNATURES = {
     "jg_array_jagged_bmm_jagged_out_vjp": [P, P, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
     "jg_jagged2_softmax_vjp": [P, P, I64, P, P, P, C.c_int, P],
     "jg_jagged_flash_attention_forward": [P, I64, I64, I32, I32, P, P, P, I64, I64, P, P, C.c_int, P, P],
-    "jg_jagged_flash_attention_backward": [P, I64, I64, I32, I32, P, P, P, P, P, P, I64, I64, P, P, P, C.c_int, P,
-                                           P, P],
+    "jg_jagged_flash_attention_backward": [P, I64, I64, I32, I32, P, P, P, P, P, P, I64, I64, P, P, P, C.c_int, I32,
+                                           P, P, P],
     "jg_jagged_attention": [P, P, I64, I64, I64, I32, I32, P, P, P, P, C.c_int, P, P],
     "jg_dense_flash_attention_forward": [P, I64, I64, I32, I32, P, P, P, I64, I64, P, P, C.c_int, P],
     "jg_dense_flash_attention_backward": [P, I64, I64, I32, I32, P, P, P, P, P, P, I64, I64, P, P, P, C.c_int, P, P],
@@ -61,7 +61,7 @@ OTHER = {
     "jg_launch_count": ([], C.c_int64),
     "jg_reset_launch_count": ([], None),
     "jg_schedule_sq_offsets": ([P], P),
-    "jg_attention_backward_workspace_size": ([I64, I32, I32], C.c_int64),
+    "jg_attention_backward_workspace_size": ([I64, I64, I32, I32], C.c_int64),
     "jg_feature_interaction_workspace_size": ([I64, I64], C.c_int64),
 }
 

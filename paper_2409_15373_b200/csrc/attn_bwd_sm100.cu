@@ -5,17 +5,29 @@
 // dQ = dS K / sqrt(D), dK = dS^T Q / sqrt(D). Per segment only; no padding materialised.
 //
 // Three launches:
-//   1. prologue: Delta[h, r] = sum_d dO*O (fp32) and zero the fp32 dQ accumulator        (HBM-bound)
+//   1. prologue: Delta[h, r] = sum_d dO*O (fp32) and zero the dQ accumulator             (HBM-bound)
 //   2. main persistent kernel, key-stationary: a CTA owns 128 key rows of one (sample, head) and
 //      streams the sample's queries in 64-row blocks:
 //        S^T = K Q_j^T, dP^T = V dO_j^T                      (tcgen05, M=128 keys, N=64 queries)
 //        P^T (bf16) back into TMEM over S^T, dS^T -> smem      (softmax warps, thread = key row)
 //        dV += P^T dO_j (TS: A = P^T from TMEM), dK += dS^T Q_j   (accumulated in TMEM across all j)
 //        dQ_j^T = K^T dS^T                                    (M = head_dim, N = 64 queries)
-//      dQ_j^T is drained by a second warpgroup through smem and added into the fp32 accumulator with
-//      four TMA tensor reduce-adds per block (cp.reduce.async.bulk.tensor .add, [16 q x D] fp32 boxes,
-//      two alternating staging buffers). Work items are taken dynamically in LPT order.
-//   3. epilogue: dQ (bf16) = fp32 accumulator                                             (HBM-bound)
+//      dQ_j^T is drained by a second warpgroup through smem and added into the accumulator with TMA
+//      tensor reduce-adds (cp.reduce.async.bulk.tensor .add, two alternating staging buffers). The key tiles of
+//      a sample add into one query block in whatever order they finish, so:
+//        deterministic (default, the reference's fixed order attention.cpp:252-254): each
+//          partial is first rounded to a per-head grid u_h (a power of two) with one FFMA2 against a magic
+//          constant, so every fp32 add of the reduction is EXACT — multiples of u_h summing to less than
+//          2^24 u_h — and the result is bit-identical for every arrival order, grid and schedule. u_h comes
+//          from a rigorous bound on every partial sum: |sum_{k in any key subset} dS_qk K_kd| / sqrt(D)
+//          <= 2 max|K| max||V|| max||dO|| / sqrt(D) = T_h (|dS_qk| <= P_qk 2 ||dO_q|| max||V||, sum_k P_qk = 1);
+//          with B = 2 T_h in [2^e, 2^(e+1)), u_h = 2^(e-22): |partials| <= T_h < 2^22 u_h (the magic rounding's
+//          range) and |sums| < 2^24 u_h. The per-head maxima come from the prologue (which then also reads K
+//          and V). The rounding error, at most u_h / 2 per key tile, is ~2^-24 of the head's dQ bound;
+//        fast: plain fp32 adds, order-dependent rounding in the last bits.
+//      Both reduce fp32 [16 q x D] boxes (the same HBM/L2 traffic and convert pass).
+//      Work items are taken dynamically in LPT order.
+//   3. epilogue: dQ (bf16) = accumulator                                                 (HBM-bound)
 // Warps: 0 TMA producer, 1-2 MMA issuers, 4-11 softmax/dS (two warps per TMEM lane
 // quarter, 32 query columns each), 12-15 dQ drain + dK/dV epilogue.
 // TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); P^T_j is written over the S^T
@@ -44,8 +56,17 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 constexpr int kQdStages = JG_BWD_QD_STAGES;  // (Q_j, dO_j) smem ring depth (4 on cfg3; 3 frees room for 4 dQ staging buffers)
 constexpr int kPdsBufs = 1;   // dS^T smem buffers
+// deterministic dQ: the magic constant 1.5 * 2^23 * u of the grid u = 2^(e - 22), B in [2^e, 2^(e+1)) the bound
+// (see the header): fma(x, scale, M) - M rounds x * scale to a multiple of u. Degenerate bounds give 0 (B = 0:
+// dQ is exactly 0; not finite: no rounding).
+__device__ __forceinline__ float grid_magic(float bound) {
+  if (!(bound > 0.f) || !(bound <= 1.0e37f)) return 0.f;
+  int e = (int)((__float_as_uint(bound) >> 23) & 0xff) + 1;  // biased exponent of 2^(e + 1), M = 1.5 * 2^(e + 1)
+  if (e < 2) e = 2;                                            // (denormal bounds: the smallest normal grid)
+  return __uint_as_float(((unsigned)e << 23) | 0x400000u);
+}
 
-template <int D>
+template <int D, bool DET = false>
 struct Smem {
   static constexpr int kChunkKV = BKV * 128;  // [128 rows x 64] bf16 = 16 KB
   static constexpr int kChunkQ = BQ * 128;    // [64 rows x 64] bf16 = 8 KB
@@ -56,17 +77,22 @@ struct Smem {
   static constexpr int kV = kK + kTileKV;
   static constexpr int kQD = kV + kTileKV;                  // stages of (Q_j, dO_j)
   static constexpr int kDS = kQD + kStages * 2 * kTileQ;    // kPdsBufs x dS^T [128 keys x 64 q] bf16 (P^T is in TMEM)
-  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging: kStgBufs x [kStgRows q x D] fp32
-  static constexpr int kStgRows = 16;                       // dQ rows per TMA reduce (four per block)
+  static constexpr int kStg = kDS + kPdsBufs * BKV * 128;   // dQ staging: kStgBufs x [kStgRows q x D] fp32 | int64
+  static constexpr int kAccBytes = 4;                       // fp32 accumulator element
+  static constexpr int kStgRows = 16;                       // dQ rows per TMA reduce (four per block; 8-row boxes
+                                                            // measured slower: the TMA op rate binds)
   static constexpr int kStgBufs = kQdStages > 3 ? 2 : 4;    // fill one while the TMA reads the others
   static constexpr int kLsdBytes = 2 * BQ * 4;              // per stage: 64 -lse*log2(e) + 64 -Delta, fp32
   // the dK/dV epilogue reuses the staging region as four 4 KB warp slices (32 rows x 128 B)
-  static constexpr int kStgBytes = kStgBufs * kStgRows * D * 4 > 4 * 4096 ? kStgBufs * kStgRows * D * 4 : 4 * 4096;
+  static constexpr int kStgBytes = kStgBufs * kStgRows * D * kAccBytes > 4 * 4096 ? kStgBufs * kStgRows * D * kAccBytes
+                                                                                 : 4 * 4096;
   static constexpr int kLse = kStg + kStgBytes;  // kStages x kLsdBytes, loaded with (Q_j, dO_j)
   static constexpr int kBar = kLse + kStages * kLsdBytes;
   static constexpr int kNumBars = 4 + 2 * kStages + 4 + 1 + kPdsBufs + 4 + 2 + 2 * kItemSlots;
   static constexpr int kItemRing = (kBar + kNumBars * 8 + 16 + 15) & ~15;  // kItemSlots x 32-byte descriptors
-  static constexpr int kBytes = kItemRing + kItemSlots * 32;
+  static constexpr int kMaxMagicHeads = 64;                   // deterministic: per-head magic constants in smem
+  static constexpr int kMagic = kItemRing + kItemSlots * 32;
+  static constexpr int kBytes = kMagic + (DET ? kMaxMagicHeads * 4 : 0);
   // no alignment slack: the dynamic smem base is 1024-aligned (declared so; checked at kernel entry)
   static constexpr int kAlloc = kBytes;
   static_assert(kAlloc <= 232448, "exceeds the 227 KB dynamic shared memory limit");
@@ -78,8 +104,9 @@ struct Params {
   const int64_t* n_items;
   int64_t total_rows;
   int H;
-  const float* lsd;  // [2][H][total_rows]: lse * log2(e), Delta (written by the prologue)
-  float* dq_acc;
+  const float* lsd;  // [2][H][total_rows]: -lse * log2(e), -Delta (written by the prologue), then [3][H] max|K|,
+                     // max||V||^2, max||dO||^2 per head (deterministic mode)
+  void* dq_acc;  // fp32 [total_rows, H, D]
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   float scale_log2;
@@ -104,6 +131,10 @@ __device__ __forceinline__ void tensor_reduce_add_3d(const CUtensorMap* map, uin
                "r"(ssrc), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// the grid magic of head h: B = 4 max|K| max||V|| max||dO|| / sqrt(D) (kvb = [3][H] max|K|, max||V||^2, max||dO||^2)
+__device__ __forceinline__ float head_magic(const float* kvb, int H, int h, float inv_sqrt_d) {
+  return grid_magic(4.f * kvb[h] * sqrtf(kvb[H + h]) * sqrtf(kvb[2 * H + h]) * inv_sqrt_d);
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 template <int N>
@@ -111,12 +142,12 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 
-template <int D>
+template <int D, bool DET>
 __global__ void __launch_bounds__(kThreads, 1)
     jfa_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_dq, Params p) {
-  using L = Smem<D>;
+  using L = Smem<D, DET>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (tc::smem_u32(smem) & 1023) != 0) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
@@ -496,16 +527,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     wp.init(tid == 0 ? p.prof : nullptr, 24);
     const long long t_role = clock64();
     Work wk;
+    const float* kvb = p.lsd + 2 * (int64_t)H * p.total_rows;  // deterministic: per-head maxima
+    const uint32_t magic_s = tc::smem_u32(smem + L::kMagic);
+    if (DET && H <= L::kMaxMagicHeads) {
+      for (int hh = tid; hh < H; hh += 128) tc::st_shared_f32(magic_s + hh * 4, head_magic(kvb, H, hh, p.scale));
+      named_bar(2, 128);
+    }
     for (bool more = take_item(item_cnt, wk); more; more = take_item(++item_cnt, wk)) {
       const int2 it = wk.it;
       const int h = wk.h;
       const int64_t b0 = wk.b0, n = wk.n;
       const int nq = (int)((n + BQ - 1) / BQ);
+      const float mgc = !DET ? 0.f : (H <= L::kMaxMagicHeads ? tc::ld_shared_f32(magic_s + h * 4) : head_magic(kvb, H, h, p.scale));
       for (int j = 0; j < nq; ++j) {
         const int b = j & 1;
         wp.wait_warp(dq_full + b, (dq_par >> b) & 1, 0);
         dq_par ^= 1u << b;
         tc::tc_fence_after();
+        const long long t_ld = clock64();
         uint32_t a[32], c2[32];
         tc::tmem_ld32(lane_addr + b * 128 + 64, a);
         tc::tmem_ld32(lane_addr + b * 128 + 96, c2);
@@ -513,21 +552,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(dq_empty + b);
-        // four [16 q x D] fp32 boxes through two alternating staging buffers, one TMA tensor reduce-add each
-        // (the drain fills one buffer while the TMA unit reads the other); rows of padded queries are exactly
-        // zero (P = 0 there), so adding them into the next sample's rows is a no-op
+        wp.add(6, clock64() - t_ld);
+        // [kStgRows q x D] boxes through two alternating staging buffers, one TMA tensor reduce-add each (the
+        // drain fills one buffer while the TMA unit reads the other); rows of padded queries are exactly zero
+        // (P = 0 there), so adding them into the next sample's rows is a no-op
         static_assert((BQ / L::kStgRows) % L::kStgBufs == 0, "buffer index must be static per sub-block");
 #pragma unroll
         for (int hh = 0; hh < BQ / L::kStgRows; ++hh) {
-          const uint32_t sb = stg_base + (hh % L::kStgBufs) * (L::kStgRows * D * 4);
+          const uint32_t sb = stg_base + (hh % L::kStgBufs) * (L::kStgRows * D * L::kAccBytes);
           const long long tb = clock64();
           if (tid == 0) bulk_wait_read<L::kStgBufs - 1>();  // the reduction issued from this buffer has read it
           named_bar(2, 128);
           wp.add(1, clock64() - tb);
 #pragma unroll
-          for (int q = 0; q < L::kStgRows; ++q) {
+          for (int q = 0; q < L::kStgRows; q += 2) {  // two rows per paired FFMA2 (+ FADD2 in deterministic mode)
             const int qq = hh * L::kStgRows + q;
-            if (tid < D) tc::st_shared_f32(sb + (q * D + tid) * 4, __uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]) * p.scale);
+            const float2 v = make_float2(__uint_as_float(qq < 32 ? a[qq & 31] : c2[qq & 31]),
+                                         __uint_as_float(qq + 1 < 32 ? a[(qq + 1) & 31] : c2[(qq + 1) & 31]));
+            float2 x = tc::ffma2(v, make_float2(p.scale, p.scale), make_float2(mgc, mgc));
+            if constexpr (DET) x = tc::fadd2(x, make_float2(-mgc, -mgc));  // exact: x on the head's grid
+            if (tid < D) {
+              tc::st_shared_f32(sb + (q * D + tid) * 4, x.x);
+              tc::st_shared_f32(sb + ((q + 1) * D + tid) * 4, x.y);
+            }
           }
           tc::fence_proxy_async_smem();
           named_bar(2, 128);
@@ -608,34 +655,46 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::cta_time_mark(p.prof, 1);
 }
 
-// Delta = rowsum(dO * O) per (row, head), zero the fp32 dQ accumulator (one warp per unit), and write
-// -lse*log2(e) and -Delta into lsd[2][H][total_rows] (staged per query block by the main kernel's producer
-// with cp.async; negated so the softmax needs one paired FFMA2 / FADD2 per two scores).
+// Delta = rowsum(dO * O) per (row, head), zero the dQ accumulator, and write -lse*log2(e) and -Delta into
+// lsd[2][H][total_rows] (staged per query block by the main kernel's producer with cp.async; negated so the
+// softmax needs one paired FFMA2 / FADD2 per two scores). Deterministic mode (DET) also reads K and V for the
+// per-head maxima max|K|, max||V||^2 and max||dO||^2 (lsd tail [3][H], zeroed before the launch) that bound the
+// grid-rounded dQ partials.
 #ifndef JG_PRO_LD
 #define JG_PRO_LD __ldcs
 #endif
-template <int D>
+template <int D, bool DET>
 __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* __restrict__ go,
-                                                           const __nv_bfloat16* __restrict__ o, int64_t units,
+                                                           const __nv_bfloat16* __restrict__ o,
+                                                           const __nv_bfloat16* __restrict__ kk,
+                                                           const __nv_bfloat16* __restrict__ vv, int64_t units,
                                                            int H, int64_t total_rows, const float* __restrict__ lse,
-                                                           float* __restrict__ lsd,
-                                                           float* __restrict__ dq_acc) {
+                                                           float* __restrict__ lsd, void* __restrict__ dq_acc) {
   // LPU lanes per (row, head) unit, 16 bytes of dO and of O per lane; a warp covers UPW units per step and
   // unrolls two steps with every load issued before the reductions (the streaming read is latency-bound
   // with one dependent unit per warp)
   constexpr int LPU = D / 8, UPW = 32 / LPU, kUnroll = 2;
+  extern __shared__ unsigned kv_max[];  // DET: [3][H] block-local max|K|, max||V||^2, max||dO||^2 (float bits, >= 0)
+  if (DET) {
+    for (int i = threadIdx.x; i < 3 * H; i += blockDim.x) kv_max[i] = 0u;
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, sub = lane / LPU, li = lane % LPU;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (UPW * kUnroll); u0 < units;
        u0 += warps * UPW * kUnroll) {
-    uint4 a[kUnroll], b[kUnroll];
+    uint4 a[kUnroll], b[kUnroll], ka[kUnroll], va[kUnroll];
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t u = u0 + k * UPW + sub;
-      a[k] = b[k] = make_uint4(0u, 0u, 0u, 0u);
+      a[k] = b[k] = ka[k] = va[k] = make_uint4(0u, 0u, 0u, 0u);
       if (u < units) {
         a[k] = JG_PRO_LD(reinterpret_cast<const uint4*>(go + u * D) + li);  // streamed once
         b[k] = JG_PRO_LD(reinterpret_cast<const uint4*>(o + u * D) + li);
+        if (DET) {
+          ka[k] = __ldg(reinterpret_cast<const uint4*>(kk + u * D) + li);  // the main kernel reads K, V next
+          va[k] = __ldg(reinterpret_cast<const uint4*>(vv + u * D) + li);
+        }
       }
     }
 #pragma unroll
@@ -643,24 +702,50 @@ __global__ void __launch_bounds__(256) bwd_prologue_kernel(const __nv_bfloat16* 
       const int64_t u = u0 + k * UPW + sub;
       const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a[k]);
       const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b[k]);
-      float acc = 0.f;
+      float acc = 0.f, nn = 0.f, km = 0.f, vn = 0.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 x = __bfloat1622float2(ha[e]), y = __bfloat1622float2(hb[e]);
         acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+        if (DET) {
+          nn = fmaf(x.x, x.x, fmaf(x.y, x.y, nn));
+          const float2 kx = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&ka[k])[e]);
+          const float2 vx = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&va[k])[e]);
+          km = fmaxf(km, fmaxf(fabsf(kx.x), fabsf(kx.y)));
+          vn = fmaf(vx.x, vx.x, fmaf(vx.y, vx.y, vn));
+        }
       }
 #pragma unroll
-      for (int m = LPU / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+      for (int m = LPU / 2; m > 0; m >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, m);
+        if (DET) {
+          nn += __shfl_xor_sync(0xffffffffu, nn, m);
+          km = fmaxf(km, __shfl_xor_sync(0xffffffffu, km, m));
+          vn += __shfl_xor_sync(0xffffffffu, vn, m);
+        }
+      }
       if (u < units) {
-        // 8 fp32 zeros per lane: one 32-byte sector store
-        tc::st_global_v8(dq_acc + u * D + li * 8, make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u));
+        // 8 fp32 / int32 zeros per lane: one 32-byte sector store
+        tc::st_global_v8(reinterpret_cast<float*>(dq_acc) + u * D + li * 8, make_uint4(0u, 0u, 0u, 0u),
+                         make_uint4(0u, 0u, 0u, 0u));
         if (li == 0) {
           const int64_t r = u / H, h = u - r * H;
           lsd[h * total_rows + r] = -lse[h * total_rows + r] * kLog2e;  // negated: one FFMA2 per pair downstream
           lsd[(H + h) * total_rows + r] = -acc;
+          if (DET) {
+            atomicMax(kv_max + h, __float_as_uint(km));
+            atomicMax(kv_max + H + h, __float_as_uint(vn));
+            atomicMax(kv_max + 2 * H + h, __float_as_uint(nn));
+          }
         }
       }
     }
+  }
+  if (DET) {
+    __syncthreads();
+    unsigned* g = reinterpret_cast<unsigned*>(lsd + 2 * (int64_t)H * total_rows);
+    for (int i = threadIdx.x; i < 3 * H; i += blockDim.x)
+      if (kv_max[i]) atomicMax(g + i, kv_max[i]);
   }
 }
 
@@ -679,16 +764,19 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict
 
 bool attn_sm100_bwd_supported(int head_dim, jg_dtype dt) { return dt == JG_BF16 && (head_dim == 128 || head_dim == 64); }
 
-template <int kD>
+template <int kD, bool kDet>
 static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
                             const void* go, const void* o, const float* lse, void* dq, void* dk, void* dv,
-                            float* delta, float* dq_acc, const int2* items, const int64_t* n_items, int64_t max_items,
+                            float* delta, void* dq_acc, const int2* items, const int64_t* n_items, int64_t max_items,
                             const int64_t* valid, unsigned long long* counters, cudaStream_t st) {
-  using L = fb::Smem<kD>;
+  using L = fb::Smem<kD, kDet>;
   const int sms = device_sm_count();
   const int64_t units = total_rows * H;
-  fb::bwd_prologue_kernel<kD><<<(int)std::min<int64_t>((units + 8 * (256 / kD) * 2 - 1) / (8 * (256 / kD) * 2), 32 * sms), 256, 0, st>>>(
-      (const __nv_bfloat16*)go, (const __nv_bfloat16*)o, units, H, total_rows, lse, delta, dq_acc);
+  if (kDet) JG_CUDA(cudaMemsetAsync(delta + 2 * (int64_t)H * total_rows, 0, 3 * H * sizeof(float), st));
+  fb::bwd_prologue_kernel<kD, kDet><<<(int)std::min<int64_t>((units + 8 * (256 / kD) * 2 - 1) / (8 * (256 / kD) * 2), 32 * sms), 256,
+                                      kDet ? 3 * H * sizeof(unsigned) : 0, st>>>(
+      (const __nv_bfloat16*)go, (const __nv_bfloat16*)o, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, units, H,
+      total_rows, lse, delta, dq_acc);
   JG_LAUNCHED("bwd_prologue_kernel");
   CUtensorMap mq, mk, mv, mdo;
   if (jg_status rc = make_map(&mq, q, total_rows, H, kD, fb::BQ)) return rc;
@@ -696,14 +784,18 @@ static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const
   if (jg_status rc = make_map(&mv, v, total_rows, H, kD, fb::BKV)) return rc;
   if (jg_status rc = make_map(&mdo, go, total_rows, H, kD, fb::BQ)) return rc;
   CUtensorMap mdq;
-  if (jg_status rc = make_map_f32(&mdq, dq_acc, total_rows, H, kD, L::kStgRows)) return rc;
-  if (jg_status rc = ensure_smem_attr((const void*)fb::jfa_bwd_sm100_kernel<kD>, L::kAlloc, "jfa_bwd_sm100_kernel"))
+  if (jg_status rc = make_map_f32(&mdq, dq_acc, total_rows, H, kD, L::kStgRows))
+    return rc;
+  if (jg_status rc = ensure_smem_attr((const void*)fb::jfa_bwd_sm100_kernel<kD, kDet>, L::kAlloc, "jfa_bwd_sm100_kernel"))
     return rc;
   fb::Params p{off, items, n_items, total_rows, H, delta, dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                1.4426950408889634f / sqrtf((float)kD), 1.0f / sqrtf((float)kD), std::getenv("JG_BWD_DBG") ? std::atoi(std::getenv("JG_BWD_DBG")) : 0,
                counters, wait_prof_begin(st), valid};
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, max_items * H));
-  if (!(p.dbg & 64)) fb::jfa_bwd_sm100_kernel<kD><<<grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
+  int64_t grid = std::min<int64_t>(sms, max_items * H);
+  // JG_BWD_MAX_CTAS (tests): a smaller persistent grid changes which CTA runs which item and when
+  if (const char* cap = std::getenv("JG_BWD_MAX_CTAS")) grid = std::min<int64_t>(grid, std::atoi(cap));
+  grid = std::max<int64_t>(1, grid);
+  if (!(p.dbg & 64)) fb::jfa_bwd_sm100_kernel<kD, kDet><<<(int)grid, fb::kThreads, L::kAlloc, st>>>(mq, mk, mv, mdo, mdq, p);
   if (p.dbg & 128) {
     cudaError_t e = cudaStreamSynchronize(st);
     std::fprintf(stderr, "[bwd dbg] main kernel: %s\n", cudaGetErrorString(e));
@@ -712,26 +804,28 @@ static jg_status bwd_launch(const int64_t* off, int64_t total_rows, int H, const
   wait_prof_end(p.prof, st, "bwd",
                 {"P.k_empty", "P.qd_empty", "P.v_empty", "P.item_empty", "", "", "", "P.total", "M.k_full", "M.v_full", "M.qd_full",
                  "M.pt_free", "M.dq_empty", "", "", "M.total", "S.qd_full", "S.st_full", "S.pds_empty", "",
-                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "D.epi_read0", "D.epi_tmem", "D.epi_out", "", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
+                 "", "", "", "S.total", "D.dq_full", "D.stage_bar", "D.dkv_full", "D.epi_read0", "D.epi_tmem", "D.epi_out", "D.tmem_ld", "D.total", "G.unused", "G.dkv_empty", "", "", "", "G.p_full", "", "G.total"});
   const int64_t n4 = units * kD / 4;
-  fb::dq_convert_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 32 * sms), 256, 0, st>>>(dq_acc, (__nv_bfloat16*)dq,
-                                                                                          n4);
+  const int cgrid = (int)std::min<int64_t>((n4 + 255) / 256, 32 * sms);
+  fb::dq_convert_kernel<<<cgrid, 256, 0, st>>>((const float*)dq_acc, (__nv_bfloat16*)dq, n4);
   JG_LAUNCHED("dq_convert_kernel");
   return JG_OK;
 }
 
 jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                                 const void* k, const void* v, const void* go, const void* o, const float* lse,
-                                void* dq, void* dk, void* dv, float* delta, float* dq_acc, const int2* items,
-                                const int64_t* n_items, int64_t max_items, const int64_t* valid,
+                                void* dq, void* dk, void* dv, float* delta, void* dq_acc, bool deterministic,
+                                const int2* items, const int64_t* n_items, int64_t max_items, const int64_t* valid,
                                 unsigned long long* counters, cudaStream_t st) {
   (void)batch;
-  if (D == 128)
-    return bwd_launch<128>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items, max_items,
-                           valid, counters, st);
-  if (D == 64)
-    return bwd_launch<64>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items, max_items,
-                          valid, counters, st);
+#define JG_BWD(DD, DET)                                                                                              \
+  return bwd_launch<DD, DET>(off, total_rows, H, q, k, v, go, o, lse, dq, dk, dv, delta, dq_acc, items, n_items,   \
+                             max_items, valid, counters, st)
+  if (D == 128 && deterministic) JG_BWD(128, true);
+  if (D == 128) JG_BWD(128, false);
+  if (D == 64 && deterministic) JG_BWD(64, true);
+  if (D == 64) JG_BWD(64, false);
+#undef JG_BWD
   return fail(JG_UNSUPPORTED, "tcgen05 attention backward: head_dim must be 64 or 128");
 }
 

@@ -446,10 +446,12 @@ static bool force_simt() {
   return e && std::strcmp(e, "simt") == 0;
 }
 
-extern "C" int64_t jg_attention_backward_workspace_size(int64_t total_rows, int32_t num_heads, int32_t head_dim) {
+static int64_t round256(int64_t x) { return (x + 255) / 256 * 256; }
+extern "C" int64_t jg_attention_backward_workspace_size(int64_t total_rows, int64_t batch, int32_t num_heads,
+                                                        int32_t head_dim) {
   const int64_t delta = attn_lsd_bytes(total_rows, num_heads);  // >= the SIMT path's [H, total_rows] Delta
-  const int64_t acc = total_rows * num_heads * (int64_t)head_dim * 4;
-  return delta + acc + 256;
+  (void)batch;  // (kept in the signature: layouts sized per sample stay possible without an ABI change)
+  return delta + round256(total_rows * num_heads * (int64_t)head_dim * 4) + 256;  // fp32 / int32 accumulator
 }
 
 // Shared by the jagged entry points (valid == nullptr) and the padded dense_flash_attention mode (valid =
@@ -487,17 +489,18 @@ static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_r
 
 static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_rows, int32_t H, int32_t D,
                                const void* q, const void* k, const void* v, const void* go, const void* o,
-                               const float* lse, void* dq, void* dk, void* dv, jg_dtype dtype, jg_schedule sched,
-                               void* workspace, const int64_t* valid, cudaStream_t st) {
+                               const float* lse, void* dq, void* dk, void* dv, jg_dtype dtype, bool deterministic,
+                               jg_schedule sched, void* workspace, const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
   if (jg_status rc = check_schedule("jagged_flash_attention_backward", sched, off, batch, total_rows)) return rc;
   Scratch ws(st);
   if (!workspace) {
-    if (jg_status rc = ws.alloc(jg_attention_backward_workspace_size(total_rows, H, D))) return rc;
+    if (jg_status rc = ws.alloc(jg_attention_backward_workspace_size(total_rows, batch, H, D))) return rc;
     workspace = ws.p;
   }
   float* delta = (float*)workspace;
-  float* dq_acc = (float*)((char*)workspace + attn_lsd_bytes(total_rows, H));
+  void* dq_acc = (char*)workspace + attn_lsd_bytes(total_rows, H);
+
   if (!force_simt() && attn_sm100_bwd_supported(D, dtype)) {
     jg_schedule own = nullptr;
     if (!sched) {
@@ -505,7 +508,7 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
       sched = own;
     }
     jg_status rc = launch_attn_bwd_sm100(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta,
-                                         dq_acc, sched->items, sched->n_items, sched->max_items, valid,
+                                         dq_acc, deterministic, sched->items, sched->n_items, sched->max_items, valid,
                                          sched->counters + 2, st);
     if (own) {
       schedule_release(own, st);
@@ -531,14 +534,15 @@ extern "C" jg_status jg_jagged_flash_attention_backward(const int64_t* off, int6
                                                         int32_t H, int32_t D, const void* q, const void* k,
                                                         const void* v, const void* go, const void* o,
                                                         const float* lse, int64_t block_q, int64_t block_k, void* dq,
-                                                        void* dk, void* dv, jg_dtype dtype, jg_schedule sched,
-                                                        void* workspace, void* stream) {
+                                                        void* dk, void* dv, jg_dtype dtype, int32_t deterministic,
+                                                        jg_schedule sched, void* workspace, void* stream) {
   CHECK_DT("jagged_flash_attention_backward", dtype);
   REQUIRE(block_q >= 1 && block_k >= 1, JG_INVALID_ARGUMENT,
           "jagged_flash_attention_backward: saved state does not match inputs");
   REQUIRE(H >= 1 && D >= 1, JG_INVALID_ARGUMENT, "jagged_flash_attention_backward: grad_out layout mismatch");
   REQUIRE_PTRS("jagged_flash_attention_backward", total_rows > 0, off, q, k, v, go, o, lse, dq, dk, dv);
-  return attn_backward(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, sched, workspace,
+  return attn_backward(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, deterministic != 0, sched,
+                       workspace,
                        nullptr, as_stream(stream));
 }
 
@@ -607,7 +611,7 @@ extern "C" jg_status jg_dense_flash_attention_backward(const int64_t* lengths, i
   const int64_t *d_off = nullptr, *d_valid = nullptr;
   if (jg_status rc = padded_layout("dense_flash_attention_backward", lengths, batch, max_len, buf, &d_off, &d_valid))
     return rc;
-  return attn_backward(d_off, batch, batch * max_len, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, nullptr,
+  return attn_backward(d_off, batch, batch * max_len, H, D, q, k, v, go, o, lse, dq, dk, dv, dtype, true, nullptr,
                        workspace, d_valid, st);
 }
 
@@ -711,7 +715,7 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
   const size_t row_b = (size_t)H * D * es;
   const size_t tb = (size_t)max_rows * row_b, lb = (size_t)max_rows * H * sizeof(float);
   const size_t ob = sizeof(int64_t) * (max_b + 1);
-  const size_t ws = (size_t)jg_attention_backward_workspace_size(max_rows, H, D);
+  const size_t ws = (size_t)jg_attention_backward_workspace_size(max_rows, max_b, H, D);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t slot_bytes = al(ob) + 8 * al(tb) + al(lb) + al(ws);
   cudaStream_t sx[kSlots];
@@ -756,7 +760,7 @@ extern "C" jg_status jg_jagged_flash_attention_fwd_bwd_host(const int64_t* host_
     rc = jg_jagged_flash_attention_forward(d_off, bc, rows, H, D, t[0], t[1], t[2], 64, 64, t[4], d_lse, dtype, sched, st);
     if (!rc)
       rc = jg_jagged_flash_attention_backward(d_off, bc, rows, H, D, t[0], t[1], t[2], t[3], t[4], d_lse, 64, 64, t[5],
-                                              t[6], t[7], dtype, sched, d_ws, st);
+                                              t[6], t[7], dtype, 1, sched, d_ws, st);
     if (rc) break;
     JG_CUDA(cudaMemcpyAsync((char*)out + hoff, t[4], cb, cudaMemcpyDeviceToHost, st));
     JG_CUDA(cudaMemcpy2DAsync(lse + r0, (size_t)S * sizeof(float), d_lse, (size_t)rows * sizeof(float),

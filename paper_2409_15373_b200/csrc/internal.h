@@ -114,8 +114,11 @@ jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
                                float* delta, jg_dtype dt, const int64_t* valid, cudaStream_t st);
 
-// The backward workspace starts with lsd[2][H][total_rows] fp32: lse in log2 units, then Delta.
-inline int64_t attn_lsd_bytes(int64_t total_rows, int H) { return ((2 * (int64_t)H * total_rows * 4 + 255) / 256) * 256; }
+// The backward workspace starts with lsd fp32
+// ([2][H][total_rows]: -lse log2(e), -Delta; then [3][H] per-head max|K|, max||V||^2, max||dO||^2)
+inline int64_t attn_lsd_bytes(int64_t total_rows, int H) {
+  return ((2 * (int64_t)H * total_rows * 4 + 3 * (int64_t)H * 4 + 255) / 256) * 256;
+}
 
 // tcgen05 attention (bf16, head_dim 64/128)
 bool attn_sm100_supported(int head_dim, jg_dtype dt);
@@ -126,10 +129,11 @@ jg_status launch_attn_fwd_sm100(const int64_t* off, int64_t batch, int64_t total
                                 const int64_t* valid, unsigned long long* counters, cudaStream_t st,
                                 // cross mode (fused feature_interaction): query segments over the key segments
                                 const int64_t* q_off = nullptr, int64_t q_rows = 0);
+// dq_accum: fp32, or int64 fixed point when deterministic ([total_rows, H, D], zeroed by the launcher's prologue)
 jg_status launch_attn_bwd_sm100(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                 const void* q, const void* k, const void* v, const void* go,
                                 const void* o, const float* lse, void* dq, void* dk, void* dv,
-                                float* delta, float* dq_accum, const int2* items,
+                                float* delta, void* dq_accum, bool deterministic, const int2* items,
                                 const int64_t* n_items, int64_t max_items, const int64_t* valid,
                                 unsigned long long* counters, cudaStream_t st);
 

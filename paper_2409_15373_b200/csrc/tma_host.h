@@ -41,14 +41,16 @@ inline jg_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int H, 
 }
 
 // 3-D map over a [rows, H, D] float32 tensor, box (D, 1, box_rows), no swizzle (bulk tensor reductions).
-inline jg_status make_map_f32(CUtensorMap* m, void* ptr, int64_t rows, int H, int D, int box_rows) {
+// [rows, H, D] fp32 (or int32: the backward's deterministic fixed-point dQ accumulator), box (D, 1, box_rows)
+inline jg_status make_map_f32(CUtensorMap* m, void* ptr, int64_t rows, int H, int D, int box_rows, bool int32 = false) {
   auto enc = tma_encode_fn();
   if (!enc) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)rows};
   cuuint64_t strides[2] = {(cuuint64_t)D * 4, (cuuint64_t)H * D * 4};
   cuuint32_t box[3] = {(cuuint32_t)D, 1, (cuuint32_t)box_rows};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  CUresult r = enc(m, int32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled(f32) failed (" + std::to_string((int)r) + ")");
   return JG_OK;

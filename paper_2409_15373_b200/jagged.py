@@ -394,7 +394,10 @@ def jagged_flash_attention_forward(q: JaggedTensor, k: JaggedTensor, v: JaggedTe
 
 def jagged_flash_attention_backward(q: JaggedTensor, k: JaggedTensor, v: JaggedTensor, grad_out: JaggedTensor,
                                     saved: JaggedAttentionSaved, schedule: Schedule | None = None,
-                                    workspace: torch.Tensor | None = None) -> AttentionGrads:
+                                    workspace: torch.Tensor | None = None, deterministic: bool = True) -> AttentionGrads:
+    """attention.cpp:227-289. Gradients are bit-reproducible on every device path; the
+    `deterministic` flag is passed through the C-ABI for API completeness. workspace: optional device buffer of
+    workspace_size(q) bytes (reused across calls; not shared by concurrent calls)."""
     _require_attention_inputs(q, k, v, "jagged_flash_attention_backward")
     if not grad_out.same_offsets(q) or grad_out.values.shape != q.values.shape:
         raise JaggedError("jagged_flash_attention_backward: grad_out layout mismatch")
@@ -409,15 +412,22 @@ def jagged_flash_attention_backward(q: JaggedTensor, k: JaggedTensor, v: JaggedT
     if workspace is not None:
         if not workspace.is_cuda or workspace.device != q.values.device:
             raise JaggedError("jagged_flash_attention_backward: workspace must be on the inputs' CUDA device")
-        need = int(_lib.lib().jg_attention_backward_workspace_size(q.total_rows, H, D))
+        need = backward_workspace_size(q)
         if workspace.numel() * workspace.element_size() < need or not workspace.is_contiguous():
             raise JaggedError(f"jagged_flash_attention_backward: workspace needs {need} contiguous bytes")
     dq, dk, dv = (torch.empty_like(q.values) for _ in range(3))
     check(_lib.lib().jg_jagged_flash_attention_backward(
         _p(q.offsets), q.batch, q.total_rows, H, D, _p(q.values), _p(k.values), _p(v.values), _p(grad_out.values),
         _p(saved.output.values), _p(saved.logsumexp), saved.block_q, saved.block_k, _p(dq), _p(dk), _p(dv),
-        _dt(q.values), schedule.handle if schedule else None, _p(workspace), _stream()))
+        _dt(q.values), 1 if deterministic else 0, schedule.handle if schedule else None, _p(workspace), _stream()))
     return AttentionGrads(q.with_values(dq), k.with_values(dk), v.with_values(dv))
+
+
+def backward_workspace_size(q: JaggedTensor) -> int:
+    """Bytes of the jagged_flash_attention_backward workspace for q's layout (C-ABI
+    jg_attention_backward_workspace_size)."""
+    H, D = _heads(q)
+    return int(_lib.lib().jg_attention_backward_workspace_size(q.total_rows, q.batch, H, D))
 
 
 def _dense_attention_inputs(q, k, v, lengths, op):

@@ -13,7 +13,6 @@ import pytest
 import torch
 
 from oracle import restated as R
-from tests.parity import assert_fp32_close
 
 pytestmark = pytest.mark.gpu
 J = pytest.importorskip("paper_2409_15373_b200.jagged")
@@ -119,6 +118,5 @@ def test_repeated_launches_reuse_counters():
         s = J.jagged_flash_attention_forward(Q, K, V, schedule=sched)
         g = J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sched)
         assert torch.equal(s.output.values, ref.output.values)
-        for a, b in ((g.dk, ref_g.dk), (g.dv, ref_g.dv)):
+        for a, b in ((g.dq, ref_g.dq), (g.dk, ref_g.dk), (g.dv, ref_g.dv)):
             assert torch.equal(a.values, b.values)
-        assert_fp32_close(g.dq.values.float(), ref_g.dq.values.float().cpu().numpy(), tol=1e-2, what="dq")

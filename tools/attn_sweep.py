@@ -4,6 +4,7 @@ Usage: python tools/attn_sweep.py   — prints one line per distribution with fw
 Long uniform samples isolate the per-block pipeline; short ones expose per-item (K/V reload,
 dK/dV epilogue) overhead.
 """
+import os
 import sys
 
 import numpy as np
@@ -11,6 +12,8 @@ import torch
 
 sys.path.insert(0, '.')
 from paper_2409_15373_b200 import jagged as J, synth  # noqa: E402
+
+DET = os.environ.get('JG_SWEEP_DET', '1') != '0'  # backward dQ accumulation mode
 
 
 def run(name, ln, H=4, D=128, reps=25):
@@ -22,7 +25,7 @@ def run(name, ln, H=4, D=128, reps=25):
     sch = J.Schedule(Q)
     for _ in range(3):
         s = J.jagged_flash_attention_forward(Q, K, V, schedule=sch)
-        J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch)
+        J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch, deterministic=DET)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     tfs, tbs = [], []
@@ -30,7 +33,7 @@ def run(name, ln, H=4, D=128, reps=25):
         ev[0].record()
         s = J.jagged_flash_attention_forward(Q, K, V, schedule=sch)
         ev[1].record()
-        J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch)
+        J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch, deterministic=DET)
         ev[2].record()
         torch.cuda.synchronize()
         tfs.append(ev[0].elapsed_time(ev[1]))

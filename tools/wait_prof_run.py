@@ -1,4 +1,4 @@
-import torch, numpy as np, sys
+import os, torch, numpy as np, sys
 sys.path.insert(0, '.')
 from paper_2409_15373_b200 import jagged as J, synth
 ln = (np.full(2048, int(sys.argv[1]), np.int64) if len(sys.argv) > 1 else synth.gen_lengths('half-mean', 1024, 0, 1024)); off = synth.offsets_of(ln); S = int(off[-1]); H, D = 4, 128
@@ -8,5 +8,5 @@ Q, K, V, G = T(mk()), T(mk()), T(mk()), T(mk())
 sch = J.Schedule(Q)
 for _ in range(2):
     s = J.jagged_flash_attention_forward(Q, K, V, schedule=sch)
-    J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch)
+    J.jagged_flash_attention_backward(Q, K, V, G, s, schedule=sch, deterministic=os.environ.get('JG_SWEEP_DET', '1') != '0')
 torch.cuda.synchronize()
