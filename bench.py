@@ -4,11 +4,17 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
+`python bench.py --gpus N` with N > 1 outside torchrun re-launches itself through torch.distributed.run with N
+ranks (one per GPU, NCCL), so both launch forms measure N GPUs.
+
 A step = one jagged_flash_attention_forward + jagged_flash_attention_backward over the rank's
 shard of the batch (B=1024 per GPU, max_len=1024, D=128, H=4, bf16, half-mean lengths seed 0).
 Useful FLOPs = 14·H·D·ΣBi² per step (fwd 4·H·D·ΣBi², bwd 10·H·D·ΣBi²; padding never counted).
 Weak scaling: the global batch is 1024·N samples, sharded on Bi²-balanced sample boundaries, no
-collective inside the timed region. Inputs (537 MB per tensor) are larger than L2.
+collective inside the timed region. Inputs (537 MB per tensor) are larger than L2. With N > 1 a verification
+leg follows the timing: rank 0 scatters a verification batch (offsets by broadcast, shard rows by
+point-to-point sends over NCCL), every rank runs fwd+bwd on its shard, the outputs, lse and grads are gathered
+back to rank 0 and compared bit for bit with rank 0's own single-GPU run of the whole batch ("verify").
 
 --impl reference times the reference's own CPU implementation (oracle/_ref, compiled from the
 reference sources) on the host cores, on bounded samples of the same workload.
@@ -173,6 +179,50 @@ def run_reference_arm(args, rank, world):
 
 
 # ------------------------------------------------------------------ GPU arm
+def verify_sharded(world, rank, dev, n_samples=64):
+    """SURVEY §8e verification over NCCL: scatter a cfg3-shaped verification batch from rank 0, compute each
+    shard's fwd+bwd, gather outputs / lse / grads to rank 0 and compare with rank 0's unsharded run (every sample
+    depends only on its own rows and the backward is deterministic, so the results must be bit-identical)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_15373_b200 import shard, synth
+    from paper_2409_15373_b200 import jagged as J
+
+    L, D, H = CFG["max_len"], CFG["head_dim"], CFG["heads"]
+    ln = synth.gen_lengths(CFG["dist"], L, CFG["seed"] + 7, n_samples * world)
+    off = synth.offsets_of(ln)
+    S = int(off[-1])
+    full = None
+    if rank == 0:
+        g = torch.Generator(device=dev).manual_seed(123)
+        full = (torch.rand(4, S, H, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    probe = torch.empty(0, H, D, dtype=torch.bfloat16, device=dev)
+    # scatter the four operands (q, k, v, grad_out) as one [rows, 4, H, D] tensor: one transfer per rank
+    stacked = full.permute(1, 0, 2, 3).contiguous() if rank == 0 else probe.new_empty(0, 4, H, D)
+    sh, loc = shard.scatter_jagged(off, stacked, world, rank, cost="sq", src=0)
+    T = lambda a, o: J.JaggedTensor(torch.from_numpy(o).to(dev), a.contiguous(), o)  # noqa: E731
+    lo = sh.offsets
+    Q, K, V, G = (T(loc[:, i], lo) for i in range(4))
+    s = J.jagged_flash_attention_forward(Q, K, V)
+    gr = J.jagged_flash_attention_backward(Q, K, V, G, s)
+    outs = torch.stack([s.output.values, gr.dq.values, gr.dk.values, gr.dv.values], 1)  # [rows, 4, H, D]
+    lse = s.logsumexp.t().contiguous()                                                  # [rows, H]
+    g_out = shard.gather_jagged(sh, outs, off, world, rank, cost="sq", dst=0)
+    g_lse = shard.gather_jagged(sh, lse, off, world, rank, cost="sq", dst=0)
+    torch.cuda.synchronize()
+    if rank != 0:
+        return None
+    Qf, Kf, Vf, Gf = (T(full[i], off) for i in range(4))
+    sf = J.jagged_flash_attention_forward(Qf, Kf, Vf)
+    gf = J.jagged_flash_attention_backward(Qf, Kf, Vf, Gf, sf)
+    ref = torch.stack([sf.output.values, gf.dq.values, gf.dk.values, gf.dv.values], 1)
+    same = bool(torch.equal(g_out, ref)) and bool(torch.equal(g_lse, sf.logsumexp.t().contiguous()))
+    return {"samples": int(len(ln)), "rows": S, "ranks": world, "collective": dist.get_backend(),
+            "shards_rows": [int(x) for x in np.diff(off[shard.shard_bounds(ln, world, "sq")])],
+            "bit_identical": same}
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
 
@@ -266,6 +316,8 @@ def run_ours(args, rank, world, local_rank):
     h2d = 4 * hq.numel() * 2 + hoff.nbytes
     d2h = 4 * hq.numel() * 2 + hl.numel() * 4
 
+    verify = verify_sharded(world, rank, dev) if world > 1 else None  # after the timed regions
+
     t = torch.tensor([elapsed_ms, e2e_s], dtype=torch.float64, device=dev)
     nb = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)  # whole-job copy bytes per step
     if world > 1:
@@ -320,6 +372,8 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
         "gpu_launches": launches,
     }
+    if verify is not None:
+        line["verify"] = verify
     print(json.dumps(line), flush=True)
 
 
@@ -712,6 +766,37 @@ def run_table1(args, J, synth, dev, rnd, emit):
                 f.write(RP.render_report(records, fmt))
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return int(so.getsockname()[1])
+
+
+def relaunch_ranks(n: int) -> int:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks through torch.distributed.run on one
+    node (rendezvous on 127.0.0.1), so `python bench.py --gpus N` is a real N-rank run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd[2:6])} ...", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def selftest_launch(rank: int, world: int) -> None:
+    """--selftest-launch: the rank plumbing alone on CPU (gloo): every rank joins, one all-reduce, rank 0 reports."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"selftest": "launch", "n_ranks": dist.get_world_size(), "rank_sum": float(t.item()),
+                          "backend": dist.get_backend()}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -726,13 +811,19 @@ def main():
     ap.add_argument("--out", default=None, help="also append secondary-config lines to this file")
     ap.add_argument("--report", default=None,
                     help="--config table1: write the records as PATH.csv / PATH.json / PATH.md (reference formats)")
+    ap.add_argument("--selftest-launch", action="store_true", help=argparse.SUPPRESS)  # CPU test of the rank launch
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_ranks(args.gpus))
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus else 1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if "WORLD_SIZE" not in os.environ:
         world = 1  # single process
+    if args.selftest_launch:
+        selftest_launch(rank, world)
+        return
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return

@@ -74,19 +74,22 @@ def scatter_jagged(offsets, values, world: int, rank: int, cost: str = "sq", src
     import torch
     import torch.distributed as dist
 
-    off_t = torch.as_tensor(np.asarray(offsets, np.int64)) if rank == src else None
-    n = torch.tensor([0 if off_t is None else off_t.numel()], dtype=torch.int64)
+    # control tensors live where the values do (NCCL moves CUDA tensors only; gloo CPU ones)
+    dev = values.device if values is not None else torch.device("cpu")
+    off_t = torch.as_tensor(np.asarray(offsets, np.int64)).to(dev) if rank == src else None
+    n = torch.tensor([0 if off_t is None else off_t.numel()], dtype=torch.int64, device=dev)
     dist.broadcast(n, src, group=group)
     if off_t is None:
-        off_t = torch.empty(int(n.item()), dtype=torch.int64)
+        off_t = torch.empty(int(n.item()), dtype=torch.int64, device=dev)
     dist.broadcast(off_t, src, group=group)
-    off = off_t.numpy()
+    off = off_t.cpu().numpy()
     sh = make_shard(np.diff(off), world, rank, cost)
     # row shape / dtype travel with a small header from src
     if rank == src:
-        meta = torch.tensor([values.dim()] + list(values.shape[1:]) + [0] * (4 - values.dim()), dtype=torch.int64)
+        meta = torch.tensor([values.dim()] + list(values.shape[1:]) + [0] * (5 - values.dim()), dtype=torch.int64,
+                            device=dev)
     else:
-        meta = torch.empty(4, dtype=torch.int64)
+        meta = torch.empty(5, dtype=torch.int64, device=dev)
     dist.broadcast(meta, src, group=group)
     rest = [int(x) for x in meta[1:int(meta[0])].tolist()]
     bounds = shard_bounds(np.diff(off), world, cost)

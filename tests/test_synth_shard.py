@@ -157,3 +157,21 @@ def test_scatter_compute_gather_gloo_world2():
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert all(n > 0 for _, _, n in res), "both ranks hold rows"
+
+
+def test_bench_gpus2_spawns_two_ranks():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself as two ranks (torch.distributed.run,
+    rendezvous on 127.0.0.1); --selftest-launch exercises that plumbing on CPU (gloo all-reduce over the ranks)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest-launch"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert lines == [{"selftest": "launch", "n_ranks": 2, "rank_sum": 3.0, "backend": "gloo"}], p.stdout
