@@ -173,7 +173,7 @@ JaggedTensor<T> array_jagged_bmm_jagged_out(const Jagged2Tensor<T>& a, const Jag
   Dev off = Dev::from(v.offsets(), op), sqo = Dev::from(a.sq_offsets(), op);
   Dev da = Dev::from(a.values(), op), dv = Dev::from(v.values(), op), out(sizeof(T) * v.values().size(), op);
   ck(op, jg_array_jagged_bmm_jagged_out((const int64_t*)off.p, (const int64_t*)sqo.p, v.batch(), v.total_rows(),
-                                        v.dim(), da.p, dv.p, out.p, JG_F32, JG_F32, 0));
+                                        (int64_t)a.values().size(), v.dim(), da.p, dv.p, out.p, JG_F32, JG_F32, 0));
   return JaggedTensor<T>(v.offsets(), out.to<T>(v.values().size(), op), v.dim());
 }
 
@@ -288,7 +288,7 @@ BmmJaggedOutGrads<T> jagged_jagged_bmm_jagged_out_vjp(const JaggedTensor<T>& q, 
       dki = Dev::from(k.values(), op), dgo = Dev::from(grad_out.values(), op), dq(sizeof(T) * q.values().size(), op),
       dk(sizeof(T) * k.values().size(), op);
   ck(op, jg_jagged_jagged_bmm_jagged_out_vjp((const int64_t*)off.p, (const int64_t*)sqo.p, q.batch(), q.total_rows(),
-                                             q.dim(), dqi.p, dki.p, dgo.p, dq.p, dk.p, JG_F32, JG_F32, 0));
+                                             (int64_t)grad_out.values().size(), q.dim(), dqi.p, dki.p, dgo.p, dq.p, dk.p, JG_F32, JG_F32, 0));
   return {JaggedTensor<T>(q.offsets(), dq.to<T>(q.values().size(), op), q.dim()),
           JaggedTensor<T>(k.offsets(), dk.to<T>(k.values().size(), op), k.dim())};
 }
@@ -306,7 +306,7 @@ ArrayJaggedBmmGrads<T> array_jagged_bmm_jagged_out_vjp(const Jagged2Tensor<T>& a
       dvi = Dev::from(v.values(), op), dgo = Dev::from(grad_out.values(), op), da(sizeof(T) * a.values().size(), op),
       dv(sizeof(T) * v.values().size(), op);
   ck(op, jg_array_jagged_bmm_jagged_out_vjp((const int64_t*)off.p, (const int64_t*)sqo.p, v.batch(), v.total_rows(),
-                                            v.dim(), dai.p, dvi.p, dgo.p, da.p, dv.p, JG_F32, JG_F32, 0));
+                                            (int64_t)a.values().size(), v.dim(), dai.p, dvi.p, dgo.p, da.p, dv.p, JG_F32, JG_F32, 0));
   return {Jagged2Tensor<T>(a.seq_lengths(), da.to<T>(a.values().size(), op)),
           JaggedTensor<T>(v.offsets(), dv.to<T>(v.values().size(), op), v.dim())};
 }

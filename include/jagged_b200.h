@@ -15,9 +15,10 @@
  *   - errors return a jg_status; the reference's exception text is available from jg_last_error()
  *     (thread-local), e.g. "jagged_dense_bmm: dim mismatch (64 vs 32)" (linalg.cpp:42-44);
  *   - every call is stream-ordered on the caller's cudaStream_t (passed as void*) without host
- *     synchronisation, except: jg_dense_flash_attention_* (uploads the host `lengths`),
- *     jg_array_jagged_bmm_jagged_out on the tcgen05 path (reads its repack tile count), and
- *     jg_schedule_work_list (a host-side inspection helper);
+ *     synchronisation (the host `lengths` of jg_dense_flash_attention_* are staged through a buffer
+ *     released by a stream callback), except jg_schedule_work_list (a host-side inspection helper);
+ *     ops with a jagged^2 operand take its element count sum_sq (= sum Bi^2, what a Jagged2Tensor
+ *     holds) so their scratch is sized on the host (-1: unknown -> one 8-byte device read);
  *   - KernelOptions{block, threads, meter} (linalg.hpp:16-20) have no device meaning and are not
  *     taken; block_q/block_k of the flash forward are validated (>= 1) exactly as the reference does
  *     and otherwise ignored (device tiles are fixed at 128x128).
@@ -123,16 +124,17 @@ jg_status jg_jagged_jagged_bmm_jagged_out(const int64_t* offsets, const int64_t*
                                           int64_t batch, int64_t total_rows, int64_t D,
                                           const void* q, const void* k, void* out,
                                           jg_dtype in_dtype, jg_dtype out_dtype, void* stream);
-/* linalg.hpp:47-50: a jagged2, v [total_rows, D] -> [total_rows, D]. */
+/* linalg.hpp:47-50: a jagged2 [sum_sq], v [total_rows, D] -> [total_rows, D]. */
 jg_status jg_array_jagged_bmm_jagged_out(const int64_t* offsets, const int64_t* sq_offsets,
-                                         int64_t batch, int64_t total_rows, int64_t D,
+                                         int64_t batch, int64_t total_rows, int64_t sum_sq, int64_t D,
                                          const void* a, const void* v, void* out,
                                          jg_dtype in_dtype, jg_dtype out_dtype, void* stream);
 /* linalg.hpp:53-54: row softmax inside each Bi x Bi block. */
 jg_status jg_jagged2_softmax(const int64_t* offsets, const int64_t* sq_offsets, int64_t batch,
                              const void* s, void* out, jg_dtype dtype, void* stream);
 
-/* VJPs (linalg.hpp:112-146). Gradients have the layout of the matching input. */
+/* VJPs (linalg.hpp:112-146). Gradients have the layout of the matching input. bf16: all eight
+ * contractions on the tcgen05 grouped GEMM (incl. the transposed forms dO W^T, Y dZ^T, dS^T Q, A^T dO). */
 jg_status jg_jagged_dense_bmm_vjp(const int64_t* offsets, int64_t batch, int64_t total_rows,
                                   int64_t D, int64_t T, const void* x, const void* w,
                                   const void* grad_out, void* dx, void* dw, jg_dtype in_dtype,
@@ -145,12 +147,12 @@ jg_status jg_jagged_softmax_vjp(const int64_t* offsets, int64_t batch, int64_t t
                                 int64_t D, const void* x, const void* grad_out, void* dx,
                                 jg_dtype dtype, void* stream);
 jg_status jg_jagged_jagged_bmm_jagged_out_vjp(const int64_t* offsets, const int64_t* sq_offsets,
-                                              int64_t batch, int64_t total_rows, int64_t D,
+                                              int64_t batch, int64_t total_rows, int64_t sum_sq, int64_t D,
                                               const void* q, const void* k, const void* grad_out,
                                               void* dq, void* dk, jg_dtype in_dtype,
                                               jg_dtype out_dtype, void* stream);
 jg_status jg_array_jagged_bmm_jagged_out_vjp(const int64_t* offsets, const int64_t* sq_offsets,
-                                             int64_t batch, int64_t total_rows, int64_t D,
+                                             int64_t batch, int64_t total_rows, int64_t sum_sq, int64_t D,
                                              const void* a, const void* v, const void* grad_out,
                                              void* da, void* dv, jg_dtype in_dtype,
                                              jg_dtype out_dtype, void* stream);

@@ -36,13 +36,13 @@ SIGNATURES = {
     "jg_jagged_jagged_bmm": [P, I64, I64, I64, I64, P, P, P, C.c_int, C.c_int, P],
     "jg_jagged_softmax": [P, I64, I64, I64, P, P, C.c_int, P],
     "jg_jagged_jagged_bmm_jagged_out": [P, P, I64, I64, I64, P, P, P, C.c_int, C.c_int, P],
-    "jg_array_jagged_bmm_jagged_out": [P, P, I64, I64, I64, P, P, P, C.c_int, C.c_int, P],
+    "jg_array_jagged_bmm_jagged_out": [P, P, I64, I64, I64, I64, P, P, P, C.c_int, C.c_int, P],
     "jg_jagged2_softmax": [P, P, I64, P, P, C.c_int, P],
     "jg_jagged_dense_bmm_vjp": [P, I64, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
     "jg_jagged_jagged_bmm_vjp": [P, I64, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
     "jg_jagged_softmax_vjp": [P, I64, I64, I64, P, P, P, C.c_int, P],
-    "jg_jagged_jagged_bmm_jagged_out_vjp": [P, P, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
-    "jg_array_jagged_bmm_jagged_out_vjp": [P, P, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
+    "jg_jagged_jagged_bmm_jagged_out_vjp": [P, P, I64, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
+    "jg_array_jagged_bmm_jagged_out_vjp": [P, P, I64, I64, I64, I64, P, P, P, P, P, C.c_int, C.c_int, P],
     "jg_jagged2_softmax_vjp": [P, P, I64, P, P, P, C.c_int, P],
     "jg_jagged_flash_attention_forward": [P, I64, I64, I32, I32, P, P, P, I64, I64, P, P, C.c_int, P, P],
     "jg_jagged_flash_attention_backward": [P, I64, I64, I32, I32, P, P, P, P, P, P, I64, I64, P, P, P, C.c_int, I32,

@@ -133,13 +133,19 @@ static bool force_simt_gemm() {
   return e && std::strcmp(e, "simt") == 0;
 }
 
-// tcgen05 path for the forward bmm family (bf16 inputs); op codes as in internal.h
+// tcgen05 path for the bmm family and its VJP contractions (bf16 inputs); op codes as in internal.h
+enum TcOp { TC_JJJ = 0, TC_AJ = 1, TC_JJ = 2, TC_JD = 3, TC_JDT = 4, TC_AJT = 5 };
 static jg_status tc_gemm(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
-                         int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, cudaStream_t st) {
+                         int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, cudaStream_t st,
+                         int64_t sum_sq = -1) {
   if (batch == 0) return JG_OK;
   Scratch prefix(st);
   if (jg_status rc = prefix.alloc(sizeof(int64_t) * (batch + 1))) return rc;
-  return launch_gemm_sm100(op, off, sq, batch, total_rows, D, T, a, b, out, out_dt, (int64_t*)prefix.p, st);
+  return launch_gemm_sm100(op, off, sq, batch, total_rows, D, T, a, b, out, out_dt, (int64_t*)prefix.p, st, nullptr, 0,
+                           nullptr, 1, 0, sum_sq);
+}
+static bool tc_ok(int op, int64_t D, int64_t T, jg_dtype in_dt) {
+  return !force_simt_gemm() && gemm_sm100_supported(op, D, T, in_dt);
 }
 
 }  // namespace jg
@@ -356,13 +362,13 @@ extern "C" jg_status jg_jagged_jagged_bmm_jagged_out(const int64_t* off, const i
 }
 
 extern "C" jg_status jg_array_jagged_bmm_jagged_out(const int64_t* off, const int64_t* sq, int64_t batch,
-                                                    int64_t total_rows, int64_t D, const void* a, const void* v,
-                                                    void* out, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
+                                                    int64_t total_rows, int64_t sum_sq, int64_t D, const void* a,
+                                                    const void* v, void* out, jg_dtype in_dt, jg_dtype out_dt,
+                                                    void* stream) {
   if (jg_status rc = check_out("array_jagged_bmm_jagged_out", in_dt, out_dt)) return rc;
   REQUIRE(sq, JG_INVALID_ARGUMENT, "array_jagged_bmm_jagged_out: sq_offsets required");
-  (void)total_rows;
-  if (!force_simt_gemm() && gemm_sm100_supported(1, D, D, in_dt))
-    return tc_gemm(1, off, sq, batch, total_rows, D, D, a, v, out, out_dt, as_stream(stream));
+  if (tc_ok(TC_AJ, D, D, in_dt))
+    return tc_gemm(TC_AJ, off, sq, batch, total_rows, D, D, a, v, out, out_dt, as_stream(stream), sum_sq);
   GemmDesc g = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
   return gemm(g, off, sq, batch, a, v, out, in_dt, out_dt, as_stream(stream));
 }
@@ -376,14 +382,22 @@ extern "C" jg_status jg_jagged2_softmax(const int64_t* off, const int64_t* sq, i
 }
 
 // ---------------------------------------------------------------------------- VJPs
+// Every contraction of the six VJPs runs on the tcgen05 grouped GEMM for bf16 (the transposed forms JDT / AJT,
+// or a forward form); fp32 (and shapes the tensor-core path does not cover) on the SIMT grouped GEMM.
 extern "C" jg_status jg_jagged_dense_bmm_vjp(const int64_t* off, int64_t batch, int64_t total_rows, int64_t D,
                                              int64_t T, const void* x, const void* w, const void* go, void* dx,
                                              void* dw, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
   if (jg_status rc = check_out("jagged_dense_bmm_vjp", in_dt, out_dt)) return rc;
-  (void)total_rows;
   cudaStream_t st = as_stream(stream);
-  GemmDesc gx = desc(BI(), C_(D), C_(T), OFF(T), C_(T), C_(1), IDX(D * T), C_(1), C_(T), OFF(D), C_(D), C_(1));
-  if (jg_status rc = gemm(gx, off, nullptr, batch, go, w, dx, in_dt, out_dt, st)) return rc;
+  // dX = dO W^T (linalg.cpp:296-305): [rows, T] x W_i^T -> [rows, D]
+  if (tc_ok(TC_JDT, D, T, in_dt)) {
+    if (jg_status rc = tc_gemm(TC_JDT, off, nullptr, batch, total_rows, D, T, go, w, dx, out_dt, st)) return rc;
+  } else {
+    GemmDesc gx = desc(BI(), C_(D), C_(T), OFF(T), C_(T), C_(1), IDX(D * T), C_(1), C_(T), OFF(D), C_(D), C_(1));
+    if (jg_status rc = gemm(gx, off, nullptr, batch, go, w, dx, in_dt, out_dt, st)) return rc;
+  }
+  // dW = X^T dO (linalg.cpp:307-314): a jagged_jagged_bmm
+  if (tc_ok(TC_JJ, D, T, in_dt)) return tc_gemm(TC_JJ, off, nullptr, batch, total_rows, D, T, x, go, dw, out_dt, st);
   GemmDesc gw = desc(C_(D), C_(T), BI(), OFF(D), C_(1), C_(D), OFF(T), C_(T), C_(1), IDX(D * T), C_(T), C_(1));
   return gemm(gw, off, nullptr, batch, x, go, dw, in_dt, out_dt, st);
 }
@@ -392,10 +406,16 @@ extern "C" jg_status jg_jagged_jagged_bmm_vjp(const int64_t* off, int64_t batch,
                                               int64_t T, const void* x, const void* y, const void* go, void* dx,
                                               void* dy, jg_dtype in_dt, jg_dtype out_dt, void* stream) {
   if (jg_status rc = check_out("jagged_jagged_bmm_vjp", in_dt, out_dt)) return rc;
-  (void)total_rows;
   cudaStream_t st = as_stream(stream);
-  GemmDesc gx = desc(BI(), C_(D), C_(T), OFF(T), C_(T), C_(1), IDX(D * T), C_(1), C_(T), OFF(D), C_(D), C_(1));
-  if (jg_status rc = gemm(gx, off, nullptr, batch, y, go, dx, in_dt, out_dt, st)) return rc;
+  // dX = Y dZ^T (linalg.cpp:334-341): [rows, T] x dZ_i^T -> [rows, D]
+  if (tc_ok(TC_JDT, D, T, in_dt)) {
+    if (jg_status rc = tc_gemm(TC_JDT, off, nullptr, batch, total_rows, D, T, y, go, dx, out_dt, st)) return rc;
+  } else {
+    GemmDesc gx = desc(BI(), C_(D), C_(T), OFF(T), C_(T), C_(1), IDX(D * T), C_(1), C_(T), OFF(D), C_(D), C_(1));
+    if (jg_status rc = gemm(gx, off, nullptr, batch, y, go, dx, in_dt, out_dt, st)) return rc;
+  }
+  // dY = X dZ (linalg.cpp:342-349): a jagged_dense_bmm
+  if (tc_ok(TC_JD, D, T, in_dt)) return tc_gemm(TC_JD, off, nullptr, batch, total_rows, D, T, x, go, dy, out_dt, st);
   GemmDesc gy = desc(BI(), C_(T), C_(D), OFF(D), C_(D), C_(1), IDX(D * T), C_(T), C_(1), OFF(T), C_(T), C_(1));
   return gemm(gy, off, nullptr, batch, x, go, dy, in_dt, out_dt, st);
 }
@@ -408,12 +428,17 @@ extern "C" jg_status jg_jagged_softmax_vjp(const int64_t* off, int64_t batch, in
 }
 
 extern "C" jg_status jg_jagged_jagged_bmm_jagged_out_vjp(const int64_t* off, const int64_t* sq, int64_t batch,
-                                                         int64_t total_rows, int64_t D, const void* q, const void* k,
-                                                         const void* go, void* dq, void* dk, jg_dtype in_dt,
-                                                         jg_dtype out_dt, void* stream) {
+                                                         int64_t total_rows, int64_t sum_sq, int64_t D, const void* q,
+                                                         const void* k, const void* go, void* dq, void* dk,
+                                                         jg_dtype in_dt, jg_dtype out_dt, void* stream) {
   if (jg_status rc = check_out("jagged_jagged_bmm_jagged_out_vjp", in_dt, out_dt)) return rc;
-  (void)total_rows;
+  REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged_jagged_bmm_jagged_out_vjp: sq_offsets required");
   cudaStream_t st = as_stream(stream);
+  if (tc_ok(TC_AJ, D, D, in_dt) && tc_ok(TC_AJT, D, D, in_dt)) {
+    // dQ = dS K (linalg.cpp:405-412): array_jagged_bmm_jagged_out; dK = dS^T Q (:413-420): the transposed form
+    if (jg_status rc = tc_gemm(TC_AJ, off, sq, batch, total_rows, D, D, go, k, dq, out_dt, st, sum_sq)) return rc;
+    return tc_gemm(TC_AJT, off, sq, batch, total_rows, D, D, go, q, dk, out_dt, st, sum_sq);
+  }
   GemmDesc gq = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
   if (jg_status rc = gemm(gq, off, sq, batch, go, k, dq, in_dt, out_dt, st)) return rc;
   GemmDesc gk = desc(BI(), C_(D), BI(), SQ(), C_(1), BI(), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
@@ -421,12 +446,17 @@ extern "C" jg_status jg_jagged_jagged_bmm_jagged_out_vjp(const int64_t* off, con
 }
 
 extern "C" jg_status jg_array_jagged_bmm_jagged_out_vjp(const int64_t* off, const int64_t* sq, int64_t batch,
-                                                        int64_t total_rows, int64_t D, const void* a, const void* v,
-                                                        const void* go, void* da, void* dv, jg_dtype in_dt,
-                                                        jg_dtype out_dt, void* stream) {
+                                                        int64_t total_rows, int64_t sum_sq, int64_t D, const void* a,
+                                                        const void* v, const void* go, void* da, void* dv,
+                                                        jg_dtype in_dt, jg_dtype out_dt, void* stream) {
   if (jg_status rc = check_out("array_jagged_bmm_jagged_out_vjp", in_dt, out_dt)) return rc;
-  (void)total_rows;
+  REQUIRE(sq, JG_INVALID_ARGUMENT, "array_jagged_bmm_jagged_out_vjp: sq_offsets required");
   cudaStream_t st = as_stream(stream);
+  if (tc_ok(TC_JJJ, D, D, in_dt) && tc_ok(TC_AJT, D, D, in_dt)) {
+    // dA = dO V^T (linalg.cpp:447-455): jagged_jagged_bmm_jagged_out; dV = A^T dO (:456-466): the transposed form
+    if (jg_status rc = tc_gemm(TC_JJJ, off, sq, batch, total_rows, D, D, go, v, da, out_dt, st)) return rc;
+    return tc_gemm(TC_AJT, off, sq, batch, total_rows, D, D, a, go, dv, out_dt, st, sum_sq);
+  }
   GemmDesc ga = desc(BI(), BI(), C_(D), OFF(D), C_(D), C_(1), OFF(D), C_(1), C_(D), SQ(), BI(), C_(1));
   if (jg_status rc = gemm(ga, off, sq, batch, go, v, da, in_dt, out_dt, st)) return rc;
   GemmDesc gv = desc(BI(), C_(D), BI(), SQ(), C_(1), BI(), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
@@ -662,7 +692,7 @@ extern "C" jg_status jg_jagged_attention(const int64_t* off, const int64_t* sq, 
     if (jg_status rc = launch_jagged2_softmax(off, sq, batch, total_rows, Sh, nullptr, Ph, dtype, false, st)) return rc;
     if (tc) {  // array_jagged_bmm_jagged_out (attention.cpp:169) on head h, into out[:, h, :]
       if (jg_status rc = launch_gemm_sm100(1, off, sq, batch, total_rows, D, D, Ph, v, (char*)out + es * ho, dtype,
-                                           (int64_t*)prefix.p, st, nullptr, 0, nullptr, H, h))
+                                           (int64_t*)prefix.p, st, nullptr, 0, nullptr, H, h, sum_sq))
         return rc;
       continue;
     }
@@ -906,6 +936,8 @@ extern "C" jg_status jg_mlp_layer_backward(int64_t rows, int64_t d_in, int64_t d
       }
     }
   }
+  if (dx && rows > 0 && tc_ok(TC_JDT, d_in, d_out, dtype))  // dx = delta W^T: one segment, W [1, d_in, d_out]
+    return tc_gemm(TC_JDT, off, nullptr, 1, rows, d_in, d_out, delta, w, dx, dtype, st);
   if (dx && rows > 0) {  // dx = delta W^T: B(k = o, n = i) = W[i, o]
     GemmDesc g = desc(BI(), C_(d_in), C_(d_out), C_(0), C_(d_out), C_(1), C_(0), C_(1), C_(d_out), C_(0), C_(d_in),
                       C_(1));

@@ -1,11 +1,18 @@
 // gemm_sm100.cu — the jagged bmm family on tcgen05 tensor cores (bf16 inputs, fp32 accumulation).
 //
 // One persistent warp-specialized kernel, templated on the contraction, covers the four forward
-// operators of linalg.cpp (per sample i, Bi = offsets[i+1] - offsets[i]):
+// operators of linalg.cpp and, with two transposed forms, all eight contractions of their VJPs
+// (linalg.cpp:283-472; per sample i, Bi = offsets[i+1] - offsets[i]):
 //   JJJ  jagged_jagged_bmm_jagged_out (:122)  S_i = Q_i K_i^T      M=Bi N=Bi K=D   A,B K-major (TMA)
 //   AJ   array_jagged_bmm_jagged_out  (:161)  O_i = A_i V_i        M=Bi N=D  K=Bi  A jagged^2 (manual), B MN-major
 //   JJ   jagged_jagged_bmm            (:70)   Z_i = X_i^T Y_i      M=D  N=T  K=Bi  A,B MN-major (TMA)
 //   JD   jagged_dense_bmm             (:34)   O_i = X_i W_i        M=Bi N=T  K=D   A K-major, B MN-major
+//   JDT  O_i = X_i W_i^T, W [B, N, K]           M=Bi N=D  K=T   A,B K-major (TMA)
+//        (jagged_dense_bmm dX = dO W^T, :296; jagged_jagged_bmm dX = Y dZ^T, :334)
+//   AJT  O_i = A_i^T V_i (jagged^2 A)          M=Bi N=D  K=Bi  A jagged^2 transposed (manual, MN-major), B MN-major
+//        (jagged_jagged_bmm_jagged_out dK = dS^T Q, :415; array_jagged_bmm_jagged_out dV = A^T dO, :458)
+// The remaining VJP contractions are forward forms: jdbmm dW = X^T dO and jjbmm dY = X dZ (JJ / JD),
+// jjbmm_jout dQ = dS K (AJ), ajbmm dA = dO V^T (JJJ).
 // 128x128 output tiles, 64-deep K stages through a 4-stage ring (a stage skips reloading an operand block
 // it already holds), accumulators double-buffered in TMEM so the epilogue of tile t overlaps the MMAs of
 // tile t+1; each CTA walks a contiguous tile range with a sample cursor. TMA coordinates are global row indices
@@ -26,7 +33,7 @@
 namespace jg {
 namespace gm {
 
-enum Op { JJJ = 0, AJ = 1, JJ = 2, JD = 3 };
+enum Op { JJJ = 0, AJ = 1, JJ = 2, JD = 3, JDT = 4, AJT = 5 };
 
 #ifndef JG_GEMM_STAGES
 #define JG_GEMM_STAGES 4
@@ -102,6 +109,8 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int64_t t, TileCursor& 
   if (OP == AJ) { r.M = Bi; r.N = p.D; r.K = Bi; }
   if (OP == JJ) { r.M = p.D; r.N = p.T; r.K = Bi; }
   if (OP == JD) { r.M = Bi; r.N = p.T; r.K = p.D; }
+  if (OP == JDT) { r.M = Bi; r.N = p.D; r.K = p.T; }
+  if (OP == AJT) { r.M = Bi; r.N = p.D; r.K = Bi; }
   const int tn = (r.N + BN - 1) / BN;
   const int64_t local = t - c.lo;
   r.m0 = (int)(local / tn) * BM;
@@ -110,11 +119,11 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int64_t t, TileCursor& 
   return r;
 }
 
-// smem A operand is K-major for JJJ/AJ/JD ([128 m rows x 64 k]) and MN-major for JJ ([64 k rows x 128 m]
-// in two 64-wide chunks); B is K-major for JJJ ([128 n rows x 64 k]) and MN-major otherwise.
+// smem A operand is K-major for JJJ/AJ/JD/JDT ([128 m rows x 64 k]) and MN-major for JJ/AJT ([64 k rows x 128 m]
+// in two 64-wide chunks); B is K-major for JJJ/JDT ([128 n rows x 64 k]) and MN-major otherwise.
 template <int OP> struct Layout {
-  static constexpr bool a_mn = OP == JJ;
-  static constexpr bool b_mn = OP != JJJ;
+  static constexpr bool a_mn = OP == JJ || OP == AJT;
+  static constexpr bool b_mn = OP != JJJ && OP != JDT;
   static constexpr bool loader = OP == JJ;  // stages pass through the loader warpgroup (K-tail zeroing)
 };
 
@@ -129,6 +138,9 @@ __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t
 // image of a [128 m x 64 k] SWIZZLE_128B K-major stage with zeros past Bi. One CTA per tile; thread u
 // builds 16-byte units from two aligned 16-byte loads realigned with funnel shifts (the jagged^2 rows
 // start at arbitrary 2-byte offsets). Reads the A values once, writes ~1.1x their bytes.
+// TRANS (AJT): the tile is A_i^T's [128 m x 64 k] block as an MN-major image — two 64-wide m chunks, each 64 k rows of
+// 128 B — so unit (r = k row, c16) of chunk c reads A_i[k0 + r][m0 + 64 c + 8 c16 ...] (again a row segment).
+template <bool TRANS>
 __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restrict__ off, const int64_t* __restrict__ sq,
                                                         const int64_t* __restrict__ a_prefix, int64_t batch,
                                                         const __nv_bfloat16* __restrict__ a, uint8_t* __restrict__ tiles) {
@@ -146,7 +158,10 @@ __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restric
     for (int rep = 0; rep < 4; ++rep) {
       const int u = rep * 256 + threadIdx.x;  // 16-byte unit: row u/8, column chunk u%8
       const int row = u >> 3, c16 = u & 7;
-      const int m = m0 + row, kb0 = k0 + c16 * 8;
+      // source row / first column of the unit's 8 elements: A_i[m][k0 + 8 c16] (AJ) or A_i[k0 + r][m0 + 64 c + 8 c16]
+      // (AJT: chunk c = row / 64, k row r = row % 64)
+      const int m = TRANS ? k0 + (row & 63) : m0 + row;
+      const int kb0 = TRANS ? m0 + 64 * (row >> 6) + c16 * 8 : k0 + c16 * 8;
       const int nval = (m < Bi && kb0 < Bi) ? (Bi - kb0 < 8 ? Bi - kb0 : 8) : 0;
       uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
       int sh = 0;
@@ -179,6 +194,7 @@ __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restric
           else if (2 * q + 1 >= nval) o[q] &= 0xFFFFu;
         }
       }
+      // AJ: row = m of a [128 x 128 B] K-major image; AJT: chunk row>>6 (8 KB apart) of 64 k rows -> same offsets
       *reinterpret_cast<uint4*>(dst + tc::sw128_offset(row, c16)) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
@@ -241,27 +257,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           uint8_t* sb = smem + Smem::kB + s * kTileBytes;
           const int k0 = kb * BK;
           uint64_t ka = ~0ull, kbk = ~0ull;  // ~0: always load
-          if (OP == JJJ || OP == JD) ka = (uint64_t)(tl.b0 + tl.m0) * 65536u + (uint64_t)kb;
+          if (OP == JJJ || OP == JD || OP == JDT) ka = (uint64_t)(tl.b0 + tl.m0) * 65536u + (uint64_t)kb;
           if (OP == JJJ) kbk = (uint64_t)(tl.b0 + tl.n0) * 65536u + (uint64_t)kb;
+          if (OP == JDT) kbk = ((uint64_t)tl.i * p.D + tl.n0) * 65536u + (uint64_t)kb;
           if (OP == JD) kbk = ((uint64_t)tl.i * p.D + k0) * 65536u + (uint64_t)(tl.n0 / BN);
-          if (OP == AJ) kbk = (uint64_t)(tl.b0 + k0) * 65536u + (uint64_t)(tl.n0 / BN);
+          if (OP == AJ || OP == AJT) kbk = (uint64_t)(tl.b0 + k0) * 65536u + (uint64_t)(tl.n0 / BN);
           const bool load_a = ka == ~0ull || key[s] != ka, load_b = kbk == ~0ull || key[kStages + s] != kbk;
           key[s] = ka;
           key[kStages + s] = kbk;
-          tc::mbar_expect_tx(full + s, (load_a || OP == AJ ? kTileBytes : 0) + (load_b ? kTileBytes : 0));
-          if (OP == AJ) {
+          tc::mbar_expect_tx(full + s, (load_a || OP == AJ || OP == AJT ? kTileBytes : 0) + (load_b ? kTileBytes : 0));
+          if (OP == AJ || OP == AJT) {
             const int64_t at = p.a_prefix[tl.i] + (int64_t)(tl.m0 / BM) * tl.nk + kb;
             bulk_load(sa, p.a_tiles + at * kTileBytes, kTileBytes, full + s);
           }
-          if ((OP == JJJ || OP == JD) && load_a)
+          if ((OP == JJJ || OP == JD || OP == JDT) && load_a)
             tc::tma_load_3d(sa, &tm_a, full + s, k0, p.head, (int)(tl.b0 + tl.m0));
+          if (OP == JDT && load_b) tc::tma_load_3d(sb, &tm_b, full + s, k0, 0, (int)(tl.i * p.D + tl.n0));
           if (OP == JJ)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sa + c * 8192, &tm_a, full + s, tl.m0 + 64 * c, 0, (int)(tl.b0 + k0));
           if (OP == JJJ && load_b) tc::tma_load_3d(sb, &tm_b, full + s, k0, p.head, (int)(tl.b0 + tl.n0));
-          if ((OP == AJ && load_b) || OP == JJ)
+          if (((OP == AJ || OP == AJT) && load_b) || OP == JJ)
             for (int c = 0; c < 2; ++c)
-              tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, OP == AJ ? p.head : 0, (int)(tl.b0 + k0));
+              tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, OP == JJ ? 0 : p.head, (int)(tl.b0 + k0));
           if (OP == JD && load_b)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.i * p.D + k0));
@@ -282,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         for (int kb = 0; kb < tl.nk; ++kb, ++cnt) {
           const uint32_t s = cnt % kStages;
           if (Ly::loader) tc::mbar_wait(ready + s, (cnt / kStages) & 1);
-          if (OP == JJJ || OP == JD || OP == AJ) tc::mbar_wait(full + s, (cnt / kStages) & 1);
+          if (!Ly::loader) tc::mbar_wait(full + s, (cnt / kStages) & 1);
           tc::tc_fence_after();
           const uint32_t sa = tc::smem_u32(smem + Smem::kA + s * kTileBytes);
           const uint32_t sb = tc::smem_u32(smem + Smem::kB + s * kTileBytes);
@@ -633,17 +651,17 @@ bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt) {
   if (in_dt != JG_BF16) return false;
   switch (op) {
     case gm::JJJ: return D % 64 == 0;
-    case gm::AJ: return D % 64 == 0;
-    case gm::JJ: return D % 64 == 0 && T % 64 == 0;
-    case gm::JD: return D % 64 == 0 && T % 64 == 0;
+    case gm::AJ: case gm::AJT: return D % 64 == 0;
+    case gm::JJ: case gm::JD: case gm::JDT: return D % 64 == 0 && T % 64 == 0;
   }
   return false;
 }
 
-// A/B roles per op: JJJ (q, k), AJ (a_j2, v), JJ (x, y), JD (x, w)
+// A/B roles per op: JJJ (q, k), AJ / AJT (a_j2, v), JJ (x, y), JD (x, w [B, D, T]), JDT (x [rows, T], w [B, D, T])
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
-                            cudaStream_t st, const void* bias, int relu, void* preact, int heads, int head) {
+                            cudaStream_t st, const void* bias, int relu, void* preact, int heads, int head,
+                            int64_t sum_sq) {
   // tile prefix over samples with the op's (M, N)
   GemmDesc g;
   Lin bi;
@@ -652,11 +670,12 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
   if (op == gm::AJ) { g.M = bi; g.N = L_const(D); }
   if (op == gm::JJ) { g.M = L_const(D); g.N = L_const(T); }
   if (op == gm::JD) { g.M = bi; g.N = L_const(T); }
+  if (op == gm::JDT || op == gm::AJT) { g.M = bi; g.N = L_const(D); }
   if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, 128, tile_prefix, st)) return rc;
   gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32,
                nullptr, nullptr, std::getenv("JG_GEMM_DBG") ? std::atoi(std::getenv("JG_GEMM_DBG")) : 0,
                (const __nv_bfloat16*)bias, relu, (__nv_bfloat16*)preact, head,
-               heads > 1 && op == gm::AJ ? (int64_t)heads * D : 0};
+               heads > 1 && (op == gm::AJ || op == gm::AJT) ? (int64_t)heads * D : 0};
   if (bias && (op != gm::JD || out_dt != JG_BF16)) return fail(JG_UNSUPPORTED, "gemm_sm100: fused bias only for JD bf16");
   CUtensorMap ma{}, mb{};
   const int64_t rows = total_rows > 0 ? total_rows : 1;
@@ -665,7 +684,8 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       if (jg_status rc = make_map(&ma, a, rows, heads, (int)D, 128)) return rc;
       if (jg_status rc = make_map(&mb, b, rows, heads, (int)D, 128)) return rc;
       return gm::run<gm::JJJ>(p, ma, mb, st);
-    case gm::AJ: {
+    case gm::AJ:
+    case gm::AJT: {
       if (jg_status rc = make_map(&mb, b, rows, heads, (int)D, 64)) return rc;
       // A tiles per sample: ceil(Bi/128) * ceil(Bi/64) (a prefix with M = N = Bi and 128 x 64 tiles)
       int64_t* a_prefix = nullptr;
@@ -674,23 +694,31 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       ga.M = bi;
       ga.N = bi;
       jg_status rc = launch_gemm_prefix(ga, off, sq, batch, 128, 64, a_prefix, st);
-      int64_t n_at = 0;
       auto ok = [](cudaError_t e, const char* where) { return e == cudaSuccess ? JG_OK : cuda_status(e, where); };
-      // the tile count sizes the repack buffer: one 8-byte device->host read (stream-synchronising)
-      if (!rc) rc = ok(cudaMemcpyAsync(&n_at, a_prefix + batch, sizeof(int64_t), cudaMemcpyDeviceToHost, st),
-                                "aj tile count");
-      if (!rc) rc = ok(cudaStreamSynchronize(st), "aj tile count");
+      // the repack buffer is sized from the host-known sum Bi^2: sum ceil(Bi/128) ceil(Bi/64) <= sum_sq / 8192 +
+      // 3 total_rows / 128 + batch (no device->host read); without it, one 8-byte stream-synchronising read
+      int64_t n_at = 0;
+      if (sum_sq >= 0) {
+        n_at = sum_sq / 8192 + 3 * total_rows / 128 + batch + 1;
+      } else {
+        if (!rc) rc = ok(cudaMemcpyAsync(&n_at, a_prefix + batch, sizeof(int64_t), cudaMemcpyDeviceToHost, st),
+                         "aj tile count");
+        if (!rc) rc = ok(cudaStreamSynchronize(st), "aj tile count");
+      }
       uint8_t* tiles = nullptr;
       if (!rc && n_at > 0) rc = ok(cudaMallocAsync(&tiles, (size_t)n_at * gm::kTileBytes, st), "aj tiles");
       if (!rc && n_at > 0) {
-        gm::aj_repack_kernel<<<(unsigned)std::min<int64_t>(n_at, 16LL * device_sm_count()), 256, 0, st>>>(
-            off, sq, a_prefix, batch, (const __nv_bfloat16*)a, tiles);
+        const unsigned rgrid = (unsigned)std::min<int64_t>(n_at, 16LL * device_sm_count());
+        if (op == gm::AJ)
+          gm::aj_repack_kernel<false><<<rgrid, 256, 0, st>>>(off, sq, a_prefix, batch, (const __nv_bfloat16*)a, tiles);
+        else
+          gm::aj_repack_kernel<true><<<rgrid, 256, 0, st>>>(off, sq, a_prefix, batch, (const __nv_bfloat16*)a, tiles);
         rc = ok(cudaGetLastError(), "aj_repack_kernel");
         count_launch();
       }
       p.a_tiles = tiles;
       p.a_prefix = a_prefix;
-      if (!rc) rc = gm::run<gm::AJ>(p, mb, mb, st);
+      if (!rc) rc = op == gm::AJ ? gm::run<gm::AJ>(p, mb, mb, st) : gm::run<gm::AJT>(p, mb, mb, st);
       if (tiles) cudaFreeAsync(tiles, st);
       cudaFreeAsync(a_prefix, st);
       return rc;
@@ -703,6 +731,10 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       if (jg_status rc = gm::map2d(&ma, a, rows, D, 128)) return rc;
       if (jg_status rc = gm::map2d(&mb, b, batch * D > 0 ? batch * D : 1, T, 64)) return rc;
       return gm::run<gm::JD>(p, ma, mb, st);
+    case gm::JDT:  // A [rows, T] and the per-sample W [B*D rows, T] both K-major, [128 x 64] boxes
+      if (jg_status rc = gm::map2d(&ma, a, rows, T, 128)) return rc;
+      if (jg_status rc = gm::map2d(&mb, b, batch * D > 0 ? batch * D : 1, T, 128)) return rc;
+      return gm::run<gm::JDT>(p, ma, mb, st);
   }
   return fail(JG_UNSUPPORTED, "gemm_sm100: unknown op");
 }

@@ -80,7 +80,8 @@ jg_status launch_grouped_gemm(const GemmDesc& g, const int64_t* off, const int64
 jg_status launch_gemm_prefix(const GemmDesc& g, const int64_t* off, const int64_t* sq, int64_t batch, int bm, int bn,
                              int64_t* tile_prefix, cudaStream_t st);
 
-// tcgen05 bmm family (bf16 inputs): op 0 jjbmm_jout (q,k), 1 ajbmm_jout (a_j2,v), 2 jjbmm (x,y), 3 jdbmm (x,w)
+// tcgen05 bmm family (bf16 inputs): op 0 jjbmm_jout (q,k), 1 ajbmm_jout (a_j2,v), 2 jjbmm (x,y), 3 jdbmm (x,w),
+// 4 x [rows, T] . w^T (w [B, D, T]) -> [rows, D], 5 a_j2^T . v -> [rows, D] (the transposed VJP forms)
 bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt);
 // JD only: optional fused epilogue out = act(acc + bias[col]) with preact = acc + bias (jagged_mlp layers)
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
@@ -89,7 +90,10 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
                             const void* bias = nullptr, int relu = 0, void* preact = nullptr,
                             // JJJ / AJ on head `head` of [rows, heads, D] q/k (JJJ) or v (AJ); the AJ output
                             // pointer is the head's column block of a [rows, heads, D] tensor
-                            int heads = 1, int head = 0);
+                            int heads = 1, int head = 0,
+                            // AJ / AJT: sum Bi^2 (the jagged^2 operand's size) sizes the repack buffer without a
+                            // device->host read; -1: unknown (one stream-synchronising read)
+                            int64_t sum_sq = -1);
 
 // SURVEY §8f next rows (mlp_fi.cu)
 jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st);

@@ -266,7 +266,8 @@ def array_jagged_bmm_jagged_out(a: Jagged2Tensor, v: JaggedTensor, out_dtype=Non
         raise JaggedError(f"array_jagged_bmm_jagged_out: length mismatch at sample {int(diff[0])}")
     _operands("array_jagged_bmm_jagged_out", v.values, a.values)
     out = torch.empty(v.values.shape, dtype=_out_dtype(v.values, out_dtype), device=v.values.device)
-    check(_lib.lib().jg_array_jagged_bmm_jagged_out(_p(v.offsets), _p(a.sq_offsets), v.batch, v.total_rows, v.dim,
+    check(_lib.lib().jg_array_jagged_bmm_jagged_out(_p(v.offsets), _p(a.sq_offsets), v.batch, v.total_rows, a.sum_sq,
+                                                    v.dim,
                                                     _p(a.values), _p(v.values), _p(out), _dt(v.values), _dt(out),
                                                     _stream()))
     return v.with_values(out)
@@ -333,7 +334,7 @@ def jagged_jagged_bmm_jagged_out_vjp(q: JaggedTensor, k: JaggedTensor, grad_out:
     dq = torch.empty(q.values.shape, dtype=od, device=q.values.device)
     dk = torch.empty(k.values.shape, dtype=od, device=q.values.device)
     check(_lib.lib().jg_jagged_jagged_bmm_jagged_out_vjp(_p(q.offsets), _p(grad_out.sq_offsets), q.batch, q.total_rows,
-                                                         q.dim, _p(q.values), _p(k.values), _p(grad_out.values),
+                                                         grad_out.sum_sq, q.dim, _p(q.values), _p(k.values), _p(grad_out.values),
                                                          _p(dq), _p(dk), _dt(q.values), _dt(dq), _stream()))
     return q.with_values(dq), k.with_values(dk)
 
@@ -347,7 +348,8 @@ def array_jagged_bmm_jagged_out_vjp(a: Jagged2Tensor, v: JaggedTensor, grad_out:
     od = _out_dtype(v.values, out_dtype)
     da = torch.empty(a.values.shape, dtype=od, device=v.values.device)
     dv = torch.empty(v.values.shape, dtype=od, device=v.values.device)
-    check(_lib.lib().jg_array_jagged_bmm_jagged_out_vjp(_p(v.offsets), _p(a.sq_offsets), v.batch, v.total_rows, v.dim,
+    check(_lib.lib().jg_array_jagged_bmm_jagged_out_vjp(_p(v.offsets), _p(a.sq_offsets), v.batch, v.total_rows,
+                                                        a.sum_sq, v.dim,
                                                         _p(a.values), _p(v.values), _p(grad_out.values), _p(da),
                                                         _p(dv), _dt(v.values), _dt(dv), _stream()))
     return Jagged2Tensor(a.offsets, da, a.host_offsets, a.sq_offsets), v.with_values(dv)
