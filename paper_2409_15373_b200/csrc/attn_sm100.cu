@@ -93,17 +93,38 @@ struct Item {
   int store_end;      // query rows [q_row, store_end) are written ...
   int valid_end;      // ... and those below valid_end hold attention (the others zero, lse = -inf)
   bool has_b;
+  int pk_i0, pk_cnt;  // packed item (jagged mode): samples [pk_i0, pk_i0 + pk_cnt) share tile A and key block 0,
+                      // each query row attending only its own sample's keys; pk_cnt = 0 otherwise
 };
 
 __device__ __forceinline__ Item load_item(const Params& p, int64_t w) {
   const int2 it = p.items[w / p.H];
   Item r;
   r.h = (int)(w % p.H);
+  r.pk_i0 = r.pk_cnt = 0;
+  if (it.y < 0) {  // (first sample, -count): consecutive short samples inside one 128-row window (layout.cu)
+    r.pk_i0 = it.x;
+    r.pk_cnt = -it.y;
+    r.b0 = p.off[it.x];
+    r.n = p.off[it.x + r.pk_cnt] - r.b0;  // <= 128
+    r.nkv = 1;
+    r.nv = (int)r.n;
+    r.q_row = (int)r.b0;
+    r.has_b = false;
+    r.store_end = r.valid_end = (int)(r.b0 + r.n);
+    return r;
+  }
   r.b0 = p.off[it.x];
   r.n = p.off[it.x + 1] - r.b0;
   r.nkv = (int)((r.n + BN - 1) / BN);
   r.nv = (int)(p.valid ? (p.valid[it.x] < r.n ? p.valid[it.x] : r.n) : r.n);
-  if (p.q_off) {
+  if (it.y & (1 << 30)) {  // single 128-row query tile (short batches: layout.cu work list)
+    const int t = it.y & ~(1 << 30);
+    r.q_row = (int)(r.b0 + (int64_t)t * BM);
+    r.has_b = false;
+    r.store_end = (int)(r.b0 + r.n);
+    r.valid_end = (int)(r.b0 + r.nv);
+  } else if (p.q_off) {
     const int64_t qb0 = p.q_off[it.x], nq = p.q_off[it.x + 1] - qb0;
     r.q_row = (int)(qb0 + (int64_t)it.y * 2 * BM);
     r.has_b = (int64_t)it.y * 2 * BM + BM < nq;
@@ -190,6 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     it.nv = (int)b.w;
     it.store_end = (int)c.x;
     it.valid_end = (int)c.y;
+    it.pk_i0 = (int)c.z;
+    it.pk_cnt = (int)c.w;
     return (b.z >> 1) == 0;
   };
 
@@ -211,7 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                          (uint32_t)it.q_row);
         tc::st_shared_v4(item_ring + slot * 48 + 16, (uint32_t)it.h, (uint32_t)it.nkv,
                          (it.has_b ? 1u : 0u) | (w >= n_work ? 2u : 0u), (uint32_t)it.nv);
-        tc::st_shared_v4(item_ring + slot * 48 + 32, (uint32_t)it.store_end, (uint32_t)it.valid_end, 0u, 0u);
+        tc::st_shared_v4(item_ring + slot * 48 + 32, (uint32_t)it.store_end, (uint32_t)it.valid_end, (uint32_t)it.pk_i0,
+                         (uint32_t)it.pk_cnt);
         tc::mbar_arrive(item_full + slot);
         if (w >= n_work) break;
         w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
@@ -358,7 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         const int64_t rem = (int64_t)it.nv - (int64_t)j * BN;  // valid keys left (<= 0: block fully masked)
-        const bool partial = rem < BN;  // warp-uniform: a segment's last key block (or padded-mode masked blocks)
+        // warp-uniform: a segment's last key block (or padded-mode masked blocks, or a packed item)
+        const bool partial = rem < BN || it.pk_cnt > 0;
         // pass 1: raw-score row max over TMEM in 32-column chunks, 8 independent chains
         float m8[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (!partial) {
@@ -376,8 +401,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           // last key block of the segment: write -inf over the keys of the next sample back into TMEM so
-          // the exp pass needs no masking (exp2(-inf) = 0)
-          const int remi = rem > 0 ? (int)rem : 0;
+          // the exp pass needs no masking (exp2(-inf) = 0); keys [lo, hi) stay
+          int lo = 0, hi = rem > 0 ? (int)rem : 0;
+          if (it.pk_cnt > 0) {
+            // packed item (one key block): this row's own sample's keys (block-diagonal mask). The pack's
+            // offsets are read once per warp and scanned with shuffles; rows past the pack keep [0, n).
+            int k = 0;
+            for (int c0 = 1; c0 <= it.pk_cnt; c0 += 32) {
+              const int ov = c0 + lane <= it.pk_cnt ? (int)(p.off[it.pk_i0 + c0 + lane] - it.b0) : 0x7fffffff;
+#pragma unroll 8
+              for (int jj = 0; jj < 32; ++jj) k += __shfl_sync(0xffffffffu, ov, jj) <= row ? 1 : 0;
+            }
+            if (k < it.pk_cnt) {
+              lo = (int)(p.off[it.pk_i0 + k] - it.b0);
+              hi = (int)(p.off[it.pk_i0 + k + 1] - it.b0);
+            } else {
+              hi = (int)it.n;
+            }
+          }
 #pragma unroll
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t r[32];
@@ -385,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
-              r[e] = c * 32 + e < remi ? r[e] : __float_as_uint(-INFINITY);
+              r[e] = (c * 32 + e >= lo && c * 32 + e < hi) ? r[e] : __float_as_uint(-INFINITY);
               m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(r[e]));
             }
             tc::tmem_st32(s_addr + c * 32, r);

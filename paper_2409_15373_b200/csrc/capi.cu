@@ -175,17 +175,21 @@ extern "C" jg_status jg_sq_offsets(const int64_t* offsets, int64_t batch, int64_
   return launch_scan(1, offsets, batch, sq_offsets, nullptr, as_stream(stream));
 }
 
-// Two LPT lists over the same offsets: (sample, 128-row tile) items for the key-stationary backward
-// and (sample, 256-row tile pair) items for the two-tile forward.
+// Three LPT lists over the same offsets: (sample, 128-row tile) items for the key-stationary backward,
+// (sample, 256-row tile pair) items for the two-tile forward (padded and cross modes), and the same with the
+// short samples packed per 128-row window (first sample, -count) for the jagged self-attention forward.
 struct jg_schedule_s {
   const int64_t* offsets;
-  int64_t batch, total_rows, max_items, max_items2;
+  int64_t batch, total_rows, max_items, max_items2, max_itemsf, nwin;
   int64_t* lengths;
   int64_t* sq;
   int2* items;
   int64_t* n_items;
   int2* items2;
   int64_t* n_items2;
+  int2* itemsf;
+  int64_t* n_itemsf;
+  int* win;  // [2][nwin]: first and last packable sample per 128-row window
   unsigned long long* counters;  // [4]: forward kernel (next item, exited CTAs), backward kernel (same)
   void* block;
 };
@@ -201,9 +205,12 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
   s->total_rows = total_rows;
   s->max_items = total_rows / 128 + batch + 1;
   s->max_items2 = total_rows / 256 + batch + 1;
+  s->nwin = total_rows / 128 + 1;
+  s->max_itemsf = s->max_items2 + s->nwin;
   const size_t b_len = sizeof(int64_t) * (batch + 1), b_sq = sizeof(int64_t) * (batch + 1),
-               b_items = sizeof(int2) * s->max_items, b_items2 = sizeof(int2) * s->max_items2;
-  const size_t bytes = b_len + b_sq + 128 + b_items + b_items2;
+               b_items = sizeof(int2) * s->max_items, b_items2 = sizeof(int2) * s->max_items2,
+               b_itemsf = sizeof(int2) * s->max_itemsf, b_win = sizeof(int) * 2 * s->nwin;
+  const size_t bytes = b_len + b_sq + 192 + b_items + b_items2 + b_itemsf + b_win;
   cudaError_t e = cudaMallocAsync(&s->block, bytes, st);
   if (e != cudaSuccess) {
     delete s;
@@ -215,8 +222,11 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
   s->n_items = (int64_t*)p; p += 64;
   s->n_items2 = (int64_t*)p; p += 32;
   s->counters = (unsigned long long*)p; p += 32;
+  s->n_itemsf = (int64_t*)p; p += 64;
   s->items = (int2*)p; p += b_items;
-  s->items2 = (int2*)p;
+  s->items2 = (int2*)p; p += b_items2;
+  s->itemsf = (int2*)p; p += b_itemsf;
+  s->win = (int*)p;
   jg_status rc = JG_OK;
   JG_CUDA(cudaMemsetAsync(s->counters, 0, 32, st));  // self-resetting afterwards (internal.h)
   if (batch > 0) {
@@ -224,8 +234,11 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
     if ((rc = launch_scan(1, offsets, batch, s->sq, nullptr, st))) goto err;
     if ((rc = launch_work_list(offsets, batch, 128, s->items, s->n_items, st))) goto err;
     if ((rc = launch_work_list(offsets, batch, 256, s->items2, s->n_items2, st))) goto err;
+    if ((rc = launch_work_list(offsets, batch, 256, s->itemsf, s->n_itemsf, st, s->win, s->win + s->nwin, s->nwin)))
+      goto err;
   } else {
     JG_CUDA(cudaMemsetAsync(s->n_items, 0, 64, st));
+    JG_CUDA(cudaMemsetAsync(s->n_itemsf, 0, 8, st));
     JG_CUDA(cudaMemsetAsync(s->sq, 0, sizeof(int64_t), st));
   }
   *out = s;
@@ -507,8 +520,12 @@ static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_r
       if (jg_status rc = jg_schedule_create(off, batch, total_rows, st, &own)) return rc;
       sched = own;
     }
-    jg_status rc = launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
-                                         sched->n_items2, sched->max_items2, valid, sched->counters, st);
+    // jagged mode: the packed list (short samples share a query tile); padded mode: one item per segment
+    static const bool no_pack = std::getenv("JG_FWD_NOPACK") != nullptr;  // A/B knob (diagnostic)
+    jg_status rc = (valid || no_pack) ? launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->items2,
+                                                 sched->n_items2, sched->max_items2, valid, sched->counters, st)
+                         : launch_attn_fwd_sm100(off, batch, total_rows, H, D, q, k, v, out, lse, sched->itemsf,
+                                                 sched->n_itemsf, sched->max_itemsf, nullptr, sched->counters, st);
     if (own) {
       schedule_release(own, st);
     }

@@ -51,7 +51,7 @@ __device__ __forceinline__ void work_counters_exit(unsigned long long* counters)
 jg_status launch_scan(int mode, const int64_t* in, int64_t n, int64_t* out, int64_t* bad, cudaStream_t s);
 jg_status launch_lengths(const int64_t* off, int64_t n, int64_t* len, cudaStream_t s);
 jg_status launch_work_list(const int64_t* off, int64_t batch, int tile, int2* items, int64_t* count,
-                           cudaStream_t s);
+                           cudaStream_t s, int* win_first = nullptr, int* win_last = nullptr, int64_t nwin = 0);
 
 jg_status launch_jagged_to_dense(const int64_t* off, int64_t batch, int64_t dim, const void* x,
                                  int64_t max_len, double pad, void* out, jg_dtype dt, cudaStream_t s);

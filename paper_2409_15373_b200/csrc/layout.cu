@@ -78,16 +78,50 @@ jg_status launch_lengths(const int64_t* off, int64_t n, int64_t* len, cudaStream
 // last bin, still stable).
 constexpr int kMaxBins = 64;
 
+// Forward sample packing (short samples): a sample is packable when it lies inside one aligned 128-row window of
+// the flat row space; the packable samples of window w (and the empty samples between them) become ONE forward
+// item (first sample, -count) whose
+// query tile and single key block are the window's packed rows, masked block-diagonally per sample by the
+// kernel. Zipf-distributed batches (cfg2: median length 14) otherwise spend a whole item latency per sample.
+__device__ __forceinline__ bool packable(int64_t a, int64_t b) { return b > a && (a >> 7) == ((b - 1) >> 7); }
+
+__global__ void pack_mark_kernel(const int64_t* __restrict__ off, int64_t batch, int* __restrict__ win_first,
+                                 int* __restrict__ win_last) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < batch; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = off[i], b = off[i + 1];
+    if (!packable(a, b)) continue;
+    atomicMin(win_first + (a >> 7), (int)i);
+    atomicMax(win_last + (a >> 7), (int)i);
+  }
+}
+
 __global__ void __launch_bounds__(kScanThreads) work_list_kernel(const int64_t* __restrict__ off,
                                                                  int64_t batch, int tile,
                                                                  int2* __restrict__ items,
-                                                                 int64_t* __restrict__ count) {
+                                                                 int64_t* __restrict__ count,
+                                                                 const int* __restrict__ win_first,
+                                                                 const int* __restrict__ win_last, int64_t nwin,
+                                                                 int64_t split_below) {
   __shared__ int present[kMaxBins + 1];
   for (int b = threadIdx.x; b <= kMaxBins; b += blockDim.x) present[b] = 0;
   __syncthreads();
+  const bool pack = win_last != nullptr;
+  // packed (forward) list: when the tile-pair items and packs together would not fill the SMs (short batches,
+  // cfg2), the unpacked samples are listed as single 128-row query tiles instead (flag bit 30 in the tile field):
+  // the longest samples then run on twice the CTAs, and a lone tile's key loop is shorter than a pair's
+  if (pack) {
+    int64_t t_local = 0;
+    for (int64_t i = threadIdx.x; i < batch; i += blockDim.x)
+      if (!packable(off[i], off[i + 1])) t_local += (off[i + 1] - off[i] + tile - 1) / tile;
+    for (int64_t w = threadIdx.x; w < nwin; w += blockDim.x) t_local += win_last[w] >= 0 ? 1 : 0;
+    int64_t total;
+    block_exclusive_scan(t_local, &total);
+    if (total < split_below) tile = 128;
+  }
+  const int split = (pack && tile == 128) ? (1 << 30) : 0;
   for (int64_t i = threadIdx.x; i < batch; i += blockDim.x) {
     const int64_t nb = (off[i + 1] - off[i] + tile - 1) / tile;
-    if (nb > 0) present[nb < kMaxBins ? nb : kMaxBins] = 1;
+    if (nb > 0 && !(pack && packable(off[i], off[i + 1]))) present[nb < kMaxBins ? nb : kMaxBins] = 1;
   }
   __syncthreads();
   int64_t base = 0;
@@ -99,11 +133,21 @@ __global__ void __launch_bounds__(kScanThreads) work_list_kernel(const int64_t* 
       if (i < batch) {
         const int64_t nb = (off[i + 1] - off[i] + tile - 1) / tile;
         const int64_t key = nb < kMaxBins ? nb : kMaxBins;
-        nt = (key == bin) ? nb : 0;
+        nt = (key == bin && !(pack && packable(off[i], off[i + 1]))) ? nb : 0;
       }
       int64_t tot;
       const int64_t pos = base + block_exclusive_scan(nt, &tot);
-      for (int64_t t = 0; t < nt; ++t) items[pos + t] = make_int2((int)i, (int)t);
+      for (int64_t t = 0; t < nt; ++t) items[pos + t] = make_int2((int)i, (int)t | split);
+      base += tot;
+    }
+  }
+  if (pack) {  // one key block each: last in LPT order, windows ascending
+    for (int64_t w0 = 0; w0 < nwin; w0 += blockDim.x) {
+      const int64_t w = w0 + threadIdx.x;
+      const int64_t has = (w < nwin && win_last[w] >= 0) ? 1 : 0;
+      int64_t tot;
+      const int64_t pos = base + block_exclusive_scan(has, &tot);
+      if (has) items[pos] = make_int2(win_first[w], win_first[w] - win_last[w] - 1);
       base += tot;
     }
   }
@@ -111,8 +155,16 @@ __global__ void __launch_bounds__(kScanThreads) work_list_kernel(const int64_t* 
 }
 
 jg_status launch_work_list(const int64_t* off, int64_t batch, int tile, int2* items, int64_t* count,
-                           cudaStream_t s) {
-  work_list_kernel<<<1, kScanThreads, 0, s>>>(off, batch, tile, items, count);
+                           cudaStream_t s, int* win_first, int* win_last, int64_t nwin) {
+  if (win_last) {
+    JG_CUDA(cudaMemsetAsync(win_first, 0x7f, sizeof(int) * nwin, s));
+    JG_CUDA(cudaMemsetAsync(win_last, 0xff, sizeof(int) * nwin, s));  // -1: no packable sample
+    pack_mark_kernel<<<(int)std::min<int64_t>((batch + 255) / 256, 4 * kNumSMsB200), 256, 0, s>>>(off, batch, win_first,
+                                                                                                   win_last);
+    JG_LAUNCHED("pack_mark_kernel");
+  }
+  work_list_kernel<<<1, kScanThreads, 0, s>>>(off, batch, tile, items, count, win_first, win_last, nwin,
+                                              2 * (int64_t)device_sm_count());
   JG_LAUNCHED("work_list_kernel");
   return JG_OK;
 }

@@ -56,8 +56,9 @@ struct WaitProf {
   __device__ __forceinline__ void init(unsigned long long* gp, int b) {
     base = b;
     const bool cta0_mode = gp != nullptr && gp[63] != 0;   // 1: trace CTA 0; 3: per-CTA start/end times
-    tr = gp != nullptr && gp[63] == 1 && blockIdx.x == 0;
-    g = (gp && (!cta0_mode || blockIdx.x == 0)) ? gp + b : nullptr;
+    const unsigned traced = gp != nullptr ? (unsigned)gp[62] : 0u;  // JG_WAIT_PROF_CTA (default 0)
+    tr = gp != nullptr && gp[63] == 1 && blockIdx.x == traced;
+    g = (gp && (!cta0_mode || blockIdx.x == traced)) ? gp + b : nullptr;
   }
   __device__ __forceinline__ void trace(int code) {
     if (!tr || n_tr >= kRoleCap) return;

@@ -24,9 +24,46 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
   return fn;
 }
 
+// Encoded maps are cached per host thread by their full key (a tensor map is plain bytes: encoding is pure), so
+// repeated calls on the same buffers skip cuTensorMapEncodeTiled (~1 us each; it dominated small launches).
+struct MapKey {
+  const void* ptr;
+  int64_t rows;
+  int H, D, box, kind;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && H == o.H && D == o.D && box == o.box && kind == o.kind;
+  }
+};
+struct MapCache {
+  static constexpr int kSlots = 16;
+  MapKey key[kSlots];
+  CUtensorMap map[kSlots];
+  int used = 0, next = 0;
+  bool find(const MapKey& k, CUtensorMap* m) const {
+    for (int i = 0; i < used; ++i)
+      if (key[i] == k) {
+        *m = map[i];
+        return true;
+      }
+    return false;
+  }
+  void put(const MapKey& k, const CUtensorMap& m) {
+    key[next] = k;
+    map[next] = m;
+    next = (next + 1) % kSlots;
+    if (used < kSlots) ++used;
+  }
+};
+inline MapCache& map_cache() {
+  static thread_local MapCache c;
+  return c;
+}
+
 // 3-D map over a [rows, H, D] bf16 tensor: dims (D, H, rows), box (64, 1, box_rows), SWIZZLE_128B.
 // Rows past `rows` are zero-filled by the TMA unit; rows of the next sample are masked in-kernel.
 inline jg_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int H, int D, int box_rows) {
+  const MapKey key{ptr, rows, H, D, box_rows, 0};
+  if (map_cache().find(key, m)) return JG_OK;
   auto enc = tma_encode_fn();
   if (!enc) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)rows};
@@ -37,6 +74,7 @@ inline jg_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int H, 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  map_cache().put(key, *m);
   return JG_OK;
 }
 
@@ -77,6 +115,9 @@ inline unsigned long long* wait_prof_begin(cudaStream_t st) {
     static const unsigned long long mode_trace = 1, mode_times = 3;
     cudaMemcpyAsync(buf + 63, e[0] == '2' ? &mode_trace : &mode_times, sizeof(unsigned long long),
                     cudaMemcpyHostToDevice, st);
+    static unsigned long long cta = 0;
+    if (const char* c = std::getenv("JG_WAIT_PROF_CTA")) cta = std::strtoull(c, nullptr, 10);
+    cudaMemcpyAsync(buf + 62, &cta, sizeof(unsigned long long), cudaMemcpyHostToDevice, st);
     cudaStreamSynchronize(st);
   }
   return buf;
@@ -116,6 +157,11 @@ inline void wait_prof_end(unsigned long long* buf, cudaStream_t st, const char* 
     if (n)
       std::fprintf(stderr, "[cta-times %s] %d CTAs: makespan %.1f us, mean busy %.1f us, first exit %.1f us\n", tag, n,
                    (e1 - s0) * 1e-3, busy / n * 1e-3, (e0 - s0) * 1e-3);
+    if (n && std::getenv("JG_WAIT_PROF_CTAS")) {  // every CTA: start and end relative to the first start
+      for (int b = 0; b < sms; ++b)
+        if (t[2 * b] && t[2 * b + 1])
+          std::fprintf(stderr, "[cta %d] %.2f %.2f\n", b, (t[2 * b] - s0) * 1e-3, (t[2 * b + 1] - s0) * 1e-3);
+    }
   }
   if (e && e[0] == '2') {  // dump CTA 0's wait timeline
     const size_t n = 5 * 12000;

@@ -42,7 +42,14 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream():
+    # the raw cudaStream_t of torch's current stream; torch.cuda.current_stream() builds a Stream object per call
+    # (~3 us), which dominated the host cost of small launches (cfg2)
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -81,9 +88,15 @@ class JaggedTensor:
         return np.diff(self.host_offsets)
 
     def same_offsets(self, other: "JaggedTensor") -> bool:
-        return np.array_equal(self.host_offsets, other.host_offsets)
+        return self.host_offsets is other.host_offsets or np.array_equal(self.host_offsets, other.host_offsets)
 
     def with_values(self, values: torch.Tensor) -> "JaggedTensor":
+        # values of the same leading extent (an operator output): the offsets invariants already hold
+        if values.dim() >= 2 and values.shape[0] == self.values.shape[0] and values.shape[-1] > 0 \
+                and values.is_contiguous():
+            t = JaggedTensor.__new__(JaggedTensor)
+            t.host_offsets, t.offsets, t.values = self.host_offsets, self.offsets, values
+            return t
         return JaggedTensor(self.offsets, values, self.host_offsets)
 
 

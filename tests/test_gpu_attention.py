@@ -44,6 +44,9 @@ CASES = [
     ([3, 0, 128, 129, 255, 1, 64], 2, 64),
     ([200, 5, 300, 0, 131], 2, 128),
     (list(R.gen_lengths("zipf", 512, 0, 24, 1.1)), 1, 64),
+    # forward packing (layout.cu): windows with > 32 packed samples, samples crossing 128-row windows, a sample
+    # filling a window, empty samples inside a pack
+    ([1] * 70 + [2, 0, 2] * 20 + [60, 3, 126, 1, 5, 128, 0, 127] + [1] * 150 + [9, 250], 2, 64),
 ]
 
 
