@@ -551,6 +551,20 @@ def run_configs(args):
             "jagged_softmax": (lambda: J.jagged_softmax(X), 4 * S * D, 2 * S * D * eb),
             "jagged2_softmax": (lambda: J.jagged2_softmax(A), 4 * sq, 2 * sq * eb),
         }
+        # the VJPs (linalg.cpp:283-507): bytes = inputs read + gradients written, flops = their contractions
+        GX = J.JaggedTensor(X.offsets, rnd(S, D), off)
+        GA = J.Jagged2Tensor(X.offsets, rnd(sq), off)
+        GZ = rnd(B, D, D)
+        ops.update({
+            "jagged_jagged_bmm_jagged_out_vjp": (lambda: J.jagged_jagged_bmm_jagged_out_vjp(X, Y, GA), 4 * sq * D,
+                                                 (4 * S * D + sq) * eb),
+            "array_jagged_bmm_jagged_out_vjp": (lambda: J.array_jagged_bmm_jagged_out_vjp(A, X, GX), 4 * sq * D,
+                                                (2 * sq + 3 * S * D) * eb),
+            "jagged_jagged_bmm_vjp": (lambda: J.jagged_jagged_bmm_vjp(X, Y, GZ), 4 * S * D * D,
+                                      (4 * S * D + B * D * D) * eb),
+            "jagged_softmax_vjp": (lambda: J.jagged_softmax_vjp(X, GX), 6 * S * D, 3 * S * D * eb),
+            "jagged2_softmax_vjp": (lambda: J.jagged2_softmax_vjp(A, GA), 6 * sq, 3 * sq * eb),
+        })
         for name, (fn, fl, byts) in ops.items():
             ms = _events_time(fn, args.steps, args.warmup)
             gbs, tfs = byts / (ms * 1e-3) / 1e9, fl / (ms * 1e-3) / 1e12

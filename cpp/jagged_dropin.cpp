@@ -92,6 +92,37 @@ template <typename T>
 template <typename T>
 constexpr bool is_f32 = std::is_same_v<T, float>;
 
+// KernelOptions.meter (linalg.hpp:19, scratch.hpp:12-55): the device scratch a call allocates for its own
+// intermediates, in elements of T, reported as one allocation window per operator (jg_scratch_counters). The
+// reference counts its host scratch buffers the same way (e.g. attention.cpp:190-191 per-thread score rows);
+// on-chip tiles (TMEM / shared memory) are registers of the kernel, not allocations. Nested windows are safe.
+class MeterScope {
+ public:
+  MeterScope(const KernelOptions& o, size_t elem) : meter_(o.meter), elem_(elem) {
+    if (!meter_) return;
+    jg_scratch_counters(&cur0_, &peak0_);
+    jg_scratch_reset_peak();
+  }
+  ~MeterScope() {
+    if (!meter_) return;
+    int64_t cur = 0, peak = 0;
+    jg_scratch_counters(&cur, &peak);
+    const int64_t elems = (peak - cur0_ + (int64_t)elem_ - 1) / (int64_t)elem_;
+    if (elems > 0) {
+      meter_->on_alloc(elems);
+      meter_->on_release(elems);
+    }
+    jg_scratch_raise_peak(peak0_);
+  }
+  MeterScope(const MeterScope&) = delete;
+  MeterScope& operator=(const MeterScope&) = delete;
+
+ private:
+  ScratchMeter* meter_;
+  size_t elem_;
+  int64_t cur0_ = 0, peak0_ = 0;
+};
+
 std::vector<int64_t> lengths_of(const std::vector<int64_t>& off) {
   std::vector<int64_t> l(off.size() - 1);
   for (size_t i = 0; i + 1 < off.size(); ++i) l[i] = off[i + 1] - off[i];
@@ -102,7 +133,8 @@ std::vector<int64_t> lengths_of(const std::vector<int64_t>& off) {
 
 // ============================================================================ Table-1 forward ops
 template <typename T>
-JaggedTensor<T> jagged_dense_bmm(const JaggedTensor<T>& x, const DenseTensor<T>& w, const KernelOptions&) {
+JaggedTensor<T> jagged_dense_bmm(const JaggedTensor<T>& x, const DenseTensor<T>& w, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_dense_bmm";
   if (w.rank() != 3) throw std::invalid_argument("jagged_dense_bmm: w must be [B, D, T]");
   const int64_t b = x.batch(), d = x.dim(), t = w.shape()[2];
@@ -120,7 +152,8 @@ JaggedTensor<T> jagged_dense_bmm(const JaggedTensor<T>& x, const DenseTensor<T>&
 }
 
 template <typename T>
-DenseTensor<T> jagged_jagged_bmm(const JaggedTensor<T>& x, const JaggedTensor<T>& y, const KernelOptions&) {
+DenseTensor<T> jagged_jagged_bmm(const JaggedTensor<T>& x, const JaggedTensor<T>& y, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_jagged_bmm";
   require_matching_offsets(x, y, op);
   if constexpr (!is_f32<T>) no_device_path<T>(op);
@@ -132,7 +165,8 @@ DenseTensor<T> jagged_jagged_bmm(const JaggedTensor<T>& x, const JaggedTensor<T>
 }
 
 template <typename T>
-JaggedTensor<T> jagged_softmax(const JaggedTensor<T>& x, const KernelOptions&) {
+JaggedTensor<T> jagged_softmax(const JaggedTensor<T>& x, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_softmax";
   if constexpr (!is_f32<T>) no_device_path<T>(op);
   Dev off = Dev::from(x.offsets(), op), dx = Dev::from(x.values(), op), out(sizeof(T) * x.values().size(), op);
@@ -142,7 +176,8 @@ JaggedTensor<T> jagged_softmax(const JaggedTensor<T>& x, const KernelOptions&) {
 
 template <typename T>
 Jagged2Tensor<T> jagged_jagged_bmm_jagged_out(const JaggedTensor<T>& q, const JaggedTensor<T>& k,
-                                              const KernelOptions&) {
+                                              const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_jagged_bmm_jagged_out";
   require_matching_offsets(q, k, op);
   if (q.dim() != k.dim())
@@ -161,7 +196,8 @@ Jagged2Tensor<T> jagged_jagged_bmm_jagged_out(const JaggedTensor<T>& q, const Ja
 }
 
 template <typename T>
-JaggedTensor<T> array_jagged_bmm_jagged_out(const Jagged2Tensor<T>& a, const JaggedTensor<T>& v, const KernelOptions&) {
+JaggedTensor<T> array_jagged_bmm_jagged_out(const Jagged2Tensor<T>& a, const JaggedTensor<T>& v, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "array_jagged_bmm_jagged_out";
   if (a.batch() != v.batch())
     throw std::invalid_argument("array_jagged_bmm_jagged_out: batch mismatch (" + std::to_string(a.batch()) +
@@ -178,7 +214,8 @@ JaggedTensor<T> array_jagged_bmm_jagged_out(const Jagged2Tensor<T>& a, const Jag
 }
 
 template <typename T>
-Jagged2Tensor<T> jagged2_softmax(const Jagged2Tensor<T>& s, const KernelOptions&) {
+Jagged2Tensor<T> jagged2_softmax(const Jagged2Tensor<T>& s, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged2_softmax";
   if constexpr (!is_f32<T>) no_device_path<T>(op);
   std::vector<int64_t> off(s.batch() + 1, 0);
@@ -210,7 +247,8 @@ void validate_mlp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers)
 
 // linalg.cpp:265-277 via jg_mlp_layer_forward per layer (activations stay on the device between layers)
 template <typename T>
-JaggedTensor<T> jagged_mlp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers, const KernelOptions&) {
+JaggedTensor<T> jagged_mlp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_mlp";
   validate_mlp(x, layers);
   if constexpr (!is_f32<T>) no_device_path<T>(op);
@@ -230,7 +268,8 @@ JaggedTensor<T> jagged_mlp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>
 // ============================================================================ VJPs
 template <typename T>
 JaggedDenseBmmGrads<T> jagged_dense_bmm_vjp(const JaggedTensor<T>& x, const DenseTensor<T>& w,
-                                            const JaggedTensor<T>& grad_out, const KernelOptions&) {
+                                            const JaggedTensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_dense_bmm_vjp";
   if (w.rank() != 3) throw std::invalid_argument("jagged_dense_bmm_vjp: w must be [B, D, T]");
   require_matching_offsets(x, grad_out, op);
@@ -247,7 +286,8 @@ JaggedDenseBmmGrads<T> jagged_dense_bmm_vjp(const JaggedTensor<T>& x, const Dens
 
 template <typename T>
 JaggedJaggedBmmGrads<T> jagged_jagged_bmm_vjp(const JaggedTensor<T>& x, const JaggedTensor<T>& y,
-                                              const DenseTensor<T>& grad_out, const KernelOptions&) {
+                                              const DenseTensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_jagged_bmm_vjp";
   require_matching_offsets(x, y, op);
   const int64_t b = x.batch(), d = x.dim(), t = y.dim();
@@ -263,7 +303,8 @@ JaggedJaggedBmmGrads<T> jagged_jagged_bmm_vjp(const JaggedTensor<T>& x, const Ja
 }
 
 template <typename T>
-JaggedTensor<T> jagged_softmax_vjp(const JaggedTensor<T>& x, const JaggedTensor<T>& grad_out, const KernelOptions&) {
+JaggedTensor<T> jagged_softmax_vjp(const JaggedTensor<T>& x, const JaggedTensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_softmax_vjp";
   require_matching_offsets(x, grad_out, op);
   if (x.dim() != grad_out.dim()) throw std::invalid_argument("jagged_softmax_vjp: dim mismatch");
@@ -276,7 +317,8 @@ JaggedTensor<T> jagged_softmax_vjp(const JaggedTensor<T>& x, const JaggedTensor<
 
 template <typename T>
 BmmJaggedOutGrads<T> jagged_jagged_bmm_jagged_out_vjp(const JaggedTensor<T>& q, const JaggedTensor<T>& k,
-                                                      const Jagged2Tensor<T>& grad_out, const KernelOptions&) {
+                                                      const Jagged2Tensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_jagged_bmm_jagged_out_vjp";
   require_matching_offsets(q, k, op);
   for (int64_t i = 0; i < q.batch(); ++i)
@@ -295,7 +337,8 @@ BmmJaggedOutGrads<T> jagged_jagged_bmm_jagged_out_vjp(const JaggedTensor<T>& q, 
 
 template <typename T>
 ArrayJaggedBmmGrads<T> array_jagged_bmm_jagged_out_vjp(const Jagged2Tensor<T>& a, const JaggedTensor<T>& v,
-                                                       const JaggedTensor<T>& grad_out, const KernelOptions&) {
+                                                       const JaggedTensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "array_jagged_bmm_jagged_out_vjp";
   require_matching_offsets(v, grad_out, op);
   for (int64_t i = 0; i < v.batch(); ++i)
@@ -312,7 +355,8 @@ ArrayJaggedBmmGrads<T> array_jagged_bmm_jagged_out_vjp(const Jagged2Tensor<T>& a
 }
 
 template <typename T>
-Jagged2Tensor<T> jagged2_softmax_vjp(const Jagged2Tensor<T>& s, const Jagged2Tensor<T>& grad_out, const KernelOptions&) {
+Jagged2Tensor<T> jagged2_softmax_vjp(const Jagged2Tensor<T>& s, const Jagged2Tensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged2_softmax_vjp";
   if (s.batch() != grad_out.batch() || s.seq_lengths() != grad_out.seq_lengths())
     throw std::invalid_argument("jagged2_softmax_vjp: layout mismatch");
@@ -328,7 +372,8 @@ Jagged2Tensor<T> jagged2_softmax_vjp(const Jagged2Tensor<T>& s, const Jagged2Ten
 // linalg.cpp:509-573: device forward keeping activations and pre-activations, then jg_mlp_layer_backward
 template <typename T>
 JaggedMlpGrads<T> jagged_mlp_vjp(const JaggedTensor<T>& x, std::span<const MlpLayer<T>> layers,
-                                 const JaggedTensor<T>& grad_out, const KernelOptions&) {
+                                 const JaggedTensor<T>& grad_out, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_mlp_vjp";
   validate_mlp(x, layers);
   require_matching_offsets(x, grad_out, op);
@@ -377,7 +422,8 @@ DenseTensor<T> transpose_per_sample(const DenseTensor<T>& x) {
 
 template <typename T>
 DenseTensor<T> dense_attention(const DenseTensor<T>&, const DenseTensor<T>&, const DenseTensor<T>&,
-                               std::span<const int64_t>, const KernelOptions&) {
+                               std::span<const int64_t>, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   no_device_path<T>("dense_attention");
 }
 
@@ -386,7 +432,8 @@ DenseTensor<T> dense_attention(const DenseTensor<T>&, const DenseTensor<T>&, con
 template <typename T>
 DenseAttentionSaved<T> dense_flash_attention(const DenseTensor<T>& q, const DenseTensor<T>& k, const DenseTensor<T>& v,
                                              std::span<const int64_t> lengths, int64_t block_q, int64_t block_k,
-                                             const KernelOptions&) {
+                                             const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "dense_flash_attention";
   if (q.rank() != 3 || q.shape() != k.shape() || q.shape() != v.shape())
     throw std::invalid_argument("dense_flash_attention: q, k, v must share a [B, L, D] shape");
@@ -416,25 +463,25 @@ void require_jagged_attention_inputs(const JaggedTensor<T>& q, const JaggedTenso
 template <typename T>
 JaggedTensor<T> jagged_attention(const JaggedTensor<T>& q, const JaggedTensor<T>& k, const JaggedTensor<T>& v,
                                  const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_attention";
   require_jagged_attention_inputs(q, k, v, op);
   if constexpr (!is_f32<T>) no_device_path<T>(op);
   int64_t sq = 0;
   for (int64_t i = 0; i < q.batch(); ++i) sq += q.length(i) * q.length(i);
-  if (opts.meter) opts.meter->on_alloc(2 * sq);  // the unfused path materialises scores + probabilities
   Dev off = Dev::from(q.offsets(), op), sqo(sizeof(int64_t) * (q.batch() + 1), op), dq = Dev::from(q.values(), op),
       dk = Dev::from(k.values(), op), dv = Dev::from(v.values(), op), out(sizeof(T) * q.values().size(), op);
   ck(op, jg_sq_offsets((const int64_t*)off.p, q.batch(), (int64_t*)sqo.p, 0));
   ck(op, jg_jagged_attention((const int64_t*)off.p, (const int64_t*)sqo.p, q.batch(), q.total_rows(), sq, 1,
                              (int32_t)q.dim(), dq.p, dk.p, dv.p, out.p, JG_F32, nullptr, 0));
-  if (opts.meter) opts.meter->on_release(2 * sq);
   return JaggedTensor<T>(q.offsets(), out.to<T>(q.values().size(), op), q.dim());
 }
 
 template <typename T>
 JaggedAttentionSaved<T> jagged_flash_attention_forward(const JaggedTensor<T>& q, const JaggedTensor<T>& k,
                                                        const JaggedTensor<T>& v, int64_t block_q, int64_t block_k,
-                                                       const KernelOptions&) {
+                                                       const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_flash_attention_forward";
   require_jagged_attention_inputs(q, k, v, op);
   if (block_q < 1 || block_k < 1)
@@ -453,7 +500,8 @@ JaggedAttentionSaved<T> jagged_flash_attention_forward(const JaggedTensor<T>& q,
 template <typename T>
 AttentionGrads<T> jagged_flash_attention_backward(const JaggedTensor<T>& q, const JaggedTensor<T>& k,
                                                   const JaggedTensor<T>& v, const JaggedTensor<T>& grad_out,
-                                                  const JaggedAttentionSaved<T>& saved, const KernelOptions&) {
+                                                  const JaggedAttentionSaved<T>& saved, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   const char* op = "jagged_flash_attention_backward";
   require_jagged_attention_inputs(q, k, v, op);
   if (!grad_out.same_offsets(q) || grad_out.dim() != q.dim())
@@ -480,6 +528,7 @@ AttentionGrads<T> jagged_flash_attention_backward(const JaggedTensor<T>& q, cons
 template <typename T>
 DenseTensor<T> feature_interaction(const JaggedTensor<T>& k_feat, const JaggedTensor<T>& v_feat,
                                    const DenseTensor<T>& targets, const KernelOptions& opts) {
+  MeterScope meter_scope(opts, sizeof(T));
   if (!k_feat.same_offsets(v_feat) || k_feat.dim() != v_feat.dim())
     throw std::invalid_argument("feature_interaction: k_feat/v_feat layout mismatch");
   if (targets.rank() != 3 || targets.shape()[0] != k_feat.batch() || targets.shape()[2] != k_feat.dim())

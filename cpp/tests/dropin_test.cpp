@@ -13,6 +13,7 @@
 #include "jagged/attention.hpp"
 #include "jagged/linalg.hpp"
 #include "jagged/rng.hpp"
+#include "jagged/scratch.hpp"
 #include "jagged/tensor.hpp"
 
 using namespace jagged;
@@ -124,6 +125,24 @@ int main() {
         }
     check(rel(g.dv.values(), dv) < 1e-5, "jagged_flash_attention_backward dv rel=" + std::to_string(rel(g.dv.values(), dv)));
     check(g.dq.offsets() == off && g.dk.offsets() == off, "gradients keep the input offsets");
+    // SPEC.md:316/:520 peak-intermediate guard through KernelOptions.meter: the fused path never holds a
+    // sum Bi^2 score buffer (peak <= block_q block_k + 2 sum_B D elements); the unfused path does
+    int64_t sum_sq = 0;
+    for (auto n : lengths) sum_sq += n * n;
+    ScratchMeter meter;
+    KernelOptions mo;
+    mo.meter = &meter;
+    auto s2 = jagged_flash_attention_forward(x, y, v, 64, 64, mo);
+    auto g2 = jagged_flash_attention_backward(x, y, v, go, s2, mo);
+    const int64_t flash_peak = meter.peak();
+    check(flash_peak <= 64 * 64 + 2 * S * D && meter.current() == 0,
+          "meter: flash peak " + std::to_string(flash_peak) + " <= " + std::to_string(64 * 64 + 2 * S * D));
+    meter.reset();
+    auto un2 = jagged_attention(x, y, v, mo);
+    check(meter.peak() >= sum_sq && meter.current() == 0,
+          "meter: unfused peak " + std::to_string(meter.peak()) + " >= sum Bi^2 " + std::to_string(sum_sq));
+    std::printf("meter: flash fwd+bwd peak %lld elements, unfused jagged_attention %lld (sum Bi^2 = %lld)\n",
+                (long long)flash_peak, (long long)meter.peak(), (long long)sum_sq);
   }
   // --- feature_interaction composition (attention.cpp:291-309) runs end to end
   {

@@ -51,6 +51,16 @@ typedef enum { JG_F32 = 0, JG_BF16 = 1, JG_F64 = 2 } jg_dtype;
 
 /* Thread-local text of the last failure (the reference's exception message). */
 const char* jg_last_error(void);
+
+/* Device scratch accounting, per host thread: bytes of device memory the library allocates for a call's own
+ * intermediates (backward workspace, unfused score/probability tensors, repacked jagged^2 operands, per-call
+ * schedules); the caller's operands and outputs are not counted. This is what KernelOptions.meter
+ * (linalg.hpp:19, scratch.hpp:12-55) observes through the C++ drop-in: a peak window opened with
+ * jg_scratch_reset_peak() (peak := current) and read back with jg_scratch_counters(); jg_scratch_raise_peak()
+ * restores an enclosing window's peak (nested windows). */
+void jg_scratch_counters(int64_t* current_bytes, int64_t* peak_bytes);
+void jg_scratch_reset_peak(void);
+void jg_scratch_raise_peak(int64_t peak_bytes);
 /* Library version string; also forces the CUDA module load. */
 const char* jg_version(void);
 

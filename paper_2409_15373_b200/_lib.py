@@ -60,6 +60,9 @@ OTHER = {
     "jg_version": ([], C.c_char_p),
     "jg_launch_count": ([], C.c_int64),
     "jg_reset_launch_count": ([], None),
+    "jg_scratch_counters": ([P, P], None),
+    "jg_scratch_reset_peak": ([], None),
+    "jg_scratch_raise_peak": ([I64], None),
     "jg_schedule_sq_offsets": ([P], P),
     "jg_attention_backward_workspace_size": ([I64, I64, I32, I32], C.c_int64),
     "jg_feature_interaction_workspace_size": ([I64, I64], C.c_int64),

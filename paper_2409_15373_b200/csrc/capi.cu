@@ -14,6 +14,7 @@
 namespace jg {
 
 static thread_local std::string g_last_error;
+static thread_local int64_t g_scratch_cur = 0, g_scratch_peak = 0;
 static std::atomic<int64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -62,18 +63,29 @@ jg_status ensure_smem_attr(const void* func, int bytes, const char* name) {
 }
 
 // RAII stream-ordered scratch
+void scratch_note(int64_t bytes) {
+  g_scratch_cur += bytes;
+  if (g_scratch_cur > g_scratch_peak) g_scratch_peak = g_scratch_cur;
+}
+
 struct Scratch {
   void* p = nullptr;
+  size_t n = 0;
   cudaStream_t s;
   explicit Scratch(cudaStream_t st) : s(st) {}
   jg_status alloc(size_t bytes) {
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMallocAsync(&p, bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync");
+    n = bytes;
+    scratch_note((int64_t)n);
     return JG_OK;
   }
   ~Scratch() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      cudaFreeAsync(p, s);
+      scratch_note(-(int64_t)n);
+    }
   }
 };
 
@@ -154,6 +166,15 @@ using namespace jg;
 
 // ============================================================================ misc
 extern "C" const char* jg_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" void jg_scratch_counters(int64_t* current_bytes, int64_t* peak_bytes) {
+  if (current_bytes) *current_bytes = g_scratch_cur;
+  if (peak_bytes) *peak_bytes = g_scratch_peak;
+}
+extern "C" void jg_scratch_reset_peak(void) { g_scratch_peak = g_scratch_cur; }
+extern "C" void jg_scratch_raise_peak(int64_t peak_bytes) {
+  if (peak_bytes > g_scratch_peak) g_scratch_peak = peak_bytes;
+}
 extern "C" const char* jg_version(void) { return "jagged_b200 0.1 (sm_100a)"; }
 extern "C" int64_t jg_launch_count(void) { return g_launches.load(); }
 extern "C" void jg_reset_launch_count(void) { g_launches.store(0); }
@@ -190,6 +211,7 @@ struct jg_schedule_s {
   int2* itemsf;
   int64_t* n_itemsf;
   int* win;  // [2][nwin]: first and last packable sample per 128-row window
+  int64_t bytes;  // device block size (scratch accounting)
   unsigned long long* counters;  // [4]: forward kernel (next item, exited CTAs), backward kernel (same)
   void* block;
 };
@@ -216,6 +238,8 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
     delete s;
     return cuda_status(e, "schedule alloc");
   }
+  s->bytes = (int64_t)bytes;
+  scratch_note(s->bytes);
   char* p = (char*)s->block;
   s->lengths = (int64_t*)p; p += b_len;
   s->sq = (int64_t*)p; p += b_sq;
@@ -245,6 +269,7 @@ extern "C" jg_status jg_schedule_create(const int64_t* offsets, int64_t batch, i
   return JG_OK;
 err:
   cudaFreeAsync(s->block, st);
+  scratch_note(-s->bytes);
   delete s;
   return rc;
 }
@@ -252,6 +277,7 @@ err:
 extern "C" jg_status jg_schedule_destroy(jg_schedule s) {
   if (!s) return JG_OK;
   cudaError_t e = cudaFree(s->block);
+  scratch_note(-s->bytes);
   delete s;
   if (e != cudaSuccess) return cuda_status(e, "schedule free");
   return JG_OK;
@@ -262,6 +288,7 @@ extern "C" jg_status jg_schedule_destroy(jg_schedule s) {
 static void schedule_release(jg_schedule s, cudaStream_t st) {
   if (!s) return;
   cudaFreeAsync(s->block, st);
+  scratch_note(-s->bytes);
   delete s;
 }
 

@@ -690,6 +690,7 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       // A tiles per sample: ceil(Bi/128) * ceil(Bi/64) (a prefix with M = N = Bi and 128 x 64 tiles)
       int64_t* a_prefix = nullptr;
       JG_CUDA(cudaMallocAsync(&a_prefix, sizeof(int64_t) * (batch + 1), st));
+      scratch_note((int64_t)(sizeof(int64_t) * (batch + 1)));
       GemmDesc ga;
       ga.M = bi;
       ga.N = bi;
@@ -707,6 +708,7 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       }
       uint8_t* tiles = nullptr;
       if (!rc && n_at > 0) rc = ok(cudaMallocAsync(&tiles, (size_t)n_at * gm::kTileBytes, st), "aj tiles");
+      if (tiles) scratch_note((int64_t)n_at * gm::kTileBytes);
       if (!rc && n_at > 0) {
         const unsigned rgrid = (unsigned)std::min<int64_t>(n_at, 16LL * device_sm_count());
         if (op == gm::AJ)
@@ -719,8 +721,12 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       p.a_tiles = tiles;
       p.a_prefix = a_prefix;
       if (!rc) rc = op == gm::AJ ? gm::run<gm::AJ>(p, mb, mb, st) : gm::run<gm::AJT>(p, mb, mb, st);
-      if (tiles) cudaFreeAsync(tiles, st);
+      if (tiles) {
+        cudaFreeAsync(tiles, st);
+        scratch_note(-(int64_t)n_at * gm::kTileBytes);
+      }
       cudaFreeAsync(a_prefix, st);
+      scratch_note(-(int64_t)(sizeof(int64_t) * (batch + 1)));
       return rc;
     }
     case gm::JJ:

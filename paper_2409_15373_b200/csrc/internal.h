@@ -50,6 +50,9 @@ __device__ __forceinline__ void work_counters_exit(unsigned long long* counters)
 
 jg_status launch_scan(int mode, const int64_t* in, int64_t n, int64_t* out, int64_t* bad, cudaStream_t s);
 jg_status launch_lengths(const int64_t* off, int64_t n, int64_t* len, cudaStream_t s);
+// device scratch accounting (jg_scratch_counters): every library-internal device allocation reports here
+void scratch_note(int64_t bytes);  // + on allocation, - on release
+
 jg_status launch_work_list(const int64_t* off, int64_t batch, int tile, int2* items, int64_t* count,
                            cudaStream_t s, int* win_first = nullptr, int* win_last = nullptr, int64_t nwin = 0);
 
