@@ -185,9 +185,10 @@ jg_status jg_jagged_flash_attention_forward(const int64_t* offsets, int64_t batc
 /* attention.hpp:82-88 jagged_flash_attention_backward: recompute from (q, k, lse).
  * deterministic != 0 (the default of every wrapper): bit-identical gradients across runs, grid sizes and
  * schedules (the reference's fixed summation order, attention.cpp:252-254). The
- * tcgen05 kernel then accumulates the key tiles' partial dQ in 64-bit fixed point (2^-32 units; integer
- * adds are order-independent); 0 selects fp32 accumulation, whose last bits depend on the order in which
- * key tiles finish. The SIMT path is sequential per key and deterministic either way.
+ * tcgen05 kernel then rounds each key tile's partial dQ to a per-head power-of-two grid bounded from the
+ * inputs (max|K|, max||V||, max||dO||), so every fp32 reduce-add of the partials is exact and the sum is
+ * independent of the order in which key tiles finish; 0 selects plain fp32 accumulation (last bits
+ * order-dependent). The SIMT path is sequential per key and deterministic either way.
  * workspace: NULL or >= jg_attention_backward_workspace_size(total_rows, batch, ...) bytes of device
  * memory. A schedule (and a workspace) must not be shared by two concurrently running calls. */
 jg_status jg_jagged_flash_attention_backward(const int64_t* offsets, int64_t batch,

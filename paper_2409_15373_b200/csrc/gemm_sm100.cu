@@ -87,7 +87,7 @@ __device__ __forceinline__ void tile_range(const Params& p, int64_t& t0, int64_t
   t1 = n * (blockIdx.x + 1) / gridDim.x;
 }
 
-template <int OP>
+template <int OP, int TN = BN>
 __device__ __forceinline__ Tile tile_of(const Params& p, int64_t t, TileCursor& c) {
   if (c.i < 0) {
     c.i = upper_index(p.prefix, p.batch, t);
@@ -111,10 +111,10 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int64_t t, TileCursor& 
   if (OP == JD) { r.M = Bi; r.N = p.T; r.K = p.D; }
   if (OP == JDT) { r.M = Bi; r.N = p.D; r.K = p.T; }
   if (OP == AJT) { r.M = Bi; r.N = p.D; r.K = Bi; }
-  const int tn = (r.N + BN - 1) / BN;
+  const int tn = (r.N + TN - 1) / TN;
   const int64_t local = t - c.lo;
   r.m0 = (int)(local / tn) * BM;
-  r.n0 = (int)(local % tn) * BN;
+  r.n0 = (int)(local % tn) * TN;
   r.nk = (r.K + BK - 1) / BK;
   return r;
 }
@@ -200,10 +200,16 @@ __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restric
   }
 }
 
-template <int OP>
+// W (AJ / AJT with N >= 256): 128 x 256 output tiles computed as two 128-column halves that share each A stage
+// (the jagged^2 A operand is then read once per row block instead of once per 128 columns); the second half's B
+// stages live in the (JJJ-only) staging region, and TMEM holds two 256-column accumulators.
+template <int OP, bool W = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                                                                  const __grid_constant__ CUtensorMap tm_b, Params p) {
   using Ly = Layout<OP>;
+  constexpr int TN = W ? 2 * BN : BN;  // output tile width (TMEM columns per accumulator)
+  static_assert(!W || OP == AJ || OP == AJT, "wide tiles: AJ / AJT only");
+  static_assert(!W || Smem::kBar - Smem::kStg >= kStages * kTileBytes, "second-half B stages need the staging region");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Smem::kBar);
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     tc::tma_prefetch(&tm_a);
     tc::tma_prefetch(&tm_b);
   }
-  if (warp == 1) tc::tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tc::tmem_alloc<2 * TN>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       uint32_t cnt = 0;
       TileCursor cur;
       for (int64_t t = t_begin; t < t_end; ++t) {
-        const Tile tl = tile_of<OP>(p, t, cur);
+        const Tile tl = tile_of<OP, TN>(p, t, cur);
         for (int kb = 0; kb < tl.nk; ++kb, ++cnt) {
           const uint32_t s = cnt % kStages;
           tc::mbar_wait(empty + s, ((cnt / kStages) & 1) ^ 1);
@@ -261,11 +267,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           if (OP == JJJ) kbk = (uint64_t)(tl.b0 + tl.n0) * 65536u + (uint64_t)kb;
           if (OP == JDT) kbk = ((uint64_t)tl.i * p.D + tl.n0) * 65536u + (uint64_t)kb;
           if (OP == JD) kbk = ((uint64_t)tl.i * p.D + k0) * 65536u + (uint64_t)(tl.n0 / BN);
-          if (OP == AJ || OP == AJT) kbk = (uint64_t)(tl.b0 + k0) * 65536u + (uint64_t)(tl.n0 / BN);
+          if ((OP == AJ || OP == AJT) && !W) kbk = (uint64_t)(tl.b0 + k0) * 65536u + (uint64_t)(tl.n0 / BN);
+          const bool half2 = W && tl.n0 + BN < tl.N;  // wide tile: the second 128-column half exists
           const bool load_a = ka == ~0ull || key[s] != ka, load_b = kbk == ~0ull || key[kStages + s] != kbk;
           key[s] = ka;
           key[kStages + s] = kbk;
-          tc::mbar_expect_tx(full + s, (load_a || OP == AJ || OP == AJT ? kTileBytes : 0) + (load_b ? kTileBytes : 0));
+          tc::mbar_expect_tx(full + s, (load_a || OP == AJ || OP == AJT ? kTileBytes : 0) + (load_b ? kTileBytes : 0) +
+                                           (half2 ? kTileBytes : 0));
           if (OP == AJ || OP == AJT) {
             const int64_t at = p.a_prefix[tl.i] + (int64_t)(tl.m0 / BM) * tl.nk + kb;
             bulk_load(sa, p.a_tiles + at * kTileBytes, kTileBytes, full + s);
@@ -280,6 +288,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           if (((OP == AJ || OP == AJT) && load_b) || OP == JJ)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, OP == JJ ? 0 : p.head, (int)(tl.b0 + k0));
+          if (half2)
+            for (int c = 0; c < 2; ++c)
+              tc::tma_load_3d(smem + Smem::kStg + s * kTileBytes + c * 8192, &tm_b, full + s, tl.n0 + BN + 64 * c, p.head,
+                              (int)(tl.b0 + k0));
           if (OP == JD && load_b)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.i * p.D + k0));
@@ -293,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       uint32_t cnt = 0, tcount = 0;
       TileCursor cur;
       for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
-        const Tile tl = tile_of<OP>(p, t, cur);
+        const Tile tl = tile_of<OP, TN>(p, t, cur);
         const int ab = tcount & 1;
         tc::mbar_wait(acc_empty + ab, ((tcount >> 1) & 1) ^ 1);
         tc::tc_fence_after();
@@ -308,7 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t da = Ly::a_mn ? tc::sw128_desc(sa + kk * 2048, 8192, 1024) : tc::sw128_desc(sa + kk * 32, 16, 1024);
             const uint64_t db = Ly::b_mn ? tc::sw128_desc(sb + kk * 2048, 8192, 1024) : tc::sw128_desc(sb + kk * 32, 16, 1024);
-            tc::mma_bf16_ss(tmem + ab * BN, da, db, idesc, (kb > 0 || kk > 0));
+            tc::mma_bf16_ss(tmem + ab * TN, da, db, idesc, (kb > 0 || kk > 0));
+            if (W && tl.n0 + BN < tl.N) {
+              const uint32_t sb2 = tc::smem_u32(smem + Smem::kStg + s * kTileBytes);
+              tc::mma_bf16_ss(tmem + ab * TN + BN, da, tc::sw128_desc(sb2 + kk * 2048, 8192, 1024), idesc, (kb > 0 || kk > 0));
+            }
           }
           tc::mma_commit(empty + s);
         }
@@ -328,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     uint32_t tcount = 0;
     TileCursor cur;
     for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
-      const Tile tl = tile_of<OP>(p, t, cur);
+      const Tile tl = tile_of<OP, TN>(p, t, cur);
       const int ab = tcount & 1;
       tc::mbar_wait(acc_full + ab, (tcount >> 1) & 1);
       tc::tc_fence_after();
@@ -488,37 +504,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     // ============================================ epilogue: thread = output row of the tile
     // JD / AJ: 8 warps (TMEM lane quarter x column half, two 32-column chunks each); JJ: 4 warps (warps 8-11
     // are its loader)
-    constexpr int kHalves = Ly::loader ? 1 : 2, kChunks = BN / 32 / kHalves;
+    constexpr int kHalves = Ly::loader ? 1 : 2, kChunks = TN / 32 / kHalves;
     const int wq = warp & 3, hf = (warp - 4) >> 2, r = wq * 32 + lane;
     uint32_t tcount = 0;
     TileCursor cur;
     for (int64_t t = t_begin; t < t_end; ++t, ++tcount) {
-      const Tile tl = tile_of<OP>(p, t, cur);
+      const Tile tl = tile_of<OP, TN>(p, t, cur);
       const int ab = tcount & 1;
       tc::mbar_wait(acc_full + ab, (tcount >> 1) & 1);
       tc::tc_fence_after();
       const int m = tl.m0 + r;
       const bool row_ok = m < tl.M;
-      const int ncols = tl.N - tl.n0 < BN ? tl.N - tl.n0 : BN;
+      const int ncols = tl.N - tl.n0 < TN ? tl.N - tl.n0 : TN;
       int64_t base;  // element index of (m, n0) in the output
       if (OP == JJJ) base = tl.sqo + (int64_t)m * tl.n + tl.n0;
       else if (OP == JJ) base = tl.i * (int64_t)p.D * p.T + (int64_t)m * p.T + tl.n0;
       else base = (tl.b0 + m) * (p.out_ld ? p.out_ld : (int64_t)tl.N) + tl.n0;
-      const bool vec = OP != JJJ && ncols == BN;
+      const bool vec_tile = OP != JJJ && ncols == TN;
       // 32-byte alignment of every row start: N (or T) a multiple of 16 bf16 / 8 fp32 elements
-      const bool vec32 = vec && ((OP == JJ ? p.T : (p.out_ld ? p.out_ld : tl.N)) % (p.out_f32 ? 8 : 16)) == 0 &&
-                         (reinterpret_cast<uintptr_t>(p.out) & 31) == 0;
+      const bool vec32_ok = ((OP == JJ ? p.T : (p.out_ld ? p.out_ld : tl.N)) % (p.out_f32 ? 8 : 16)) == 0 &&
+                            (reinterpret_cast<uintptr_t>(p.out) & 31) == 0;
 #pragma unroll
       for (int cc = 0; cc < kChunks; ++cc) {
         const int c = hf * kChunks + cc;
+        if (W && c * 32 >= ncols) continue;  // wide tile without its second half
+        const bool vec = vec_tile || (W && OP != JJJ && (c + 1) * 32 <= ncols);
         uint32_t v[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * BN + c * 32, v);
+        tc::tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ab * TN + c * 32, v);
         tc::tmem_wait_ld();
         if (tl.nk == 0) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0u;
         }
         if (!row_ok) continue;
+        const bool vec32 = vec && vec32_ok;
         if (p.out_f32) {
           float* o = reinterpret_cast<float*>(p.out) + base + c * 32;
           if (vec32) {
@@ -599,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     uint32_t cnt = 0;
     TileCursor cur;
     for (int64_t t = t_begin; t < t_end; ++t) {
-      const Tile tl = tile_of<OP>(p, t, cur);
+      const Tile tl = tile_of<OP, TN>(p, t, cur);
       for (int kb = 0; kb < tl.nk; ++kb, ++cnt) {
         const uint32_t s = cnt % kStages;
         uint8_t* sa = smem + Smem::kA + s * kTileBytes;
@@ -628,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<256>(tmem);
+    tc::tmem_dealloc<2 * TN>(tmem);
   }
 }
 
@@ -637,10 +656,10 @@ static jg_status map2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t co
   return make_map(m, ptr, rows, 1, (int)cols, box_rows);
 }
 
-template <int OP>
+template <int OP, bool W = false>
 static jg_status run(const Params& p, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t st) {
-  if (jg_status rc = ensure_smem_attr((const void*)gemm_sm100_kernel<OP>, Smem::kAlloc, "gemm_sm100_kernel")) return rc;
-  gemm_sm100_kernel<OP><<<device_sm_count(), kThreads, Smem::kAlloc, st>>>(ma, mb, p);
+  if (jg_status rc = ensure_smem_attr((const void*)gemm_sm100_kernel<OP, W>, Smem::kAlloc, "gemm_sm100_kernel")) return rc;
+  gemm_sm100_kernel<OP, W><<<device_sm_count(), kThreads, Smem::kAlloc, st>>>(ma, mb, p);
   JG_LAUNCHED("gemm_sm100_kernel");
   return JG_OK;
 }
@@ -671,7 +690,9 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
   if (op == gm::JJ) { g.M = L_const(D); g.N = L_const(T); }
   if (op == gm::JD) { g.M = bi; g.N = L_const(T); }
   if (op == gm::JDT || op == gm::AJT) { g.M = bi; g.N = L_const(D); }
-  if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, 128, tile_prefix, st)) return rc;
+  // AJ / AJT with D >= 256: 128 x 256 output tiles (the jagged^2 A stages are shared by both column halves)
+  const bool wide = (op == gm::AJ || op == gm::AJT) && D >= 256;
+  if (jg_status rc = launch_gemm_prefix(g, off, sq, batch, 128, wide ? 256 : 128, tile_prefix, st)) return rc;
   gm::Params p{off, sq, tile_prefix, batch, (int)D, (int)T, (const __nv_bfloat16*)a, out, out_dt == JG_F32,
                nullptr, nullptr, std::getenv("JG_GEMM_DBG") ? std::atoi(std::getenv("JG_GEMM_DBG")) : 0,
                (const __nv_bfloat16*)bias, relu, (__nv_bfloat16*)preact, head,
@@ -720,7 +741,10 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
       }
       p.a_tiles = tiles;
       p.a_prefix = a_prefix;
-      if (!rc) rc = op == gm::AJ ? gm::run<gm::AJ>(p, mb, mb, st) : gm::run<gm::AJT>(p, mb, mb, st);
+      if (!rc) {
+        if (wide) rc = op == gm::AJ ? gm::run<gm::AJ, true>(p, mb, mb, st) : gm::run<gm::AJT, true>(p, mb, mb, st);
+        else rc = op == gm::AJ ? gm::run<gm::AJ>(p, mb, mb, st) : gm::run<gm::AJT>(p, mb, mb, st);
+      }
       if (tiles) {
         cudaFreeAsync(tiles, st);
         scratch_note(-(int64_t)n_at * gm::kTileBytes);
