@@ -149,12 +149,12 @@ static bool force_simt_gemm() {
 enum TcOp { TC_JJJ = 0, TC_AJ = 1, TC_JJ = 2, TC_JD = 3, TC_JDT = 4, TC_AJT = 5 };
 static jg_status tc_gemm(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                          int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, cudaStream_t st,
-                         int64_t sum_sq = -1) {
+                         int64_t sum_sq = -1, const AjBlocks* pre = nullptr) {
   if (batch == 0) return JG_OK;
   Scratch prefix(st);
   if (jg_status rc = prefix.alloc(sizeof(int64_t) * (batch + 1))) return rc;
   return launch_gemm_sm100(op, off, sq, batch, total_rows, D, T, a, b, out, out_dt, (int64_t*)prefix.p, st, nullptr, 0,
-                           nullptr, 1, 0, sum_sq);
+                           nullptr, 1, 0, sum_sq, pre);
 }
 static bool tc_ok(int op, int64_t D, int64_t T, jg_dtype in_dt) {
   return !force_simt_gemm() && gemm_sm100_supported(op, D, T, in_dt);
@@ -475,9 +475,14 @@ extern "C" jg_status jg_jagged_jagged_bmm_jagged_out_vjp(const int64_t* off, con
   REQUIRE(sq, JG_INVALID_ARGUMENT, "jagged_jagged_bmm_jagged_out_vjp: sq_offsets required");
   cudaStream_t st = as_stream(stream);
   if (tc_ok(TC_AJ, D, D, in_dt) && tc_ok(TC_AJT, D, D, in_dt)) {
-    // dQ = dS K (linalg.cpp:405-412): array_jagged_bmm_jagged_out; dK = dS^T Q (:413-420): the transposed form
-    if (jg_status rc = tc_gemm(TC_AJ, off, sq, batch, total_rows, D, D, go, k, dq, out_dt, st, sum_sq)) return rc;
-    return tc_gemm(TC_AJT, off, sq, batch, total_rows, D, D, go, q, dk, out_dt, st, sum_sq);
+    // dQ = dS K (linalg.cpp:405-412): array_jagged_bmm_jagged_out; dK = dS^T Q (:413-420): the transposed form.
+    // Both read dS through the same repacked 64 x 64 sub-block images: one repack pass for the two contractions.
+    AjBlocks ds;
+    if (jg_status rc = aj_repack(off, sq, batch, total_rows, sum_sq, go, &ds, st)) return rc;
+    jg_status rc = tc_gemm(TC_AJ, off, sq, batch, total_rows, D, D, go, k, dq, out_dt, st, sum_sq, &ds);
+    if (!rc) rc = tc_gemm(TC_AJT, off, sq, batch, total_rows, D, D, go, q, dk, out_dt, st, sum_sq, &ds);
+    aj_release(&ds, st);
+    return rc;
   }
   GemmDesc gq = desc(BI(), C_(D), BI(), SQ(), BI(), C_(1), OFF(D), C_(D), C_(1), OFF(D), C_(D), C_(1));
   if (jg_status rc = gemm(gq, off, sq, batch, go, k, dq, in_dt, out_dt, st)) return rc;

@@ -59,8 +59,8 @@ struct Params {
   const __nv_bfloat16* a_j2;  // AJ: jagged^2 A values
   void* out;
   int out_f32;
-  const uint8_t* a_tiles;     // AJ: repacked A stages (16 KB each)
-  const int64_t* a_prefix;    // AJ: A tiles per sample, exclusive prefix (ceil(Bi/128) * ceil(Bi/64))
+  const uint8_t* a_tiles;     // AJ / AJT: repacked 64 x 64 sub-block images (8 KB each, aj_repack_kernel)
+  const int64_t* a_prefix;    // AJ / AJT: 128 x 128 tiles per sample, exclusive prefix (sub-block base = 4x)
   int dbg;                    // JG_GEMM_DBG (diagnostic, results invalid): 1 = JJJ epilogue skips the stores
   const __nv_bfloat16* bias;  // JD only (jagged_mlp layer, bf16 out): out = act(acc + bias[col]), preact = acc + bias
   int relu;
@@ -134,34 +134,46 @@ __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t
                : "memory");
 }
 
-// AJ A-operand repack: tile t of sample i (local index = m-block * nkb + k-block) becomes the exact smem
-// image of a [128 m x 64 k] SWIZZLE_128B K-major stage with zeros past Bi. One CTA per tile; thread u
-// builds 16-byte units from two aligned 16-byte loads realigned with funnel shifts (the jagged^2 rows
-// start at arbitrary 2-byte offsets). Reads the A values once, writes ~1.1x their bytes.
-// TRANS (AJT): the tile is A_i^T's [128 m x 64 k] block as an MN-major image — two 64-wide m chunks, each 64 k rows of
-// 128 B — so unit (r = k row, c16) of chunk c reads A_i[k0 + r][m0 + 64 c + 8 c16 ...] (again a row segment).
-template <bool TRANS>
+// Jagged^2 A-operand repack (AJ and AJT): sample i's Bi x Bi block (row stride Bi, arbitrary 2-byte alignment,
+// unusable by TMA) becomes a grid of nb x nb images of 64 x 64 sub-blocks, nb = 2 ceil(Bi/128), each the exact
+// 8 KB SWIZZLE_128B image of 64 rows x 128 B (zeros past Bi). Both GEMM forms read the SAME images: an AJ stage
+// ([128 m x 64 k] K-major) is sub-blocks (m0/64, kb) and (m0/64 + 1, kb) stacked; an AJT stage (A^T's block as
+// two MN-major 64-wide chunks of 64 k rows) is sub-blocks (kb, m0/64) and (kb, m0/64 + 1) — so a VJP that needs
+// A and A^T (jagged_jagged_bmm_jagged_out: dQ = dS K, dK = dS^T Q) repacks once. Sub-block base of sample i:
+// 4 tile128_prefix[i] (nb^2 = 4 ceil(Bi/128)^2). One CTA per sub-block; thread u builds 16-byte units from two
+// aligned 16-byte loads realigned with funnel shifts.
+__device__ __forceinline__ int64_t aj_block(const int64_t* pref128, int64_t i, int Bi, int br, int bc) {
+  const int nb = 2 * ((Bi + 127) / 128);
+  return 4 * pref128[i] + (int64_t)br * nb + bc;
+}
 __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restrict__ off, const int64_t* __restrict__ sq,
-                                                        const int64_t* __restrict__ a_prefix, int64_t batch,
-                                                        const __nv_bfloat16* __restrict__ a, uint8_t* __restrict__ tiles) {
-  const int64_t n_tiles = a_prefix[batch];
+                                                        const int64_t* __restrict__ pref128, int64_t batch,
+                                                        const __nv_bfloat16* __restrict__ a, uint8_t* __restrict__ blocks) {
+  const int64_t n_blocks = 4 * pref128[batch];
   const char* base = reinterpret_cast<const char*>(a);
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const int64_t i = upper_index(a_prefix, batch, t);
-    const int Bi = (int)(off[i + 1] - off[i]);
-    const int64_t sqo = sq[i];
-    const int nkb = (Bi + BK - 1) / BK;
-    const int64_t local = t - a_prefix[i];
-    const int m0 = (int)(local / nkb) * BM, k0 = (int)(local % nkb) * BK;
-    uint8_t* dst = tiles + t * kTileBytes;
+  // each CTA takes a contiguous range of sub-blocks and walks it with a sample cursor (one search per CTA)
+  const int64_t t0 = n_blocks * blockIdx.x / gridDim.x, t1 = n_blocks * (blockIdx.x + 1) / gridDim.x;
+  if (t0 >= t1) return;
+  int64_t i = upper_index(pref128, batch, t0 >> 2), lo = 4 * pref128[i], hi = 4 * pref128[i + 1];
+  int Bi = (int)(off[i + 1] - off[i]);
+  int64_t sqo = sq[i];
+  for (int64_t t = t0; t < t1; ++t) {
+    while (t >= hi) {  // next sample with sub-blocks
+      ++i;
+      lo = hi;
+      hi = 4 * pref128[i + 1];
+      Bi = (int)(off[i + 1] - off[i]);
+      sqo = sq[i];
+    }
+    const int nb = 2 * ((Bi + 127) / 128);
+    const int64_t local = t - lo;
+    const int br = (int)(local / nb), bc = (int)(local % nb);
+    uint8_t* dst = blocks + t * (kTileBytes / 2);
 #pragma unroll
-    for (int rep = 0; rep < 4; ++rep) {
+    for (int rep = 0; rep < 2; ++rep) {
       const int u = rep * 256 + threadIdx.x;  // 16-byte unit: row u/8, column chunk u%8
       const int row = u >> 3, c16 = u & 7;
-      // source row / first column of the unit's 8 elements: A_i[m][k0 + 8 c16] (AJ) or A_i[k0 + r][m0 + 64 c + 8 c16]
-      // (AJT: chunk c = row / 64, k row r = row % 64)
-      const int m = TRANS ? k0 + (row & 63) : m0 + row;
-      const int kb0 = TRANS ? m0 + 64 * (row >> 6) + c16 * 8 : k0 + c16 * 8;
+      const int m = br * 64 + row, kb0 = bc * 64 + c16 * 8;
       const int nval = (m < Bi && kb0 < Bi) ? (Bi - kb0 < 8 ? Bi - kb0 : 8) : 0;
       uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
       int sh = 0;
@@ -194,15 +206,11 @@ __global__ void __launch_bounds__(256) aj_repack_kernel(const int64_t* __restric
           else if (2 * q + 1 >= nval) o[q] &= 0xFFFFu;
         }
       }
-      // AJ: row = m of a [128 x 128 B] K-major image; AJT: chunk row>>6 (8 KB apart) of 64 k rows -> same offsets
       *reinterpret_cast<uint4*>(dst + tc::sw128_offset(row, c16)) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }
 
-// W (AJ / AJT with N >= 256): 128 x 256 output tiles computed as two 128-column halves that share each A stage
-// (the jagged^2 A operand is then read once per row block instead of once per 128 columns); the second half's B
-// stages live in the (JJJ-only) staging region, and TMEM holds two 256-column accumulators.
 template <int OP, bool W = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                                                                  const __grid_constant__ CUtensorMap tm_b, Params p) {
@@ -274,9 +282,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           key[kStages + s] = kbk;
           tc::mbar_expect_tx(full + s, (load_a || OP == AJ || OP == AJT ? kTileBytes : 0) + (load_b ? kTileBytes : 0) +
                                            (half2 ? kTileBytes : 0));
-          if (OP == AJ || OP == AJT) {
-            const int64_t at = p.a_prefix[tl.i] + (int64_t)(tl.m0 / BM) * tl.nk + kb;
-            bulk_load(sa, p.a_tiles + at * kTileBytes, kTileBytes, full + s);
+          if (OP == AJ || OP == AJT) {  // two 8 KB sub-block images: rows m0..+63 / m0+64..+127 (AJ), chunks (AJT)
+            for (int c = 0; c < 2; ++c) {
+              const int64_t blk = OP == AJ ? aj_block(p.a_prefix, tl.i, (int)tl.n, tl.m0 / 64 + c, kb)
+                                           : aj_block(p.a_prefix, tl.i, (int)tl.n, kb, tl.m0 / 64 + c);
+              bulk_load(sa + c * (kTileBytes / 2), p.a_tiles + blk * (kTileBytes / 2), kTileBytes / 2, full + s);
+            }
           }
           if ((OP == JJJ || OP == JD || OP == JDT) && load_a)
             tc::tma_load_3d(sa, &tm_a, full + s, k0, p.head, (int)(tl.b0 + tl.m0));
@@ -676,11 +687,64 @@ bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt) {
   return false;
 }
 
+// Repack a jagged^2 operand into 64 x 64 sub-block images (aj_repack_kernel) for AJ / AJT GEMMs; the buffer is sized
+// from the host-known sum Bi^2 (sum 4 ceil(Bi/128)^2 <= sum_sq / 4096 + total_rows / 16 + 4 batch + 4), or with one
+// stream-synchronising read of the block count when it is unknown (sum_sq < 0).
+jg_status aj_repack(const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t sum_sq,
+                    const void* a, AjBlocks* out, cudaStream_t st) {
+  *out = AjBlocks{};
+  if (batch == 0) return JG_OK;
+  auto ok = [](cudaError_t e, const char* where) { return e == cudaSuccess ? JG_OK : cuda_status(e, where); };
+  if (jg_status rc = ok(cudaMallocAsync(&out->prefix, sizeof(int64_t) * (batch + 1), st), "aj prefix")) return rc;
+  out->prefix_bytes = (int64_t)sizeof(int64_t) * (batch + 1);
+  scratch_note(out->prefix_bytes);
+  GemmDesc ga;
+  Lin bi;
+  bi.bi = 1;
+  ga.M = bi;
+  ga.N = bi;
+  jg_status rc = launch_gemm_prefix(ga, off, sq, batch, 128, 128, out->prefix, st);
+  int64_t n = 0;
+  if (sum_sq >= 0) {
+    n = sum_sq / 4096 + total_rows / 16 + 4 * batch + 4;
+  } else if (!rc) {
+    rc = ok(cudaMemcpyAsync(&n, out->prefix + batch, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "aj block count");
+    if (!rc) rc = ok(cudaStreamSynchronize(st), "aj block count");
+    n *= 4;
+  }
+  out->n_blocks = n;
+  if (!rc && n > 0) {
+    rc = ok(cudaMallocAsync(&out->blocks, (size_t)n * (gm::kTileBytes / 2), st), "aj blocks");
+    if (!rc) {
+      out->blocks_bytes = n * (gm::kTileBytes / 2);
+      scratch_note(out->blocks_bytes);
+      const unsigned rgrid = (unsigned)std::min<int64_t>(n, 32LL * device_sm_count());
+      gm::aj_repack_kernel<<<rgrid, 256, 0, st>>>(off, sq, out->prefix, batch, (const __nv_bfloat16*)a, out->blocks);
+      rc = ok(cudaGetLastError(), "aj_repack_kernel");
+      count_launch();
+    }
+  }
+  if (rc) aj_release(out, st);
+  return rc;
+}
+
+void aj_release(AjBlocks* b, cudaStream_t st) {
+  if (b->blocks) {
+    cudaFreeAsync(b->blocks, st);
+    scratch_note(-b->blocks_bytes);
+  }
+  if (b->prefix) {
+    cudaFreeAsync(b->prefix, st);
+    scratch_note(-b->prefix_bytes);
+  }
+  *b = AjBlocks{};
+}
+
 // A/B roles per op: JJJ (q, k), AJ / AJT (a_j2, v), JJ (x, y), JD (x, w [B, D, T]), JDT (x [rows, T], w [B, D, T])
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
                             int64_t T, const void* a, const void* b, void* out, jg_dtype out_dt, int64_t* tile_prefix,
                             cudaStream_t st, const void* bias, int relu, void* preact, int heads, int head,
-                            int64_t sum_sq) {
+                            int64_t sum_sq, const AjBlocks* pre) {
   // tile prefix over samples with the op's (M, N)
   GemmDesc g;
   Lin bi;
@@ -708,49 +772,20 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
     case gm::AJ:
     case gm::AJT: {
       if (jg_status rc = make_map(&mb, b, rows, heads, (int)D, 64)) return rc;
-      // A tiles per sample: ceil(Bi/128) * ceil(Bi/64) (a prefix with M = N = Bi and 128 x 64 tiles)
-      int64_t* a_prefix = nullptr;
-      JG_CUDA(cudaMallocAsync(&a_prefix, sizeof(int64_t) * (batch + 1), st));
-      scratch_note((int64_t)(sizeof(int64_t) * (batch + 1)));
-      GemmDesc ga;
-      ga.M = bi;
-      ga.N = bi;
-      jg_status rc = launch_gemm_prefix(ga, off, sq, batch, 128, 64, a_prefix, st);
-      auto ok = [](cudaError_t e, const char* where) { return e == cudaSuccess ? JG_OK : cuda_status(e, where); };
-      // the repack buffer is sized from the host-known sum Bi^2: sum ceil(Bi/128) ceil(Bi/64) <= sum_sq / 8192 +
-      // 3 total_rows / 128 + batch (no device->host read); without it, one 8-byte stream-synchronising read
-      int64_t n_at = 0;
-      if (sum_sq >= 0) {
-        n_at = sum_sq / 8192 + 3 * total_rows / 128 + batch + 1;
-      } else {
-        if (!rc) rc = ok(cudaMemcpyAsync(&n_at, a_prefix + batch, sizeof(int64_t), cudaMemcpyDeviceToHost, st),
-                         "aj tile count");
-        if (!rc) rc = ok(cudaStreamSynchronize(st), "aj tile count");
+      AjBlocks own;
+      const AjBlocks* blk = pre;
+      if (!blk) {
+        if (jg_status rc = aj_repack(off, sq, batch, total_rows, sum_sq, a, &own, st)) return rc;
+        blk = &own;
       }
-      uint8_t* tiles = nullptr;
-      if (!rc && n_at > 0) rc = ok(cudaMallocAsync(&tiles, (size_t)n_at * gm::kTileBytes, st), "aj tiles");
-      if (tiles) scratch_note((int64_t)n_at * gm::kTileBytes);
-      if (!rc && n_at > 0) {
-        const unsigned rgrid = (unsigned)std::min<int64_t>(n_at, 16LL * device_sm_count());
-        if (op == gm::AJ)
-          gm::aj_repack_kernel<false><<<rgrid, 256, 0, st>>>(off, sq, a_prefix, batch, (const __nv_bfloat16*)a, tiles);
-        else
-          gm::aj_repack_kernel<true><<<rgrid, 256, 0, st>>>(off, sq, a_prefix, batch, (const __nv_bfloat16*)a, tiles);
-        rc = ok(cudaGetLastError(), "aj_repack_kernel");
-        count_launch();
-      }
-      p.a_tiles = tiles;
-      p.a_prefix = a_prefix;
-      if (!rc) {
+      p.a_tiles = blk->blocks;
+      p.a_prefix = blk->prefix;
+      jg_status rc = JG_OK;
+      if (blk->n_blocks > 0) {
         if (wide) rc = op == gm::AJ ? gm::run<gm::AJ, true>(p, mb, mb, st) : gm::run<gm::AJT, true>(p, mb, mb, st);
         else rc = op == gm::AJ ? gm::run<gm::AJ>(p, mb, mb, st) : gm::run<gm::AJT>(p, mb, mb, st);
       }
-      if (tiles) {
-        cudaFreeAsync(tiles, st);
-        scratch_note(-(int64_t)n_at * gm::kTileBytes);
-      }
-      cudaFreeAsync(a_prefix, st);
-      scratch_note(-(int64_t)(sizeof(int64_t) * (batch + 1)));
+      if (!pre) aj_release(&own, st);
       return rc;
     }
     case gm::JJ:

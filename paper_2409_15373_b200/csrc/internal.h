@@ -85,6 +85,14 @@ jg_status launch_gemm_prefix(const GemmDesc& g, const int64_t* off, const int64_
 
 // tcgen05 bmm family (bf16 inputs): op 0 jjbmm_jout (q,k), 1 ajbmm_jout (a_j2,v), 2 jjbmm (x,y), 3 jdbmm (x,w),
 // 4 x [rows, T] . w^T (w [B, D, T]) -> [rows, D], 5 a_j2^T . v -> [rows, D] (the transposed VJP forms)
+struct AjBlocks {  // a jagged^2 operand repacked into 64 x 64 SW128 sub-block images (gemm_sm100.cu)
+  uint8_t* blocks = nullptr;
+  int64_t* prefix = nullptr;  // 128 x 128 tiles per sample, exclusive prefix
+  int64_t n_blocks = 0, blocks_bytes = 0, prefix_bytes = 0;
+};
+jg_status aj_repack(const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t sum_sq,
+                    const void* a, AjBlocks* out, cudaStream_t st);
+void aj_release(AjBlocks* b, cudaStream_t st);
 bool gemm_sm100_supported(int op, int64_t D, int64_t T, jg_dtype in_dt);
 // JD only: optional fused epilogue out = act(acc + bias[col]) with preact = acc + bias (jagged_mlp layers)
 jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64_t batch, int64_t total_rows, int64_t D,
@@ -96,7 +104,9 @@ jg_status launch_gemm_sm100(int op, const int64_t* off, const int64_t* sq, int64
                             int heads = 1, int head = 0,
                             // AJ / AJT: sum Bi^2 (the jagged^2 operand's size) sizes the repack buffer without a
                             // device->host read; -1: unknown (one stream-synchronising read)
-                            int64_t sum_sq = -1);
+                            int64_t sum_sq = -1,
+                            // AJ / AJT: already repacked sub-block images of `a` (aj_repack), shared by several GEMMs
+                            const struct AjBlocks* pre = nullptr);
 
 // SURVEY §8f next rows (mlp_fi.cu)
 jg_status launch_two_offsets(int64_t* o, int64_t rows, cudaStream_t st);
