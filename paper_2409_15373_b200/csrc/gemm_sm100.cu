@@ -127,6 +127,13 @@ template <int OP> struct Layout {
   static constexpr bool loader = OP == JJ;  // stages pass through the loader warpgroup (K-tail zeroing)
 };
 
+__device__ __forceinline__ void bulk_load_hint(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                               uint64_t policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   tc::smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(tc::smem_u32(bar)), "l"(policy)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    tc::smem_u32(sdst)),
@@ -259,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       // sample JD weights across a sample's row tiles, JJJ query panels across a row of tiles. Keys identify
       // the operand block; JJ stages are rewritten by the loader (K-tail zeroing), so they always reload.
       uint64_t* key = reinterpret_cast<uint64_t*>(smem + Smem::kKeys);  // [2][kStages], producer-private
+      const uint64_t pol_first = tc::l2_policy_evict_first(), pol_last = tc::l2_policy_evict_last();
       for (int s = 0; s < 2 * kStages; ++s) key[s] = ~0ull;
       uint32_t cnt = 0;
       TileCursor cur;
@@ -286,7 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
             for (int c = 0; c < 2; ++c) {
               const int64_t blk = OP == AJ ? aj_block(p.a_prefix, tl.i, (int)tl.n, tl.m0 / 64 + c, kb)
                                            : aj_block(p.a_prefix, tl.i, (int)tl.n, kb, tl.m0 / 64 + c);
-              bulk_load(sa + c * (kTileBytes / 2), p.a_tiles + blk * (kTileBytes / 2), kTileBytes / 2, full + s);
+              // the sub-block images are read once: evict-first, so they do not push V (re-read by every row
+              // block of its sample) out of L2
+              bulk_load_hint(sa + c * (kTileBytes / 2), p.a_tiles + blk * (kTileBytes / 2), kTileBytes / 2, full + s,
+                             pol_first);
             }
           }
           if ((OP == JJJ || OP == JD || OP == JDT) && load_a)
@@ -296,13 +307,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sa + c * 8192, &tm_a, full + s, tl.m0 + 64 * c, 0, (int)(tl.b0 + k0));
           if (OP == JJJ && load_b) tc::tma_load_3d(sb, &tm_b, full + s, k0, p.head, (int)(tl.b0 + tl.n0));
-          if (((OP == AJ || OP == AJT) && load_b) || OP == JJ)
+          if ((OP == AJ || OP == AJT) && load_b)
             for (int c = 0; c < 2; ++c)
-              tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, OP == JJ ? 0 : p.head, (int)(tl.b0 + k0));
+              tc::tma_load_3d_hint(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, p.head, (int)(tl.b0 + k0), pol_last);
+          if (OP == JJ)
+            for (int c = 0; c < 2; ++c) tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.b0 + k0));
           if (half2)
             for (int c = 0; c < 2; ++c)
-              tc::tma_load_3d(smem + Smem::kStg + s * kTileBytes + c * 8192, &tm_b, full + s, tl.n0 + BN + 64 * c, p.head,
-                              (int)(tl.b0 + k0));
+              tc::tma_load_3d_hint(smem + Smem::kStg + s * kTileBytes + c * 8192, &tm_b, full + s, tl.n0 + BN + 64 * c,
+                                   p.head, (int)(tl.b0 + k0), pol_last);
           if (OP == JD && load_b)
             for (int c = 0; c < 2; ++c)
               tc::tma_load_3d(sb + c * 8192, &tm_b, full + s, tl.n0 + 64 * c, 0, (int)(tl.i * p.D + k0));
