@@ -238,14 +238,28 @@ struct Chunk {
   }
 };
 
-template <typename T>
+// LPR: lanes per row — 32 (a warp per row) or 16 (two rows per warp, one per half-warp: half the per-row
+// reduction and bookkeeping overhead per element for rows that fit)
+template <int LPR>
+__device__ __forceinline__ float grp_max(float v) {
+#pragma unroll
+  for (int m = LPR / 2; m > 0; m >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
+}
+template <int LPR>
+__device__ __forceinline__ float grp_sum(float v) {
+#pragma unroll
+  for (int m = LPR / 2; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+template <typename T, int LPR = 32>
 __device__ __forceinline__ bool j2_fits(int64_t base, int64_t n) {
   constexpr int E = Chunk<T>::E;
-  return (base + n - (base & ~(int64_t)(E - 1)) + E - 1) / E <= 32 * kCh;
+  return (base + n - (base & ~(int64_t)(E - 1)) + E - 1) / E <= LPR * kCh;
 }
 // the aligned chunks of row [base, base + n) owned by this lane; elements outside the row read as -inf (inputs:
 // weight 0) or 0 (gradients)
-template <typename T, bool kZero = false>
+template <typename T, bool kZero = false, int LPR = 32>
 __device__ __forceinline__ void j2_load(const T* __restrict__ p, int64_t base, int64_t n, int lane, uint4 (&c)[kCh]) {
   constexpr int E = Chunk<T>::E;
   constexpr uint32_t kNegInf2 = kZero ? 0u : std::is_same_v<T, float> ? 0xff800000u : 0xff80ff80u;  // fill, every element
@@ -254,9 +268,9 @@ __device__ __forceinline__ void j2_load(const T* __restrict__ p, int64_t base, i
   const int lo = (int)(base - a0), hi = lo + (int)n;
 #pragma unroll
   for (int k = 0; k < kCh; ++k) {
-    const int e0 = (lane + 32 * k) * E;
+    const int e0 = (lane + LPR * k) * E;
     c[k] = make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
-    if (e0 < hi) c[k] = __ldcs(reinterpret_cast<const uint4*>(p + a0) + lane + 32 * k);
+    if (e0 < hi) c[k] = __ldcs(reinterpret_cast<const uint4*>(p + a0) + lane + LPR * k);
     if (e0 < lo || e0 + E > hi) {  // edge chunk (at most two per row): mask the neighbours' elements
       uint32_t* w = reinterpret_cast<uint32_t*>(&c[k]);
 #pragma unroll
@@ -278,7 +292,7 @@ __device__ __forceinline__ float2 j2_pair(const uint4& c, int j) {  // elements 
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
   }
 }
-template <typename T, int MODE>
+template <typename T, int MODE, int LPR = 32>
 __device__ __forceinline__ void j2_row_regs(const uint4 (&xc)[kCh], const uint4 (&gc)[kCh], T* __restrict__ out,
                                             int64_t base, int64_t n, int lane) {
   using C = Chunk<T>;
@@ -299,7 +313,7 @@ __device__ __forceinline__ void j2_row_regs(const uint4 (&xc)[kCh], const uint4 
       m = tc::fmax3(m, __low2float(mm), __high2float(mm));
     }
   }
-  const float Ml = __fmul_rn(warp_max(m), kLog2e);
+  const float Ml = __fmul_rn(grp_max<LPR>(m), kLog2e);
   const float2 l2 = make_float2(kLog2e, kLog2e), nM = make_float2(-Ml, -Ml);
   float2 ev[kCh][P];  // 2^(y - M), kept for the output pass (one exponential per element)
   float2 sum2 = make_float2(0.f, 0.f);
@@ -312,7 +326,7 @@ __device__ __forceinline__ void j2_row_regs(const uint4 (&xc)[kCh], const uint4 
       sum2 = tc::fadd2(sum2, ev[k][j]);
     }
   }
-  const float inv = 1.0f / warp_sum(sum2.x + sum2.y);
+  const float inv = 1.0f / grp_sum<LPR>(sum2.x + sum2.y);
   const float2 inv2 = make_float2(inv, inv);
   float2 dot2 = make_float2(0.f, 0.f);
   if constexpr (MODE == 1) {
@@ -323,11 +337,11 @@ __device__ __forceinline__ void j2_row_regs(const uint4 (&xc)[kCh], const uint4 
         dot2 = tc::ffma2(j2_pair<T>(gc[k], j), tc::fmul2(ev[k][j], inv2), dot2);  // masked g elements are 0
       }
   }
-  const float dot = MODE == 1 ? warp_sum(dot2.x + dot2.y) : 0.f;
+  const float dot = MODE == 1 ? grp_sum<LPR>(dot2.x + dot2.y) : 0.f;
   const float2 nd = make_float2(-dot, -dot);
 #pragma unroll
   for (int k = 0; k < kCh; ++k) {
-    const int e0 = (lane + 32 * k) * E;
+    const int e0 = (lane + LPR * k) * E;
     if (e0 >= hi) break;
     float v[E];
 #pragma unroll
@@ -338,7 +352,7 @@ __device__ __forceinline__ void j2_row_regs(const uint4 (&xc)[kCh], const uint4 
       v[2 * j + 1] = pe.y;
     }
     if (e0 >= lo && e0 + E <= hi) {
-      __stcs(reinterpret_cast<uint4*>(out + a0) + lane + 32 * k, C::pack(v));
+      __stcs(reinterpret_cast<uint4*>(out + a0) + lane + LPR * k, C::pack(v));
     } else {
 #pragma unroll
       for (int e = 0; e < E; ++e)
@@ -391,6 +405,7 @@ __global__ void __launch_bounds__(256, 3) jagged2_softmax_kernel(const int64_t* 
                                                                                  const T* __restrict__ s,
                                                                                  const T* __restrict__ g,
                                                                                  T* __restrict__ out) {
+  static_assert(MODE == 0, "the VJP runs jagged2_softmax_vjp_kernel");
   constexpr int E = Chunk<T>::E;
   const int lane = threadIdx.x & 31;
   __shared__ int64_t coarse_sq[257];
@@ -419,8 +434,10 @@ __global__ void __launch_bounds__(256, 3) jagged2_softmax_kernel(const int64_t* 
   const bool aligned = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(out) |
                          reinterpret_cast<uintptr_t>(MODE ? g : s)) % 16) == 0;
   // register path: the row's aligned chunks fit the lane registers and stay inside the tensor
-  auto regs_ok = [&](int64_t b, int64_t len) {
-    return aligned && j2_fits<T>(b, len) && ((b + len + E - 1) & ~(int64_t)(E - 1)) <= total_al;
+  // register paths: the row's aligned chunks fit LPR lanes' registers and stay inside the tensor
+  auto regs_ok = [&](int64_t b, int64_t len, auto lpr) {
+    return aligned && j2_fits<T, decltype(lpr)::value>(b, len) &&
+           ((b + len + E - 1) & ~(int64_t)(E - 1)) <= total_al;
   };
   // advance the cursor to the next row start (rolling over empty samples); false past the warp's range
   auto settle = [&]() -> bool {
@@ -432,45 +449,58 @@ __global__ void __launch_bounds__(256, 3) jagged2_softmax_kernel(const int64_t* 
     }
     return sq_i + r * n < e_hi;
   };
-  uint4 cur[kCh], nxt[kCh], gcur[kCh];
-  if (!settle()) return;
-  int64_t base = sq_i + r * n, len = n;
-  bool cur_regs = regs_ok(base, len);
-  if (cur_regs) j2_load(s, base, len, lane, cur);
-  for (;;) {
+  using L16 = std::integral_constant<int, 16>;
+  using L32 = std::integral_constant<int, 32>;
+  // a unit: one row on the whole warp (mode 1), two consecutive short rows on the two half-warps (mode 2), or a
+  // long row on the two-pass loop (mode 3); mode 0: the warp's range is done
+  struct Unit {
+    int64_t b0, n0, b1, n1;
+    int mode;
+  };
+  auto next_unit = [&]() -> Unit {
+    Unit u{0, 0, 0, 0, 0};
+    if (!settle()) return u;
+    u.b0 = sq_i + r * n;
+    u.n0 = n;
     ++r;
-    const bool more = settle();
-    const int64_t nbase = sq_i + r * n, nlen = n;
-    const bool nxt_regs = more && regs_ok(nbase, nlen);
-    if constexpr (MODE == 0) {
-      if (nxt_regs) j2_load(s, nbase, nlen, lane, nxt);  // in flight while this row is reduced
+    if (!regs_ok(u.b0, u.n0, L32{})) {
+      u.mode = 3;
+      return u;
     }
-    if (cur_regs) {
-      if constexpr (MODE == 1) {
-        j2_load<T, true>(g, base, len, lane, gcur);
-        j2_row_regs<T, MODE>(cur, gcur, out, base, len, lane);
-      } else {
-        j2_row_regs<T, MODE>(cur, cur, out, base, len, lane);
+    u.mode = 1;
+    if (regs_ok(u.b0, u.n0, L16{}) && settle()) {
+      const int64_t b1 = sq_i + r * n;
+      if (regs_ok(b1, n, L16{})) {
+        u.b1 = b1;
+        u.n1 = n;
+        ++r;
+        u.mode = 2;
       }
-    } else {
-      j2_row_loop<T, MODE>(s, g, out, base, len, lane);
     }
-    if (!more) break;
-    base = nbase;
-    len = nlen;
-    cur_regs = nxt_regs;
-    if constexpr (MODE == 0) {
+    return u;
+  };
+  const int half = lane >> 4, sub = lane & 15;
+  auto load_unit = [&](const Unit& u, uint4 (&c)[kCh]) {
+    if (u.mode == 1) j2_load<T, false, 32>(s, u.b0, u.n0, lane, c);
+    if (u.mode == 2) j2_load<T, false, 16>(s, half ? u.b1 : u.b0, half ? u.n1 : u.n0, sub, c);
+  };
+  uint4 cur[kCh], nxt[kCh];
+  Unit uc = next_unit();
+  if (uc.mode == 0) return;
+  load_unit(uc, cur);
+  for (;;) {
+    const Unit un = next_unit();
+    load_unit(un, nxt);  // in flight while this unit is reduced
+    if (uc.mode == 1) j2_row_regs<T, MODE, 32>(cur, cur, out, uc.b0, uc.n0, lane);
+    else if (uc.mode == 2) j2_row_regs<T, MODE, 16>(cur, cur, out, half ? uc.b1 : uc.b0, half ? uc.n1 : uc.n0, sub);
+    else j2_row_loop<T, MODE>(s, g, out, uc.b0, uc.n0, lane);
+    if (un.mode == 0) break;
+    uc = un;
 #pragma unroll
-      for (int k = 0; k < kCh; ++k) cur[k] = nxt[k];
-    } else {
-      if (cur_regs) j2_load(s, base, len, lane, cur);
-    }
+    for (int k = 0; k < kCh; ++k) cur[k] = nxt[k];
   }
 }
 
-// VJP: one warp per row over a grid-stride row loop (the row's sample from a 257-point smem copy of the offsets
-// plus a short global search), two-pass loop per row. Measured faster for the VJP than the warp-range walk
-// above (2.11 vs 2.49 ms at cfg4): more rows in flight per SM.
 template <typename T>
 __global__ void __launch_bounds__(256) jagged2_softmax_vjp_kernel(const int64_t* __restrict__ off,
                                                                   const int64_t* __restrict__ sq, int64_t batch,
@@ -544,13 +574,14 @@ jg_status launch_jagged2_softmax(const int64_t* off, const int64_t* sq, int64_t 
                                                           (T*)out);
       JG_LAUNCHED("jagged2_softmax_vjp_kernel");
       return JG_OK;
-    }
-    // 24 resident warps per SM (16 for the VJP), each with its element range; the grid covers 64 ranges per SM so
-    // the per-range imbalance (one row) averages out over several waves
-    jagged2_softmax_kernel<T, M><<<8 * device_sm_count(), 256, 0, st>>>(off, sq, batch, (const T*)s, (const T*)g,
+    } else {
+      // 24 resident warps per SM, each with its element range; the grid covers 64 ranges per SM so the per-range
+      // imbalance (one row) averages out over several waves
+      jagged2_softmax_kernel<T, M><<<8 * device_sm_count(), 256, 0, st>>>(off, sq, batch, (const T*)s, (const T*)g,
                                                                          (T*)out);
-    JG_LAUNCHED("jagged2_softmax_kernel");
-    return JG_OK;
+      JG_LAUNCHED("jagged2_softmax_kernel");
+      return JG_OK;
+    }
   };
   if (dt == JG_F32) return vjp ? go(float{}, std::integral_constant<int, 1>{}) : go(float{}, std::integral_constant<int, 0>{});
   if (dt == JG_BF16)
