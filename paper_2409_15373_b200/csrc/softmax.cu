@@ -399,13 +399,12 @@ __device__ __noinline__ void j2_row_loop(const T* __restrict__ s, const T* __res
 // 1.26 ms vs 1.44 ms for a lane-strided two-pass warp per row, and 1.53 ms for a CTA variant that stages 32 KB
 // spans in shared memory with 1-D bulk copies — the bound is issue/latency per row, not load bandwidth.)
 template <typename T, int MODE>
-__global__ void __launch_bounds__(256, 3) jagged2_softmax_kernel(const int64_t* __restrict__ off,
+__global__ void __launch_bounds__(256, MODE == 0 ? 3 : 2) jagged2_softmax_kernel(const int64_t* __restrict__ off,
                                                                                  const int64_t* __restrict__ sq,
                                                                                  int64_t batch,
                                                                                  const T* __restrict__ s,
                                                                                  const T* __restrict__ g,
                                                                                  T* __restrict__ out) {
-  static_assert(MODE == 0, "the VJP runs jagged2_softmax_vjp_kernel");
   constexpr int E = Chunk<T>::E;
   const int lane = threadIdx.x & 31;
   __shared__ int64_t coarse_sq[257];
@@ -480,52 +479,36 @@ __global__ void __launch_bounds__(256, 3) jagged2_softmax_kernel(const int64_t* 
     return u;
   };
   const int half = lane >> 4, sub = lane & 15;
-  auto load_unit = [&](const Unit& u, uint4 (&c)[kCh]) {
-    if (u.mode == 1) j2_load<T, false, 32>(s, u.b0, u.n0, lane, c);
-    if (u.mode == 2) j2_load<T, false, 16>(s, half ? u.b1 : u.b0, half ? u.n1 : u.n0, sub, c);
+  auto load_unit = [&](const Unit& u, uint4 (&c)[kCh], const T* src, auto zero) {
+    constexpr bool Z = decltype(zero)::value;  // grad_out: elements outside the row read as 0
+    if (u.mode == 1) j2_load<T, Z, 32>(src, u.b0, u.n0, lane, c);
+    if (u.mode == 2) j2_load<T, Z, 16>(src, half ? u.b1 : u.b0, half ? u.n1 : u.n0, sub, c);
   };
-  uint4 cur[kCh], nxt[kCh];
+  // the VJP also keeps grad_out's chunks (x and g read once)
+  uint4 cur[kCh], nxt[kCh], gcur[MODE ? kCh : 1], gnxt[MODE ? kCh : 1];
   Unit uc = next_unit();
   if (uc.mode == 0) return;
-  load_unit(uc, cur);
+  load_unit(uc, cur, s, std::false_type{});
+  if constexpr (MODE == 1) load_unit(uc, gcur, g, std::true_type{});
   for (;;) {
     const Unit un = next_unit();
-    load_unit(un, nxt);  // in flight while this unit is reduced
-    if (uc.mode == 1) j2_row_regs<T, MODE, 32>(cur, cur, out, uc.b0, uc.n0, lane);
-    else if (uc.mode == 2) j2_row_regs<T, MODE, 16>(cur, cur, out, half ? uc.b1 : uc.b0, half ? uc.n1 : uc.n0, sub);
+    load_unit(un, nxt, s, std::false_type{});  // in flight while this unit is reduced
+    if constexpr (MODE == 1) load_unit(un, gnxt, g, std::true_type{});
+    const uint4(&gc)[kCh] = [&]() -> const uint4(&)[kCh] {
+      if constexpr (MODE == 1) return gcur;
+      else return cur;
+    }();
+    if (uc.mode == 1) j2_row_regs<T, MODE, 32>(cur, gc, out, uc.b0, uc.n0, lane);
+    else if (uc.mode == 2) j2_row_regs<T, MODE, 16>(cur, gc, out, half ? uc.b1 : uc.b0, half ? uc.n1 : uc.n0, sub);
     else j2_row_loop<T, MODE>(s, g, out, uc.b0, uc.n0, lane);
     if (un.mode == 0) break;
     uc = un;
 #pragma unroll
     for (int k = 0; k < kCh; ++k) cur[k] = nxt[k];
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) jagged2_softmax_vjp_kernel(const int64_t* __restrict__ off,
-                                                                  const int64_t* __restrict__ sq, int64_t batch,
-                                                                  int64_t total_rows, const T* __restrict__ s,
-                                                                  const T* __restrict__ g, T* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  __shared__ int64_t coarse_off[257];
-  for (int k = threadIdx.x; k <= 256; k += blockDim.x) coarse_off[k] = off[(int64_t)k * batch / 256];
-  __syncthreads();
-  if (total_rows < 0) total_rows = coarse_off[256];  // device-resident row count (no host sync)
-  for (int64_t R = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; R < total_rows;
-       R += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    int klo = 0, khi = 256;  // largest k with coarse_off[k] <= R
-    while (klo < khi) {
-      const int mid = (klo + khi + 1) >> 1;
-      if (coarse_off[mid] <= R) klo = mid; else khi = mid - 1;
+    if constexpr (MODE == 1) {
+#pragma unroll
+      for (int k = 0; k < kCh; ++k) gcur[k] = gnxt[k];
     }
-    int64_t lo = (int64_t)klo * batch / 256, hi = klo < 256 ? (int64_t)(klo + 1) * batch / 256 : batch;
-    if (hi > batch - 1) hi = batch - 1;
-    while (lo < hi) {  // sample_of_row restricted to [lo, hi]
-      const int64_t mid = (lo + hi) >> 1;
-      if (off[mid + 1] <= R) lo = mid + 1; else hi = mid;
-    }
-    const int64_t n = off[lo + 1] - off[lo];
-    j2_row_loop<T, 1>(s, g, out, sq[lo] + (R - off[lo]) * n, n, lane);
   }
 }
 
@@ -567,21 +550,12 @@ jg_status launch_jagged2_softmax(const int64_t* off, const int64_t* sq, int64_t 
   auto go = [&](auto tag, auto mode) -> jg_status {
     using T = decltype(tag);
     constexpr int M = decltype(mode)::value;
-    if constexpr (M == 1) {
-      const int grid = total_rows < 0 ? 8 * device_sm_count()
-                                      : (int)std::min<int64_t>((total_rows + 7) / 8, 16 * device_sm_count());
-      jagged2_softmax_vjp_kernel<T><<<grid, 256, 0, st>>>(off, sq, batch, total_rows, (const T*)s, (const T*)g,
-                                                          (T*)out);
-      JG_LAUNCHED("jagged2_softmax_vjp_kernel");
-      return JG_OK;
-    } else {
-      // 24 resident warps per SM, each with its element range; the grid covers 64 ranges per SM so the per-range
-      // imbalance (one row) averages out over several waves
-      jagged2_softmax_kernel<T, M><<<8 * device_sm_count(), 256, 0, st>>>(off, sq, batch, (const T*)s, (const T*)g,
-                                                                         (T*)out);
-      JG_LAUNCHED("jagged2_softmax_kernel");
-      return JG_OK;
-    }
+    // 24 (forward) / 16 (VJP) resident warps per SM, each with its element range; the grid covers 64 ranges per
+    // SM so the per-range imbalance (one row) averages out over several waves
+    jagged2_softmax_kernel<T, M><<<8 * device_sm_count(), 256, 0, st>>>(off, sq, batch, (const T*)s, (const T*)g,
+                                                                       (T*)out);
+    JG_LAUNCHED("jagged2_softmax_kernel");
+    return JG_OK;
   };
   if (dt == JG_F32) return vjp ? go(float{}, std::integral_constant<int, 1>{}) : go(float{}, std::integral_constant<int, 0>{});
   if (dt == JG_BF16)
