@@ -238,8 +238,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                          (uint32_t)it.pk_cnt);
         tc::mbar_arrive(item_full + slot);
         if (w >= n_work) break;
-        w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
-        if (it.nkv == 0) continue;  // cross mode, sample without keys: the softmax warps write zeros
+        // the next item is claimed once this item's loads are issued (the ring blocks the producer until the
+        // consumers are within a few stages of the item's end), not when it starts: with about one item per CTA
+        // (short batches) an early claim hands the second-round items to CTAs still busy with long first items
+        if (it.nkv == 0) {  // cross mode, sample without keys: the softmax warps write zeros
+          w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
+          continue;
+        }
         wp.wait(q_empty, (q_cnt++ & 1) ^ 1, 0);
         tc::mbar_expect_tx(q_full, (it.has_b ? 2 : 1) * L::kTile);
         for (int t = 0; t < (it.has_b ? 2 : 1); ++t)
@@ -256,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < L::kChunks; ++c) tc::tma_load_3d(dst + c * L::kChunk, tm, kv_full + s, c * 64, it.h, row);
           ++kv_cnt;
         }
+        w_next = (int64_t)gridDim.x + (int64_t)atomicAdd(p.work_counter, 1ull);
       }
       wp.add(7, clock64() - t_role);
       wp.flush();
