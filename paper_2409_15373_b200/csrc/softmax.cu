@@ -86,6 +86,21 @@ __device__ __forceinline__ void online_update(float& m, float& s, float y) {
   }
 }
 
+// VJP: the same running update also carries d = sum g 2^(y - m) (rescaled with s), so dot = d / s comes out of
+// the statistics pass and x is read twice instead of three times
+__device__ __forceinline__ void online_update_d(float& m, float& s, float& d, float y, float g) {
+  if (y > m) {
+    const float c = ex2a(m - y);
+    s = s * c + 1.0f;
+    d = d * c + g;
+    m = y;
+  } else if (m != -INFINITY) {
+    const float e = ex2a(y - m);
+    s += e;
+    d += g * e;
+  }
+}
+
 // Combine the kSmWarps partial (m, s) of every column held by this thread; result in m, s.
 template <int VEC>
 __device__ __forceinline__ void combine_ms(float (&m)[VEC], float (&s)[VEC], float* sm_m, float* sm_s,
@@ -125,34 +140,50 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
   const int col_local = lane * VEC;
   const int64_t col = (int64_t)blockIdx.y * 32 * VEC + col_local;
   const bool active = col < D;  // D % VEC == 0 is guaranteed by the launcher
-  float m[VEC], s[VEC];
+  float m[VEC], s[VEC], d[VEC];  // d: VJP only (sum g 2^(y - m))
 #pragma unroll
-  for (int j = 0; j < VEC; ++j) { m[j] = -INFINITY; s[j] = 0.f; }
+  for (int j = 0; j < VEC; ++j) { m[j] = -INFINITY; s[j] = 0.f; d[j] = 0.f; }
   if (active) {
     // four rows per step: their loads in flight together, one branch-free running-max update per column
     // (s = s * 2^(m - m') + sum_k 2^(y_k - m'), MUFU ex2) instead of a branchy update per element
     int64_t r = b0 + w;
     for (; r + 3 * kSmWarps < b1; r += 4 * kSmWarps) {
-      float v[4][VEC];
+      float v[4][VEC], gv[MODE ? 4 : 1][VEC];
 #pragma unroll
       for (int u = 0; u < 4; ++u) VecIO<T, VEC>::load(x + (r + u * kSmWarps) * D + col, v[u]);
+      if constexpr (MODE == 1) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) VecIO<T, VEC>::load(g + (r + u * kSmWarps) * D + col, gv[u]);
+      }
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
         const float y0 = __fmul_rn(v[0][j], kLog2e), y1 = __fmul_rn(v[1][j], kLog2e);
         const float y2 = __fmul_rn(v[2][j], kLog2e), y3 = __fmul_rn(v[3][j], kLog2e);
         const float mn = fmaxf(m[j], fmaxf(fmaxf(y0, y1), fmaxf(y2, y3)));
         const float ms = mn == -INFINITY ? 0.f : mn;  // safe max: all -inf so far gives weights 0, not NaN
-        s[j] = s[j] * ex2a(m[j] - ms) + ((ex2a(y0 - ms) + ex2a(y1 - ms)) + (ex2a(y2 - ms) + ex2a(y3 - ms)));
+        const float c = ex2a(m[j] - ms);
+        const float e0 = ex2a(y0 - ms), e1 = ex2a(y1 - ms), e2 = ex2a(y2 - ms), e3 = ex2a(y3 - ms);
+        s[j] = s[j] * c + ((e0 + e1) + (e2 + e3));
+        if constexpr (MODE == 1)
+          d[j] = d[j] * c + ((gv[0][j] * e0 + gv[1][j] * e1) + (gv[2][j] * e2 + gv[3][j] * e3));
         m[j] = mn;
       }
     }
     for (; r < b1; r += kSmWarps) {
-      float v[VEC];
+      float v[VEC], gv[VEC];
       VecIO<T, VEC>::load(x + r * D + col, v);
+      if constexpr (MODE == 1) VecIO<T, VEC>::load(g + r * D + col, gv);
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) online_update(m[j], s[j], __fmul_rn(v[j], kLog2e));
+      for (int j = 0; j < VEC; ++j) {
+        if constexpr (MODE == 1) online_update_d(m[j], s[j], d[j], __fmul_rn(v[j], kLog2e), gv[j]);
+        else online_update(m[j], s[j], __fmul_rn(v[j], kLog2e));
+      }
     }
   }
+  // VJP: fold d into the per-warp partials before combine_ms overwrites m (d_w 2^(m_w - M), summed below)
+  float mw[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) mw[j] = m[j];
   combine_ms<VEC>(m, s, sm_m, sm_s, col_local);
   float inv[VEC];
 #pragma unroll
@@ -167,28 +198,18 @@ __global__ void __launch_bounds__(kSmWarps * 32) jagged_softmax_kernel(
       VecIO<T, VEC>::store(out + r * D + col, v);
     }
   } else {
-    // dot = sum_rows g * p, then dx = p (g - dot)
+    // dot = sum_rows g p = (sum_w d_w 2^(m_w - M)) / S, then dx = p (g - dot)
     float dot[VEC];
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) dot[j] = 0.f;
-    if (active) {
-      for (int64_t r = b0 + w; r < b1; r += kSmWarps) {
-        float v[VEC], gv[VEC];
-        VecIO<T, VEC>::load(x + r * D + col, v);
-        VecIO<T, VEC>::load(g + r * D + col, gv);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) dot[j] += gv[j] * (ex2a(__fmul_rn(v[j], kLog2e) - m[j]) * inv[j]);
-      }
-    }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) sm_s[w * 32 * VEC + col_local + j] = dot[j];
+    for (int j = 0; j < VEC; ++j)
+      sm_s[w * 32 * VEC + col_local + j] = mw[j] == -INFINITY ? 0.f : d[j] * exp2f(mw[j] - m[j]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
       float t = 0.f;
       for (int ww = 0; ww < kSmWarps; ++ww) t += sm_s[ww * 32 * VEC + col_local + j];
-      dot[j] = t;
+      dot[j] = t * inv[j];
     }
     if (!active) return;
     for (int64_t r = b0 + w; r < b1; r += kSmWarps) {
