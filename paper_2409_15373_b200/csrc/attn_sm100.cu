@@ -447,15 +447,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           alpha = j == 0 ? 0.f : tc::ex2(m - mx);
           m = mx;
         }
-        // O_t is stable here: PV_t(j-1) completed before S_t(j) (in-order tcgen05 completion)
-        if (rescale) {
+        // O_t is stable here: PV_t(j-1) completed before S_t(j) (in-order tcgen05 completion). Warp-uniform
+        // (tcgen05.ld/st are .sync.aligned, so every lane takes part): rows without a rescale scale by 1
+        if (__any_sync(0xffffffffu, rescale)) {
+          const float a = rescale ? alpha : 1.f;
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
             tc::tmem_ld32(o_addr + c * 32, o);
             tc::tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * a);
             tc::tmem_st32(o_addr + c * 32, o);
           }
           tc::tmem_wait_st();
