@@ -23,4 +23,4 @@ def test_verify_leg_nccl_world1():
         v = bench.verify_sharded(1, 0, torch.device("cuda", 0), n_samples=48)
     finally:
         dist.destroy_process_group()
-    assert v["bit_identical"] and v["collective"] == "nccl" and v["samples"] == 48
+    assert v["bit_identical"] and v["unsharded_match"] and v["collective"] == "nccl" and v["samples"] == 48
