@@ -19,10 +19,11 @@
 // (offsets[i] + local row), so no padding is materialised; rows of the next sample that a tail tile
 // picks up are masked: never stored (M/N tails) or zeroed in smem before the MMA (K tails of JJ, where
 // the reduction runs over the jagged axis). Jagged^2 A operands (row stride Bi, arbitrary 2-byte
-// alignment, unusable by TMA) are first repacked by aj_repack_kernel into 16 KB tiles that are already
-// the smem image of one [128 m x 64 k] SWIZZLE_128B stage (zeros past Bi); the producer then moves each
-// stage with a single bulk copy (cp.async.bulk) — one pass of HBM traffic instead of a latency-bound
-// per-stage gather. Warps: 0 TMA producer, 1 MMA issuer, 4-11 epilogue (TMEM -> registers -> global; lane
+// alignment, unusable by TMA) are first repacked by aj_repack_kernel into 64 x 64 SWIZZLE_128B sub-block
+// images (zeros past Bi) that the AJ and AJT stages are assembled from with two 8 KB bulk copies
+// (cp.async.bulk) — one pass of HBM traffic instead of a latency-bound per-stage gather, and one repack for a
+// VJP that needs both A and A^T. AJ / AJT with D >= 256 compute 128 x 256 tiles (two column halves share each
+// A stage). Warps: 0 TMA producer, 1 MMA issuer, 4-11 epilogue (TMEM -> registers -> global; lane
 // quarter x column half; JJJ stages through smem and writes aligned 16-byte chunks; JD can fuse the jagged_mlp
 // bias + ReLU), except JJ: 4-7 epilogue and 8-11 loader (K-tail zeroing).
 #include "common.cuh"

@@ -79,7 +79,7 @@ inline jg_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int H, 
 }
 
 // 3-D map over a [rows, H, D] float32 tensor, box (D, 1, box_rows), no swizzle (bulk tensor reductions).
-// [rows, H, D] fp32 (or int32: the backward's deterministic fixed-point dQ accumulator), box (D, 1, box_rows)
+// [rows, H, D] fp32 (the backward's dQ accumulator) or int32, box (D, 1, box_rows)
 inline jg_status make_map_f32(CUtensorMap* m, void* ptr, int64_t rows, int H, int D, int box_rows, bool int32 = false) {
   auto enc = tma_encode_fn();
   if (!enc) return fail(JG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
