@@ -563,7 +563,16 @@ static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_r
     }
     return rc;
   }
-  return launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, valid, st);
+  // fp32 (or forced SIMT): tiled FFMA kernel over the (sample, 128-row tile) list
+  jg_schedule own = nullptr;
+  if (!sched) {
+    if (jg_status rc = jg_schedule_create(off, batch, total_rows, st, &own)) return rc;
+    sched = own;
+  }
+  jg_status rc = launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, sched->items,
+                                      sched->n_items, sched->max_items, valid, st);
+  if (own) schedule_release(own, st);
+  return rc;
 }
 
 static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_rows, int32_t H, int32_t D,
@@ -594,7 +603,15 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
     }
     return rc;
   }
-  return launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype, valid, st);
+  jg_schedule own = nullptr;  // fp32 (or forced SIMT): tiled FFMA kernels over the (sample, 128-row tile) list
+  if (!sched) {
+    if (jg_status rc = jg_schedule_create(off, batch, total_rows, st, &own)) return rc;
+    sched = own;
+  }
+  jg_status rc = launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype,
+                                      sched->items, sched->n_items, sched->max_items, valid, st);
+  if (own) schedule_release(own, st);
+  return rc;
 }
 
 extern "C" jg_status jg_jagged_flash_attention_forward(const int64_t* off, int64_t batch, int64_t total_rows,

@@ -125,11 +125,13 @@ jg_status launch_cast_f32(const float* a, int64_t n, void* out, jg_dtype dt, cud
 // keys past the valid length are masked, rows past it produce zeros / lse = -inf / zero gradients).
 jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, void* out, float* lse,
-                               jg_dtype dt, const int64_t* valid, cudaStream_t st);
+                               jg_dtype dt, const int2* items, const int64_t* n_items, int64_t max_items,
+                               const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, const void* go,
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
-                               float* delta, jg_dtype dt, const int64_t* valid, cudaStream_t st);
+                               float* delta, jg_dtype dt, const int2* items, const int64_t* n_items,
+                               int64_t max_items, const int64_t* valid, cudaStream_t st);
 
 // The backward workspace starts with lsd fp32
 // ([2][H][total_rows]: -lse log2(e), -Delta; then [3][H] per-head max|K|, max||V||^2, max||dO||^2)

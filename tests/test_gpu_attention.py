@@ -43,6 +43,7 @@ CASES = [
     ([0, 1, 2, 5, 7, 17, 33, 70, 130, 257], 1, 16),
     ([3, 0, 128, 129, 255, 1, 64], 2, 64),
     ([200, 5, 300, 0, 131], 2, 128),
+    ([33, 0, 1, 190, 64, 65], 3, 32),
     (list(R.gen_lengths("zipf", 512, 0, 24, 1.1)), 1, 64),
     # forward packing (layout.cu): windows with > 32 packed samples, samples crossing 128-row windows, a sample
     # filling a window, empty samples inside a pack
