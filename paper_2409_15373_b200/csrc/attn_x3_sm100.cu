@@ -1,0 +1,283 @@
+// attn_x3_sm100.cu — fp32 Jagged Flash Attention forward on tcgen05 tensor cores (split-bf16 emulation).
+//
+// Semantics: attention.cpp:172-225 in fp32 mode (the reference's float instantiation, attention.cpp:311-331),
+// same outputs as the tiled FFMA kernels in attn_simt.cu up to fp32 rounding.
+//
+// tcgen05 has no fp32 MMA. Every fp32 operand x is split into three bf16 pieces x = x1 + x2 + x3 (x1 = bf16(x),
+// x2 = bf16(x - x1), x3 = bf16(x - x1 - x2); the residual is below 2^-26 |x|), and a product a*b is the sum of
+// the piece products with i + j <= 4: a1b1 + a1b2 + a2b1 + a1b3 + a2b2 + a3b1 (the dropped terms are below
+// 2^-24 |ab|), all accumulated in fp32 in TMEM — fp32-level scores for the softmax. P in [0, 1] is split the same
+// way (two pieces leave a 2^-17 relative error per P that the cancellation in sum_k P V amplifies past 1e-5).
+// That is 6 bf16 MMAs for S and 6 for P V per block: 6x the tensor work of the bf16 kernel.
+//
+// One CTA (8 warps) per (sample, 128-row query tile, head) item of the schedule's LPT list (persistent,
+// round-robin); keys stream in 64-row blocks:
+//   all warps   stage K_j, V_j: fp32 global -> three bf16 pieces in SWIZZLE_128B smem (K K-major, V MN-major)
+//   warp 0      issues S = sum Qi Kj^T (6 x D/16 SS MMAs, M=128, N=64) into TMEM [0, 64)
+//   warps 0-3   thread = query row: online softmax (exact fp32, attention.cpp:205-214), P1 | P2 (bf16 packed
+//               two per column) back into TMEM over S and P3 at [64 + D, 96 + D): the A operands of the
+//               TS-form P V MMAs
+//   warp 0      issues P V (6 x 4 TS MMAs, N=D) into TMEM [64, 64 + D)
+//   all warps   O (registers; warp w owns lanes 32(w%4).. and half w/4 of the columns) = alpha O + P V
+// Epilogue: O / l and lse = m + log l (fp32) straight to global; padded mode masks keys / rows past `valid`.
+#include "common.cuh"
+#include "internal.h"
+#include "tc.cuh"
+
+namespace jg {
+namespace x3 {
+
+constexpr int BM = 128, BN = 64, kThreads = 256;
+constexpr float kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
+
+template <int D>
+struct Lay {
+  static constexpr int kQChunk = BM * 128;             // [128 rows x 64] bf16
+  static constexpr int kKChunk = BN * 128;             // [64 rows x 64] bf16
+  static constexpr int kQPiece = (D / 64) * kQChunk;
+  static constexpr int kKPiece = (D / 64) * kKChunk;
+  static constexpr int kQ = 0;                         // Q1 Q2 Q3
+  static constexpr int kK = kQ + 3 * kQPiece;          // K1 K2 K3 (K-major)
+  static constexpr int kV = kK + 3 * kKPiece;          // V1 V2 V3 (MN-major: key rows, 64-wide D chunks)
+  static constexpr int kBar = kV + 3 * kKPiece;        // bar_s, bar_o, tmem slot
+  static constexpr int kAlpha = kBar + 64;             // float[128]
+  static constexpr int kL = kAlpha + 4 * BM;           // float[128]
+  static constexpr int kBytes = kL + 4 * BM;
+  static constexpr int kAlloc = kBytes + 1024;         // + alignment slack
+};
+
+__device__ __forceinline__ uint32_t bf16_bits_hi(float x) {  // bf16(x) in the high half of a float
+  return __float_as_uint(__bfloat162float(__float2bfloat16_rn(x)));
+}
+
+// rows [r0, r0 + ROWS) of a fp32 [*, H, D] tensor (rows >= n zero) as three bf16 pieces, each [ROWS x D] in
+// SWIZZLE_128B 64-column chunks of ROWS x 128 B at base + piece * piece_bytes + chunk * ROWS * 128
+template <int D, int ROWS>
+__device__ __forceinline__ void stage_split3(const float* __restrict__ src, int64_t b0, int64_t r0, int64_t n,
+                                             int64_t rs, uint32_t base) {
+  constexpr int kUnits = D / 8;  // 8 floats = one 16-byte bf16 unit per piece
+  constexpr int kPiece = (D / 64) * ROWS * 128;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < ROWS * kUnits; e += kThreads) {
+    const int r = e / kUnits, u = e % kUnits;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (r0 + r < n) {
+      const float4* p = reinterpret_cast<const float4*>(src + (b0 + r0 + r) * rs + u * 8);
+      a = __ldg(p);
+      b = __ldg(p + 1);
+    }
+    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t w1[4], w2[4], w3[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float x0 = x[2 * c], x1 = x[2 * c + 1];
+      const float h0 = __uint_as_float(bf16_bits_hi(x0)), h1 = __uint_as_float(bf16_bits_hi(x1));
+      const float r0v = x0 - h0, r1v = x1 - h1;  // exact
+      const float m0 = __uint_as_float(bf16_bits_hi(r0v)), m1 = __uint_as_float(bf16_bits_hi(r1v));
+      w1[c] = tc::pack_bf16(h0, h1);
+      w2[c] = tc::pack_bf16(m0, m1);
+      w3[c] = tc::pack_bf16(r0v - m0, r1v - m1);
+    }
+    const uint32_t off = (u >> 3) * (ROWS * 128) + tc::sw128_offset(r, u & 7);
+    tc::st_shared_v4(base + off, w1[0], w1[1], w1[2], w1[3]);
+    tc::st_shared_v4(base + kPiece + off, w2[0], w2[1], w2[2], w2[3]);
+    tc::st_shared_v4(base + 2 * kPiece + off, w3[0], w3[1], w3[2], w3[3]);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    float* __restrict__ out, float* __restrict__ lse, float scale_log2, const int64_t* __restrict__ valid) {
+  using L = Lay<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  float* alpha_s = reinterpret_cast<float*>(smem + L::kAlpha);
+  float* l_s = reinterpret_cast<float*>(smem + L::kL);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;  // TMEM lane = query row in the tile
+  if (tid == 0) {
+    tc::mbar_init(bar_s, 1);
+    tc::mbar_init(bar_o, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<256>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_o = tmem + 64, t_p3 = tmem + 64 + D;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
+  constexpr int DH = D / 2;  // output columns per thread
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  uint32_t ph = 0;
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int q0 = it.y * BM;
+    float o[DH];
+#pragma unroll
+    for (int j = 0; j < DH; ++j) o[j] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    const int64_t kend = q0 < nv ? nv : 0;  // an all-padding tile attends nothing
+    __syncthreads();  // the previous item's smem / TMEM reads are done
+    if (kend > 0) stage_split3<D, BM>(q + (int64_t)h * D, b0, q0, seg, rs, sbase + L::kQ);
+    for (int64_t k0 = 0; k0 < kend; k0 += BN) {
+      stage_split3<D, BN>(k + (int64_t)h * D, b0, k0, nv, rs, sbase + L::kK);
+      stage_split3<D, BN>(v + (int64_t)h * D, b0, k0, nv, rs, sbase + L::kV);
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // S = Q1K1 + Q1K2 + Q2K1 + Q1K3 + Q2K2 + Q3K1
+        constexpr int kQi[6] = {0, 0, 1, 0, 1, 2}, kKj[6] = {0, 1, 0, 2, 1, 0};
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t qa = sbase + L::kQ + kQi[c] * L::kQPiece, ka = sbase + L::kK + kKj[c] * L::kKPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            tc::mma_bf16_ss_warp(t_s, tc::sw128_desc(qa + (kk >> 2) * L::kQChunk + (kk & 3) * 32, 16, 1024),
+                                 tc::sw128_desc(ka + (kk >> 2) * L::kKChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+          }
+        }
+        tc::mma_commit_warp(bar_s);
+      }
+      if (half == 0) {
+        tc::mbar_wait(bar_s, ph);
+        tc::tc_fence_after();
+        uint32_t sr[2][32];
+        tc::tmem_ld32(t_s + lane_off, sr[0]);
+        tc::tmem_ld32(t_s + lane_off + 32, sr[1]);
+        tc::tmem_wait_ld();
+        float s[64];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          s[j] = (k0 + j < nv) ? __uint_as_float(sr[j >> 5][j & 31]) * scale_log2 : -INFINITY;
+          mx = fmaxf(mx, s[j]);
+        }
+        const float mn = fmaxf(m, mx);  // finite: the block holds at least one valid key
+        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+        float ps = 0.f;
+        uint32_t p1[32], p2[32], p3[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float a = exp2f(s[2 * j] - mn), b = exp2f(s[2 * j + 1] - mn);
+          ps += a + b;
+          const float ha = __uint_as_float(bf16_bits_hi(a)), hb = __uint_as_float(bf16_bits_hi(b));
+          const float ra = a - ha, rb = b - hb;
+          const float ma = __uint_as_float(bf16_bits_hi(ra)), mb = __uint_as_float(bf16_bits_hi(rb));
+          p1[j] = tc::pack_bf16(ha, hb);
+          p2[j] = tc::pack_bf16(ma, mb);
+          p3[j] = tc::pack_bf16(ra - ma, rb - mb);
+        }
+        l = l * alpha + ps;
+        m = mn;
+        tc::tmem_st32(t_s + lane_off, p1);       // P1: keys 2c, 2c+1 at column c
+        tc::tmem_st32(t_s + lane_off + 32, p2);  // P2 at columns [32, 64)
+        tc::tmem_st32(t_p3 + lane_off, p3);      // P3 past O
+        tc::tmem_wait_st();
+        alpha_s[row] = alpha;
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // O_j = P1V1 + P1V2 + P2V1 + P1V3 + P2V2 + P3V1
+        constexpr int kPi[6] = {0, 0, 1, 0, 1, 2}, kVj[6] = {0, 1, 0, 2, 1, 0};
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t va = sbase + L::kV + kVj[c] * L::kKPiece;
+          const uint32_t pa = kPi[c] == 2 ? t_p3 : t_s + kPi[c] * 32;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            tc::mma_bf16_ts_warp(t_o, pa + kk * 8, tc::sw128_desc(va + kk * 16 * 128, L::kKChunk, 1024),
+                                 kIdescO, (c > 0 || kk > 0) ? 1u : 0u);
+          }
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      tc::mbar_wait(bar_o, ph);
+      tc::tc_fence_after();
+      const float alpha = alpha_s[row];
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32) {
+        uint32_t pv[32];
+        tc::tmem_ld32(t_o + lane_off + half * DH + c0, pv);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[c0 + j] = fmaf(o[c0 + j], alpha, __uint_as_float(pv[j]));
+      }
+      tc::tc_fence_before();
+      ph ^= 1;
+      __syncthreads();  // S/P, O TMEM and the K/V stages are free for the next block
+    }
+    if (half == 0) l_s[row] = l;
+    __syncthreads();
+    const int64_t r = q0 + row;
+    if (r < seg) {
+      const bool ok = r < nv;
+      const float inv = ok ? 1.0f / l_s[row] : 0.f;
+      float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + (int64_t)h * D + half * DH);
+#pragma unroll
+      for (int j = 0; j < DH; j += 4)
+        dst[j / 4] = make_float4(o[j] * inv, o[j + 1] * inv, o[j + 2] * inv, o[j + 3] * inv);
+      if (half == 0) lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(l)) * kLn2 : -INFINITY;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<256>(tmem);
+}
+
+template <int D>
+static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
+                        void* out, float* lse, const int2* items, const int64_t* n_items, int64_t max_items,
+                        const int64_t* valid, cudaStream_t st) {
+  const size_t smem = Lay<D>::kAlloc;
+  static thread_local int attr_dev = -1;  // per-device kernel attribute
+  int dev = 0;
+  JG_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    JG_CUDA(cudaFuncSetAttribute(attn_fwd_x3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_dev = dev;
+  }
+  int per_sm = 1;
+  JG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_fwd_x3_kernel<D>, kThreads, smem));
+  per_sm = std::max(1, std::min(per_sm, 2));  // TMEM: 256 columns per CTA
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)per_sm * device_sm_count()));
+  attn_fwd_x3_kernel<D><<<grid, kThreads, smem, st>>>(off, items, n_items, H, total_rows, (const float*)q,
+                                                       (const float*)k, (const float*)v, (float*)out, lse,
+                                                       kLog2e / sqrtf((float)D), valid);
+  JG_LAUNCHED("attn_fwd_x3_kernel");
+  return JG_OK;
+}
+
+}  // namespace x3
+
+bool attn_x3_supported(int head_dim, jg_dtype dt) {
+  static const bool off_ = std::getenv("JG_FP32_SIMT") != nullptr;  // A/B knob: the tiled FFMA kernels
+  return !off_ && dt == JG_F32 && (head_dim == 64 || head_dim == 128);
+}
+
+jg_status launch_attn_fwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
+                             const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
+                             int64_t max_items, const int64_t* valid, cudaStream_t st) {
+  if (total_rows == 0) return JG_OK;
+  if (D == 64) return x3::fwd_x3<64>(off, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
+  if (D == 128) return x3::fwd_x3<128>(off, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
+  return fail(JG_UNSUPPORTED, "jagged_flash_attention_forward: split-bf16 path needs head_dim 64 or 128");
+}
+
+}  // namespace jg

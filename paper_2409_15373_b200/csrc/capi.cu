@@ -569,8 +569,11 @@ static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_r
     if (jg_status rc = jg_schedule_create(off, batch, total_rows, st, &own)) return rc;
     sched = own;
   }
-  jg_status rc = launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, sched->items,
-                                      sched->n_items, sched->max_items, valid, st);
+  jg_status rc = (!force_simt() && attn_x3_supported(D, dtype))
+                     ? launch_attn_fwd_x3(off, total_rows, H, D, q, k, v, out, lse, sched->items, sched->n_items,
+                                          sched->max_items, valid, st)
+                     : launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, sched->items,
+                                            sched->n_items, sched->max_items, valid, st);
   if (own) schedule_release(own, st);
   return rc;
 }

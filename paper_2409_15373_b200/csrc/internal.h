@@ -127,6 +127,11 @@ jg_status launch_attn_fwd_simt(const int64_t* off, int64_t batch, int64_t total_
                                const void* q, const void* k, const void* v, void* out, float* lse,
                                jg_dtype dt, const int2* items, const int64_t* n_items, int64_t max_items,
                                const int64_t* valid, cudaStream_t st);
+// fp32 attention on tcgen05 through a split-bf16 emulation (attn_x3_sm100.cu), head_dim 64 / 128
+bool attn_x3_supported(int head_dim, jg_dtype dt);
+jg_status launch_attn_fwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
+                             const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
+                             int64_t max_items, const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, const void* go,
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
