@@ -397,6 +397,8 @@ __global__ void __launch_bounds__(ft::kThreads, 1) attn_bwd_tiled_kernel(
   }
 }
 
+// Delta = rowsum(dO * O), accumulated in fp64: the fp32 backward's dS = P (dP - Delta) cancels when P is
+// concentrated, so Delta's own rounding must stay well below dP's
 template <typename T>
 __global__ void attn_delta_kernel(int64_t units, int H, int D, const T* __restrict__ go,
                                   const T* __restrict__ o, int64_t total_rows, float* __restrict__ delta) {
@@ -406,10 +408,11 @@ __global__ void attn_delta_kernel(int64_t units, int H, int D, const T* __restri
     const int64_t r = u / H;
     const int h = (int)(u - r * H);
     const int64_t base = u * D;  // [r, h, :] is contiguous at (r*H + h)*D
-    float acc = 0.f;
-    for (int d = lane; d < D; d += 32) acc = fmaf(ld(go + base + d), ld(o + base + d), acc);
-    acc = warp_sum(acc);
-    if (lane == 0) delta[(int64_t)h * total_rows + r] = acc;
+    double acc = 0.0;
+    for (int d = lane; d < D; d += 32) acc = fma((double)ld(go + base + d), (double)ld(o + base + d), acc);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (lane == 0) delta[(int64_t)h * total_rows + r] = (float)acc;
   }
 }
 
@@ -588,12 +591,15 @@ template <typename T>
 static jg_status bwd_t(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D, const void* q,
                        const void* k, const void* v, const void* go, const void* o, const float* lse, void* dq,
                        void* dk, void* dv, float* delta, const int2* items, const int64_t* n_items,
-                       int64_t max_items, const int64_t* valid, cudaStream_t st) {
+                       int64_t max_items, const int64_t* valid, bool x3, cudaStream_t st) {
   const int64_t units = total_rows * H;
   const int sms = device_sm_count();
   attn_delta_kernel<T><<<(int)std::min<int64_t>((units + 7) / 8, 16 * sms), 256, 0, st>>>(
       units, H, D, (const T*)go, (const T*)o, total_rows, delta);
   JG_LAUNCHED("attn_delta_kernel");
+  if (x3 && items)  // fp32 on tcgen05 (attn_x3_sm100.cu)
+    return launch_attn_bwd_x3(off, total_rows, H, D, q, k, v, go, lse, delta, dq, dk, dv, items, n_items, max_items,
+                              valid, st);
   static const bool rowwise = std::getenv("JG_SIMT_ROWWISE") != nullptr;  // A/B knob: the row-per-warp kernels
   if (items && !rowwise) {
     if (D == 32)
@@ -636,15 +642,15 @@ jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_
                                const void* q, const void* k, const void* v, const void* go,
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
                                float* delta, jg_dtype dt, const int2* items, const int64_t* n_items,
-                               int64_t max_items, const int64_t* valid, cudaStream_t st) {
+                               int64_t max_items, const int64_t* valid, bool x3, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
   if (D > 32 * kMaxDPL) return fail(JG_UNSUPPORTED, "jagged_flash_attention_backward: head_dim > 256 unsupported");
   if (dt == JG_F32)
     return bwd_t<float>(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, items, n_items,
-                         max_items, valid, st);
+                         max_items, valid, x3, st);
   if (dt == JG_BF16)
     return bwd_t<__nv_bfloat16>(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, items, n_items,
-                                  max_items, valid, st);
+                                  max_items, valid, false, st);
   return fail(JG_UNSUPPORTED, "jagged_flash_attention_backward: dtype not supported on device (no CPU fallback)");
 }
 

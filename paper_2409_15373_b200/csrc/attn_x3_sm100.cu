@@ -8,7 +8,10 @@
 // the piece products with i + j <= 4: a1b1 + a1b2 + a2b1 + a1b3 + a2b2 + a3b1 (the dropped terms are below
 // 2^-24 |ab|), all accumulated in fp32 in TMEM — fp32-level scores for the softmax. P in [0, 1] is split the same
 // way (two pieces leave a 2^-17 relative error per P that the cancellation in sum_k P V amplifies past 1e-5).
-// That is 6 bf16 MMAs for S and 6 for P V per block: 6x the tensor work of the bf16 kernel.
+// That is 6 bf16 MMAs for S and 6 for P V per block: 6x the tensor work of the bf16 kernel. The small products
+// go first: the tensor core's fp32 accumulation truncates each addend to the running sum's exponent, so adding
+// the cross terms into an accumulator that already holds a1b1 would cost ~2^-23 |ab| per MMA; this order leaves
+// only the D/16 k-steps of a1b1 at that magnitude (the difference shows in dS = P (dP - Delta), which cancels).
 //
 // One CTA (8 warps) per (sample, 128-row query tile, head) item of the schedule's LPT list (persistent,
 // round-robin); keys stream in 64-row blocks:
@@ -140,8 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
       tc::tc_fence_before();
       __syncthreads();
       tc::tc_fence_after();
-      if (warp == 0) {  // S = Q1K1 + Q1K2 + Q2K1 + Q1K3 + Q2K2 + Q3K1
-        constexpr int kQi[6] = {0, 0, 1, 0, 1, 2}, kKj[6] = {0, 1, 0, 2, 1, 0};
+      if (warp == 0) {  // S = Q3K1 + Q2K2 + Q1K3 + Q2K1 + Q1K2 + Q1K1 (small terms first, see above)
+        constexpr int kQi[6] = {2, 1, 0, 1, 0, 0}, kKj[6] = {0, 1, 2, 0, 1, 0};
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
           const uint32_t qa = sbase + L::kQ + kQi[c] * L::kQPiece, ka = sbase + L::kK + kKj[c] * L::kKPiece;
@@ -194,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
       tc::tc_fence_before();
       __syncthreads();
       tc::tc_fence_after();
-      if (warp == 0) {  // O_j = P1V1 + P1V2 + P2V1 + P1V3 + P2V2 + P3V1
-        constexpr int kPi[6] = {0, 0, 1, 0, 1, 2}, kVj[6] = {0, 1, 0, 2, 1, 0};
+      if (warp == 0) {  // O_j = P3V1 + P2V2 + P1V3 + P2V1 + P1V2 + P1V1
+        constexpr int kPi[6] = {2, 1, 0, 1, 0, 0}, kVj[6] = {0, 1, 2, 0, 1, 0};
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
           const uint32_t va = sbase + L::kV + kVj[c] * L::kKPiece;
@@ -264,6 +267,449 @@ static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const voi
   return JG_OK;
 }
 
+
+// ------------------------------------------------------------------ backward (attention.cpp:227-289)
+// Two deterministic passes, like the FFMA kernels: query-stationary dQ, key-stationary dK / dV; every product is
+// the six-MMA split-bf16 sum. The stationary operand whose products are TS-form MMAs lives in TMEM.
+//   dQ pass   TMEM: Q1 Q2 Q3 [0, 3D/2) | S [3D/2, +64) | dP [+64) | dQ [+D) ; smem: dO pieces, K_j, V_j pieces
+//             S = Q K_j^T (TS), dP = dO V_j^T (SS); dS = P (dP - Delta) -> TMEM over S / dP; dQ += dS K_j (TS,
+//             K_j read MN-major from the same staging)
+//   dK/dV pass TMEM: K1 K2 [0, D) | S^T [D, +64) | dP^T [+64) | dV [+D) | dK [+D) ; smem: K3, V pieces, Q_j, dO_j
+//             S^T = K Q_j^T (TS for K1, K2; SS for K3), dP^T = V dO_j^T (SS); P^T -> TMEM, dV += P^T dO_j;
+//             dS^T -> TMEM, dK += dS^T Q_j
+template <int D, bool KV>
+struct BwdLay {
+  static constexpr int kXChunk = BM * 128, kYChunk = BN * 128;
+  static constexpr int kXPiece = (D / 64) * kXChunk, kYPiece = (D / 64) * kYChunk;
+  // dQ pass: X = dO (3 pieces); dK/dV pass: X = K3 then V (1 + 3 pieces)
+  static constexpr int kX = 0;
+  static constexpr int kXn = KV ? 4 : 3;
+  static constexpr int kYa = kX + kXn * kXPiece;        // K_j (dQ pass) or Q_j (dK/dV pass), 3 pieces
+  static constexpr int kYb = kYa + 3 * kYPiece;         // V_j or dO_j, 3 pieces
+  static constexpr int kBar = kYb + 3 * kYPiece;        // bar_s, bar_o, tmem slot
+  static constexpr int kLs = kBar + 64;                 // float[64] lse*log2e of the moving block (dK/dV pass)
+  static constexpr int kDs = kLs + 4 * BN;              // float[64] Delta
+  static constexpr int kBytes = kDs + 4 * BN;
+  static constexpr int kAlloc = kBytes + 1024;
+};
+
+__device__ __forceinline__ void split3(float a, float b, uint32_t& w1, uint32_t& w2, uint32_t& w3) {
+  const float ha = __uint_as_float(bf16_bits_hi(a)), hb = __uint_as_float(bf16_bits_hi(b));
+  const float ra = a - ha, rb = b - hb;
+  const float ma = __uint_as_float(bf16_bits_hi(ra)), mb = __uint_as_float(bf16_bits_hi(rb));
+  w1 = tc::pack_bf16(ha, hb);
+  w2 = tc::pack_bf16(ma, mb);
+  w3 = tc::pack_bf16(ra - ma, rb - mb);
+}
+
+// This thread's half (columns [half*D/2, +D/2)) of row `row` of a fp32 [*, H, D] tensor, split into bf16 pieces:
+// pieces 0 .. NT-1 into TMEM (piece p at column t_base + p*D/2, packed two per column), piece 2 (when NT == 2)
+// into the K-major SWIZZLE_128B smem tile at s3 ([128 rows x D], chunks of 128 x 128 B).
+template <int D, int NT>
+__device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bool in, uint32_t t_base,
+                                               uint32_t lane_off, int half, int row, uint32_t s3) {
+  constexpr int kCols = D / 4;  // packed columns per half per piece
+#pragma unroll
+  for (int c0 = 0; c0 < kCols; c0 += 8) {  // 16 elements -> 8 packed columns per step
+    uint32_t w[3][8];
+    const int e0 = half * (D / 2) + 2 * c0;  // first element
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (in) x = __ldg(reinterpret_cast<const float4*>(src + e0 + 4 * g));
+      split3(x.x, x.y, w[0][2 * g], w[1][2 * g], w[2][2 * g]);
+      split3(x.z, x.w, w[0][2 * g + 1], w[1][2 * g + 1], w[2][2 * g + 1]);
+    }
+#pragma unroll
+    for (int p = 0; p < NT; ++p) {
+      const uint32_t ta = t_base + p * (D / 2) + half * kCols + c0 + lane_off;
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+                   "r"(w[p][0]), "r"(w[p][1]), "r"(w[p][2]), "r"(w[p][3]), "r"(w[p][4]), "r"(w[p][5]), "r"(w[p][6]),
+                   "r"(w[p][7])
+                   : "memory");
+    }
+    if (NT == 2) {  // two 16-byte units (8 elements each) of the third piece
+#pragma unroll
+      for (int uu = 0; uu < 2; ++uu) {
+        const int u = e0 / 8 + uu;
+        tc::st_shared_v4(s3 + (u >> 3) * (BM * 128) + tc::sw128_offset(row, u & 7), w[2][4 * uu], w[2][4 * uu + 1],
+                         w[2][4 * uu + 2], w[2][4 * uu + 3]);
+      }
+    }
+  }
+}
+
+// tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows inside the segment store
+template <int D>
+__device__ __forceinline__ void ld_half_store(uint32_t t_acc, uint32_t lane_off, int half, float* __restrict__ dst,
+                                              float scale, bool zero, bool store) {
+#pragma unroll
+  for (int c0 = 0; c0 < D / 2; c0 += 32) {
+    uint32_t r[32];
+    tc::tmem_ld32(t_acc + lane_off + half * (D / 2) + c0, r);
+    tc::tmem_wait_ld();
+    if (!store) continue;
+    float4* d4 = reinterpret_cast<float4*>(dst + half * (D / 2) + c0);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      d4[j / 4] = zero ? make_float4(0.f, 0.f, 0.f, 0.f)
+                       : make_float4(__uint_as_float(r[j]) * scale, __uint_as_float(r[j + 1]) * scale,
+                                     __uint_as_float(r[j + 2]) * scale, __uint_as_float(r[j + 3]) * scale);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    const float* __restrict__ go, const float* __restrict__ lse, const float* __restrict__ delta,
+    float* __restrict__ dq, float scale_log2, float scale, const int64_t* __restrict__ valid) {
+  using L = BwdLay<D, false>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  if (tid == 0) {
+    tc::mbar_init(bar_s, 1);
+    tc::mbar_init(bar_o, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_q = tmem, t_s = tmem + 3 * D / 2, t_dp = t_s + 64, t_dq = t_dp + 64;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescQ = tc::idesc_bf16_f32(BM, D, false, true);
+  constexpr int kPa[6] = {2, 1, 0, 1, 0, 0}, kPb[6] = {0, 1, 2, 0, 1, 0};
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  uint32_t ph = 0;
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t hd = (int64_t)h * D, hr = (int64_t)h * total_rows;
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int q0 = it.y * BM;
+    const int64_t r = q0 + row;
+    const bool rin = r < nv;
+    const int64_t kend = q0 < nv ? nv : 0;
+    float lr = 0.f, dr = 0.f;
+    if (rin) {
+      lr = lse[hr + b0 + r] * kLog2e;
+      dr = delta[hr + b0 + r];
+    }
+    __syncthreads();  // previous item: TMEM dQ read, smem free
+    if (kend > 0) {
+      stage_row_tmem<D, 3>(q + (b0 + r) * rs + hd, rin, t_q, lane_off, half, row, 0);
+      stage_split3<D, BM>(go + hd, b0, q0, nv, rs, sbase + L::kX);
+    }
+    for (int64_t k0 = 0; k0 < kend; k0 += BN) {
+      stage_split3<D, BN>(k + hd, b0, k0, nv, rs, sbase + L::kYa);
+      stage_split3<D, BN>(v + hd, b0, k0, nv, rs, sbase + L::kYb);
+      tc::tmem_wait_st();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {  // S = sum Qa Kb^T (A = Q pieces in TMEM)
+          const uint32_t kb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_s, t_q + kPa[c] * (D / 2) + kk * 8,
+                                 tc::sw128_desc(kb + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {  // dP = sum dOa Vb^T
+          const uint32_t xa = sbase + L::kX + kPa[c] * L::kXPiece, vb = sbase + L::kYb + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ss_warp(t_dp, tc::sw128_desc(xa + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
+                                 tc::sw128_desc(vb + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_s);
+      }
+      if (half == 0) {
+        tc::mbar_wait(bar_s, ph);
+        tc::tc_fence_after();
+        uint32_t sr[64], pr[64];  // all of S and dP first: the dS pieces are written over both
+        tc::tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tc::tmem_ld32(t_s + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tc::tmem_ld32(t_dp + lane_off, *reinterpret_cast<uint32_t(*)[32]>(pr));
+        tc::tmem_ld32(t_dp + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(pr + 32));
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          const bool in = rin && (k0 + j < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[j]) * scale_log2 - lr) : 0.f;
+          sr[j] = __float_as_uint(p * (__uint_as_float(pr[j]) - dr));
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {  // dS1 over S [0, 32), dS2 over S [32, 64), dS3 over dP [0, 32)
+          uint32_t w1[16], w2[16], w3[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            split3(__uint_as_float(sr[32 * g + j]), __uint_as_float(sr[32 * g + j + 1]), w1[j / 2], w2[j / 2],
+                   w3[j / 2]);
+          tc::tmem_st16(t_s + lane_off + 16 * g, w1);
+          tc::tmem_st16(t_s + lane_off + 32 + 16 * g, w2);
+          tc::tmem_st16(t_dp + lane_off + 16 * g, w3);
+        }
+        tc::tmem_wait_st();
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // dQ += sum dSa Kb (B = K_j MN-major: key rows, 64-wide D chunks)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t pa = kPa[c] == 2 ? t_dp : t_s + kPa[c] * 32;
+          const uint32_t kb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_dq, pa + kk * 8, tc::sw128_desc(kb + kk * 16 * 128, L::kYChunk, 1024), kIdescQ,
+                                 (k0 > 0 || c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      tc::mbar_wait(bar_o, ph);
+      tc::tc_fence_after();
+      ph ^= 1;
+    }
+    ld_half_store<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, scale, !rin || kend == 0, r < seg);
+    tc::tc_fence_before();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    const float* __restrict__ go, const float* __restrict__ lse, const float* __restrict__ delta,
+    float* __restrict__ dk, float* __restrict__ dv, float scale_log2, float scale, const int64_t* __restrict__ valid) {
+  using L = BwdLay<D, true>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  float* ls = reinterpret_cast<float*>(smem + L::kLs);
+  float* dls = reinterpret_cast<float*>(smem + L::kDs);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;  // key row in the tile
+  if (tid == 0) {
+    tc::mbar_init(bar_s, 1);
+    tc::mbar_init(bar_o, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_k = tmem, t_s = tmem + D, t_dp = t_s + 64, t_dv = t_dp + 64, t_dk = t_dv + D;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
+  constexpr int kPa[6] = {2, 1, 0, 1, 0, 0}, kPb[6] = {0, 1, 2, 0, 1, 0};
+  const uint32_t s_k3 = sbase + L::kX, s_v = s_k3 + L::kXPiece;
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  uint32_t ph_s = 0, ph_o = 0;
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t hd = (int64_t)h * D, hr = (int64_t)h * total_rows;
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int x0 = it.y * BM;
+    const int64_t r = x0 + row;
+    const bool rin = r < nv;
+    const int64_t qend = x0 < nv ? nv : 0;
+    __syncthreads();
+    if (qend > 0) {
+      stage_row_tmem<D, 2>(k + (b0 + r) * rs + hd, rin, t_k, lane_off, half, row, s_k3);
+      stage_split3<D, BM>(v + hd, b0, x0, nv, rs, s_v);
+    }
+    for (int64_t y0 = 0; y0 < qend; y0 += BN) {
+      stage_split3<D, BN>(q + hd, b0, y0, nv, rs, sbase + L::kYa);
+      stage_split3<D, BN>(go + hd, b0, y0, nv, rs, sbase + L::kYb);
+      if (tid < BN) {
+        const bool in = y0 + tid < nv;
+        ls[tid] = in ? lse[hr + b0 + y0 + tid] * kLog2e : 0.f;
+        dls[tid] = in ? delta[hr + b0 + y0 + tid] : 0.f;
+      }
+      tc::tmem_wait_st();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {  // S^T = sum Ka Qb^T (K1, K2 from TMEM; K3 from smem)
+          const uint32_t qb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t bdesc = tc::sw128_desc(qb + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024);
+            const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+            if (kPa[c] < 2)
+              tc::mma_bf16_ts_warp(t_s, t_k + kPa[c] * (D / 2) + kk * 8, bdesc, kIdescS, acc);
+            else
+              tc::mma_bf16_ss_warp(t_s, tc::sw128_desc(s_k3 + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
+                                   bdesc, kIdescS, acc);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {  // dP^T = sum Va dOb^T
+          const uint32_t va = s_v + kPa[c] * L::kXPiece, ob = sbase + L::kYb + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ss_warp(t_dp, tc::sw128_desc(va + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
+                                 tc::sw128_desc(ob + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_s);
+      }
+      float dsv[64];  // dS^T (64 queries), split into TMEM once P^T's MMAs are done
+      if (half == 0) {
+        tc::mbar_wait(bar_s, ph_s);
+        tc::tc_fence_after();
+        uint32_t sr[64], pr[64];  // all of S^T and dP^T first: the P^T pieces are written over both
+        tc::tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tc::tmem_ld32(t_s + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tc::tmem_ld32(t_dp + lane_off, *reinterpret_cast<uint32_t(*)[32]>(pr));
+        tc::tmem_ld32(t_dp + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(pr + 32));
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          const bool in = rin && (y0 + j < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[j]) * scale_log2 - ls[j]) : 0.f;
+          dsv[j] = p * (__uint_as_float(pr[j]) - dls[j]);
+          sr[j] = __float_as_uint(p);
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {  // P1 [0, 32), P2 [32, 64), P3 [64, 96) of t_s; queries 32g.. at 16g
+          uint32_t p1[16], p2[16], p3[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            split3(__uint_as_float(sr[32 * g + j]), __uint_as_float(sr[32 * g + j + 1]), p1[j / 2], p2[j / 2],
+                   p3[j / 2]);
+          tc::tmem_st16(t_s + lane_off + 16 * g, p1);
+          tc::tmem_st16(t_s + lane_off + 32 + 16 * g, p2);
+          tc::tmem_st16(t_s + lane_off + 64 + 16 * g, p3);
+        }
+        tc::tmem_wait_st();
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // dV += sum P^T_a dO_b (B = dO_j MN-major)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t ob = sbase + L::kYb + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_dv, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(ob + kk * 16 * 128, L::kYChunk, 1024),
+                                 kIdescO, (y0 > 0 || c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      if (half == 0) {
+        tc::mbar_wait(bar_o, ph_o);  // the P^T pieces are consumed
+        tc::tc_fence_after();
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          uint32_t d1[16], d2[16], d3[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) split3(dsv[32 * g + j], dsv[32 * g + j + 1], d1[j / 2], d2[j / 2], d3[j / 2]);
+          tc::tmem_st16(t_s + lane_off + 16 * g, d1);
+          tc::tmem_st16(t_s + lane_off + 32 + 16 * g, d2);
+          tc::tmem_st16(t_s + lane_off + 64 + 16 * g, d3);
+        }
+        tc::tmem_wait_st();
+      }
+      ph_o ^= 1;
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // dK += sum dS^T_a Q_b (B = Q_j MN-major)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t qb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_dk, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(qb + kk * 16 * 128, L::kYChunk, 1024),
+                                 kIdescO, (y0 > 0 || c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      tc::mbar_wait(bar_o, ph_o);
+      tc::tc_fence_after();
+      ph_o ^= 1;
+      ph_s ^= 1;
+    }
+    const bool z = !rin || qend == 0;
+    ld_half_store<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, 1.f, z, r < seg);
+    ld_half_store<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, scale, z, r < seg);
+    tc::tc_fence_before();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+template <typename K>
+static jg_status prep(K kernel, size_t smem) {
+  JG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return JG_OK;
+}
+
+template <int D>
+static jg_status bwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
+                        const void* go, const float* lse, const float* delta, void* dq, void* dk, void* dv,
+                        const int2* items, const int64_t* n_items, int64_t max_items, const int64_t* valid,
+                        cudaStream_t st) {
+  // at least half the SM's shared memory: one CTA per SM, since each allocates all 512 TMEM columns
+  const size_t sm_q = std::max<size_t>(BwdLay<D, false>::kAlloc, 120 * 1024);
+  const size_t sm_kv = std::max<size_t>(BwdLay<D, true>::kAlloc, 120 * 1024);
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  JG_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    if (jg_status rc = prep(attn_bwd_x3_dq_kernel<D>, sm_q)) return rc;
+    if (jg_status rc = prep(attn_bwd_x3_dkdv_kernel<D>, sm_kv)) return rc;
+    attr_dev = dev;
+  }
+  // one CTA per SM: each allocates all 512 TMEM columns
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)device_sm_count()));
+  const float scale = 1.0f / sqrtf((float)D), scale_log2 = kLog2e * scale;
+  attn_bwd_x3_dq_kernel<D><<<grid, kThreads, sm_q, st>>>(off, items, n_items, H, total_rows, (const float*)q,
+                                                          (const float*)k, (const float*)v, (const float*)go, lse,
+                                                          delta, (float*)dq, scale_log2, scale, valid);
+  JG_LAUNCHED("attn_bwd_x3_dq_kernel");
+  attn_bwd_x3_dkdv_kernel<D><<<grid, kThreads, sm_kv, st>>>(off, items, n_items, H, total_rows, (const float*)q,
+                                                             (const float*)k, (const float*)v, (const float*)go, lse,
+                                                             delta, (float*)dk, (float*)dv, scale_log2, scale, valid);
+  JG_LAUNCHED("attn_bwd_x3_dkdv_kernel");
+  return JG_OK;
+}
 }  // namespace x3
 
 bool attn_x3_supported(int head_dim, jg_dtype dt) {
@@ -278,6 +724,20 @@ jg_status launch_attn_fwd_x3(const int64_t* off, int64_t total_rows, int H, int 
   if (D == 64) return x3::fwd_x3<64>(off, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
   if (D == 128) return x3::fwd_x3<128>(off, total_rows, H, q, k, v, out, lse, items, n_items, max_items, valid, st);
   return fail(JG_UNSUPPORTED, "jagged_flash_attention_forward: split-bf16 path needs head_dim 64 or 128");
+}
+
+jg_status launch_attn_bwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
+                             const void* v, const void* go, const float* lse, const float* delta, void* dq, void* dk,
+                             void* dv, const int2* items, const int64_t* n_items, int64_t max_items,
+                             const int64_t* valid, cudaStream_t st) {
+  if (total_rows == 0) return JG_OK;
+  if (D == 64)
+    return x3::bwd_x3<64>(off, total_rows, H, q, k, v, go, lse, delta, dq, dk, dv, items, n_items, max_items, valid,
+                          st);
+  if (D == 128)
+    return x3::bwd_x3<128>(off, total_rows, H, q, k, v, go, lse, delta, dq, dk, dv, items, n_items, max_items, valid,
+                           st);
+  return fail(JG_UNSUPPORTED, "jagged_flash_attention_backward: split-bf16 path needs head_dim 64 or 128");
 }
 
 }  // namespace jg

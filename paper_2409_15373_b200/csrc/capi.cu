@@ -612,7 +612,8 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
     sched = own;
   }
   jg_status rc = launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype,
-                                      sched->items, sched->n_items, sched->max_items, valid, st);
+                                      sched->items, sched->n_items, sched->max_items, valid,
+                                      !force_simt() && attn_x3_supported(D, dtype), st);
   if (own) schedule_release(own, st);
   return rc;
 }

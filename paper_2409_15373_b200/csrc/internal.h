@@ -132,11 +132,15 @@ bool attn_x3_supported(int head_dim, jg_dtype dt);
 jg_status launch_attn_fwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
                              const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
                              int64_t max_items, const int64_t* valid, cudaStream_t st);
+jg_status launch_attn_bwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
+                             const void* v, const void* go, const float* lse, const float* delta, void* dq, void* dk,
+                             void* dv, const int2* items, const int64_t* n_items, int64_t max_items,
+                             const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
                                const void* q, const void* k, const void* v, const void* go,
                                const void* o, const float* lse, void* dq, void* dk, void* dv,
                                float* delta, jg_dtype dt, const int2* items, const int64_t* n_items,
-                               int64_t max_items, const int64_t* valid, cudaStream_t st);
+                               int64_t max_items, const int64_t* valid, bool x3, cudaStream_t st);
 
 // The backward workspace starts with lsd fp32
 // ([2][H][total_rows]: -lse log2(e), -Delta; then [3][H] per-head max|K|, max||V||^2, max||dO||^2)
