@@ -14,13 +14,13 @@
 // only the D/16 k-steps of a1b1 at that magnitude (the difference shows in dS = P (dP - Delta), which cancels).
 //
 // One CTA (8 warps) per (sample, 128-row query tile, head) item of the schedule's LPT list (persistent,
-// round-robin); keys stream in 64-row blocks:
-//   all warps   stage K_j, V_j: fp32 global -> three bf16 pieces in SWIZZLE_128B smem (K K-major, V MN-major)
-//   warp 0      issues S = sum Qi Kj^T (6 x D/16 SS MMAs, M=128, N=64) into TMEM [0, 64)
+// round-robin); Q's pieces sit in TMEM [0, 3D/2) (split on the fly per item); keys stream in 64-row blocks through
+// two smem stages of bf16 pieces (SWIZZLE_128B; K K-major, V MN-major), split on the fly from fp32 (no scratch):
+//   warp 0      issues S = sum Qi Kj^T (6 x D/16 TS MMAs, M=128, N=64) into TMEM [3D/2, +64)
+//   warps 4-7   split block j+1 into the other stage meanwhile
 //   warps 0-3   thread = query row: online softmax (exact fp32, attention.cpp:205-214), P1 | P2 (bf16 packed
-//               two per column) back into TMEM over S and P3 at [64 + D, 96 + D): the A operands of the
-//               TS-form P V MMAs
-//   warp 0      issues P V (6 x 4 TS MMAs, N=D) into TMEM [64, 64 + D)
+//               two per column) back into TMEM over S and P3 past O: the A operands of the TS-form P V MMAs
+//   warp 0      issues P V (6 x 4 TS MMAs, N=D) into TMEM O [.., +D)
 //   all warps   O (registers; warp w owns lanes 32(w%4).. and half w/4 of the columns) = alpha O + P V
 // Epilogue: O / l and lse = m + log l (fp32) straight to global; padded mode masks keys / rows past `valid`.
 #include "common.cuh"
@@ -35,18 +35,16 @@ constexpr float kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
 
 template <int D>
 struct Lay {
-  static constexpr int kQChunk = BM * 128;             // [128 rows x 64] bf16
   static constexpr int kKChunk = BN * 128;             // [64 rows x 64] bf16
-  static constexpr int kQPiece = (D / 64) * kQChunk;
   static constexpr int kKPiece = (D / 64) * kKChunk;
-  static constexpr int kQ = 0;                         // Q1 Q2 Q3
-  static constexpr int kK = kQ + 3 * kQPiece;          // K1 K2 K3 (K-major)
-  static constexpr int kV = kK + 3 * kKPiece;          // V1 V2 V3 (MN-major: key rows, 64-wide D chunks)
-  static constexpr int kBar = kV + 3 * kKPiece;        // bar_s, bar_o, tmem slot
+  static constexpr int kStage = 6 * kKPiece;           // K1 K2 K3 V1 V2 V3 of one 64-key block
+  static constexpr int kKV = 0;                        // two stages
+  static constexpr int kBar = kKV + 2 * kStage;        // bar_s, bar_o, tmem slot
   static constexpr int kAlpha = kBar + 64;             // float[128]
   static constexpr int kL = kAlpha + 4 * BM;           // float[128]
   static constexpr int kBytes = kL + 4 * BM;
   static constexpr int kAlloc = kBytes + 1024;         // + alignment slack
+  static constexpr int kTmemCols = D == 128 ? 512 : 256;  // Q pieces 3D/2 | S 64 | O D | P3 32
 };
 
 __device__ __forceinline__ uint32_t bf16_bits_hi(float x) {  // bf16(x) in the high half of a float
@@ -55,13 +53,14 @@ __device__ __forceinline__ uint32_t bf16_bits_hi(float x) {  // bf16(x) in the h
 
 // rows [r0, r0 + ROWS) of a fp32 [*, H, D] tensor (rows >= n zero) as three bf16 pieces, each [ROWS x D] in
 // SWIZZLE_128B 64-column chunks of ROWS x 128 B at base + piece * piece_bytes + chunk * ROWS * 128
-template <int D, int ROWS>
+// (threads [T0, T0 + NT) of the CTA take part)
+template <int D, int ROWS, int T0 = 0, int NT = kThreads>
 __device__ __forceinline__ void stage_split3(const float* __restrict__ src, int64_t b0, int64_t r0, int64_t n,
                                              int64_t rs, uint32_t base) {
   constexpr int kUnits = D / 8;  // 8 floats = one 16-byte bf16 unit per piece
   constexpr int kPiece = (D / 64) * ROWS * 128;
 #pragma unroll 4
-  for (int e = threadIdx.x; e < ROWS * kUnits; e += kThreads) {
+  for (int e = (int)threadIdx.x - T0; e < ROWS * kUnits; e += NT) {
     const int r = e / kUnits, u = e % kUnits;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
     if (r0 + r < n) {
@@ -88,211 +87,6 @@ __device__ __forceinline__ void stage_split3(const float* __restrict__ src, int6
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
-    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
-    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
-    float* __restrict__ out, float* __restrict__ lse, float scale_log2, const int64_t* __restrict__ valid) {
-  using L = Lay<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sbase = tc::smem_u32(smem);
-  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* bar_o = bar_s + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
-  float* alpha_s = reinterpret_cast<float*>(smem + L::kAlpha);
-  float* l_s = reinterpret_cast<float*>(smem + L::kL);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quarter = warp & 3, half = warp >> 2;
-  const int row = quarter * 32 + lane;  // TMEM lane = query row in the tile
-  if (tid == 0) {
-    tc::mbar_init(bar_s, 1);
-    tc::mbar_init(bar_o, 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == 0) tc::tmem_alloc<256>(tmem_slot);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_o = tmem + 64, t_p3 = tmem + 64 + D;
-  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-  constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
-  constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
-  constexpr int DH = D / 2;  // output columns per thread
-  const int64_t rs = (int64_t)H * D;
-  const int64_t n_work = *n_items * H;
-  uint32_t ph = 0;
-  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-    const int2 it = items[w / H];
-    const int h = (int)(w % H);
-    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
-    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
-    const int q0 = it.y * BM;
-    float o[DH];
-#pragma unroll
-    for (int j = 0; j < DH; ++j) o[j] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    const int64_t kend = q0 < nv ? nv : 0;  // an all-padding tile attends nothing
-    __syncthreads();  // the previous item's smem / TMEM reads are done
-    if (kend > 0) stage_split3<D, BM>(q + (int64_t)h * D, b0, q0, seg, rs, sbase + L::kQ);
-    for (int64_t k0 = 0; k0 < kend; k0 += BN) {
-      stage_split3<D, BN>(k + (int64_t)h * D, b0, k0, nv, rs, sbase + L::kK);
-      stage_split3<D, BN>(v + (int64_t)h * D, b0, k0, nv, rs, sbase + L::kV);
-      tc::fence_proxy_async_smem();
-      tc::tc_fence_before();
-      __syncthreads();
-      tc::tc_fence_after();
-      if (warp == 0) {  // S = Q3K1 + Q2K2 + Q1K3 + Q2K1 + Q1K2 + Q1K1 (small terms first, see above)
-        constexpr int kQi[6] = {2, 1, 0, 1, 0, 0}, kKj[6] = {0, 1, 2, 0, 1, 0};
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const uint32_t qa = sbase + L::kQ + kQi[c] * L::kQPiece, ka = sbase + L::kK + kKj[c] * L::kKPiece;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            tc::mma_bf16_ss_warp(t_s, tc::sw128_desc(qa + (kk >> 2) * L::kQChunk + (kk & 3) * 32, 16, 1024),
-                                 tc::sw128_desc(ka + (kk >> 2) * L::kKChunk + (kk & 3) * 32, 16, 1024), kIdescS,
-                                 (c > 0 || kk > 0) ? 1u : 0u);
-          }
-        }
-        tc::mma_commit_warp(bar_s);
-      }
-      if (half == 0) {
-        tc::mbar_wait(bar_s, ph);
-        tc::tc_fence_after();
-        uint32_t sr[2][32];
-        tc::tmem_ld32(t_s + lane_off, sr[0]);
-        tc::tmem_ld32(t_s + lane_off + 32, sr[1]);
-        tc::tmem_wait_ld();
-        float s[64];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          s[j] = (k0 + j < nv) ? __uint_as_float(sr[j >> 5][j & 31]) * scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[j]);
-        }
-        const float mn = fmaxf(m, mx);  // finite: the block holds at least one valid key
-        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mn);
-        float ps = 0.f;
-        uint32_t p1[32], p2[32], p3[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float a = exp2f(s[2 * j] - mn), b = exp2f(s[2 * j + 1] - mn);
-          ps += a + b;
-          const float ha = __uint_as_float(bf16_bits_hi(a)), hb = __uint_as_float(bf16_bits_hi(b));
-          const float ra = a - ha, rb = b - hb;
-          const float ma = __uint_as_float(bf16_bits_hi(ra)), mb = __uint_as_float(bf16_bits_hi(rb));
-          p1[j] = tc::pack_bf16(ha, hb);
-          p2[j] = tc::pack_bf16(ma, mb);
-          p3[j] = tc::pack_bf16(ra - ma, rb - mb);
-        }
-        l = l * alpha + ps;
-        m = mn;
-        tc::tmem_st32(t_s + lane_off, p1);       // P1: keys 2c, 2c+1 at column c
-        tc::tmem_st32(t_s + lane_off + 32, p2);  // P2 at columns [32, 64)
-        tc::tmem_st32(t_p3 + lane_off, p3);      // P3 past O
-        tc::tmem_wait_st();
-        alpha_s[row] = alpha;
-      }
-      tc::tc_fence_before();
-      __syncthreads();
-      tc::tc_fence_after();
-      if (warp == 0) {  // O_j = P3V1 + P2V2 + P1V3 + P2V1 + P1V2 + P1V1
-        constexpr int kPi[6] = {2, 1, 0, 1, 0, 0}, kVj[6] = {0, 1, 2, 0, 1, 0};
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const uint32_t va = sbase + L::kV + kVj[c] * L::kKPiece;
-          const uint32_t pa = kPi[c] == 2 ? t_p3 : t_s + kPi[c] * 32;
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            tc::mma_bf16_ts_warp(t_o, pa + kk * 8, tc::sw128_desc(va + kk * 16 * 128, L::kKChunk, 1024),
-                                 kIdescO, (c > 0 || kk > 0) ? 1u : 0u);
-          }
-        }
-        tc::mma_commit_warp(bar_o);
-      }
-      tc::mbar_wait(bar_o, ph);
-      tc::tc_fence_after();
-      const float alpha = alpha_s[row];
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) {
-        uint32_t pv[32];
-        tc::tmem_ld32(t_o + lane_off + half * DH + c0, pv);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[c0 + j] = fmaf(o[c0 + j], alpha, __uint_as_float(pv[j]));
-      }
-      tc::tc_fence_before();
-      ph ^= 1;
-      __syncthreads();  // S/P, O TMEM and the K/V stages are free for the next block
-    }
-    if (half == 0) l_s[row] = l;
-    __syncthreads();
-    const int64_t r = q0 + row;
-    if (r < seg) {
-      const bool ok = r < nv;
-      const float inv = ok ? 1.0f / l_s[row] : 0.f;
-      float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + (int64_t)h * D + half * DH);
-#pragma unroll
-      for (int j = 0; j < DH; j += 4)
-        dst[j / 4] = make_float4(o[j] * inv, o[j + 1] * inv, o[j + 2] * inv, o[j + 3] * inv);
-      if (half == 0) lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(l)) * kLn2 : -INFINITY;
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<256>(tmem);
-}
-
-template <int D>
-static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
-                        void* out, float* lse, const int2* items, const int64_t* n_items, int64_t max_items,
-                        const int64_t* valid, cudaStream_t st) {
-  const size_t smem = Lay<D>::kAlloc;
-  static thread_local int attr_dev = -1;  // per-device kernel attribute
-  int dev = 0;
-  JG_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    JG_CUDA(cudaFuncSetAttribute(attn_fwd_x3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_dev = dev;
-  }
-  int per_sm = 1;
-  JG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_fwd_x3_kernel<D>, kThreads, smem));
-  per_sm = std::max(1, std::min(per_sm, 2));  // TMEM: 256 columns per CTA
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)per_sm * device_sm_count()));
-  attn_fwd_x3_kernel<D><<<grid, kThreads, smem, st>>>(off, items, n_items, H, total_rows, (const float*)q,
-                                                       (const float*)k, (const float*)v, (float*)out, lse,
-                                                       kLog2e / sqrtf((float)D), valid);
-  JG_LAUNCHED("attn_fwd_x3_kernel");
-  return JG_OK;
-}
-
-
-// ------------------------------------------------------------------ backward (attention.cpp:227-289)
-// Two deterministic passes, like the FFMA kernels: query-stationary dQ, key-stationary dK / dV; every product is
-// the six-MMA split-bf16 sum. The stationary operand whose products are TS-form MMAs lives in TMEM.
-//   dQ pass   TMEM: Q1 Q2 Q3 [0, 3D/2) | S [3D/2, +64) | dP [+64) | dQ [+D) ; smem: dO pieces, K_j, V_j pieces
-//             S = Q K_j^T (TS), dP = dO V_j^T (SS); dS = P (dP - Delta) -> TMEM over S / dP; dQ += dS K_j (TS,
-//             K_j read MN-major from the same staging)
-//   dK/dV pass TMEM: K1 K2 [0, D) | S^T [D, +64) | dP^T [+64) | dV [+D) | dK [+D) ; smem: K3, V pieces, Q_j, dO_j
-//             S^T = K Q_j^T (TS for K1, K2; SS for K3), dP^T = V dO_j^T (SS); P^T -> TMEM, dV += P^T dO_j;
-//             dS^T -> TMEM, dK += dS^T Q_j
-template <int D, bool KV>
-struct BwdLay {
-  static constexpr int kXChunk = BM * 128, kYChunk = BN * 128;
-  static constexpr int kXPiece = (D / 64) * kXChunk, kYPiece = (D / 64) * kYChunk;
-  // dQ pass: X = dO (3 pieces); dK/dV pass: X = K3 then V (1 + 3 pieces)
-  static constexpr int kX = 0;
-  static constexpr int kXn = KV ? 4 : 3;
-  static constexpr int kYa = kX + kXn * kXPiece;        // K_j (dQ pass) or Q_j (dK/dV pass), 3 pieces
-  static constexpr int kYb = kYa + 3 * kYPiece;         // V_j or dO_j, 3 pieces
-  static constexpr int kBar = kYb + 3 * kYPiece;        // bar_s, bar_o, tmem slot
-  static constexpr int kLs = kBar + 64;                 // float[64] lse*log2e of the moving block (dK/dV pass)
-  static constexpr int kDs = kLs + 4 * BN;              // float[64] Delta
-  static constexpr int kBytes = kDs + 4 * BN;
-  static constexpr int kAlloc = kBytes + 1024;
-};
-
 __device__ __forceinline__ void split3(float a, float b, uint32_t& w1, uint32_t& w2, uint32_t& w3) {
   const float ha = __uint_as_float(bf16_bits_hi(a)), hb = __uint_as_float(bf16_bits_hi(b));
   const float ra = a - ha, rb = b - hb;
@@ -303,9 +97,9 @@ __device__ __forceinline__ void split3(float a, float b, uint32_t& w1, uint32_t&
 }
 
 // This thread's half (columns [half*D/2, +D/2)) of row `row` of a fp32 [*, H, D] tensor, split into bf16 pieces:
-// pieces 0 .. NT-1 into TMEM (piece p at column t_base + p*D/2, packed two per column), piece 2 (when NT == 2)
+// pieces 0 .. NT-1 into TMEM (piece p at column t_base + p*D/2, packed two per column), piece 2 (when kS3)
 // into the K-major SWIZZLE_128B smem tile at s3 ([128 rows x D], chunks of 128 x 128 B).
-template <int D, int NT>
+template <int D, int NT, bool kS3 = false>
 __device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bool in, uint32_t t_base,
                                                uint32_t lane_off, int half, int row, uint32_t s3) {
   constexpr int kCols = D / 4;  // packed columns per half per piece
@@ -328,7 +122,7 @@ __device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bo
                    "r"(w[p][7])
                    : "memory");
     }
-    if (NT == 2) {  // two 16-byte units (8 elements each) of the third piece
+    if (kS3) {  // two 16-byte units (8 elements each) of the third piece
 #pragma unroll
       for (int uu = 0; uu < 2; ++uu) {
         const int u = e0 / 8 + uu;
@@ -338,6 +132,210 @@ __device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bo
     }
   }
 }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    float* __restrict__ out, float* __restrict__ lse, float scale_log2, const int64_t* __restrict__ valid) {
+  using L = Lay<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  float* alpha_s = reinterpret_cast<float*>(smem + L::kAlpha);
+  float* l_s = reinterpret_cast<float*>(smem + L::kL);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;  // TMEM lane = query row in the tile
+  if (tid == 0) {
+    tc::mbar_init(bar_s, 1);
+    tc::mbar_init(bar_o, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<L::kTmemCols>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_q = tmem, t_s = tmem + 3 * D / 2, t_o = t_s + 64, t_p3 = t_o + D;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
+  constexpr int DH = D / 2;  // output columns per thread
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  uint32_t ph = 0;
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int q0 = it.y * BM;
+    float o[DH];
+#pragma unroll
+    for (int j = 0; j < DH; ++j) o[j] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    const int64_t kend = q0 < nv ? nv : 0;  // an all-padding tile attends nothing
+    const int nblk = (int)((kend + BN - 1) / BN);
+    __syncthreads();  // the previous item's smem / TMEM reads are done
+    if (nblk > 0) {  // Q pieces into TMEM, block 0 into stage 0
+      stage_row_tmem<D, 3>(q + (b0 + q0 + row) * rs + (int64_t)h * D, q0 + row < seg, t_q, lane_off, half, row, 0);
+      stage_split3<D, BN>(k + (int64_t)h * D, b0, 0, nv, rs, sbase);
+      stage_split3<D, BN>(v + (int64_t)h * D, b0, 0, nv, rs, sbase + 3 * L::kKPiece);
+    }
+    for (int j = 0; j < nblk; ++j) {
+      const int64_t k0 = (int64_t)j * BN;
+      const int st = j & 1;
+      const uint32_t kv = sbase + st * L::kStage;
+      tc::tmem_wait_st();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // S = Q3K1 + Q2K2 + Q1K3 + Q2K1 + Q1K2 + Q1K1 (small terms first, see above)
+        constexpr int kQi[6] = {2, 1, 0, 1, 0, 0}, kKj[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t ka = kv + kKj[c] * L::kKPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_s, t_q + kQi[c] * (D / 2) + kk * 8,
+                                 tc::sw128_desc(ka + (kk >> 2) * L::kKChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_s);
+      }
+      if (half == 1 && j + 1 < nblk) {  // warps 4-7 split block j + 1 into the other stage (block j - 1's is free)
+        const uint32_t nx = sbase + (st ^ 1) * L::kStage;
+        stage_split3<D, BN, 128, 128>(k + (int64_t)h * D, b0, k0 + BN, nv, rs, nx);
+        stage_split3<D, BN, 128, 128>(v + (int64_t)h * D, b0, k0 + BN, nv, rs, nx + 3 * L::kKPiece);
+      }
+      if (half == 0) {
+        tc::mbar_wait(bar_s, ph);
+        tc::tc_fence_after();
+        uint32_t sr[2][32];
+        tc::tmem_ld32(t_s + lane_off, sr[0]);
+        tc::tmem_ld32(t_s + lane_off + 32, sr[1]);
+        tc::tmem_wait_ld();
+        float s[64];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int jj = 0; jj < 64; ++jj) {
+          s[jj] = (k0 + jj < nv) ? __uint_as_float(sr[jj >> 5][jj & 31]) * scale_log2 : -INFINITY;
+          mx = fmaxf(mx, s[jj]);
+        }
+        const float mn = fmaxf(m, mx);  // finite: the block holds at least one valid key
+        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+        float ps = 0.f;
+        uint32_t p1[32], p2[32], p3[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const float a = exp2f(s[2 * jj] - mn), b = exp2f(s[2 * jj + 1] - mn);
+          ps += a + b;
+          split3(a, b, p1[jj], p2[jj], p3[jj]);
+        }
+        l = l * alpha + ps;
+        m = mn;
+        tc::tmem_st32(t_s + lane_off, p1);       // P1: keys 2c, 2c+1 at column c
+        tc::tmem_st32(t_s + lane_off + 32, p2);  // P2 at columns [32, 64)
+        tc::tmem_st32(t_p3 + lane_off, p3);      // P3 past O
+        tc::tmem_wait_st();
+        alpha_s[row] = alpha;
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // O_j = P3V1 + P2V2 + P1V3 + P2V1 + P1V2 + P1V1 (V MN-major: key rows, 64-wide D chunks)
+        constexpr int kPi[6] = {2, 1, 0, 1, 0, 0}, kVj[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const uint32_t va = kv + (3 + kVj[c]) * L::kKPiece;
+          const uint32_t pa = kPi[c] == 2 ? t_p3 : t_s + kPi[c] * 32;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_o, pa + kk * 8, tc::sw128_desc(va + kk * 16 * 128, L::kKChunk, 1024), kIdescO,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      tc::mbar_wait(bar_o, ph);
+      tc::tc_fence_after();
+      const float alpha = alpha_s[row];
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32) {
+        uint32_t pv[32];
+        tc::tmem_ld32(t_o + lane_off + half * DH + c0, pv);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) o[c0 + jj] = fmaf(o[c0 + jj], alpha, __uint_as_float(pv[jj]));
+      }
+      ph ^= 1;
+    }
+    if (half == 0) l_s[row] = l;
+    tc::tc_fence_before();
+    __syncthreads();
+    const int64_t r = q0 + row;
+    if (r < seg) {
+      const bool ok = r < nv;
+      const float inv = ok ? 1.0f / l_s[row] : 0.f;
+      float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + (int64_t)h * D + half * DH);
+#pragma unroll
+      for (int jj = 0; jj < DH; jj += 4)
+        dst[jj / 4] = make_float4(o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
+      if (half == 0) lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(l)) * kLn2 : -INFINITY;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<L::kTmemCols>(tmem);
+}
+
+template <int D>
+static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
+                        void* out, float* lse, const int2* items, const int64_t* n_items, int64_t max_items,
+                        const int64_t* valid, cudaStream_t st) {
+  const int smem = Lay<D>::kAlloc;
+  if (jg_status rc = ensure_smem_attr((const void*)attn_fwd_x3_kernel<D>, smem, "attn_fwd_x3_kernel")) return rc;
+  int per_sm = 1;
+  JG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_fwd_x3_kernel<D>, kThreads, smem));
+  per_sm = std::max(1, std::min(per_sm, 512 / Lay<D>::kTmemCols));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)per_sm * device_sm_count()));
+  attn_fwd_x3_kernel<D><<<grid, kThreads, smem, st>>>(off, items, n_items, H, total_rows, (const float*)q,
+                                                       (const float*)k, (const float*)v, (float*)out, lse,
+                                                       kLog2e / sqrtf((float)D), valid);
+  JG_LAUNCHED("attn_fwd_x3_kernel");
+  return JG_OK;
+}
+
+// ------------------------------------------------------------------ backward (attention.cpp:227-289)
+// Two deterministic passes, like the FFMA kernels: query-stationary dQ, key-stationary dK / dV; every product is
+// the six-MMA split-bf16 sum. Operands are split on the fly from fp32 (no scratch beyond the backward workspace: the
+// SPEC.md:316 peak-intermediate bound); the stationary operand of the TS-form score MMAs lives in TMEM.
+//   dQ pass   TMEM: Q1 Q2 Q3 [0, 3D/2) | S [3D/2, +64) | dP [+64) | dQ [+D) ; smem: dO pieces, K_j, V_j pieces
+//             S = Q K_j^T (TS), dP = dO V_j^T (SS); dS = P (dP - Delta) -> TMEM over S / dP; dQ += dS K_j (TS,
+//             K_j read MN-major from the same staging). Warps 4-7 split V_{j+1} while warps 0-3 form dS;
+//             K_{j+1} is split by all warps after dQ_j.
+//   dK/dV pass TMEM: K1 K2 [0, D) | S^T [D, +64) | dP^T [+64) | dV [+D) | dK [+D) ; smem: K3, V pieces, Q_j, dO_j
+//             S^T = K Q_j^T (TS for K1, K2; SS for K3), dP^T = V dO_j^T (SS); P^T -> TMEM, dV += P^T dO_j;
+//             dS^T -> TMEM, dK += dS^T Q_j. Warps 4-7 split dO_{j+1} while warps 0-3 store dS^T; Q_{j+1} after dK_j.
+template <int D, bool KV>
+struct BwdLay {
+  static constexpr int kXChunk = BM * 128, kYChunk = BN * 128;
+  static constexpr int kXPiece = (D / 64) * kXChunk, kYPiece = (D / 64) * kYChunk;
+  // dQ pass: X = dO (3 pieces); dK/dV pass: X = K3 then V1 V2 V3 (stationary)
+  static constexpr int kX = 0;
+  static constexpr int kXn = KV ? 4 : 3;
+  static constexpr int kYa = kX + kXn * kXPiece;        // K_j (dQ pass) or Q_j (dK/dV pass), 3 pieces
+  static constexpr int kYb = kYa + 3 * kYPiece;         // V_j or dO_j, 3 pieces
+  static constexpr int kBar = kYb + 3 * kYPiece;        // bar_s, bar_o, tmem slot
+  static constexpr int kLs = kBar + 64;                 // float[64] lse*log2e of the moving block (dK/dV pass)
+  static constexpr int kDs = kLs + 4 * BN;              // float[64] Delta
+  static constexpr int kBytes = kDs + 4 * BN;
+  static constexpr int kAlloc = kBytes + 1024;
+};
 
 // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows inside the segment store
 template <int D>
@@ -375,8 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
   if (tid == 0) {
-    tc::mbar_init(bar_s, 1);
-    tc::mbar_init(bar_o, 1);
+    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_s + i, 1);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
@@ -401,20 +398,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
     const int q0 = it.y * BM;
     const int64_t r = q0 + row;
     const bool rin = r < nv;
-    const int64_t kend = q0 < nv ? nv : 0;
+    const int nblk = q0 < nv ? (int)((nv + BN - 1) / BN) : 0;
     float lr = 0.f, dr = 0.f;
     if (rin) {
       lr = lse[hr + b0 + r] * kLog2e;
       dr = delta[hr + b0 + r];
     }
     __syncthreads();  // previous item: TMEM dQ read, smem free
-    if (kend > 0) {
+    if (nblk > 0) {  // Q pieces -> TMEM; dO pieces, K_0, V_0 -> smem
       stage_row_tmem<D, 3>(q + (b0 + r) * rs + hd, rin, t_q, lane_off, half, row, 0);
       stage_split3<D, BM>(go + hd, b0, q0, nv, rs, sbase + L::kX);
+      stage_split3<D, BN>(k + hd, b0, 0, nv, rs, sbase + L::kYa);
+      stage_split3<D, BN>(v + hd, b0, 0, nv, rs, sbase + L::kYb);
     }
-    for (int64_t k0 = 0; k0 < kend; k0 += BN) {
-      stage_split3<D, BN>(k + hd, b0, k0, nv, rs, sbase + L::kYa);
-      stage_split3<D, BN>(v + hd, b0, k0, nv, rs, sbase + L::kYb);
+    for (int j = 0; j < nblk; ++j) {
+      const int64_t k0 = (int64_t)j * BN;
       tc::tmem_wait_st();
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
@@ -441,9 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
         }
         tc::mma_commit_warp(bar_s);
       }
+      tc::mbar_wait(bar_s, ph);  // (all threads: V_j is free once the scores are done)
+      tc::tc_fence_after();
+      if (half == 1 && j + 1 < nblk)  // warps 4-7 split V_{j+1} while warps 0-3 form dS
+        stage_split3<D, BN, 128, 128>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb);
       if (half == 0) {
-        tc::mbar_wait(bar_s, ph);
-        tc::tc_fence_after();
         uint32_t sr[64], pr[64];  // all of S and dP first: the dS pieces are written over both
         tc::tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
         tc::tmem_ld32(t_s + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
@@ -451,18 +451,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
         tc::tmem_ld32(t_dp + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(pr + 32));
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          const bool in = rin && (k0 + j < nv);
-          const float p = in ? exp2f(__uint_as_float(sr[j]) * scale_log2 - lr) : 0.f;
-          sr[j] = __float_as_uint(p * (__uint_as_float(pr[j]) - dr));
+        for (int jj = 0; jj < 64; ++jj) {
+          const bool in = rin && (k0 + jj < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[jj]) * scale_log2 - lr) : 0.f;
+          sr[jj] = __float_as_uint(p * (__uint_as_float(pr[jj]) - dr));
         }
 #pragma unroll
         for (int g = 0; g < 2; ++g) {  // dS1 over S [0, 32), dS2 over S [32, 64), dS3 over dP [0, 32)
           uint32_t w1[16], w2[16], w3[16];
 #pragma unroll
-          for (int j = 0; j < 32; j += 2)
-            split3(__uint_as_float(sr[32 * g + j]), __uint_as_float(sr[32 * g + j + 1]), w1[j / 2], w2[j / 2],
-                   w3[j / 2]);
+          for (int jj = 0; jj < 32; jj += 2)
+            split3(__uint_as_float(sr[32 * g + jj]), __uint_as_float(sr[32 * g + jj + 1]), w1[jj / 2], w2[jj / 2],
+                   w3[jj / 2]);
           tc::tmem_st16(t_s + lane_off + 16 * g, w1);
           tc::tmem_st16(t_s + lane_off + 32 + 16 * g, w2);
           tc::tmem_st16(t_dp + lane_off + 16 * g, w3);
@@ -486,9 +486,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
       }
       tc::mbar_wait(bar_o, ph);
       tc::tc_fence_after();
+      if (j + 1 < nblk) stage_split3<D, BN>(k + hd, b0, k0 + BN, nv, rs, sbase + L::kYa);  // K_j is free
       ph ^= 1;
     }
-    ld_half_store<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, scale, !rin || kend == 0, r < seg);
+    ld_half_store<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, scale, !rin || nblk == 0, r < seg);
     tc::tc_fence_before();
   }
   tc::tc_fence_before();
@@ -515,8 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;  // key row in the tile
   if (tid == 0) {
-    tc::mbar_init(bar_s, 1);
-    tc::mbar_init(bar_o, 1);
+    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_s + i, 1);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
@@ -542,15 +542,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
     const int x0 = it.y * BM;
     const int64_t r = x0 + row;
     const bool rin = r < nv;
-    const int64_t qend = x0 < nv ? nv : 0;
+    const int nblk = x0 < nv ? (int)((nv + BN - 1) / BN) : 0;
     __syncthreads();
-    if (qend > 0) {
-      stage_row_tmem<D, 2>(k + (b0 + r) * rs + hd, rin, t_k, lane_off, half, row, s_k3);
+    if (nblk > 0) {  // K1, K2 -> TMEM and K3 -> smem; V pieces, Q_0, dO_0 -> smem
+      stage_row_tmem<D, 2, true>(k + (b0 + r) * rs + hd, rin, t_k, lane_off, half, row, s_k3);
       stage_split3<D, BM>(v + hd, b0, x0, nv, rs, s_v);
+      stage_split3<D, BN>(q + hd, b0, 0, nv, rs, sbase + L::kYa);
+      stage_split3<D, BN>(go + hd, b0, 0, nv, rs, sbase + L::kYb);
     }
-    for (int64_t y0 = 0; y0 < qend; y0 += BN) {
-      stage_split3<D, BN>(q + hd, b0, y0, nv, rs, sbase + L::kYa);
-      stage_split3<D, BN>(go + hd, b0, y0, nv, rs, sbase + L::kYb);
+    for (int j = 0; j < nblk; ++j) {
+      const int64_t y0 = (int64_t)j * BN;
       if (tid < BN) {
         const bool in = y0 + tid < nv;
         ls[tid] = in ? lse[hr + b0 + y0 + tid] * kLog2e : 0.f;
@@ -598,19 +599,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
         tc::tmem_ld32(t_dp + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(pr + 32));
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          const bool in = rin && (y0 + j < nv);
-          const float p = in ? exp2f(__uint_as_float(sr[j]) * scale_log2 - ls[j]) : 0.f;
-          dsv[j] = p * (__uint_as_float(pr[j]) - dls[j]);
-          sr[j] = __float_as_uint(p);
+        for (int jj = 0; jj < 64; ++jj) {
+          const bool in = rin && (y0 + jj < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[jj]) * scale_log2 - ls[jj]) : 0.f;
+          dsv[jj] = p * (__uint_as_float(pr[jj]) - dls[jj]);
+          sr[jj] = __float_as_uint(p);
         }
 #pragma unroll
         for (int g = 0; g < 2; ++g) {  // P1 [0, 32), P2 [32, 64), P3 [64, 96) of t_s; queries 32g.. at 16g
           uint32_t p1[16], p2[16], p3[16];
 #pragma unroll
-          for (int j = 0; j < 32; j += 2)
-            split3(__uint_as_float(sr[32 * g + j]), __uint_as_float(sr[32 * g + j + 1]), p1[j / 2], p2[j / 2],
-                   p3[j / 2]);
+          for (int jj = 0; jj < 32; jj += 2)
+            split3(__uint_as_float(sr[32 * g + jj]), __uint_as_float(sr[32 * g + jj + 1]), p1[jj / 2], p2[jj / 2],
+                   p3[jj / 2]);
           tc::tmem_st16(t_s + lane_off + 16 * g, p1);
           tc::tmem_st16(t_s + lane_off + 32 + 16 * g, p2);
           tc::tmem_st16(t_s + lane_off + 64 + 16 * g, p3);
@@ -631,14 +632,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
+      tc::mbar_wait(bar_o, ph_o);  // (all threads) the P^T pieces and dO_j are consumed
+      tc::tc_fence_after();
+      if (half == 1 && j + 1 < nblk)  // warps 4-7 split dO_{j+1} while warps 0-3 store dS^T
+        stage_split3<D, BN, 128, 128>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb);
       if (half == 0) {
-        tc::mbar_wait(bar_o, ph_o);  // the P^T pieces are consumed
-        tc::tc_fence_after();
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           uint32_t d1[16], d2[16], d3[16];
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) split3(dsv[32 * g + j], dsv[32 * g + j + 1], d1[j / 2], d2[j / 2], d3[j / 2]);
+          for (int jj = 0; jj < 32; jj += 2)
+            split3(dsv[32 * g + jj], dsv[32 * g + jj + 1], d1[jj / 2], d2[jj / 2], d3[jj / 2]);
           tc::tmem_st16(t_s + lane_off + 16 * g, d1);
           tc::tmem_st16(t_s + lane_off + 32 + 16 * g, d2);
           tc::tmem_st16(t_s + lane_off + 64 + 16 * g, d3);
@@ -662,10 +666,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
       }
       tc::mbar_wait(bar_o, ph_o);
       tc::tc_fence_after();
+      if (j + 1 < nblk) stage_split3<D, BN>(q + hd, b0, y0 + BN, nv, rs, sbase + L::kYa);  // Q_j is free
       ph_o ^= 1;
       ph_s ^= 1;
     }
-    const bool z = !rin || qend == 0;
+    const bool z = !rin || nblk == 0;
     ld_half_store<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, 1.f, z, r < seg);
     ld_half_store<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, scale, z, r < seg);
     tc::tc_fence_before();
@@ -675,29 +680,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-template <typename K>
-static jg_status prep(K kernel, size_t smem) {
-  JG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  return JG_OK;
-}
-
 template <int D>
 static jg_status bwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
                         const void* go, const float* lse, const float* delta, void* dq, void* dk, void* dv,
                         const int2* items, const int64_t* n_items, int64_t max_items, const int64_t* valid,
                         cudaStream_t st) {
   // at least half the SM's shared memory: one CTA per SM, since each allocates all 512 TMEM columns
-  const size_t sm_q = std::max<size_t>(BwdLay<D, false>::kAlloc, 120 * 1024);
-  const size_t sm_kv = std::max<size_t>(BwdLay<D, true>::kAlloc, 120 * 1024);
-  static thread_local int attr_dev = -1;
-  int dev = 0;
-  JG_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    if (jg_status rc = prep(attn_bwd_x3_dq_kernel<D>, sm_q)) return rc;
-    if (jg_status rc = prep(attn_bwd_x3_dkdv_kernel<D>, sm_kv)) return rc;
-    attr_dev = dev;
-  }
-  // one CTA per SM: each allocates all 512 TMEM columns
+  const int sm_q = std::max<int>(BwdLay<D, false>::kAlloc, 120 * 1024);
+  const int sm_kv = std::max<int>(BwdLay<D, true>::kAlloc, 120 * 1024);
+  if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_x3_dq_kernel<D>, sm_q, "attn_bwd_x3_dq_kernel")) return rc;
+  if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_x3_dkdv_kernel<D>, sm_kv, "attn_bwd_x3_dkdv_kernel"))
+    return rc;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)device_sm_count()));
   const float scale = 1.0f / sqrtf((float)D), scale_log2 = kLog2e * scale;
   attn_bwd_x3_dq_kernel<D><<<grid, kThreads, sm_q, st>>>(off, items, n_items, H, total_rows, (const float*)q,
@@ -710,6 +703,7 @@ static jg_status bwd_x3(const int64_t* off, int64_t total_rows, int H, const voi
   JG_LAUNCHED("attn_bwd_x3_dkdv_kernel");
   return JG_OK;
 }
+
 }  // namespace x3
 
 bool attn_x3_supported(int head_dim, jg_dtype dt) {
