@@ -223,3 +223,46 @@ def test_full_size_cfg3_properties():
     # dS is rounded to bf16 before the dK MMA, so its rows sum to 0 only up to bf16 rounding: the identity is
     # checked at the product's max-abs tolerance (sum_k |dK_k| is O(1-5) per (sample, head, d) here)
     assert float(sdk.abs().max()) < 2e-2, "sum_k dK != 0"
+
+
+def _dense_sample_ref64(q, k, v, go):
+    """fp64 torch reference of one sample's attention fwd + bwd ([n, H, D] inputs)."""
+    D = q.shape[-1]
+    q, k, v, go = (t.double().transpose(0, 1).requires_grad_() for t in (q, k, v, go))  # [H, n, D]
+    s = torch.matmul(q, k.transpose(1, 2)) / D ** 0.5
+    lse = torch.logsumexp(s, dim=-1)
+    o = torch.matmul(torch.softmax(s, dim=-1), v)
+    dq, dk, dv = torch.autograd.grad(o, (q, k, v), go)
+    return (o.detach().transpose(0, 1), lse.detach(), dq.transpose(0, 1), dk.transpose(0, 1), dv.transpose(0, 1))
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_fp32_tensor_core_path_multi_block(D):
+    """fp32 mode on tcgen05 (attn_x3_sm100.cu, split-bf16 emulation) at sizes with many 64-key blocks and 128-row
+    tiles per sample (up to 1,500 rows): every sample against an fp64 torch reference at the fp32 tolerance, and
+    the results bit-identical across two runs (two deterministic passes, no atomics)."""
+    ln = np.array([1500, 1, 0, 129, 700, 64, 65, 1023, 257], np.int64)
+    off = R.make_offsets(ln)
+    S, H = int(off[-1]), 2
+    g = torch.Generator(device=DEV).manual_seed(11)
+    q, k, v, go = ((torch.rand(S, H, D, device=DEV, generator=g) * 2 - 1) for _ in range(4))
+    T = lambda a: J.JaggedTensor(torch.from_numpy(off).to(DEV), a, off)  # noqa: E731
+    Q, K, V, G = T(q), T(k), T(v), T(go)
+    runs = []
+    for _ in range(2):
+        saved = J.jagged_flash_attention_forward(Q, K, V)
+        gr = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+        torch.cuda.synchronize()
+        runs.append((saved.output.values.clone(), saved.logsumexp.clone(), gr.dq.values.clone(),
+                     gr.dk.values.clone(), gr.dv.values.clone()))
+    for a, b in zip(*runs):
+        assert torch.equal(a, b), "fp32 attention is not bit-identical across runs"
+    out, lse, dq, dk, dv = runs[0]
+    ref = [np.zeros((S, H, D)), np.zeros((H, S)), np.zeros((S, H, D)), np.zeros((S, H, D)), np.zeros((S, H, D))]
+    for i in np.nonzero(ln)[0]:
+        a, b = int(off[i]), int(off[i + 1])
+        o, l, rq, rk, rv = _dense_sample_ref64(q[a:b], k[a:b], v[a:b], go[a:b])
+        ref[0][a:b], ref[1][:, a:b], ref[2][a:b], ref[3][a:b], ref[4][a:b] = (
+            t.cpu().numpy() for t in (o, l, rq, rk, rv))
+    for got, r, nm in zip((out, lse, dq, dk, dv), ref, ("out", "lse", "dq", "dk", "dv")):
+        assert_fp32_close(got, r, what=f"fp32 tcgen05 {nm} (D={D})")
