@@ -333,6 +333,37 @@ def run_ours(args, rank, world, local_rank):
 
     verify = verify_sharded(world, rank, dev) if world > 1 else None  # after the timed regions
 
+    # fp32 mode (the reference's float instantiation, attention.cpp:311-331) on the same shard, after the timed
+    # regions: the split-bf16 tcgen05 kernels (attn_x3_sm100.cu); reported beside the bf16 headline, not in it
+    fp32 = None
+    if not args.no_fp32 and rank == 0:
+        Qf, Kf, Vf, Gf = (T(t.float()) for t in (q, k, v, go))
+        schf = J.Schedule(Qf)
+
+        def step32(e=None):
+            if e:
+                e[0].record(stream)
+            sv = J.jagged_flash_attention_forward(Qf, Kf, Vf, 64, 64, schedule=schf)
+            if e:
+                e[1].record(stream)
+            J.jagged_flash_attention_backward(Qf, Kf, Vf, Gf, sv, schedule=schf)
+            if e:
+                e[2].record(stream)
+
+        for _ in range(2):
+            step32()
+        ev32 = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2)]
+        for e in ev32:
+            step32(e)
+        torch.cuda.synchronize()
+        f_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev32]))
+        b_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev32]))
+        fp32 = {"fwd_ms": f_ms, "bwd_ms": b_ms, "ms_per_step": f_ms + b_ms,
+                "tflops": (fwd_fl + bwd_fl) / ((f_ms + b_ms) * 1e-3) / 1e12,
+                "x_bf16_step": (f_ms + b_ms) / (elapsed_ms / args.steps),
+                "path": "tcgen05 split-bf16 emulation (attn_x3_sm100.cu), fp32 in/out, 2 timed steps"}
+        del Qf, Kf, Vf, Gf, schf
+
     t = torch.tensor([elapsed_ms, e2e_s], dtype=torch.float64, device=dev)
     nb = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)  # whole-job copy bytes per step
     if world > 1:
@@ -389,6 +420,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if verify is not None:
         line["verify"] = verify
+    if fp32 is not None:
+        line["fp32_mode"] = fp32
     print(json.dumps(line), flush=True)
 
 
@@ -835,6 +868,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-mode leg (profiling runs)")
     ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "dense", "table1"],
                     help="cfg3 = the headline JSON line; the others measure the secondary BASELINE configs")
     ap.add_argument("--out", default=None, help="also append secondary-config lines to this file")

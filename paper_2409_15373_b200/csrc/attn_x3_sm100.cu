@@ -47,8 +47,13 @@ struct Lay {
   static constexpr int kTmemCols = D == 128 ? 512 : 256;  // Q pieces 3D/2 | S 64 | O D | P3 32
 };
 
-__device__ __forceinline__ uint32_t bf16_bits_hi(float x) {  // bf16(x) in the high half of a float
-  return __float_as_uint(__bfloat162float(__float2bfloat16_rn(x)));
+
+// one paired conversion (cvt.rn.bf16x2) per piece; the pieces' fp32 values are the packed halves shifted into place
+__device__ __forceinline__ void split3(float a, float b, uint32_t& w1, uint32_t& w2, uint32_t& w3) {
+  w1 = tc::pack_bf16(a, b);
+  const float ra = a - __uint_as_float(w1 << 16), rb = b - __uint_as_float(w1 & 0xffff0000u);  // exact
+  w2 = tc::pack_bf16(ra, rb);
+  w3 = tc::pack_bf16(ra - __uint_as_float(w2 << 16), rb - __uint_as_float(w2 & 0xffff0000u));
 }
 
 // rows [r0, r0 + ROWS) of a fp32 [*, H, D] tensor (rows >= n zero) as three bf16 pieces, each [ROWS x D] in
@@ -59,42 +64,40 @@ __device__ __forceinline__ void stage_split3(const float* __restrict__ src, int6
                                              int64_t rs, uint32_t base) {
   constexpr int kUnits = D / 8;  // 8 floats = one 16-byte bf16 unit per piece
   constexpr int kPiece = (D / 64) * ROWS * 128;
-#pragma unroll 4
-  for (int e = (int)threadIdx.x - T0; e < ROWS * kUnits; e += NT) {
-    const int r = e / kUnits, u = e % kUnits;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (r0 + r < n) {
-      const float4* p = reinterpret_cast<const float4*>(src + (b0 + r0 + r) * rs + u * 8);
-      a = __ldg(p);
-      b = __ldg(p + 1);
-    }
-    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    uint32_t w1[4], w2[4], w3[4];
+  constexpr int kTotal = ROWS * kUnits;
+  constexpr int kIter = (kTotal + NT - 1) / NT;
+  constexpr int kBatch = kIter < 4 ? kIter : 4;  // loads of a batch all in flight before its shared stores
+  const int t = (int)threadIdx.x - T0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float x0 = x[2 * c], x1 = x[2 * c + 1];
-      const float h0 = __uint_as_float(bf16_bits_hi(x0)), h1 = __uint_as_float(bf16_bits_hi(x1));
-      const float r0v = x0 - h0, r1v = x1 - h1;  // exact
-      const float m0 = __uint_as_float(bf16_bits_hi(r0v)), m1 = __uint_as_float(bf16_bits_hi(r1v));
-      w1[c] = tc::pack_bf16(h0, h1);
-      w2[c] = tc::pack_bf16(m0, m1);
-      w3[c] = tc::pack_bf16(r0v - m0, r1v - m1);
+  for (int i0 = 0; i0 < kIter; i0 += kBatch) {
+    float4 a[kBatch], b[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int e = t + (i0 + i) * NT, r = e / kUnits, u = e % kUnits;
+      a[i] = b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < kTotal && r0 + r < n) {
+        const float4* p = reinterpret_cast<const float4*>(src + (b0 + r0 + r) * rs + u * 8);
+        a[i] = __ldg(p);
+        b[i] = __ldg(p + 1);
+      }
     }
-    const uint32_t off = (u >> 3) * (ROWS * 128) + tc::sw128_offset(r, u & 7);
-    tc::st_shared_v4(base + off, w1[0], w1[1], w1[2], w1[3]);
-    tc::st_shared_v4(base + kPiece + off, w2[0], w2[1], w2[2], w2[3]);
-    tc::st_shared_v4(base + 2 * kPiece + off, w3[0], w3[1], w3[2], w3[3]);
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int e = t + (i0 + i) * NT, r = e / kUnits, u = e % kUnits;
+      if (e >= kTotal) continue;
+      uint32_t w1[4], w2[4], w3[4];
+      split3(a[i].x, a[i].y, w1[0], w2[0], w3[0]);
+      split3(a[i].z, a[i].w, w1[1], w2[1], w3[1]);
+      split3(b[i].x, b[i].y, w1[2], w2[2], w3[2]);
+      split3(b[i].z, b[i].w, w1[3], w2[3], w3[3]);
+      const uint32_t off = (u >> 3) * (ROWS * 128) + tc::sw128_offset(r, u & 7);
+      tc::st_shared_v4(base + off, w1[0], w1[1], w1[2], w1[3]);
+      tc::st_shared_v4(base + kPiece + off, w2[0], w2[1], w2[2], w2[3]);
+      tc::st_shared_v4(base + 2 * kPiece + off, w3[0], w3[1], w3[2], w3[3]);
+    }
   }
 }
 
-__device__ __forceinline__ void split3(float a, float b, uint32_t& w1, uint32_t& w2, uint32_t& w3) {
-  const float ha = __uint_as_float(bf16_bits_hi(a)), hb = __uint_as_float(bf16_bits_hi(b));
-  const float ra = a - ha, rb = b - hb;
-  const float ma = __uint_as_float(bf16_bits_hi(ra)), mb = __uint_as_float(bf16_bits_hi(rb));
-  w1 = tc::pack_bf16(ha, hb);
-  w2 = tc::pack_bf16(ma, mb);
-  w3 = tc::pack_bf16(ra - ma, rb - mb);
-}
 
 // This thread's half (columns [half*D/2, +D/2)) of row `row` of a fp32 [*, H, D] tensor, split into bf16 pieces:
 // pieces 0 .. NT-1 into TMEM (piece p at column t_base + p*D/2, packed two per column), piece 2 (when kS3)
@@ -103,14 +106,19 @@ template <int D, int NT, bool kS3 = false>
 __device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bool in, uint32_t t_base,
                                                uint32_t lane_off, int half, int row, uint32_t s3) {
   constexpr int kCols = D / 4;  // packed columns per half per piece
+  float4 xs[D / 8];             // the whole half row in flight before any store
+#pragma unroll
+  for (int g = 0; g < D / 8; ++g) {
+    xs[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (in) xs[g] = __ldg(reinterpret_cast<const float4*>(src + half * (D / 2) + 4 * g));
+  }
 #pragma unroll
   for (int c0 = 0; c0 < kCols; c0 += 8) {  // 16 elements -> 8 packed columns per step
     uint32_t w[3][8];
     const int e0 = half * (D / 2) + 2 * c0;  // first element
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (in) x = __ldg(reinterpret_cast<const float4*>(src + e0 + 4 * g));
+      const float4 x = xs[c0 / 2 + g];
       split3(x.x, x.y, w[0][2 * g], w[1][2 * g], w[2][2 * g]);
       split3(x.z, x.w, w[0][2 * g + 1], w[1][2 * g + 1], w[2][2 * g + 1]);
     }
