@@ -508,13 +508,8 @@ static jg_status fwd_tiled_t(const int64_t* off, int64_t total_rows, int H, cons
                              const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
                              int64_t max_items, const int64_t* valid, cudaStream_t st) {
   const size_t smem = sizeof(float) * ft::FwdLay<D>::kFloats;
-  static thread_local int attr_dev = -1;  // per-device kernel attribute
-  int dev = 0;
-  JG_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    JG_CUDA(cudaFuncSetAttribute(attn_fwd_tiled_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_dev = dev;
-  }
+  if (jg_status rc = ensure_smem_attr((const void*)attn_fwd_tiled_kernel<T, D>, (int)smem, "attn_fwd_tiled_kernel"))
+    return rc;
   int per_sm = 1;
   JG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_fwd_tiled_kernel<T, D>, ft::kThreads, smem));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)std::max(per_sm, 1) *
@@ -554,14 +549,9 @@ static jg_status bwd_tiled_pass(const int64_t* off, int64_t total_rows, int H, c
                                 void* o2, const int2* items, const int64_t* n_items, int64_t max_items,
                                 const int64_t* valid, cudaStream_t st) {
   const size_t smem = sizeof(float) * ft::BwdLay<D, MODE>::kFloats;
-  static thread_local int attr_dev = -1;
-  int dev = 0;
-  JG_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    JG_CUDA(cudaFuncSetAttribute(attn_bwd_tiled_kernel<T, D, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr_dev = dev;
-  }
+  if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_tiled_kernel<T, D, MODE>, (int)smem,
+                                      "attn_bwd_tiled_kernel"))
+    return rc;
   int per_sm = 1;
   JG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_bwd_tiled_kernel<T, D, MODE>, ft::kThreads,
                                                         smem));
