@@ -37,15 +37,18 @@ template <int D>
 struct Lay {
   static constexpr int kKChunk = BN * 128;             // [64 rows x 64] bf16
   static constexpr int kKPiece = (D / 64) * kKChunk;
-  static constexpr int kStage = 6 * kKPiece;           // K1 K2 K3 V1 V2 V3 of one 64-key block
-  static constexpr int kKV = 0;                        // two stages
-  static constexpr int kBar = kKV + 2 * kStage;        // bar_s, bar_o, tmem slot
-  static constexpr int kAlpha = kBar + 64;             // float[128]
-  static constexpr int kL = kAlpha + 4 * BM;           // float[128]
+  static constexpr int kKStage = 3 * kKPiece;          // K1 K2 K3 (or V1 V2 V3) of one 64-key block
+  static constexpr int kK = 0;                         // K ring: 2 stages
+  static constexpr int kV = kK + 2 * kKStage;          // V ring: 2 stages
+  static constexpr int kBar = kV + 2 * kKStage;        // 10 mbarriers + tmem slot
+  static constexpr int kAlpha = kBar + 128;            // float[3][128]
+  static constexpr int kL = kAlpha + 3 * 4 * BM;       // float[128]
   static constexpr int kBytes = kL + 4 * BM;
   static constexpr int kAlloc = kBytes + 1024;         // + alignment slack
-  static constexpr int kTmemCols = D == 128 ? 512 : 256;  // Q pieces 3D/2 | S 64 | O D | P3 32
+  // TMEM: Q1 Q2 Q3 [0, 3D/2) | S0 | S1 (64 each) | O (D) | P3_0 | P3_1 (32 each)
+  static constexpr int kTmemCols = 512;
 };
+constexpr int kFwdThreads = 256;  // 4 softmax warps (warp 0 also issues the MMAs), 4 O / staging warps
 
 
 // one paired conversion (cvt.rn.bf16x2) per piece; the pieces' fp32 values are the packed halves shifted into place
@@ -59,14 +62,14 @@ __device__ __forceinline__ void split3(float a, float b, uint32_t& w1, uint32_t&
 // rows [r0, r0 + ROWS) of a fp32 [*, H, D] tensor (rows >= n zero) as three bf16 pieces, each [ROWS x D] in
 // SWIZZLE_128B 64-column chunks of ROWS x 128 B at base + piece * piece_bytes + chunk * ROWS * 128
 // (threads [T0, T0 + NT) of the CTA take part)
-template <int D, int ROWS, int T0 = 0, int NT = kThreads>
+template <int D, int ROWS, int T0 = 0, int NT = kThreads, int kMaxBatch = 4>
 __device__ __forceinline__ void stage_split3(const float* __restrict__ src, int64_t b0, int64_t r0, int64_t n,
                                              int64_t rs, uint32_t base) {
   constexpr int kUnits = D / 8;  // 8 floats = one 16-byte bf16 unit per piece
   constexpr int kPiece = (D / 64) * ROWS * 128;
   constexpr int kTotal = ROWS * kUnits;
   constexpr int kIter = (kTotal + NT - 1) / NT;
-  constexpr int kBatch = kIter < 4 ? kIter : 4;  // loads of a batch all in flight before its shared stores
+  constexpr int kBatch = kIter < kMaxBatch ? kIter : kMaxBatch;  // loads of a batch in flight before its stores
   const int t = (int)threadIdx.x - T0;
 #pragma unroll
   for (int i0 = 0; i0 < kIter; i0 += kBatch) {
@@ -141,8 +144,16 @@ __device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bo
   }
 }
 
+// Forward (warp-specialised pipeline; attention.cpp:172-225):
+//   warps 0-3   softmax of block j (thread = query row) while the tensor core runs S_{j+1} / PV_{j-1};
+//               warp 0 also issues the MMAs: S_0, S_1, then per block j PV_j (after every P_j and the previous O
+//               read-out) and S_{j+2} into the score buffer P_j occupied (in-order tcgen05 execution orders it)
+//   warps 4-7   K_{j+2} split into the freed K stage once S_j is done; O = alpha O + PV_j in registers (thread =
+//               row, all D columns); V_{j+2} split into the freed V stage once PV_j is done
+// The score MMAs of block j+1 therefore overlap the softmax of block j, and the P V of block j overlaps the softmax
+// of block j+1.
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
+__global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_x3_kernel(
     const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
     int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     float* __restrict__ out, float* __restrict__ lse, float scale_log2, const int64_t* __restrict__ valid) {
@@ -150,17 +161,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = tc::smem_u32(smem);
-  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* bar_o = bar_s + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_s = bars;        // [2] score MMAs of the buffer done (commit)
+  uint64_t* bar_o = bars + 2;    // PV_j done (commit)
+  uint64_t* p_ready = bars + 3;  // softmax wrote P_j (128 arrivals)
+  uint64_t* o_free = bars + 4;   // O read out (128 arrivals)
+  uint64_t* k_ready = bars + 5;  // [2] K stage split (128 arrivals)
+  uint64_t* v_ready = bars + 7;  // [2] V stage split (128 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
   float* alpha_s = reinterpret_cast<float*>(smem + L::kAlpha);
   float* l_s = reinterpret_cast<float*>(smem + L::kL);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
-  const int row = quarter * 32 + lane;  // TMEM lane = query row in the tile
+  const int row = quarter * 32 + lane;
   if (tid == 0) {
-    tc::mbar_init(bar_s, 1);
-    tc::mbar_init(bar_o, 1);
+    for (int i = 0; i < 3; ++i) tc::mbar_init(bars + i, 1);
+    for (int i = 3; i < 9; ++i) tc::mbar_init(bars + i, 128);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -168,65 +184,85 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_q = tmem, t_s = tmem + 3 * D / 2, t_o = t_s + 64, t_p3 = t_o + D;
+  const uint32_t t_q = tmem, t_s0 = tmem + 3 * D / 2, t_o = t_s0 + 128, t_p30 = t_o + D;
   const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
   constexpr uint32_t kIdescS = tc::idesc_bf16_f32(BM, BN, false, false);
   constexpr uint32_t kIdescO = tc::idesc_bf16_f32(BM, D, false, true);
-  constexpr int DH = D / 2;  // output columns per thread
   const int64_t rs = (int64_t)H * D;
   const int64_t n_work = *n_items * H;
-  uint32_t ph = 0;
+  // barrier use counters (each role tracks the completions it waits for; all are CTA-global across items)
+  // (per-parity counters as scalars: a dynamically indexed pair would live in local memory)
+  uint32_t cs0 = 0, cs1 = 0, c_o = 0, c_p = 0, c_of = 0, ck0 = 0, ck1 = 0, cv0 = 0, cv1 = 0;
+  auto take = [](uint32_t& c0, uint32_t& c1, int b) {  // parity of the next completion of buffer b's barrier
+    const uint32_t v = b ? c1 : c0;
+    if (b) ++c1; else ++c0;
+    return v & 1u;
+  };
   for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
     const int2 it = items[w / H];
     const int h = (int)(w % H);
+    const int64_t hd = (int64_t)h * D;
     const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
     const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
     const int q0 = it.y * BM;
-    float o[DH];
-#pragma unroll
-    for (int j = 0; j < DH; ++j) o[j] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    const int64_t kend = q0 < nv ? nv : 0;  // an all-padding tile attends nothing
-    const int nblk = (int)((kend + BN - 1) / BN);
-    __syncthreads();  // the previous item's smem / TMEM reads are done
-    if (nblk > 0) {  // Q pieces into TMEM, block 0 into stage 0
-      stage_row_tmem<D, 3>(q + (b0 + q0 + row) * rs + (int64_t)h * D, q0 + row < seg, t_q, lane_off, half, row, 0);
-      stage_split3<D, BN>(k + (int64_t)h * D, b0, 0, nv, rs, sbase);
-      stage_split3<D, BN>(v + (int64_t)h * D, b0, 0, nv, rs, sbase + 3 * L::kKPiece);
+    const int nblk = q0 < nv ? (int)((nv + BN - 1) / BN) : 0;  // an all-padding tile attends nothing
+    __syncthreads();  // the previous item's TMEM / smem reads are done
+    if (nblk > 0) {  // Q pieces -> TMEM; blocks 0 and 1 -> stages 0 and 1
+      stage_row_tmem<D, 3>(q + (b0 + q0 + row) * rs + hd, q0 + row < seg, t_q, lane_off, half, row, 0);
+      for (int j = 0; j < 2 && j < nblk; ++j) {
+        stage_split3<D, BN>(k + hd, b0, (int64_t)j * BN, nv, rs, sbase + L::kK + j * L::kKStage);
+        stage_split3<D, BN>(v + hd, b0, (int64_t)j * BN, nv, rs, sbase + L::kV + j * L::kKStage);
+      }
     }
-    for (int j = 0; j < nblk; ++j) {
-      const int64_t k0 = (int64_t)j * BN;
-      const int st = j & 1;
-      const uint32_t kv = sbase + st * L::kStage;
-      tc::tmem_wait_st();
-      tc::fence_proxy_async_smem();
-      tc::tc_fence_before();
-      __syncthreads();
-      tc::tc_fence_after();
-      if (warp == 0) {  // S = Q3K1 + Q2K2 + Q1K3 + Q2K1 + Q1K2 + Q1K1 (small terms first, see above)
-        constexpr int kQi[6] = {2, 1, 0, 1, 0, 0}, kKj[6] = {0, 1, 2, 0, 1, 0};
+    tc::tmem_wait_st();
+    tc::fence_proxy_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    // warp 0 doubles as the MMA issuer (a ninth warp would not fit the per-SMSP register file at this size)
+    auto issue_s = [&](int j) {  // S = Q3K1 + Q2K2 + Q1K3 + Q2K1 + Q1K2 + Q1K1 (small terms first)
+      constexpr int kQi[6] = {2, 1, 0, 1, 0, 0}, kKj[6] = {0, 1, 2, 0, 1, 0};
+      const uint32_t kst = sbase + L::kK + (j & 1) * L::kKStage, ts = t_s0 + (j & 1) * 64;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const uint32_t ka = kv + kKj[c] * L::kKPiece;
+      for (int c = 0; c < 6; ++c) {
+        const uint32_t ka = kst + kKj[c] * L::kKPiece;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            tc::mma_bf16_ts_warp(t_s, t_q + kQi[c] * (D / 2) + kk * 8,
-                                 tc::sw128_desc(ka + (kk >> 2) * L::kKChunk + (kk & 3) * 32, 16, 1024), kIdescS,
-                                 (c > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit_warp(bar_s);
+        for (int kk = 0; kk < D / 16; ++kk)
+          tc::mma_bf16_ts_warp(ts, t_q + kQi[c] * (D / 2) + kk * 8,
+                               tc::sw128_desc(ka + (kk >> 2) * L::kKChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                               (c > 0 || kk > 0) ? 1u : 0u);
       }
-      if (half == 1 && j + 1 < nblk) {  // warps 4-7 split block j + 1 into the other stage (block j - 1's is free)
-        const uint32_t nx = sbase + (st ^ 1) * L::kStage;
-        stage_split3<D, BN, 128, 128>(k + (int64_t)h * D, b0, k0 + BN, nv, rs, nx);
-        stage_split3<D, BN, 128, 128>(v + (int64_t)h * D, b0, k0 + BN, nv, rs, nx + 3 * L::kKPiece);
+      tc::mma_commit_warp(bar_s + (j & 1));
+    };
+    auto issue_pv = [&](int j) {  // O_j = P3V1 + P2V2 + P1V3 + P2V1 + P1V2 + P1V1 (V MN-major)
+      constexpr int kPi[6] = {2, 1, 0, 1, 0, 0}, kVj[6] = {0, 1, 2, 0, 1, 0};
+      const int b = j & 1;
+      const uint32_t vst = sbase + L::kV + b * L::kKStage, ts = t_s0 + b * 64, tp3 = t_p30 + b * 32;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const uint32_t va = vst + kVj[c] * L::kKPiece;
+        const uint32_t pa = kPi[c] == 2 ? tp3 : ts + kPi[c] * 32;
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          tc::mma_bf16_ts_warp(t_o, pa + kk * 8, tc::sw128_desc(va + kk * 16 * 128, L::kKChunk, 1024), kIdescO,
+                               (c > 0 || kk > 0) ? 1u : 0u);
       }
-      if (half == 0) {
-        tc::mbar_wait(bar_s, ph);
+      tc::mma_commit_warp(bar_o);
+    };
+    if (warp == 0)
+      for (int j = 0; j < 2 && j < nblk; ++j) issue_s(j);
+    if (half == 0) {
+      // ===================================================== softmax (thread = query row)
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nblk; ++j) {
+        const int b = j & 1;
+        const int64_t k0 = (int64_t)j * BN;
+        tc::mbar_wait(bar_s + b, take(cs0, cs1, b));
         tc::tc_fence_after();
+        const uint32_t ts = t_s0 + b * 64;
         uint32_t sr[2][32];
-        tc::tmem_ld32(t_s + lane_off, sr[0]);
-        tc::tmem_ld32(t_s + lane_off + 32, sr[1]);
+        tc::tmem_ld32(ts + lane_off, sr[0]);
+        tc::tmem_ld32(ts + lane_off + 32, sr[1]);
         tc::tmem_wait_ld();
         float s[64];
         float mx = -INFINITY;
@@ -241,59 +277,84 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_x3_kernel(
         uint32_t p1[32], p2[32], p3[32];
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
-          const float a = exp2f(s[2 * jj] - mn), b = exp2f(s[2 * jj + 1] - mn);
-          ps += a + b;
-          split3(a, b, p1[jj], p2[jj], p3[jj]);
+          const float a = exp2f(s[2 * jj] - mn), bb = exp2f(s[2 * jj + 1] - mn);
+          ps += a + bb;
+          split3(a, bb, p1[jj], p2[jj], p3[jj]);
         }
         l = l * alpha + ps;
         m = mn;
-        tc::tmem_st32(t_s + lane_off, p1);       // P1: keys 2c, 2c+1 at column c
-        tc::tmem_st32(t_s + lane_off + 32, p2);  // P2 at columns [32, 64)
-        tc::tmem_st32(t_p3 + lane_off, p3);      // P3 past O
+        tc::tmem_st32(ts + lane_off, p1);                  // P1: keys 2c, 2c+1 at column c
+        tc::tmem_st32(ts + lane_off + 32, p2);             // P2 at columns [32, 64)
+        tc::tmem_st32(t_p30 + b * 32 + lane_off, p3);      // P3 in its own slot
         tc::tmem_wait_st();
-        alpha_s[row] = alpha;
-      }
-      tc::tc_fence_before();
-      __syncthreads();
-      tc::tc_fence_after();
-      if (warp == 0) {  // O_j = P3V1 + P2V2 + P1V3 + P2V1 + P1V2 + P1V1 (V MN-major: key rows, 64-wide D chunks)
-        constexpr int kPi[6] = {2, 1, 0, 1, 0, 0}, kVj[6] = {0, 1, 2, 0, 1, 0};
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const uint32_t va = kv + (3 + kVj[c]) * L::kKPiece;
-          const uint32_t pa = kPi[c] == 2 ? t_p3 : t_s + kPi[c] * 32;
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            tc::mma_bf16_ts_warp(t_o, pa + kk * 8, tc::sw128_desc(va + kk * 16 * 128, L::kKChunk, 1024), kIdescO,
-                                 (c > 0 || kk > 0) ? 1u : 0u);
+        alpha_s[(j % 3) * BM + row] = alpha;
+        tc::tc_fence_before();
+        tc::mbar_arrive(p_ready);
+        if (warp == 0) {  // issuer: PV_j once every P_j is in and O is free; then S_{j+2}
+          tc::mbar_wait(p_ready, c_p++ & 1);
+          if (j >= 1) tc::mbar_wait(o_free, c_of++ & 1);
+          if (j >= 2) tc::mbar_wait(v_ready + b, take(cv0, cv1, b));
+          tc::tc_fence_after();
+          issue_pv(j);
+          if (j + 2 < nblk) {
+            tc::mbar_wait(k_ready + b, take(ck0, ck1, b));
+            tc::tc_fence_after();
+            issue_s(j + 2);
+          }
         }
-        tc::mma_commit_warp(bar_o);
       }
-      tc::mbar_wait(bar_o, ph);
-      tc::tc_fence_after();
-      const float alpha = alpha_s[row];
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) {
-        uint32_t pv[32];
-        tc::tmem_ld32(t_o + lane_off + half * DH + c0, pv);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) o[c0 + jj] = fmaf(o[c0 + jj], alpha, __uint_as_float(pv[jj]));
+      if (warp == 0 && nblk > 0) tc::mbar_wait(o_free, c_of++ & 1);  // last O read-out: TMEM free next item
+      l_s[row] = l;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // l_s for the O warps
+      const int64_t r = q0 + row;
+      if (r < seg) {
+        const bool ok = r < nv && nblk > 0;
+        lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(l)) * kLn2 : -INFINITY;
       }
-      ph ^= 1;
-    }
-    if (half == 0) l_s[row] = l;
-    tc::tc_fence_before();
-    __syncthreads();
-    const int64_t r = q0 + row;
-    if (r < seg) {
-      const bool ok = r < nv;
-      const float inv = ok ? 1.0f / l_s[row] : 0.f;
-      float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + (int64_t)h * D + half * DH);
+    } else {
+      // ===================================================== O accumulation + K / V staging (thread = row)
+      float o[D];
 #pragma unroll
-      for (int jj = 0; jj < DH; jj += 4)
-        dst[jj / 4] = make_float4(o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
-      if (half == 0) lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(l)) * kLn2 : -INFINITY;
+      for (int jj = 0; jj < D; ++jj) o[jj] = 0.f;
+      for (int j = 0; j < nblk; ++j) {
+        const int b = j & 1;
+        if (j + 2 < nblk) {  // K_j is consumed once S_j is done: split K_{j+2} into its stage
+          tc::mbar_wait(bar_s + b, take(cs0, cs1, b));
+          stage_split3<D, BN, 128, 128, 8>(k + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kK + b * L::kKStage);
+          tc::fence_proxy_async_smem();
+          tc::mbar_arrive(k_ready + b);
+        } else {
+          take(cs0, cs1, b);  // (this completion is not waited for here; keep the count in step)
+        }
+        tc::mbar_wait(bar_o, c_o++ & 1);
+        tc::tc_fence_after();
+        const float alpha = alpha_s[(j % 3) * BM + row];
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t pv[32];
+          tc::tmem_ld32(t_o + lane_off + c0, pv);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) o[c0 + jj] = fmaf(o[c0 + jj], alpha, __uint_as_float(pv[jj]));
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(o_free);
+        if (j + 2 < nblk) {  // V_j is consumed once PV_j is done
+          stage_split3<D, BN, 128, 128, 8>(v + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kV + b * L::kKStage);
+          tc::fence_proxy_async_smem();
+          tc::mbar_arrive(v_ready + b);
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // l_s from the softmax warps
+      const int64_t r = q0 + row;
+      if (r < seg) {
+        const bool ok = r < nv && nblk > 0;
+        const float inv = ok ? 1.0f / l_s[row] : 0.f;
+        float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + hd);
+#pragma unroll
+        for (int jj = 0; jj < D; jj += 4)
+          dst[jj / 4] = make_float4(o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
+      }
     }
   }
   tc::tc_fence_before();
@@ -306,12 +367,12 @@ static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const voi
                         void* out, float* lse, const int2* items, const int64_t* n_items, int64_t max_items,
                         const int64_t* valid, cudaStream_t st) {
   const int smem = Lay<D>::kAlloc;
-  if (jg_status rc = ensure_smem_attr((const void*)attn_fwd_x3_kernel<D>, smem, "attn_fwd_x3_kernel")) return rc;
-  int per_sm = 1;
-  JG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_fwd_x3_kernel<D>, kThreads, smem));
-  per_sm = std::max(1, std::min(per_sm, 512 / Lay<D>::kTmemCols));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)per_sm * device_sm_count()));
-  attn_fwd_x3_kernel<D><<<grid, kThreads, smem, st>>>(off, items, n_items, H, total_rows, (const float*)q,
+  if (jg_status rc = ensure_smem_attr((const void*)attn_fwd_x3_kernel<D>, std::max(smem, 120 * 1024),
+                                      "attn_fwd_x3_kernel"))
+    return rc;
+  // one CTA per SM (all 512 TMEM columns)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)device_sm_count()));
+  attn_fwd_x3_kernel<D><<<grid, kFwdThreads, std::max(smem, 120 * 1024), st>>>(off, items, n_items, H, total_rows, (const float*)q,
                                                        (const float*)k, (const float*)v, (float*)out, lse,
                                                        kLog2e / sqrtf((float)D), valid);
   JG_LAUNCHED("attn_fwd_x3_kernel");
