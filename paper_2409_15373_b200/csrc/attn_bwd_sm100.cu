@@ -9,8 +9,8 @@
 //   2. main persistent kernel, key-stationary: a CTA owns 128 key rows of one (sample, head) and
 //      streams the sample's queries in 64-row blocks:
 //        S^T = K Q_j^T, dP^T = V dO_j^T                      (tcgen05, M=128 keys, N=64 queries)
-//        P^T (bf16) back into TMEM over S^T, dS^T -> smem      (softmax warps, thread = key row)
-//        dV += P^T dO_j (TS: A = P^T from TMEM), dK += dS^T Q_j   (accumulated in TMEM across all j)
+//        P^T and dS^T (bf16) back into TMEM over S^T, dS^T also -> smem   (softmax warps, thread = key row)
+//        dV += P^T dO_j, dK += dS^T Q_j (TS: A from TMEM; accumulated in TMEM across all j)
 //        dQ_j^T = K^T dS^T                                    (M = head_dim, N = 64 queries)
 //      dQ_j^T is drained by a second warpgroup through smem and added into the accumulator with TMA
 //      tensor reduce-adds (cp.reduce.async.bulk.tensor .add, two alternating staging buffers). The key tiles of
@@ -30,8 +30,9 @@
 //   3. epilogue: dQ (bf16) = accumulator                                                 (HBM-bound)
 // Warps: 0 TMA producer, 1-2 MMA issuers, 4-11 softmax/dS (two warps per TMEM lane
 // quarter, 32 query columns each), 12-15 dQ drain + dK/dV epilogue.
-// TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); P^T_j is written over the S^T
-// slot and dQ_j^T into the dP^T slot of buffer j&1 once its scores are consumed; dV [256,384), dK [384,512). S_{j+1} is issued before
+// TMEM columns: two score buffers b at [128b, 128b+128) = S^T (64) + dP^T (64); P^T_j and dS^T_j (16 packed
+// columns per 32 queries each, interleaved) are written over the S^T slot and dQ_j^T into the dP^T slot of buffer
+// j&1 once its scores are consumed; dV [256,384), dK [384,512). S_{j+1} is issued before
 // dV_j/dK_j/dQ_j so the softmax warpgroup works on block j+1 while the tensor core finishes block j.
 #include "common.cuh"
 #include "internal.h"
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* qd_full = bars + 4;
   uint64_t* qd_empty = qd_full + L::kStages;
   uint64_t* st_full = qd_empty + L::kStages;  // [2] per TMEM score buffer
-  uint64_t* pt_free = st_full + 2;            // [2] dV finished reading P^T from TMEM buffer b
+  uint64_t* pt_free = st_full + 2;            // [2] dV / dK finished reading P^T / dS^T from TMEM buffer b
   uint64_t* p_full = pt_free + 2;
   uint64_t* pds_empty = p_full + 1;            // [kPdsBufs]
   uint64_t* dq_full = pds_empty + kPdsBufs;          // [2] one per score buffer: a single barrier could complete
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int b = j & 1;
             const uint32_t s = qd_cnt % L::kStages;
             wp.wait_warp(qd_full + s, (qd_cnt / L::kStages) & 1, 2);
-            wp.wait_warp(pt_free + b, ((fill_par >> b) & 1) ^ 1, 3);  // dV of the block that used b read its P^T
+            wp.wait_warp(pt_free + b, ((fill_par >> b) & 1) ^ 1, 3);  // dV / dK of the block that used b are done
             wp.wait_warp(dq_empty + b, ((fill_par >> b) & 1) ^ 1, 4);  // dQ^T previously written here was drained
             fill_par ^= 1u << b;
             tc::tc_fence_after();
@@ -397,23 +398,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < BQ / 16; ++kk)
               tc::mma_bf16_ts_warp(tmem + 256, tmem + col + 32 * (kk >> 1) + 8 * (kk & 1),
                                    tc::sw128_desc(do_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
-            tc::mma_commit_warp(pt_free + (j & 1));
-            // dQ_j^T = K^T dS^T into the consumed dP^T slot of buffer j&1
+            // dQ_j^T = K^T dS^T into the consumed dP^T slot of buffer j&1 (B = dS^T from smem)
 #pragma unroll
             for (int kk = 0; kk < BKV / 16; ++kk)
               tc::mma_bf16_ss_warp(tmem + col + 64, tc::sw128_desc(k_base + kk * 2048, L::kChunkKV, 1024),
                                    tc::sw128_desc(ds_cur + kk * 2048, 16, 1024), kIdQ, kk > 0);
             tc::mma_commit_warp(dq_full + (j & 1));
+            tc::mma_commit_warp(pds_empty + pb);  // the smem dS^T's only reader is done
             if (j == nq - 1) tc::mma_commit_warp(k_empty);  // the item's last read of K: reload during dK
             if (wp.g) wp.trace(84);
-            // dK += dS^T Q_j (A K-major [128 x 64 q] smem; B MN-major [64 q x D])
+            // dK += dS^T Q_j (TS: A = dS^T from TMEM, packed by the softmax into the S^T columns P^T leaves free:
+            // col + 32(kk/2) + 16 + 8(kk&1); B MN-major [64 q x D])
 #pragma unroll
             for (int kk = 0; kk < BQ / 16; ++kk)
-              tc::mma_bf16_ss_warp(tmem + 384, tc::sw128_desc(ds_cur + kk * 32, 16, 1024),
+              tc::mma_bf16_ts_warp(tmem + 384, tmem + col + 32 * (kk >> 1) + 16 + 8 * (kk & 1),
                                    tc::sw128_desc(q_base + kk * 2048, L::kChunkQ, 1024), kIdKV, (j > 0 || kk > 0));
+            tc::mma_commit_warp(pt_free + (j & 1));  // P^T and dS^T of buffer j&1 are consumed
             // Q_j, dO_j are no longer needed (warp 1's S/dP_j completed before the softmax published P_j)
             tc::mma_commit_warp(qd_empty + (qd_cnt % L::kStages));
-            tc::mma_commit_warp(pds_empty + pb);
             if (wp.g) wp.trace(82);
           }
           tc::mma_commit_warp(dkv_full);
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           body(std::true_type{});
         // P^T (bf16) back over the S^T columns this thread read: the A operand of the dV MMA
         tc::tmem_st16(lane_addr + b * 128 + half * 32, pk);
+        tc::tmem_st16(lane_addr + b * 128 + half * 32 + 16, dk2);  // dS^T for the TS-form dK MMA
         const uint32_t pb = pds_cnt % kPdsBufs;
         wp.wait_warp(pds_empty + pb, ((pds_cnt / kPdsBufs) & 1) ^ 1, 2);
         ++pds_cnt;
