@@ -541,11 +541,17 @@ static jg_status check_schedule(const char* op, jg_schedule s, const int64_t* of
   return JG_OK;
 }
 
+// The tensor-core and tiled kernels move 16-byte vectors (TMA boxes, float4 / uint2 loads): tensors whose base is
+// not 16-byte aligned (views into a larger buffer) take the row-per-warp kernels, which load scalars.
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 static jg_status attn_forward(const int64_t* off, int64_t batch, int64_t total_rows, int32_t H, int32_t D,
                               const void* q, const void* k, const void* v, void* out, float* lse, jg_dtype dtype,
                               jg_schedule sched, const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
   if (jg_status rc = check_schedule("jagged_flash_attention_forward", sched, off, batch, total_rows)) return rc;
+  if (!(al16(q) && al16(k) && al16(v) && al16(out)))
+    return launch_attn_fwd_simt(off, batch, total_rows, H, D, q, k, v, out, lse, dtype, nullptr, nullptr, 0, valid, st);
   if (!force_simt() && attn_sm100_supported(D, dtype)) {
     jg_schedule own = nullptr;
     if (!sched) {
@@ -591,6 +597,9 @@ static jg_status attn_backward(const int64_t* off, int64_t batch, int64_t total_
   }
   float* delta = (float*)workspace;
   void* dq_acc = (char*)workspace + attn_lsd_bytes(total_rows, H);
+  if (!(al16(q) && al16(k) && al16(v) && al16(go) && al16(o) && al16(dq) && al16(dk) && al16(dv)))
+    return launch_attn_bwd_simt(off, batch, total_rows, H, D, q, k, v, go, o, lse, dq, dk, dv, delta, dtype, nullptr,
+                                nullptr, 0, valid, false, st);
 
   if (!force_simt() && attn_sm100_bwd_supported(D, dtype)) {
     jg_schedule own = nullptr;

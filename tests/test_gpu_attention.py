@@ -266,3 +266,29 @@ def test_fp32_tensor_core_path_multi_block(D):
             t.cpu().numpy() for t in (o, l, rq, rk, rv))
     for got, r, nm in zip((out, lse, dq, dk, dv), ref, ("out", "lse", "dq", "dk", "dv")):
         assert_fp32_close(got, r, what=f"fp32 tcgen05 {nm} (D={D})")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_unaligned_views_take_scalar_kernels(dtype):
+    """Tensors whose base is not 16-byte aligned (views one element into a larger buffer) must not reach the
+    16-byte vector paths (TMA boxes, float4 loads): the C-ABI routes them to the row-per-warp kernels. Results agree
+    with the aligned run (fp32 1e-5 / bf16 2e-2) instead of faulting."""
+    ln = [5, 0, 130, 64, 257]
+    off, _, (Q, K, V, G) = make(ln, 2, 64, 13, dtype)
+    close = assert_fp32_close if dtype == torch.float32 else assert_bf16_close
+
+    def shifted(t):
+        buf = torch.empty(t.values.numel() + 1, dtype=dtype, device=DEV)
+        view = buf[1:].view_as(t.values)
+        view.copy_(t.values)
+        assert view.data_ptr() % 16 != 0
+        return J.JaggedTensor(t.offsets, view, off)
+
+    Qs, Ks, Vs, Gs = (shifted(t) for t in (Q, K, V, G))
+    ref = J.jagged_flash_attention_forward(Q, K, V)
+    got = J.jagged_flash_attention_forward(Qs, Ks, Vs)
+    close(got.output.values, ref.output.values.double().cpu().numpy(), what="out (unaligned)")
+    gr = J.jagged_flash_attention_backward(Q, K, V, G, ref)
+    gg = J.jagged_flash_attention_backward(Qs, Ks, Vs, Gs, got)
+    for a, b, nm in ((gg.dq, gr.dq, "dq"), (gg.dk, gr.dk, "dk"), (gg.dv, gr.dv, "dv")):
+        close(a.values, b.values.double().cpu().numpy(), what=f"{nm} (unaligned)")
