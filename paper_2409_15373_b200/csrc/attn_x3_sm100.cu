@@ -530,34 +530,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
         }
         tc::mma_commit_warp(bar_s);
       }
-      tc::mbar_wait(bar_s, ph);  // (all threads: V_j is free once the scores are done)
+      tc::mbar_wait(bar_s, ph);
       tc::tc_fence_after();
-      if (half == 1 && j + 1 < nblk)  // warps 4-7 split V_{j+1} while warps 0-3 form dS
-        stage_split3<D, BN, 128, 128>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb);
-      if (half == 0) {
-        uint32_t sr[64], pr[64];  // all of S and dP first: the dS pieces are written over both
-        tc::tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
-        tc::tmem_ld32(t_s + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-        tc::tmem_ld32(t_dp + lane_off, *reinterpret_cast<uint32_t(*)[32]>(pr));
-        tc::tmem_ld32(t_dp + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(pr + 32));
+      {  // dS = P (dP - Delta) on both warpgroups: warp half h takes keys [32h, 32h + 32) of its lane quarter
+        uint32_t sr[32], pr[32];
+        tc::tmem_ld32(t_s + lane_off + 32 * half, sr);
+        tc::tmem_ld32(t_dp + lane_off + 32 * half, pr);
         tc::tmem_wait_ld();
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every S / dP column is read before the pieces overwrite them
 #pragma unroll
-        for (int jj = 0; jj < 64; ++jj) {
-          const bool in = rin && (k0 + jj < nv);
+        for (int jj = 0; jj < 32; ++jj) {
+          const bool in = rin && (k0 + 32 * half + jj < nv);
           const float p = in ? exp2f(__uint_as_float(sr[jj]) * scale_log2 - lr) : 0.f;
           sr[jj] = __float_as_uint(p * (__uint_as_float(pr[jj]) - dr));
         }
+        // dS1 over S [0, 32), dS2 over S [32, 64), dS3 over dP [0, 32): keys 32h.. packed at column 16h
+        uint32_t w1[16], w2[16], w3[16];
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {  // dS1 over S [0, 32), dS2 over S [32, 64), dS3 over dP [0, 32)
-          uint32_t w1[16], w2[16], w3[16];
-#pragma unroll
-          for (int jj = 0; jj < 32; jj += 2)
-            split3(__uint_as_float(sr[32 * g + jj]), __uint_as_float(sr[32 * g + jj + 1]), w1[jj / 2], w2[jj / 2],
-                   w3[jj / 2]);
-          tc::tmem_st16(t_s + lane_off + 16 * g, w1);
-          tc::tmem_st16(t_s + lane_off + 32 + 16 * g, w2);
-          tc::tmem_st16(t_dp + lane_off + 16 * g, w3);
-        }
+        for (int jj = 0; jj < 32; jj += 2)
+          split3(__uint_as_float(sr[jj]), __uint_as_float(sr[jj + 1]), w1[jj / 2], w2[jj / 2], w3[jj / 2]);
+        tc::tmem_st16(t_s + lane_off + 16 * half, w1);
+        tc::tmem_st16(t_s + lane_off + 32 + 16 * half, w2);
+        tc::tmem_st16(t_dp + lane_off + 16 * half, w3);
         tc::tmem_wait_st();
       }
       tc::tc_fence_before();
@@ -575,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
+      if (j + 1 < nblk) stage_split3<D, BN>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb);  // under dQ_j (V_j is free)
       tc::mbar_wait(bar_o, ph);
       tc::tc_fence_after();
       if (j + 1 < nblk) stage_split3<D, BN>(k + hd, b0, k0 + BN, nv, rs, sbase + L::kYa);  // K_j is free
