@@ -385,11 +385,12 @@ static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const voi
 // SPEC.md:316 peak-intermediate bound); the stationary operand of the TS-form score MMAs lives in TMEM.
 //   dQ pass   TMEM: Q1 Q2 Q3 [0, 3D/2) | S [3D/2, +64) | dP [+64) | dQ [+D) ; smem: dO pieces, K_j, V_j pieces
 //             S = Q K_j^T (TS), dP = dO V_j^T (SS); dS = P (dP - Delta) -> TMEM over S / dP; dQ += dS K_j (TS,
-//             K_j read MN-major from the same staging). Warps 4-7 split V_{j+1} while warps 0-3 form dS;
-//             K_{j+1} is split by all warps after dQ_j.
+//             K_j read MN-major from the same staging). dS is formed on both warpgroups (32 keys each); V_{j+1}
+//             is split under the dQ MMA, K_{j+1} after it.
 //   dK/dV pass TMEM: K1 K2 [0, D) | S^T [D, +64) | dP^T [+64) | dV [+D) | dK [+D) ; smem: K3, V pieces, Q_j, dO_j
 //             S^T = K Q_j^T (TS for K1, K2; SS for K3), dP^T = V dO_j^T (SS); P^T -> TMEM, dV += P^T dO_j;
-//             dS^T -> TMEM, dK += dS^T Q_j. Warps 4-7 split dO_{j+1} while warps 0-3 store dS^T; Q_{j+1} after dK_j.
+//             dS^T -> TMEM, dK += dS^T Q_j. The elementwise work runs on both warpgroups (32 queries each); dO_{j+1}
+//             is split under the dK MMA, Q_{j+1} after it.
 template <int D, bool KV>
 struct BwdLay {
   static constexpr int kXChunk = BM * 128, kYChunk = BN * 128;
@@ -676,34 +677,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
         }
         tc::mma_commit_warp(bar_s);
       }
-      float dsv[64];  // dS^T (64 queries), split into TMEM once P^T's MMAs are done
-      if (half == 0) {
-        tc::mbar_wait(bar_s, ph_s);
-        tc::tc_fence_after();
-        uint32_t sr[64], pr[64];  // all of S^T and dP^T first: the P^T pieces are written over both
-        tc::tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
-        tc::tmem_ld32(t_s + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-        tc::tmem_ld32(t_dp + lane_off, *reinterpret_cast<uint32_t(*)[32]>(pr));
-        tc::tmem_ld32(t_dp + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(pr + 32));
+      // P^T and dS^T on both warpgroups: warp half h takes queries [32h, 32h + 32) of its key quarter
+      float dsv[32];  // dS^T, split into TMEM once P^T's MMAs are done
+      tc::mbar_wait(bar_s, ph_s);
+      tc::tc_fence_after();
+      {
+        uint32_t sr[32], pr[32];
+        tc::tmem_ld32(t_s + lane_off + 32 * half, sr);
+        tc::tmem_ld32(t_dp + lane_off + 32 * half, pr);
         tc::tmem_wait_ld();
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every S^T / dP^T column is read before the pieces land
 #pragma unroll
-        for (int jj = 0; jj < 64; ++jj) {
-          const bool in = rin && (y0 + jj < nv);
-          const float p = in ? exp2f(__uint_as_float(sr[jj]) * scale_log2 - ls[jj]) : 0.f;
-          dsv[jj] = p * (__uint_as_float(pr[jj]) - dls[jj]);
+        for (int jj = 0; jj < 32; ++jj) {
+          const int qc = 32 * half + jj;
+          const bool in = rin && (y0 + qc < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[jj]) * scale_log2 - ls[qc]) : 0.f;
+          dsv[jj] = p * (__uint_as_float(pr[jj]) - dls[qc]);
           sr[jj] = __float_as_uint(p);
         }
+        // P1 [0, 32), P2 [32, 64), P3 [64, 96) of t_s; queries 32h.. packed at column 16h
+        uint32_t p1[16], p2[16], p3[16];
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {  // P1 [0, 32), P2 [32, 64), P3 [64, 96) of t_s; queries 32g.. at 16g
-          uint32_t p1[16], p2[16], p3[16];
-#pragma unroll
-          for (int jj = 0; jj < 32; jj += 2)
-            split3(__uint_as_float(sr[32 * g + jj]), __uint_as_float(sr[32 * g + jj + 1]), p1[jj / 2], p2[jj / 2],
-                   p3[jj / 2]);
-          tc::tmem_st16(t_s + lane_off + 16 * g, p1);
-          tc::tmem_st16(t_s + lane_off + 32 + 16 * g, p2);
-          tc::tmem_st16(t_s + lane_off + 64 + 16 * g, p3);
-        }
+        for (int jj = 0; jj < 32; jj += 2)
+          split3(__uint_as_float(sr[jj]), __uint_as_float(sr[jj + 1]), p1[jj / 2], p2[jj / 2], p3[jj / 2]);
+        tc::tmem_st16(t_s + lane_off + 16 * half, p1);
+        tc::tmem_st16(t_s + lane_off + 32 + 16 * half, p2);
+        tc::tmem_st16(t_s + lane_off + 64 + 16 * half, p3);
         tc::tmem_wait_st();
       }
       tc::tc_fence_before();
@@ -722,19 +721,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
       }
       tc::mbar_wait(bar_o, ph_o);  // (all threads) the P^T pieces and dO_j are consumed
       tc::tc_fence_after();
-      if (half == 1 && j + 1 < nblk)  // warps 4-7 split dO_{j+1} while warps 0-3 store dS^T
-        stage_split3<D, BN, 128, 128>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb);
-      if (half == 0) {
+      {
+        uint32_t d1[16], d2[16], d3[16];
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          uint32_t d1[16], d2[16], d3[16];
-#pragma unroll
-          for (int jj = 0; jj < 32; jj += 2)
-            split3(dsv[32 * g + jj], dsv[32 * g + jj + 1], d1[jj / 2], d2[jj / 2], d3[jj / 2]);
-          tc::tmem_st16(t_s + lane_off + 16 * g, d1);
-          tc::tmem_st16(t_s + lane_off + 32 + 16 * g, d2);
-          tc::tmem_st16(t_s + lane_off + 64 + 16 * g, d3);
-        }
+        for (int jj = 0; jj < 32; jj += 2) split3(dsv[jj], dsv[jj + 1], d1[jj / 2], d2[jj / 2], d3[jj / 2]);
+        tc::tmem_st16(t_s + lane_off + 16 * half, d1);
+        tc::tmem_st16(t_s + lane_off + 32 + 16 * half, d2);
+        tc::tmem_st16(t_s + lane_off + 64 + 16 * half, d3);
         tc::tmem_wait_st();
       }
       ph_o ^= 1;
@@ -752,6 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
+      if (j + 1 < nblk) stage_split3<D, BN>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb);  // under dK_j (dO_j free)
       tc::mbar_wait(bar_o, ph_o);
       tc::tc_fence_after();
       if (j + 1 < nblk) stage_split3<D, BN>(q + hd, b0, y0 + BN, nv, rs, sbase + L::kYa);  // Q_j is free
