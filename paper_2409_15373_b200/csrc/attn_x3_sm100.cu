@@ -102,6 +102,43 @@ __device__ __forceinline__ void stage_split3(const float* __restrict__ src, int6
 }
 
 
+// A moving block held in registers between its global loads and its split into smem: the loads go out while the
+// tensor core still reads the block's buffer, the split + stores once it is free.
+template <int D, int ROWS, int NT = kThreads>
+struct Pre {
+  static constexpr int kUnits = D / 8, kTotal = ROWS * kUnits, kIter = kTotal / NT;
+  static constexpr int kPiece = (D / 64) * ROWS * 128;
+  float4 a[kIter], b[kIter];
+  __device__ __forceinline__ void load(const float* __restrict__ src, int64_t b0, int64_t r0, int64_t n, int64_t rs,
+                                       int t) {
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+      const int e = t + i * NT, r = e / kUnits, u = e % kUnits;
+      a[i] = b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r0 + r < n) {
+        const float4* p = reinterpret_cast<const float4*>(src + (b0 + r0 + r) * rs + u * 8);
+        a[i] = __ldg(p);
+        b[i] = __ldg(p + 1);
+      }
+    }
+  }
+  __device__ __forceinline__ void store(uint32_t base, int t) const {
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+      const int e = t + i * NT, r = e / kUnits, u = e % kUnits;
+      uint32_t w1[4], w2[4], w3[4];
+      split3(a[i].x, a[i].y, w1[0], w2[0], w3[0]);
+      split3(a[i].z, a[i].w, w1[1], w2[1], w3[1]);
+      split3(b[i].x, b[i].y, w1[2], w2[2], w3[2]);
+      split3(b[i].z, b[i].w, w1[3], w2[3], w3[3]);
+      const uint32_t off = (u >> 3) * (ROWS * 128) + tc::sw128_offset(r, u & 7);
+      tc::st_shared_v4(base + off, w1[0], w1[1], w1[2], w1[3]);
+      tc::st_shared_v4(base + kPiece + off, w2[0], w2[1], w2[2], w2[3]);
+      tc::st_shared_v4(base + 2 * kPiece + off, w3[0], w3[1], w3[2], w3[3]);
+    }
+  }
+};
+
 // This thread's half (columns [half*D/2, +D/2)) of row `row` of a fp32 [*, H, D] tensor, split into bf16 pieces:
 // pieces 0 .. NT-1 into TMEM (piece p at column t_base + p*D/2, packed two per column), piece 2 (when kS3)
 // into the K-major SWIZZLE_128B smem tile at s3 ([128 rows x D], chunks of 128 x 128 B).
@@ -570,10 +607,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
-      if (j + 1 < nblk) stage_split3<D, BN>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb);  // under dQ_j (V_j is free)
+      Pre<D, BN> kpre;
+      if (j + 1 < nblk) {  // under dQ_j: split V_{j+1} (V_j is free) and load K_{j+1}
+        stage_split3<D, BN>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb);
+        kpre.load(k + hd, b0, k0 + BN, nv, rs, tid);
+      }
       tc::mbar_wait(bar_o, ph);
       tc::tc_fence_after();
-      if (j + 1 < nblk) stage_split3<D, BN>(k + hd, b0, k0 + BN, nv, rs, sbase + L::kYa);  // K_j is free
+      if (j + 1 < nblk) kpre.store(sbase + L::kYa, tid);  // K_j is free
       if (j % kFlush == kFlush - 1 || j + 1 == nblk)
         ld_half_flush<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, scale, j >= kFlush, r < seg);
       tc::tc_fence_before();
@@ -745,10 +786,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
-      if (j + 1 < nblk) stage_split3<D, BN>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb);  // under dK_j (dO_j free)
+      Pre<D, BN> qpre;
+      if (j + 1 < nblk) {  // under dK_j: split dO_{j+1} (dO_j is free) and load Q_{j+1}
+        stage_split3<D, BN>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb);
+        qpre.load(q + hd, b0, y0 + BN, nv, rs, tid);
+      }
       tc::mbar_wait(bar_o, ph_o);
       tc::tc_fence_after();
-      if (j + 1 < nblk) stage_split3<D, BN>(q + hd, b0, y0 + BN, nv, rs, sbase + L::kYa);  // Q_j is free
+      if (j + 1 < nblk) qpre.store(sbase + L::kYa, tid);  // Q_j is free
       if (j % kFlush == kFlush - 1 || j + 1 == nblk) {
         ld_half_flush<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, 1.f, j >= kFlush, r < seg);
         ld_half_flush<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, scale, j >= kFlush, r < seg);
