@@ -534,11 +534,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
       dr = delta[hr + b0 + r];
     }
     __syncthreads();  // previous item: TMEM dQ read, smem free
-    if (nblk > 0) {  // Q pieces -> TMEM; dO pieces, K_0, V_0 -> smem
+    if (nblk > 0) {  // Q pieces -> TMEM; dO pieces, K_0, V_0 -> smem (K_0 / V_0 loads in flight throughout)
+      Pre<D, BN> k0p, v0p;
+      k0p.load(k + hd, b0, 0, nv, rs, tid);
+      v0p.load(v + hd, b0, 0, nv, rs, tid);
       stage_row_tmem<D, 3>(q + (b0 + r) * rs + hd, rin, t_q, lane_off, half, row, 0);
-      stage_split3<D, BM>(go + hd, b0, q0, nv, rs, sbase + L::kX);
-      stage_split3<D, BN>(k + hd, b0, 0, nv, rs, sbase + L::kYa);
-      stage_split3<D, BN>(v + hd, b0, 0, nv, rs, sbase + L::kYb);
+      stage_split3<D, BM, 0, kThreads, 8>(go + hd, b0, q0, nv, rs, sbase + L::kX);
+      k0p.store(sbase + L::kYa, tid);
+      v0p.store(sbase + L::kYb, tid);
     }
     for (int j = 0; j < nblk; ++j) {
       const int64_t k0 = (int64_t)j * BN;
@@ -674,11 +677,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
     const bool rin = r < nv;
     const int nblk = x0 < nv ? (int)((nv + BN - 1) / BN) : 0;
     __syncthreads();
-    if (nblk > 0) {  // K1, K2 -> TMEM and K3 -> smem; V pieces, Q_0, dO_0 -> smem
+    if (nblk > 0) {  // K1, K2 -> TMEM and K3 -> smem; V pieces, Q_0, dO_0 -> smem (Q_0 / dO_0 loads in flight)
+      Pre<D, BN> q0p, g0p;
+      q0p.load(q + hd, b0, 0, nv, rs, tid);
+      g0p.load(go + hd, b0, 0, nv, rs, tid);
       stage_row_tmem<D, 2, true>(k + (b0 + r) * rs + hd, rin, t_k, lane_off, half, row, s_k3);
-      stage_split3<D, BM>(v + hd, b0, x0, nv, rs, s_v);
-      stage_split3<D, BN>(q + hd, b0, 0, nv, rs, sbase + L::kYa);
-      stage_split3<D, BN>(go + hd, b0, 0, nv, rs, sbase + L::kYb);
+      stage_split3<D, BM, 0, kThreads, 8>(v + hd, b0, x0, nv, rs, s_v);
+      q0p.store(sbase + L::kYa, tid);
+      g0p.store(sbase + L::kYb, tid);
     }
     for (int j = 0; j < nblk; ++j) {
       const int64_t y0 = (int64_t)j * BN;
