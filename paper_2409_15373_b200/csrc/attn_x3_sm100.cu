@@ -1,6 +1,6 @@
-// attn_x3_sm100.cu — fp32 Jagged Flash Attention forward on tcgen05 tensor cores (split-bf16 emulation).
+// attn_x3_sm100.cu — fp32 Jagged Flash Attention forward + backward on tcgen05 tensor cores (split-bf16 emulation).
 //
-// Semantics: attention.cpp:172-225 in fp32 mode (the reference's float instantiation, attention.cpp:311-331),
+// Semantics: attention.cpp:172-289 in fp32 mode (the reference's float instantiation, attention.cpp:311-331),
 // same outputs as the tiled FFMA kernels in attn_simt.cu up to fp32 rounding.
 //
 // tcgen05 has no fp32 MMA. Every fp32 operand x is split into three bf16 pieces x = x1 + x2 + x3 (x1 = bf16(x),
@@ -13,16 +13,11 @@
 // the cross terms into an accumulator that already holds a1b1 would cost ~2^-23 |ab| per MMA; this order leaves
 // only the D/16 k-steps of a1b1 at that magnitude (the difference shows in dS = P (dP - Delta), which cancels).
 //
-// One CTA (8 warps) per (sample, 128-row query tile, head) item of the schedule's LPT list (persistent,
+// Forward: one CTA (8 warps) per (sample, 128-row query tile, head) item of the schedule's LPT list (persistent,
 // round-robin); Q's pieces sit in TMEM [0, 3D/2) (split on the fly per item); keys stream in 64-row blocks through
-// two smem stages of bf16 pieces (SWIZZLE_128B; K K-major, V MN-major), split on the fly from fp32 (no scratch):
-//   warp 0      issues S = sum Qi Kj^T (6 x D/16 TS MMAs, M=128, N=64) into TMEM [3D/2, +64)
-//   warps 4-7   split block j+1 into the other stage meanwhile
-//   warps 0-3   thread = query row: online softmax (exact fp32, attention.cpp:205-214), P1 | P2 (bf16 packed
-//               two per column) back into TMEM over S and P3 past O: the A operands of the TS-form P V MMAs
-//   warp 0      issues P V (6 x 4 TS MMAs, N=D) into TMEM O [.., +D)
-//   all warps   O (registers; warp w owns lanes 32(w%4).. and half w/4 of the columns) = alpha O + P V
-// Epilogue: O / l and lse = m + log l (fp32) straight to global; padded mode masks keys / rows past `valid`.
+// two-stage K and V rings of bf16 pieces (SWIZZLE_128B; K K-major, V MN-major) split on the fly from fp32 (no
+// scratch). The warp roles and the pipeline are described at attn_fwd_x3_kernel; the backward's two passes at
+// BwdLay. Epilogues write fp32 straight to global; padded mode masks keys / rows past `valid`.
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
