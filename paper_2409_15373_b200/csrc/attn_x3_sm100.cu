@@ -36,14 +36,14 @@ struct Lay {
   static constexpr int kK = 0;                         // K ring: 2 stages
   static constexpr int kV = kK + 2 * kKStage;          // V ring: 2 stages
   static constexpr int kBar = kV + 2 * kKStage;        // 10 mbarriers + tmem slot
-  static constexpr int kAlpha = kBar + 128;            // float[3][128]
-  static constexpr int kL = kAlpha + 3 * 4 * BM;       // float[128]
-  static constexpr int kBytes = kL + 4 * BM;
+  static constexpr int kAlpha = kBar + 128;            // float[2][128] (block maxima of the two key halves)
+  static constexpr int kL = kAlpha + 2 * 4 * BM;       // float[2][128]
+  static constexpr int kBytes = kL + 2 * 4 * BM;
   static constexpr int kAlloc = kBytes + 1024;         // + alignment slack
   // TMEM: Q1 Q2 Q3 [0, 3D/2) | S0 | S1 (64 each) | O (D) | P3_0 | P3_1 (32 each)
   static constexpr int kTmemCols = 512;
 };
-constexpr int kFwdThreads = 256;  // 4 softmax warps (warp 0 also issues the MMAs), 4 O / staging warps
+constexpr int kFwdThreads = 256;  // 8 warps (warp 0 also issues the MMAs)
 
 
 // one paired conversion (cvt.rn.bf16x2) per piece; the pieces' fp32 values are the packed halves shifted into place
@@ -176,14 +176,13 @@ __device__ __forceinline__ void stage_row_tmem(const float* __restrict__ src, bo
   }
 }
 
-// Forward (warp-specialised pipeline; attention.cpp:172-225):
-//   warps 0-3   softmax of block j (thread = query row) while the tensor core runs S_{j+1} / PV_{j-1};
-//               warp 0 also issues the MMAs: S_0, S_1, then per block j PV_j (after every P_j and the previous O
-//               read-out) and S_{j+2} into the score buffer P_j occupied (in-order tcgen05 execution orders it)
-//   warps 4-7   K_{j+2} split into the freed K stage once S_j is done; O = alpha O + PV_j in registers (thread =
-//               row, all D columns); V_{j+2} split into the freed V stage once PV_j is done
-// The score MMAs of block j+1 therefore overlap the softmax of block j, and the P V of block j overlaps the softmax
-// of block j+1.
+// Forward (pipelined; attention.cpp:172-225). Two TMEM score buffers and two-stage K / V rings let the tensor core
+// run PV_j and S_{j+2} back to back while the warps work on block j+1. Every warp does every phase on its share:
+// warp half h takes keys [32h, 32h + 32) of the softmax (the two halves of a row exchange block maxima through
+// shared memory; their sums combine at the end) and output columns [h D/2, (h + 1) D/2) of O (registers), and all
+// 256 threads split K_{j+2} (under PV_j, once S_j released the stage) and V_{j+2} (once PV_j released its stage).
+// Warp 0 also issues the MMAs: S_0, S_1, then per block PV_j (after every P_j and the previous O read-out) and
+// S_{j+2} into the score buffer P_j occupied (in-order tcgen05 execution orders the overwrite).
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_x3_kernel(
     const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
@@ -196,19 +195,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_x3_kernel(
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_s = bars;        // [2] score MMAs of the buffer done (commit)
   uint64_t* bar_o = bars + 2;    // PV_j done (commit)
-  uint64_t* p_ready = bars + 3;  // softmax wrote P_j (128 arrivals)
-  uint64_t* o_free = bars + 4;   // O read out (128 arrivals)
-  uint64_t* k_ready = bars + 5;  // [2] K stage split (128 arrivals)
-  uint64_t* v_ready = bars + 7;  // [2] V stage split (128 arrivals)
+  uint64_t* p_ready = bars + 3;  // P_j written (256 arrivals)
+  uint64_t* o_free = bars + 4;   // O read out (256 arrivals)
+  uint64_t* k_ready = bars + 5;  // [2] K stage split (256 arrivals)
+  uint64_t* v_ready = bars + 7;  // [2] V stage split (256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-  float* alpha_s = reinterpret_cast<float*>(smem + L::kAlpha);
-  float* l_s = reinterpret_cast<float*>(smem + L::kL);
+  float* mx_s = reinterpret_cast<float*>(smem + L::kAlpha);  // [2][128] block maxima of the two key halves
+  float* l_s = reinterpret_cast<float*>(smem + L::kL);       // [2][128] final row sums of the two halves
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) tc::mbar_init(bars + i, 1);
-    for (int i = 3; i < 9; ++i) tc::mbar_init(bars + i, 128);
+    for (int i = 3; i < 9; ++i) tc::mbar_init(bars + i, 256);
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -283,109 +282,97 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_x3_kernel(
     };
     if (warp == 0)
       for (int j = 0; j < 2 && j < nblk; ++j) issue_s(j);
-    if (half == 0) {
-      // ===================================================== softmax (thread = query row)
-      float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < nblk; ++j) {
-        const int b = j & 1;
-        const int64_t k0 = (int64_t)j * BN;
-        tc::mbar_wait(bar_s + b, take(cs0, cs1, b));
+    // ===================================================== all 8 warps: warp half h owns keys [32h, 32h + 32) of
+    // each block and output columns [h D/2, (h + 1) D/2) of its lane quarter's rows (thread = query row)
+    float m = -INFINITY, l = 0.f;  // running max (both halves agree), this half's running sum
+    float o[D / 2];
+#pragma unroll
+    for (int jj = 0; jj < D / 2; ++jj) o[jj] = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int b = j & 1;
+      const int64_t k0 = (int64_t)j * BN;
+      tc::mbar_wait(bar_s + b, take(cs0, cs1, b));
+      tc::tc_fence_after();
+      const uint32_t ts = t_s0 + b * 64;
+      uint32_t sr[32];
+      tc::tmem_ld32(ts + lane_off + 32 * half, sr);
+      tc::tmem_wait_ld();
+      float s[32];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        s[jj] = (k0 + 32 * half + jj < nv) ? __uint_as_float(sr[jj]) * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[jj]);
+      }
+      mx_s[half * BM + row] = mx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // both halves' maxima; every S column is read before P lands
+      const float mn = fmaxf(m, fmaxf(mx, mx_s[(half ^ 1) * BM + row]));  // finite: the block has a valid key
+      const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+      float ps = 0.f;
+      uint32_t p1[16], p2[16], p3[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const float a = exp2f(s[2 * jj] - mn), bb = exp2f(s[2 * jj + 1] - mn);
+        ps += a + bb;
+        split3(a, bb, p1[jj], p2[jj], p3[jj]);
+      }
+      l = l * alpha + ps;
+      m = mn;
+      tc::tmem_st16(ts + lane_off + 16 * half, p1);               // P1: keys 2c, 2c+1 at column c
+      tc::tmem_st16(ts + lane_off + 32 + 16 * half, p2);          // P2 at columns [32, 64)
+      tc::tmem_st16(t_p30 + b * 32 + lane_off + 16 * half, p3);   // P3 in its own slot
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      tc::mbar_arrive(p_ready);
+      if (warp == 0) {  // issuer: PV_j once every P_j is in and O is free
+        tc::mbar_wait(p_ready, c_p++ & 1);
+        if (j >= 1) tc::mbar_wait(o_free, c_of++ & 1);
+        if (j >= 2) tc::mbar_wait(v_ready + b, take(cv0, cv1, b));
         tc::tc_fence_after();
-        const uint32_t ts = t_s0 + b * 64;
-        uint32_t sr[2][32];
-        tc::tmem_ld32(ts + lane_off, sr[0]);
-        tc::tmem_ld32(ts + lane_off + 32, sr[1]);
-        tc::tmem_wait_ld();
-        float s[64];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int jj = 0; jj < 64; ++jj) {
-          s[jj] = (k0 + jj < nv) ? __uint_as_float(sr[jj >> 5][jj & 31]) * scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[jj]);
-        }
-        const float mn = fmaxf(m, mx);  // finite: the block holds at least one valid key
-        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mn);
-        float ps = 0.f;
-        uint32_t p1[32], p2[32], p3[32];
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const float a = exp2f(s[2 * jj] - mn), bb = exp2f(s[2 * jj + 1] - mn);
-          ps += a + bb;
-          split3(a, bb, p1[jj], p2[jj], p3[jj]);
-        }
-        l = l * alpha + ps;
-        m = mn;
-        tc::tmem_st32(ts + lane_off, p1);                  // P1: keys 2c, 2c+1 at column c
-        tc::tmem_st32(ts + lane_off + 32, p2);             // P2 at columns [32, 64)
-        tc::tmem_st32(t_p30 + b * 32 + lane_off, p3);      // P3 in its own slot
-        tc::tmem_wait_st();
-        alpha_s[(j % 3) * BM + row] = alpha;
-        tc::tc_fence_before();
-        tc::mbar_arrive(p_ready);
-        if (warp == 0) {  // issuer: PV_j once every P_j is in and O is free; then S_{j+2}
-          tc::mbar_wait(p_ready, c_p++ & 1);
-          if (j >= 1) tc::mbar_wait(o_free, c_of++ & 1);
-          if (j >= 2) tc::mbar_wait(v_ready + b, take(cv0, cv1, b));
+        issue_pv(j);
+      }
+      if (j + 2 < nblk) {  // K_j is consumed (S_j done): split K_{j+2} into its stage under PV_j
+        stage_split3<D, BN>(k + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kK + b * L::kKStage);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(k_ready + b);
+        if (warp == 0) {
+          tc::mbar_wait(k_ready + b, take(ck0, ck1, b));
           tc::tc_fence_after();
-          issue_pv(j);
-          if (j + 2 < nblk) {
-            tc::mbar_wait(k_ready + b, take(ck0, ck1, b));
-            tc::tc_fence_after();
-            issue_s(j + 2);
-          }
+          issue_s(j + 2);
         }
       }
-      if (warp == 0 && nblk > 0) tc::mbar_wait(o_free, c_of++ & 1);  // last O read-out: TMEM free next item
-      l_s[row] = l;
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // l_s for the O warps
+      tc::mbar_wait(bar_o, c_o++ & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < D / 2; c0 += 32) {
+        uint32_t pv[32];
+        tc::tmem_ld32(t_o + lane_off + half * (D / 2) + c0, pv);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) o[c0 + jj] = fmaf(o[c0 + jj], alpha, __uint_as_float(pv[jj]));
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(o_free);
+      if (j + 2 < nblk) {  // V_j is consumed (PV_j done)
+        stage_split3<D, BN>(v + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kV + b * L::kKStage);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(v_ready + b);
+      }
+    }
+    if (warp == 0 && nblk > 0) tc::mbar_wait(o_free, c_of++ & 1);  // last O read-out: TMEM free next item
+    l_s[half * BM + row] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    {
+      const float lt = l + l_s[(half ^ 1) * BM + row];
       const int64_t r = q0 + row;
       if (r < seg) {
         const bool ok = r < nv && nblk > 0;
-        lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(l)) * kLn2 : -INFINITY;
-      }
-    } else {
-      // ===================================================== O accumulation + K / V staging (thread = row)
-      float o[D];
+        const float inv = ok ? 1.0f / lt : 0.f;
+        float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + hd + half * (D / 2));
 #pragma unroll
-      for (int jj = 0; jj < D; ++jj) o[jj] = 0.f;
-      for (int j = 0; j < nblk; ++j) {
-        const int b = j & 1;
-        if (j + 2 < nblk) {  // K_j is consumed once S_j is done: split K_{j+2} into its stage
-          tc::mbar_wait(bar_s + b, take(cs0, cs1, b));
-          stage_split3<D, BN, 128, 128, 8>(k + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kK + b * L::kKStage);
-          tc::fence_proxy_async_smem();
-          tc::mbar_arrive(k_ready + b);
-        } else {
-          take(cs0, cs1, b);  // (this completion is not waited for here; keep the count in step)
-        }
-        tc::mbar_wait(bar_o, c_o++ & 1);
-        tc::tc_fence_after();
-        const float alpha = alpha_s[(j % 3) * BM + row];
-#pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t pv[32];
-          tc::tmem_ld32(t_o + lane_off + c0, pv);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) o[c0 + jj] = fmaf(o[c0 + jj], alpha, __uint_as_float(pv[jj]));
-        }
-        tc::tc_fence_before();
-        tc::mbar_arrive(o_free);
-        if (j + 2 < nblk) {  // V_j is consumed once PV_j is done
-          stage_split3<D, BN, 128, 128, 8>(v + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kV + b * L::kKStage);
-          tc::fence_proxy_async_smem();
-          tc::mbar_arrive(v_ready + b);
-        }
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // l_s from the softmax warps
-      const int64_t r = q0 + row;
-      if (r < seg) {
-        const bool ok = r < nv && nblk > 0;
-        const float inv = ok ? 1.0f / l_s[row] : 0.f;
-        float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + hd);
-#pragma unroll
-        for (int jj = 0; jj < D; jj += 4)
+        for (int jj = 0; jj < D / 2; jj += 4)
           dst[jj / 4] = make_float4(o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
+        if (half == 0) lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(lt)) * kLn2 : -INFINITY;
       }
     }
   }
