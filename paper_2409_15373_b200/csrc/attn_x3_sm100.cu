@@ -440,21 +440,17 @@ __device__ __forceinline__ void ld_half_flush(uint32_t t_acc, uint32_t lane_off,
   for (int c0 = 0; c0 < D / 2; c0 += 32) {
     uint32_t r[32];
     tc::tmem_ld32(t_acc + lane_off + half * (D / 2) + c0, r);
+    float4* d4 = reinterpret_cast<float4*>(dst + half * (D / 2) + c0);
+    float4 y[8];  // the previous partial sums: all eight loads in flight before any store (no aliasing stalls)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = (add && store) ? d4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     tc::tmem_wait_ld();
     if (!store) continue;
-    float4* d4 = reinterpret_cast<float4*>(dst + half * (D / 2) + c0);
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      float4 x = make_float4(__uint_as_float(r[j]) * scale, __uint_as_float(r[j + 1]) * scale,
-                             __uint_as_float(r[j + 2]) * scale, __uint_as_float(r[j + 3]) * scale);
-      if (add) {
-        const float4 y = d4[j / 4];
-        x.x += y.x;
-        x.y += y.y;
-        x.z += y.z;
-        x.w += y.w;
-      }
-      d4[j / 4] = x;
+    for (int q = 0; q < 8; ++q) {
+      const int jj = 4 * q;
+      d4[q] = make_float4(fmaf(__uint_as_float(r[jj]), scale, y[q].x), fmaf(__uint_as_float(r[jj + 1]), scale, y[q].y),
+                          fmaf(__uint_as_float(r[jj + 2]), scale, y[q].z), fmaf(__uint_as_float(r[jj + 3]), scale, y[q].w));
     }
   }
 }
