@@ -292,3 +292,33 @@ def test_unaligned_views_take_scalar_kernels(dtype):
     gg = J.jagged_flash_attention_backward(Qs, Ks, Vs, Gs, got)
     for a, b, nm in ((gg.dq, gr.dq, "dq"), (gg.dk, gr.dk, "dk"), (gg.dv, gr.dv, "dv")):
         close(a.values, b.values.double().cpu().numpy(), what=f"{nm} (unaligned)")
+
+
+def test_full_size_cfg3_fp32_tensor_core_path():
+    """BASELINE cfg3 at full size in fp32 mode (the split-bf16 tcgen05 kernels): whole samples (largest, smallest
+    non-empty, random ones) against an fp64 torch reference at the fp32 tolerance, and the size-independent
+    identities on every sample: sum_k dV_k = sum_q dO_q and sum_k dK_k = 0 (to fp32 accumulation error)."""
+    ln = R.gen_lengths("half-mean", 1024, 0, 1024)
+    off = R.make_offsets(ln)
+    S, H, D = int(off[-1]), 4, 128
+    g = torch.Generator(device=DEV).manual_seed(5)
+    q, k, v, go = ((torch.rand(S, H, D, device=DEV, generator=g) * 2 - 1) for _ in range(4))
+    T = lambda a: J.JaggedTensor(torch.from_numpy(off).to(DEV), a, off)  # noqa: E731
+    Q, K, V, G = T(q), T(k), T(v), T(go)
+    saved = J.jagged_flash_attention_forward(Q, K, V)
+    gr = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+    nz = np.nonzero(ln)[0]
+    picks = {int(nz[np.argmax(ln[nz])]), int(nz[np.argmin(ln[nz])])} | set(np.random.default_rng(1).choice(nz, 3).tolist())
+    for i in sorted(picks):
+        a, b = int(off[i]), int(off[i + 1])
+        o, lse, dq, dk, dv = _dense_sample_ref64(q[a:b], k[a:b], v[a:b], go[a:b])
+        assert_fp32_close(saved.output.values[a:b], o.cpu().numpy(), what=f"out sample {i} (n={b - a})")
+        assert_fp32_close(saved.logsumexp[:, a:b], lse.cpu().numpy(), what=f"lse sample {i}")
+        for got, ref, nm in ((gr.dq, dq, "dq"), (gr.dk, dk, "dk"), (gr.dv, dv, "dv")):
+            assert_fp32_close(got.values[a:b], ref.cpu().numpy(), what=f"{nm} sample {i} (n={b - a})")
+    seg = torch.repeat_interleave(torch.arange(len(ln), device=DEV), torch.from_numpy(ln).to(DEV))
+    segsum = lambda t: torch.zeros(len(ln), H, D, device=DEV, dtype=torch.float64).index_add_(0, seg, t.double())  # noqa
+    sdv, sdo, sdk = segsum(gr.dv.values), segsum(go), segsum(gr.dk.values)
+    scale = segsum(go.abs()).clamp_min(1.0)
+    assert float(((sdv - sdo).abs() / scale).max()) < 1e-5, "sum_k dV != sum_q dO"
+    assert float((sdk.abs() / segsum(gr.dk.values.abs()).clamp_min(1.0)).max()) < 1e-5, "sum_k dK != 0"
