@@ -18,6 +18,8 @@
 // two-stage K and V rings of bf16 pieces (SWIZZLE_128B; K K-major, V MN-major) split on the fly from fp32 (no
 // scratch). The warp roles and the pipeline are described at attn_fwd_x3_kernel; the backward's two passes at
 // BwdLay. Epilogues write fp32 straight to global; padded mode masks keys / rows past `valid`.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tc.cuh"
@@ -381,10 +383,378 @@ __global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_x3_kernel(
   if (warp == 0) tc::tmem_dealloc<L::kTmemCols>(tmem);
 }
 
+
+// ------------------------------------------------------------------ fp16 two-piece variant (x2h)
+// x = x1 + x2 with x1 = fp16(x s), x2 = fp16(x s - x1) for a power-of-two operand scale s (max |x s| <= 2^14 keeps
+// both pieces inside fp16's normal range for all but tiny elements): 11-bit significands leave ~2^-22, so three
+// products (x2y1, x1y2, x1y1) give ~5e-7 per product — half the MMAs of the bf16 three-piece split. P <= 1 is scaled
+// by 2^14; every scale is undone in fp32 (scores in the softmax's exponent scale, O at the end). V keeps three pieces
+// (P V = P1V3 + P2V1 + P1V2 + P1V1) so that a one-key row reproduces its V row exactly, as the reference does.
+constexpr float kPScale = 16384.f;
+__host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4)  // D f32; A, B f16 (format 0)
+         | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+__device__ __forceinline__ float pow2_scale(float amax) {  // 2^(14 - e) with amax < 2^e; 1 for amax == 0
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  int e;
+  frexpf(amax, &e);
+  return ldexpf(1.f, 14 - e);
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f16(uint32_t w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+__device__ __forceinline__ void split2h(float a, float b, uint32_t& w1, uint32_t& w2) {
+  w1 = pack_f16(a, b);
+  const float2 h = unpack_f16(w1);
+  w2 = pack_f16(a - h.x, b - h.y);  // the residuals are exact in fp32
+}
+__device__ __forceinline__ void split3h(float a, float b, uint32_t& w1, uint32_t& w2, uint32_t& w3) {
+  w1 = pack_f16(a, b);
+  const float2 h = unpack_f16(w1);
+  const float ra = a - h.x, rb = b - h.y;
+  w2 = pack_f16(ra, rb);
+  const float2 m = unpack_f16(w2);
+  w3 = pack_f16(ra - m.x, rb - m.y);  // x1 + x2 + x3 reproduces x exactly (33 significand bits >= 24)
+}
+template <int D, int ROWS, int NP, int T0 = 0, int NT = kThreads, int kMaxBatch = 4>
+__device__ __forceinline__ void stage_splith(const float* __restrict__ src, int64_t b0, int64_t r0, int64_t n,
+                                              int64_t rs, uint32_t base, float mul) {
+  constexpr int kUnits = D / 8;
+  constexpr int kPiece = (D / 64) * ROWS * 128;
+  constexpr int kTotal = ROWS * kUnits;
+  constexpr int kIter = (kTotal + NT - 1) / NT;
+  constexpr int kBatch = kIter < kMaxBatch ? kIter : kMaxBatch;
+  const int t = (int)threadIdx.x - T0;
+#pragma unroll
+  for (int i0 = 0; i0 < kIter; i0 += kBatch) {
+    float4 a[kBatch], b[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int e = t + (i0 + i) * NT, r = e / kUnits, u = e % kUnits;
+      a[i] = b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < kTotal && r0 + r < n) {
+        const float4* p = reinterpret_cast<const float4*>(src + (b0 + r0 + r) * rs + u * 8);
+        a[i] = __ldg(p);
+        b[i] = __ldg(p + 1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int e = t + (i0 + i) * NT, r = e / kUnits, u = e % kUnits;
+      if (e >= kTotal) continue;
+      uint32_t w1[4], w2[4], w3[4];
+      const float x[8] = {a[i].x, a[i].y, a[i].z, a[i].w, b[i].x, b[i].y, b[i].z, b[i].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (NP == 3) split3h(x[2 * c] * mul, x[2 * c + 1] * mul, w1[c], w2[c], w3[c]);
+        else split2h(x[2 * c] * mul, x[2 * c + 1] * mul, w1[c], w2[c]);
+      }
+      const uint32_t off = (u >> 3) * (ROWS * 128) + tc::sw128_offset(r, u & 7);
+      tc::st_shared_v4(base + off, w1[0], w1[1], w1[2], w1[3]);
+      tc::st_shared_v4(base + kPiece + off, w2[0], w2[1], w2[2], w2[3]);
+      if (NP == 3) tc::st_shared_v4(base + 2 * kPiece + off, w3[0], w3[1], w3[2], w3[3]);
+    }
+  }
+}
+// this thread's half row, two fp16 pieces into TMEM (piece p at t_base + p*D/2)
+template <int D>
+__device__ __forceinline__ void stage_row_tmem2h(const float* __restrict__ src, bool in, uint32_t t_base,
+                                                 uint32_t lane_off, int half, float mul) {
+  constexpr int kCols = D / 4;
+  float4 xs[D / 8];
+#pragma unroll
+  for (int g = 0; g < D / 8; ++g) {
+    xs[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (in) xs[g] = __ldg(reinterpret_cast<const float4*>(src + half * (D / 2) + 4 * g));
+  }
+#pragma unroll
+  for (int c0 = 0; c0 < kCols; c0 += 8) {
+    uint32_t w[2][8];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const float4 x = xs[c0 / 2 + g];
+      split2h(x.x * mul, x.y * mul, w[0][2 * g], w[1][2 * g]);
+      split2h(x.z * mul, x.w * mul, w[0][2 * g + 1], w[1][2 * g + 1]);
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const uint32_t ta = t_base + p * (D / 2) + half * kCols + c0 + lane_off;
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+                   "r"(w[p][0]), "r"(w[p][1]), "r"(w[p][2]), "r"(w[p][3]), "r"(w[p][4]), "r"(w[p][5]), "r"(w[p][6]),
+                   "r"(w[p][7])
+                   : "memory");
+    }
+  }
+}
+template <int D>
+struct Lay2 {
+  static constexpr int kKChunk = BN * 128;
+  static constexpr int kKPiece = (D / 64) * kKChunk;
+  static constexpr int kKStage = 2 * kKPiece;          // K1 K2 of one 64-key block
+  static constexpr int kVStage = 3 * kKPiece;          // V1 V2 V3 (three pieces: P = 1 reproduces V exactly)
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + 2 * kKStage;
+  static constexpr int kBar = kV + 2 * kVStage;
+  static constexpr int kAlpha = kBar + 128;
+  static constexpr int kL = kAlpha + 2 * 4 * BM;
+  static constexpr int kBytes = kL + 2 * 4 * BM;
+  static constexpr int kAlloc = kBytes + 1024;
+  // TMEM: Q1 Q2 [0, D) | S0 | S1 (64 each; P1 | P2 land over them) | O (D)
+  static constexpr int kTmemCols = D == 128 ? 512 : 256;
+};
+
+// max |x| of up to three fp32 tensors of n elements (n % 4 == 0) into amax[0..2] (zeroed; floats as ordered ints)
+__global__ void absmax3_kernel(const float4* __restrict__ a, const float4* __restrict__ b, const float4* __restrict__ c,
+                               int64_t n4, unsigned* __restrict__ amax) {
+  const float4* src[3] = {a, b, c};
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    if (!src[t]) continue;
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 x = __ldg(src[t] + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax + t, __float_as_uint(m));
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFwdThreads, 1) attn_fwd_x2h_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    float* __restrict__ out, float* __restrict__ lse, float scale_log2, const int64_t* __restrict__ valid,
+    const float* __restrict__ amax) {
+  using L = Lay2<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_s = bars;        // [2] score MMAs of the buffer done (commit)
+  uint64_t* bar_o = bars + 2;    // PV_j done (commit)
+  uint64_t* p_ready = bars + 3;  // P_j written (256 arrivals)
+  uint64_t* o_free = bars + 4;   // O read out (256 arrivals)
+  uint64_t* k_ready = bars + 5;  // [2] K stage split (256 arrivals)
+  uint64_t* v_ready = bars + 7;  // [2] V stage split (256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  float* mx_s = reinterpret_cast<float*>(smem + L::kAlpha);  // [2][128] block maxima of the two key halves
+  float* l_s = reinterpret_cast<float*>(smem + L::kL);       // [2][128] final row sums of the two halves
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) tc::mbar_init(bars + i, 1);
+    for (int i = 3; i < 9; ++i) tc::mbar_init(bars + i, 256);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<L::kTmemCols>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_q = tmem, t_s0 = tmem + D, t_o = t_s0 + 128;
+  // power-of-two operand scales (fp16 range: max |x s| <= 2^14), P scaled by 2^14
+  const float sq = pow2_scale(amax[0]), sk = pow2_scale(amax[1]), sv = pow2_scale(amax[2]);
+  const float s_log2 = scale_log2 / (sq * sk);
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = idesc_f16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescO = idesc_f16_f32(BM, D, false, true);
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  // barrier use counters (each role tracks the completions it waits for; all are CTA-global across items)
+  // (per-parity counters as scalars: a dynamically indexed pair would live in local memory)
+  uint32_t cs0 = 0, cs1 = 0, c_o = 0, c_p = 0, c_of = 0, ck0 = 0, ck1 = 0, cv0 = 0, cv1 = 0;
+  auto take = [](uint32_t& c0, uint32_t& c1, int b) {  // parity of the next completion of buffer b's barrier
+    const uint32_t v = b ? c1 : c0;
+    if (b) ++c1; else ++c0;
+    return v & 1u;
+  };
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t hd = (int64_t)h * D;
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int q0 = it.y * BM;
+    const int nblk = q0 < nv ? (int)((nv + BN - 1) / BN) : 0;  // an all-padding tile attends nothing
+    __syncthreads();  // the previous item's TMEM / smem reads are done
+    if (nblk > 0) {  // Q pieces -> TMEM; blocks 0 and 1 -> stages 0 and 1
+      stage_row_tmem2h<D>(q + (b0 + q0 + row) * rs + hd, q0 + row < seg, t_q, lane_off, half, sq);
+      for (int j = 0; j < 2 && j < nblk; ++j) {
+        stage_splith<D, BN, 2>(k + hd, b0, (int64_t)j * BN, nv, rs, sbase + L::kK + j * L::kKStage, sk);
+        stage_splith<D, BN, 3>(v + hd, b0, (int64_t)j * BN, nv, rs, sbase + L::kV + j * L::kVStage, sv);
+      }
+    }
+    tc::tmem_wait_st();
+    tc::fence_proxy_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    // warp 0 doubles as the MMA issuer (a ninth warp would not fit the per-SMSP register file at this size)
+    auto issue_s = [&](int j) {  // S = Q2K1 + Q1K2 + Q1K1 (small terms first)
+      constexpr int kQi[3] = {1, 0, 0}, kKj[3] = {0, 1, 0};
+      const uint32_t kst = sbase + L::kK + (j & 1) * L::kKStage, ts = t_s0 + (j & 1) * 64;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t ka = kst + kKj[c] * L::kKPiece;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          tc::mma_bf16_ts_warp(ts, t_q + kQi[c] * (D / 2) + kk * 8,
+                               tc::sw128_desc(ka + (kk >> 2) * L::kKChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                               (c > 0 || kk > 0) ? 1u : 0u);
+      }
+      tc::mma_commit_warp(bar_s + (j & 1));
+    };
+    auto issue_pv = [&](int j) {  // O_j = P1V3 + P2V1 + P1V2 + P1V1 (V MN-major; small terms first)
+      constexpr int kPi[4] = {0, 1, 0, 0}, kVj[4] = {2, 0, 1, 0};
+      const int b = j & 1;
+      const uint32_t vst = sbase + L::kV + b * L::kVStage, ts = t_s0 + b * 64;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t va = vst + kVj[c] * L::kKPiece;
+        const uint32_t pa = ts + kPi[c] * 32;
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          tc::mma_bf16_ts_warp(t_o, pa + kk * 8, tc::sw128_desc(va + kk * 16 * 128, L::kKChunk, 1024), kIdescO,
+                               (c > 0 || kk > 0) ? 1u : 0u);
+      }
+      tc::mma_commit_warp(bar_o);
+    };
+    if (warp == 0)
+      for (int j = 0; j < 2 && j < nblk; ++j) issue_s(j);
+    // ===================================================== all 8 warps: warp half h owns keys [32h, 32h + 32) of
+    // each block and output columns [h D/2, (h + 1) D/2) of its lane quarter's rows (thread = query row)
+    float m = -INFINITY, l = 0.f;  // running max (both halves agree), this half's running sum
+    float o[D / 2];
+#pragma unroll
+    for (int jj = 0; jj < D / 2; ++jj) o[jj] = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int b = j & 1;
+      const int64_t k0 = (int64_t)j * BN;
+      tc::mbar_wait(bar_s + b, take(cs0, cs1, b));
+      tc::tc_fence_after();
+      const uint32_t ts = t_s0 + b * 64;
+      uint32_t sr[32];
+      tc::tmem_ld32(ts + lane_off + 32 * half, sr);
+      tc::tmem_wait_ld();
+      float s[32];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        s[jj] = (k0 + 32 * half + jj < nv) ? __uint_as_float(sr[jj]) * s_log2 : -INFINITY;
+        mx = fmaxf(mx, s[jj]);
+      }
+      mx_s[half * BM + row] = mx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // both halves' maxima; every S column is read before P lands
+      const float mn = fmaxf(m, fmaxf(mx, mx_s[(half ^ 1) * BM + row]));  // finite: the block has a valid key
+      const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+      float ps = 0.f;
+      uint32_t p1[16], p2[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const float a = exp2f(s[2 * jj] - mn), bb = exp2f(s[2 * jj + 1] - mn);
+        ps += a + bb;
+        split2h(a * kPScale, bb * kPScale, p1[jj], p2[jj]);
+      }
+      l = l * alpha + ps;
+      m = mn;
+      tc::tmem_st16(ts + lane_off + 16 * half, p1);               // P1: keys 2c, 2c+1 at column c
+      tc::tmem_st16(ts + lane_off + 32 + 16 * half, p2);          // P2 at columns [32, 64)
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      tc::mbar_arrive(p_ready);
+      if (warp == 0) {  // issuer: PV_j once every P_j is in and O is free
+        tc::mbar_wait(p_ready, c_p++ & 1);
+        if (j >= 1) tc::mbar_wait(o_free, c_of++ & 1);
+        if (j >= 2) tc::mbar_wait(v_ready + b, take(cv0, cv1, b));
+        tc::tc_fence_after();
+        issue_pv(j);
+      }
+      if (j + 2 < nblk) {  // K_j is consumed (S_j done): split K_{j+2} into its stage under PV_j
+        stage_splith<D, BN, 2>(k + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kK + b * L::kKStage, sk);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(k_ready + b);
+        if (warp == 0) {
+          tc::mbar_wait(k_ready + b, take(ck0, ck1, b));
+          tc::tc_fence_after();
+          issue_s(j + 2);
+        }
+      }
+      tc::mbar_wait(bar_o, c_o++ & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < D / 2; c0 += 32) {
+        uint32_t pv[32];
+        tc::tmem_ld32(t_o + lane_off + half * (D / 2) + c0, pv);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) o[c0 + jj] = fmaf(o[c0 + jj], alpha, __uint_as_float(pv[jj]));
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(o_free);
+      if (j + 2 < nblk) {  // V_j is consumed (PV_j done)
+        stage_splith<D, BN, 3>(v + hd, b0, (int64_t)(j + 2) * BN, nv, rs, sbase + L::kV + b * L::kVStage, sv);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(v_ready + b);
+      }
+    }
+    if (warp == 0 && nblk > 0) tc::mbar_wait(o_free, c_of++ & 1);  // last O read-out: TMEM free next item
+    l_s[half * BM + row] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    {
+      const float lt = l + l_s[(half ^ 1) * BM + row];
+      const int64_t r = q0 + row;
+      if (r < seg) {
+        const bool ok = r < nv && nblk > 0;
+        const float inv = ok ? 1.0f / (lt * kPScale * sv) : 0.f;
+        float4* dst = reinterpret_cast<float4*>(out + (b0 + r) * rs + hd + half * (D / 2));
+#pragma unroll
+        for (int jj = 0; jj < D / 2; jj += 4)
+          dst[jj / 4] = make_float4(o[jj] * inv, o[jj + 1] * inv, o[jj + 2] * inv, o[jj + 3] * inv);
+        if (half == 0) lse[(int64_t)h * total_rows + b0 + r] = ok ? (m + log2f(lt)) * kLn2 : -INFINITY;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<L::kTmemCols>(tmem);
+}
+
 template <int D>
 static jg_status fwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
                         void* out, float* lse, const int2* items, const int64_t* n_items, int64_t max_items,
                         const int64_t* valid, cudaStream_t st) {
+  static const bool bf16x3 = std::getenv("JG_FP32_X3") != nullptr;  // A/B knob: the bf16 three-piece kernels
+  if (!bf16x3) {  // fp16 two-piece kernels with per-tensor power-of-two scales from one max pass
+    const int smem2 = Lay2<D>::kAlloc;
+    if (jg_status rc = ensure_smem_attr((const void*)attn_fwd_x2h_kernel<D>, std::max(smem2, 120 * 1024),
+                                        "attn_fwd_x2h_kernel"))
+      return rc;
+    unsigned* amax = nullptr;
+    JG_CUDA(cudaMallocAsync(&amax, 16, st));
+    scratch_note(16);
+    JG_CUDA(cudaMemsetAsync(amax, 0, 16, st));
+    const int64_t n4 = total_rows * H * D / 4;
+    absmax3_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 4 * device_sm_count())), 256, 0,
+                     st>>>((const float4*)q, (const float4*)k, (const float4*)v, n4, amax);
+    JG_LAUNCHED("absmax3_kernel");
+    const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)device_sm_count()));
+    attn_fwd_x2h_kernel<D><<<grid2, kFwdThreads, std::max(smem2, 120 * 1024), st>>>(
+        off, items, n_items, H, total_rows, (const float*)q, (const float*)k, (const float*)v, (float*)out, lse,
+        kLog2e / sqrtf((float)D), valid, (const float*)amax);
+    JG_LAUNCHED("attn_fwd_x2h_kernel");
+    cudaFreeAsync(amax, st);
+    scratch_note(-16);
+    return JG_OK;
+  }
   const int smem = Lay<D>::kAlloc;
   if (jg_status rc = ensure_smem_attr((const void*)attn_fwd_x3_kernel<D>, std::max(smem, 120 * 1024),
                                       "attn_fwd_x3_kernel"))
