@@ -978,6 +978,207 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dq_kernel(
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
+
+// fp16-piece variants of the backward's staging (x2h)
+template <int D, int ROWS, int NP, int NT = kThreads>
+struct PreH {
+  static constexpr int kUnits = D / 8, kTotal = ROWS * kUnits, kIter = kTotal / NT;
+  static constexpr int kPiece = (D / 64) * ROWS * 128;
+  float4 a[kIter], b[kIter];
+  __device__ __forceinline__ void load(const float* __restrict__ src, int64_t b0, int64_t r0, int64_t n, int64_t rs,
+                                       int t) {
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+      const int e = t + i * NT, r = e / kUnits, u = e % kUnits;
+      a[i] = b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r0 + r < n) {
+        const float4* p = reinterpret_cast<const float4*>(src + (b0 + r0 + r) * rs + u * 8);
+        a[i] = __ldg(p);
+        b[i] = __ldg(p + 1);
+      }
+    }
+  }
+  __device__ __forceinline__ void store(uint32_t base, int t, float mul) const {
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+      const int e = t + i * NT, r = e / kUnits, u = e % kUnits;
+      uint32_t w1[4], w2[4], w3[4];
+      const float x[8] = {a[i].x, a[i].y, a[i].z, a[i].w, b[i].x, b[i].y, b[i].z, b[i].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (NP == 3) split3h(x[2 * c] * mul, x[2 * c + 1] * mul, w1[c], w2[c], w3[c]);
+        else split2h(x[2 * c] * mul, x[2 * c + 1] * mul, w1[c], w2[c]);
+      }
+      const uint32_t off = (u >> 3) * (ROWS * 128) + tc::sw128_offset(r, u & 7);
+      tc::st_shared_v4(base + off, w1[0], w1[1], w1[2], w1[3]);
+      tc::st_shared_v4(base + kPiece + off, w2[0], w2[1], w2[2], w2[3]);
+      if (NP == 3) tc::st_shared_v4(base + 2 * kPiece + off, w3[0], w3[1], w3[2], w3[3]);
+    }
+  }
+};
+template <int D, bool KV>
+struct BwdLay2 {
+  static constexpr int kXChunk = BM * 128, kYChunk = BN * 128;
+  static constexpr int kXPiece = (D / 64) * kXChunk, kYPiece = (D / 64) * kYChunk;
+  static constexpr int kX = 0;                          // dQ pass: dO1 dO2; dK/dV pass: V1 V2 (stationary)
+  static constexpr int kYa = kX + 2 * kXPiece;          // K_j (dQ pass) or Q_j (dK/dV pass), 2 pieces
+  static constexpr int kYb = kYa + 2 * kYPiece;         // V_j or dO_j, 2 pieces
+  static constexpr int kBar = kYb + 2 * kYPiece;
+  static constexpr int kLs = kBar + 64;
+  static constexpr int kDs = kLs + 4 * BN;
+  static constexpr int kBytes = kDs + 4 * BN;
+  static constexpr int kAlloc = kBytes + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    const float* __restrict__ go, const float* __restrict__ lse, const float* __restrict__ delta,
+    float* __restrict__ dq, float scale_log2, float scale, const int64_t* __restrict__ valid,
+    const float* __restrict__ amax) {
+  using L = BwdLay2<D, false>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_s + i, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_q = tmem, t_s = tmem + D, t_dp = t_s + 64, t_dq = t_dp + 64;
+  const float sq = pow2_scale(amax[0]), sk = pow2_scale(amax[1]), sv = pow2_scale(amax[2]), sdo = pow2_scale(amax[3]);
+  const float sds = pow2_scale(2.f * D * amax[3] * amax[2]);  // |dS| <= 2 max||dO|| max||V||
+  const float s_log2 = scale_log2 / (sq * sk), ipd = 1.f / (sdo * sv), fl_scale = scale / (sds * sk);
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = idesc_f16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescQ = idesc_f16_f32(BM, D, false, true);
+  constexpr int kPa[3] = {1, 0, 0}, kPb[3] = {0, 1, 0};
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  uint32_t ph = 0;
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t hd = (int64_t)h * D, hr = (int64_t)h * total_rows;
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int q0 = it.y * BM;
+    const int64_t r = q0 + row;
+    const bool rin = r < nv;
+    const int nblk = q0 < nv ? (int)((nv + BN - 1) / BN) : 0;
+    float lr = 0.f, dr = 0.f;
+    if (rin) {
+      lr = lse[hr + b0 + r] * kLog2e;
+      dr = delta[hr + b0 + r];
+    }
+    __syncthreads();  // previous item: TMEM dQ read, smem free
+    if (nblk > 0) {  // Q pieces -> TMEM; dO pieces, K_0, V_0 -> smem (K_0 / V_0 loads in flight throughout)
+      PreH<D, BN, 2> k0p, v0p;
+      k0p.load(k + hd, b0, 0, nv, rs, tid);
+      v0p.load(v + hd, b0, 0, nv, rs, tid);
+      stage_row_tmem2h<D>(q + (b0 + r) * rs + hd, rin, t_q, lane_off, half, sq);
+      stage_splith<D, BM, 2, 0, kThreads, 8>(go + hd, b0, q0, nv, rs, sbase + L::kX, sdo);
+      k0p.store(sbase + L::kYa, tid, sk);
+      v0p.store(sbase + L::kYb, tid, sv);
+    }
+    for (int j = 0; j < nblk; ++j) {
+      const int64_t k0 = (int64_t)j * BN;
+      tc::tmem_wait_st();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // S = Q2K1 + Q1K2 + Q1K1 (A = Q pieces in TMEM)
+          const uint32_t kb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_s, t_q + kPa[c] * (D / 2) + kk * 8,
+                                 tc::sw128_desc(kb + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // dP = dO2V1 + dO1V2 + dO1V1
+          const uint32_t xa = sbase + L::kX + kPa[c] * L::kXPiece, vb = sbase + L::kYb + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ss_warp(t_dp, tc::sw128_desc(xa + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
+                                 tc::sw128_desc(vb + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_s);
+      }
+      tc::mbar_wait(bar_s, ph);
+      tc::tc_fence_after();
+      {  // dS = P (dP - Delta) on both warpgroups: warp half h takes keys [32h, 32h + 32) of its lane quarter
+        uint32_t sr[32], pr[32];
+        tc::tmem_ld32(t_s + lane_off + 32 * half, sr);
+        tc::tmem_ld32(t_dp + lane_off + 32 * half, pr);
+        tc::tmem_wait_ld();
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every S / dP column is read before the pieces overwrite them
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const bool in = rin && (k0 + 32 * half + jj < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[jj]) * s_log2 - lr) : 0.f;
+          sr[jj] = __float_as_uint(p * (__uint_as_float(pr[jj]) * ipd - dr) * sds);
+        }
+        // dS1 over S [0, 32), dS2 over S [32, 64): keys 32h.. packed at column 16h
+        uint32_t w1[16], w2[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2)
+          split2h(__uint_as_float(sr[jj]), __uint_as_float(sr[jj + 1]), w1[jj / 2], w2[jj / 2]);
+        tc::tmem_st16(t_s + lane_off + 16 * half, w1);
+        tc::tmem_st16(t_s + lane_off + 32 + 16 * half, w2);
+        tc::tmem_wait_st();
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // dQ += sum dSa Kb (B = K_j MN-major: key rows, 64-wide D chunks)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // dQ += dS2K1 + dS1K2 + dS1K1
+          const uint32_t pa = t_s + kPa[c] * 32;
+          const uint32_t kb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_dq, pa + kk * 8, tc::sw128_desc(kb + kk * 16 * 128, L::kYChunk, 1024), kIdescQ,
+                                 (j % kFlush != 0 || c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      PreH<D, BN, 2> kpre;
+      if (j + 1 < nblk) {  // under dQ_j: split V_{j+1} (V_j is free) and load K_{j+1}
+        stage_splith<D, BN, 2>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb, sv);
+        kpre.load(k + hd, b0, k0 + BN, nv, rs, tid);
+      }
+      tc::mbar_wait(bar_o, ph);
+      tc::tc_fence_after();
+      if (j + 1 < nblk) kpre.store(sbase + L::kYa, tid, sk);  // K_j is free
+      if (j % kFlush == kFlush - 1 || j + 1 == nblk)
+        ld_half_flush<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, fl_scale, j >= kFlush, r < seg);
+      tc::tc_fence_before();
+      ph ^= 1;
+    }
+    if (nblk == 0 && r < seg) zero_half<D>(dq + (b0 + r) * rs + hd, half);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
     const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
@@ -1167,10 +1368,228 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x3_dkdv_kernel(
 }
 
 template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
+    const int64_t* __restrict__ off, const int2* __restrict__ items, const int64_t* __restrict__ n_items, int H,
+    int64_t total_rows, const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    const float* __restrict__ go, const float* __restrict__ lse, const float* __restrict__ delta,
+    float* __restrict__ dk, float* __restrict__ dv, float scale_log2, float scale, const int64_t* __restrict__ valid,
+    const float* __restrict__ amax) {
+  using L = BwdLay2<D, true>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc::smem_u32(smem);
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
+  float* ls = reinterpret_cast<float*>(smem + L::kLs);
+  float* dls = reinterpret_cast<float*>(smem + L::kDs);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;  // key row in the tile
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_s + i, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_k = tmem, t_s = tmem + D, t_dp = t_s + 64, t_dv = t_dp + 64, t_dk = t_dv + D;
+  const float sq = pow2_scale(amax[0]), sk = pow2_scale(amax[1]), sv = pow2_scale(amax[2]), sdo = pow2_scale(amax[3]);
+  const float sds = pow2_scale(2.f * D * amax[3] * amax[2]);  // |dS| <= 2 max||dO|| max||V||
+  const float s_log2 = scale_log2 / (sk * sq), ipd = 1.f / (sv * sdo);
+  const float fl_dv = 1.f / (kPScale * sdo), fl_dk = scale / (sds * sq);
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr uint32_t kIdescS = idesc_f16_f32(BM, BN, false, false);
+  constexpr uint32_t kIdescO = idesc_f16_f32(BM, D, false, true);
+  constexpr int kPa[3] = {1, 0, 0}, kPb[3] = {0, 1, 0};
+  const uint32_t s_v = sbase + L::kX;
+  const int64_t rs = (int64_t)H * D;
+  const int64_t n_work = *n_items * H;
+  uint32_t ph_s = 0, ph_o = 0;
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const int2 it = items[w / H];
+    const int h = (int)(w % H);
+    const int64_t hd = (int64_t)h * D, hr = (int64_t)h * total_rows;
+    const int64_t b0 = off[it.x], seg = off[it.x + 1] - b0;
+    const int64_t nv = valid ? (valid[it.x] < seg ? valid[it.x] : seg) : seg;
+    const int x0 = it.y * BM;
+    const int64_t r = x0 + row;
+    const bool rin = r < nv;
+    const int nblk = x0 < nv ? (int)((nv + BN - 1) / BN) : 0;
+    __syncthreads();
+    if (nblk > 0) {  // K1, K2 -> TMEM and K3 -> smem; V pieces, Q_0, dO_0 -> smem (Q_0 / dO_0 loads in flight)
+      PreH<D, BN, 2> q0p, g0p;
+      q0p.load(q + hd, b0, 0, nv, rs, tid);
+      g0p.load(go + hd, b0, 0, nv, rs, tid);
+      stage_row_tmem2h<D>(k + (b0 + r) * rs + hd, rin, t_k, lane_off, half, sk);
+      stage_splith<D, BM, 2, 0, kThreads, 8>(v + hd, b0, x0, nv, rs, s_v, sv);
+      q0p.store(sbase + L::kYa, tid, sq);
+      g0p.store(sbase + L::kYb, tid, sdo);
+    }
+    for (int j = 0; j < nblk; ++j) {
+      const int64_t y0 = (int64_t)j * BN;
+      if (tid < BN) {
+        const bool in = y0 + tid < nv;
+        ls[tid] = in ? lse[hr + b0 + y0 + tid] * kLog2e : 0.f;
+        dls[tid] = in ? delta[hr + b0 + y0 + tid] : 0.f;
+      }
+      tc::tmem_wait_st();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // S^T = K2Q1 + K1Q2 + K1Q1 (K pieces in TMEM)
+          const uint32_t qb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_s, t_k + kPa[c] * (D / 2) + kk * 8,
+                                 tc::sw128_desc(qb + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // dP^T = V2dO1 + V1dO2 + V1dO1
+          const uint32_t va = s_v + kPa[c] * L::kXPiece, ob = sbase + L::kYb + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16_ss_warp(t_dp, tc::sw128_desc(va + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
+                                 tc::sw128_desc(ob + (kk >> 2) * L::kYChunk + (kk & 3) * 32, 16, 1024), kIdescS,
+                                 (c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_s);
+      }
+      // P^T and dS^T on both warpgroups: warp half h takes queries [32h, 32h + 32) of its key quarter
+      float dsv[32];  // dS^T, split into TMEM once P^T's MMAs are done
+      tc::mbar_wait(bar_s, ph_s);
+      tc::tc_fence_after();
+      {
+        uint32_t sr[32], pr[32];
+        tc::tmem_ld32(t_s + lane_off + 32 * half, sr);
+        tc::tmem_ld32(t_dp + lane_off + 32 * half, pr);
+        tc::tmem_wait_ld();
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every S^T / dP^T column is read before the pieces land
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+          const int qc = 32 * half + jj;
+          const bool in = rin && (y0 + qc < nv);
+          const float p = in ? exp2f(__uint_as_float(sr[jj]) * s_log2 - ls[qc]) : 0.f;
+          dsv[jj] = p * (__uint_as_float(pr[jj]) * ipd - dls[qc]) * sds;
+          sr[jj] = __float_as_uint(p * kPScale);
+        }
+        // P1 [0, 32), P2 [32, 64) of t_s; queries 32h.. packed at column 16h
+        uint32_t p1[16], p2[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2)
+          split2h(__uint_as_float(sr[jj]), __uint_as_float(sr[jj + 1]), p1[jj / 2], p2[jj / 2]);
+        tc::tmem_st16(t_s + lane_off + 16 * half, p1);
+        tc::tmem_st16(t_s + lane_off + 32 + 16 * half, p2);
+        tc::tmem_wait_st();
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // dV += P2dO1 + P1dO2 + P1dO1 (B = dO_j MN-major)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const uint32_t ob = sbase + L::kYb + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_dv, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(ob + kk * 16 * 128, L::kYChunk, 1024),
+                                 kIdescO, (j % kFlush != 0 || c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      tc::mbar_wait(bar_o, ph_o);  // (all threads) the P^T pieces and dO_j are consumed
+      tc::tc_fence_after();
+      {
+        uint32_t d1[16], d2[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2) split2h(dsv[jj], dsv[jj + 1], d1[jj / 2], d2[jj / 2]);
+        tc::tmem_st16(t_s + lane_off + 16 * half, d1);
+        tc::tmem_st16(t_s + lane_off + 32 + 16 * half, d2);
+        tc::tmem_wait_st();
+      }
+      ph_o ^= 1;
+      tc::tc_fence_before();
+      __syncthreads();
+      tc::tc_fence_after();
+      if (warp == 0) {  // dK += dS2Q1 + dS1Q2 + dS1Q1 (B = Q_j MN-major)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const uint32_t qb = sbase + L::kYa + kPb[c] * L::kYPiece;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            tc::mma_bf16_ts_warp(t_dk, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(qb + kk * 16 * 128, L::kYChunk, 1024),
+                                 kIdescO, (j % kFlush != 0 || c > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_warp(bar_o);
+      }
+      PreH<D, BN, 2> qpre;
+      if (j + 1 < nblk) {  // under dK_j: split dO_{j+1} (dO_j is free) and load Q_{j+1}
+        stage_splith<D, BN, 2>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb, sdo);
+        qpre.load(q + hd, b0, y0 + BN, nv, rs, tid);
+      }
+      tc::mbar_wait(bar_o, ph_o);
+      tc::tc_fence_after();
+      if (j + 1 < nblk) qpre.store(sbase + L::kYa, tid, sq);  // Q_j is free
+      if (j % kFlush == kFlush - 1 || j + 1 == nblk) {
+        ld_half_flush<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, fl_dv, j >= kFlush, r < seg);
+        ld_half_flush<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, fl_dk, j >= kFlush, r < seg);
+      }
+      tc::tc_fence_before();
+      ph_o ^= 1;
+      ph_s ^= 1;
+    }
+    if (nblk == 0 && r < seg) {
+      zero_half<D>(dv + (b0 + r) * rs + hd, half);
+      zero_half<D>(dk + (b0 + r) * rs + hd, half);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+
+template <int D>
 static jg_status bwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
                         const void* go, const float* lse, const float* delta, void* dq, void* dk, void* dv,
                         const int2* items, const int64_t* n_items, int64_t max_items, const int64_t* valid,
                         cudaStream_t st) {
+  static const bool bf16x3 = std::getenv("JG_FP32_X3") != nullptr;  // A/B knob: the bf16 three-piece kernels
+  if (!bf16x3) {  // fp16 two-piece kernels with per-tensor power-of-two scales (one max pass over q, k, v, dO)
+    const int sm_q2 = std::max<int>(BwdLay2<D, false>::kAlloc, 120 * 1024);
+    const int sm_kv2 = std::max<int>(BwdLay2<D, true>::kAlloc, 120 * 1024);
+    if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_x2h_dq_kernel<D>, sm_q2, "attn_bwd_x2h_dq_kernel"))
+      return rc;
+    if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_x2h_dkdv_kernel<D>, sm_kv2, "attn_bwd_x2h_dkdv_kernel"))
+      return rc;
+    unsigned* amax = nullptr;
+    JG_CUDA(cudaMallocAsync(&amax, 16, st));
+    scratch_note(16);
+    JG_CUDA(cudaMemsetAsync(amax, 0, 16, st));
+    const int64_t n4 = total_rows * H * D / 4;
+    const int mg = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 4 * device_sm_count()));
+    absmax3_kernel<<<mg, 256, 0, st>>>((const float4*)q, (const float4*)k, (const float4*)v, n4, amax);
+    absmax3_kernel<<<mg, 256, 0, st>>>((const float4*)go, nullptr, nullptr, n4, amax + 3);
+    JG_LAUNCHED("absmax3_kernel");
+    const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)device_sm_count()));
+    const float scale2 = 1.0f / sqrtf((float)D);
+    attn_bwd_x2h_dq_kernel<D><<<grid2, kThreads, sm_q2, st>>>(
+        off, items, n_items, H, total_rows, (const float*)q, (const float*)k, (const float*)v, (const float*)go, lse,
+        delta, (float*)dq, kLog2e * scale2, scale2, valid, (const float*)amax);
+    JG_LAUNCHED("attn_bwd_x2h_dq_kernel");
+    attn_bwd_x2h_dkdv_kernel<D><<<grid2, kThreads, sm_kv2, st>>>(
+        off, items, n_items, H, total_rows, (const float*)q, (const float*)k, (const float*)v, (const float*)go, lse,
+        delta, (float*)dk, (float*)dv, kLog2e * scale2, scale2, valid, (const float*)amax);
+    JG_LAUNCHED("attn_bwd_x2h_dkdv_kernel");
+    cudaFreeAsync(amax, st);
+    scratch_note(-16);
+    return JG_OK;
+  }
   // at least half the SM's shared memory: one CTA per SM, since each allocates all 512 TMEM columns
   const int sm_q = std::max<int>(BwdLay<D, false>::kAlloc, 120 * 1024);
   const int sm_kv = std::max<int>(BwdLay<D, true>::kAlloc, 120 * 1024);
