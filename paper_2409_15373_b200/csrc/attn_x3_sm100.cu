@@ -1021,9 +1021,11 @@ struct BwdLay2 {
   static constexpr int kXChunk = BM * 128, kYChunk = BN * 128;
   static constexpr int kXPiece = (D / 64) * kXChunk, kYPiece = (D / 64) * kYChunk;
   static constexpr int kX = 0;                          // dQ pass: dO1 dO2; dK/dV pass: V1 V2 (stationary)
-  static constexpr int kYa = kX + 2 * kXPiece;          // K_j (dQ pass) or Q_j (dK/dV pass), 2 pieces
-  static constexpr int kYb = kYa + 2 * kYPiece;         // V_j or dO_j, 2 pieces
-  static constexpr int kBar = kYb + 2 * kYPiece;
+  // two stages of the moving block: [Ya: K_j (dQ pass) or Q_j (dK/dV pass) | Yb: V_j or dO_j], 2 pieces each
+  static constexpr int kYa = kX + 2 * kXPiece;
+  static constexpr int kYb = kYa + 2 * kYPiece;
+  static constexpr int kYStage = 4 * kYPiece;
+  static constexpr int kBar = kYa + 2 * kYStage;
   static constexpr int kLs = kBar + 64;
   static constexpr int kDs = kLs + 4 * BN;
   static constexpr int kBytes = kDs + 4 * BN;
@@ -1094,6 +1096,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
     }
     for (int j = 0; j < nblk; ++j) {
       const int64_t k0 = (int64_t)j * BN;
+      const uint32_t ya = sbase + L::kYa + (j & 1) * L::kYStage, yb = sbase + L::kYb + (j & 1) * L::kYStage;
       tc::tmem_wait_st();
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
@@ -1102,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
       if (warp == 0) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {  // S = Q2K1 + Q1K2 + Q1K1 (A = Q pieces in TMEM)
-          const uint32_t kb = sbase + L::kYa + kPb[c] * L::kYPiece;
+          const uint32_t kb = ya + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             tc::mma_bf16_ts_warp(t_s, t_q + kPa[c] * (D / 2) + kk * 8,
@@ -1111,7 +1114,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {  // dP = dO2V1 + dO1V2 + dO1V1
-          const uint32_t xa = sbase + L::kX + kPa[c] * L::kXPiece, vb = sbase + L::kYb + kPb[c] * L::kYPiece;
+          const uint32_t xa = sbase + L::kX + kPa[c] * L::kXPiece, vb = yb + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             tc::mma_bf16_ss_warp(t_dp, tc::sw128_desc(xa + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
@@ -1119,6 +1122,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
                                  (c > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit_warp(bar_s);
+      }
+      if (j + 1 < nblk) {  // under S_j / dP_j: split K_{j+1}, V_{j+1} into the other stage (dQ_{j-1} released it)
+        const uint32_t na = sbase + L::kYa + ((j + 1) & 1) * L::kYStage, nb = na + 2 * L::kYPiece;
+        PreH<D, BN, 2> vp;
+        vp.load(v + hd, b0, k0 + BN, nv, rs, tid);
+        stage_splith<D, BN, 2>(k + hd, b0, k0 + BN, nv, rs, na, sk);
+        vp.store(nb, tid, sv);
       }
       tc::mbar_wait(bar_s, ph);
       tc::tc_fence_after();
@@ -1150,7 +1160,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
 #pragma unroll
         for (int c = 0; c < 3; ++c) {  // dQ += dS2K1 + dS1K2 + dS1K1
           const uint32_t pa = t_s + kPa[c] * 32;
-          const uint32_t kb = sbase + L::kYa + kPb[c] * L::kYPiece;
+          const uint32_t kb = ya + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             tc::mma_bf16_ts_warp(t_dq, pa + kk * 8, tc::sw128_desc(kb + kk * 16 * 128, L::kYChunk, 1024), kIdescQ,
@@ -1158,14 +1168,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
-      PreH<D, BN, 2> kpre;
-      if (j + 1 < nblk) {  // under dQ_j: split V_{j+1} (V_j is free) and load K_{j+1}
-        stage_splith<D, BN, 2>(v + hd, b0, k0 + BN, nv, rs, sbase + L::kYb, sv);
-        kpre.load(k + hd, b0, k0 + BN, nv, rs, tid);
-      }
       tc::mbar_wait(bar_o, ph);
       tc::tc_fence_after();
-      if (j + 1 < nblk) kpre.store(sbase + L::kYa, tid, sk);  // K_j is free
       if (j % kFlush == kFlush - 1 || j + 1 == nblk)
         ld_half_flush<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, fl_scale, j >= kFlush, r < seg);
       tc::tc_fence_before();
@@ -1430,6 +1434,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
     }
     for (int j = 0; j < nblk; ++j) {
       const int64_t y0 = (int64_t)j * BN;
+      const uint32_t ya = sbase + L::kYa + (j & 1) * L::kYStage, yb = sbase + L::kYb + (j & 1) * L::kYStage;
       if (tid < BN) {
         const bool in = y0 + tid < nv;
         ls[tid] = in ? lse[hr + b0 + y0 + tid] * kLog2e : 0.f;
@@ -1443,7 +1448,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
       if (warp == 0) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {  // S^T = K2Q1 + K1Q2 + K1Q1 (K pieces in TMEM)
-          const uint32_t qb = sbase + L::kYa + kPb[c] * L::kYPiece;
+          const uint32_t qb = ya + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             tc::mma_bf16_ts_warp(t_s, t_k + kPa[c] * (D / 2) + kk * 8,
@@ -1452,7 +1457,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {  // dP^T = V2dO1 + V1dO2 + V1dO1
-          const uint32_t va = s_v + kPa[c] * L::kXPiece, ob = sbase + L::kYb + kPb[c] * L::kYPiece;
+          const uint32_t va = s_v + kPa[c] * L::kXPiece, ob = yb + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             tc::mma_bf16_ss_warp(t_dp, tc::sw128_desc(va + (kk >> 2) * L::kXChunk + (kk & 3) * 32, 16, 1024),
@@ -1460,6 +1465,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
                                  (c > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit_warp(bar_s);
+      }
+      if (j + 1 < nblk) {  // under S^T_j / dP^T_j: split Q_{j+1}, dO_{j+1} into the other stage (dK_{j-1} released it)
+        const uint32_t na = sbase + L::kYa + ((j + 1) & 1) * L::kYStage, nb = na + 2 * L::kYPiece;
+        PreH<D, BN, 2> gp;
+        gp.load(go + hd, b0, y0 + BN, nv, rs, tid);
+        stage_splith<D, BN, 2>(q + hd, b0, y0 + BN, nv, rs, na, sq);
+        gp.store(nb, tid, sdo);
       }
       // P^T and dS^T on both warpgroups: warp half h takes queries [32h, 32h + 32) of its key quarter
       float dsv[32];  // dS^T, split into TMEM once P^T's MMAs are done
@@ -1494,7 +1506,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
       if (warp == 0) {  // dV += P2dO1 + P1dO2 + P1dO1 (B = dO_j MN-major)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const uint32_t ob = sbase + L::kYb + kPb[c] * L::kYPiece;
+          const uint32_t ob = yb + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             tc::mma_bf16_ts_warp(t_dv, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(ob + kk * 16 * 128, L::kYChunk, 1024),
@@ -1519,7 +1531,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
       if (warp == 0) {  // dK += dS2Q1 + dS1Q2 + dS1Q1 (B = Q_j MN-major)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const uint32_t qb = sbase + L::kYa + kPb[c] * L::kYPiece;
+          const uint32_t qb = ya + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             tc::mma_bf16_ts_warp(t_dk, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(qb + kk * 16 * 128, L::kYChunk, 1024),
@@ -1527,14 +1539,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
         }
         tc::mma_commit_warp(bar_o);
       }
-      PreH<D, BN, 2> qpre;
-      if (j + 1 < nblk) {  // under dK_j: split dO_{j+1} (dO_j is free) and load Q_{j+1}
-        stage_splith<D, BN, 2>(go + hd, b0, y0 + BN, nv, rs, sbase + L::kYb, sdo);
-        qpre.load(q + hd, b0, y0 + BN, nv, rs, tid);
-      }
       tc::mbar_wait(bar_o, ph_o);
       tc::tc_fence_after();
-      if (j + 1 < nblk) qpre.store(sbase + L::kYa, tid, sq);  // Q_j is free
       if (j % kFlush == kFlush - 1 || j + 1 == nblk) {
         ld_half_flush<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, fl_dv, j >= kFlush, r < seg);
         ld_half_flush<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, fl_dk, j >= kFlush, r < seg);
