@@ -1,4 +1,7 @@
-// attn_x3_sm100.cu — fp32 Jagged Flash Attention forward + backward on tcgen05 tensor cores (split-bf16 emulation).
+// attn_x3_sm100.cu — fp32 Jagged Flash Attention forward + backward on tcgen05 tensor cores (split emulation).
+//
+// Two splits: the default fp16 two-piece kernels (x2h, further below: per-tensor power-of-two scales, three MMAs per
+// product) and the bf16 three-piece kernels described first (JG_FP32_X3=1: no scales, six MMAs per product).
 //
 // Semantics: attention.cpp:172-289 in fp32 mode (the reference's float instantiation, attention.cpp:311-331),
 // same outputs as the tiled FFMA kernels in attn_simt.cu up to fp32 rounding.
