@@ -361,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
         fp32 = {"fwd_ms": f_ms, "bwd_ms": b_ms, "ms_per_step": f_ms + b_ms,
                 "tflops": (fwd_fl + bwd_fl) / ((f_ms + b_ms) * 1e-3) / 1e12,
                 "x_bf16_step": (f_ms + b_ms) / (elapsed_ms / args.steps),
-                "path": "tcgen05 split-bf16 emulation (attn_x3_sm100.cu), fp32 in/out, 2 timed steps"}
+                "path": "tcgen05 fp16 two-piece emulation (attn_x3_sm100.cu; JG_FP32_X3=1: bf16 three-piece), fp32 in/out, 2 timed steps"}
         del Qf, Kf, Vf, Gf, schf
 
     t = torch.tensor([elapsed_ms, e2e_s], dtype=torch.float64, device=dev)
