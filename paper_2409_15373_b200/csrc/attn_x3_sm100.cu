@@ -803,27 +803,29 @@ struct BwdLay {
 // output rows (owned by this item: no races, fixed order) — the tensor core's truncating fp32 accumulation would
 // otherwise lose ~2^-23 of the running sum per MMA over thousands of MMAs (measured 5e-6 norm-wise at 1,500 rows).
 constexpr int kFlush = 4;
+constexpr int kFlushH = 8;  // fp16 two-piece kernels: 3 MMAs per product, so twice the blocks per flush for the same drift
 
 // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows inside the segment store.
 // dst (+)= scale * acc (add = false: the first flush of the item stores).
 template <int D>
 __device__ __forceinline__ void ld_half_flush(uint32_t t_acc, uint32_t lane_off, int half, float* __restrict__ dst,
                                               float scale, bool add, bool store) {
+  float4* d4 = reinterpret_cast<float4*>(dst + half * (D / 2));
+  float4 y[D / 8];  // the previous partial sums: every load in flight before any store
+#pragma unroll
+  for (int q = 0; q < D / 8; ++q) y[q] = (add && store) ? d4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int c0 = 0; c0 < D / 2; c0 += 32) {
     uint32_t r[32];
     tc::tmem_ld32(t_acc + lane_off + half * (D / 2) + c0, r);
-    float4* d4 = reinterpret_cast<float4*>(dst + half * (D / 2) + c0);
-    float4 y[8];  // the previous partial sums: all eight loads in flight before any store (no aliasing stalls)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) y[q] = (add && store) ? d4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     tc::tmem_wait_ld();
     if (!store) continue;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int jj = 4 * q;
-      d4[q] = make_float4(fmaf(__uint_as_float(r[jj]), scale, y[q].x), fmaf(__uint_as_float(r[jj + 1]), scale, y[q].y),
-                          fmaf(__uint_as_float(r[jj + 2]), scale, y[q].z), fmaf(__uint_as_float(r[jj + 3]), scale, y[q].w));
+      const float4 o = y[c0 / 4 + q];
+      d4[c0 / 4 + q] = make_float4(fmaf(__uint_as_float(r[jj]), scale, o.x), fmaf(__uint_as_float(r[jj + 1]), scale, o.y),
+                                   fmaf(__uint_as_float(r[jj + 2]), scale, o.z), fmaf(__uint_as_float(r[jj + 3]), scale, o.w));
     }
   }
 }
@@ -1167,14 +1169,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             tc::mma_bf16_ts_warp(t_dq, pa + kk * 8, tc::sw128_desc(kb + kk * 16 * 128, L::kYChunk, 1024), kIdescQ,
-                                 (j % kFlush != 0 || c > 0 || kk > 0) ? 1u : 0u);
+                                 (j % kFlushH != 0 || c > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit_warp(bar_o);
       }
       tc::mbar_wait(bar_o, ph);
       tc::tc_fence_after();
-      if (j % kFlush == kFlush - 1 || j + 1 == nblk)
-        ld_half_flush<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, fl_scale, j >= kFlush, r < seg);
+      if (j % kFlushH == kFlushH - 1 || j + 1 == nblk)
+        ld_half_flush<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, fl_scale, j >= kFlushH, r < seg);
       tc::tc_fence_before();
       ph ^= 1;
     }
@@ -1513,7 +1515,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             tc::mma_bf16_ts_warp(t_dv, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(ob + kk * 16 * 128, L::kYChunk, 1024),
-                                 kIdescO, (j % kFlush != 0 || c > 0 || kk > 0) ? 1u : 0u);
+                                 kIdescO, (j % kFlushH != 0 || c > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit_warp(bar_o);
       }
@@ -1538,15 +1540,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             tc::mma_bf16_ts_warp(t_dk, t_s + kPa[c] * 32 + kk * 8, tc::sw128_desc(qb + kk * 16 * 128, L::kYChunk, 1024),
-                                 kIdescO, (j % kFlush != 0 || c > 0 || kk > 0) ? 1u : 0u);
+                                 kIdescO, (j % kFlushH != 0 || c > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit_warp(bar_o);
       }
       tc::mbar_wait(bar_o, ph_o);
       tc::tc_fence_after();
-      if (j % kFlush == kFlush - 1 || j + 1 == nblk) {
-        ld_half_flush<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, fl_dv, j >= kFlush, r < seg);
-        ld_half_flush<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, fl_dk, j >= kFlush, r < seg);
+      if (j % kFlushH == kFlushH - 1 || j + 1 == nblk) {
+        ld_half_flush<D>(t_dv, lane_off, half, dv + (b0 + r) * rs + hd, fl_dv, j >= kFlushH, r < seg);
+        ld_half_flush<D>(t_dk, lane_off, half, dk + (b0 + r) * rs + hd, fl_dk, j >= kFlushH, r < seg);
       }
       tc::tc_fence_before();
       ph_o ^= 1;
