@@ -803,6 +803,7 @@ struct BwdLay {
 // output rows (owned by this item: no races, fixed order) — the tensor core's truncating fp32 accumulation would
 // otherwise lose ~2^-23 of the running sum per MMA over thousands of MMAs (measured 5e-6 norm-wise at 1,500 rows).
 constexpr int kFlush = 4;
+constexpr int kFlushQ = 16;  // x2h dQ pass: two alternating accumulators, each flushed after 8 of its blocks
 constexpr int kFlushH = 8;  // fp16 two-piece kernels: 3 MMAs per product, so twice the blocks per flush for the same drift
 
 // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only rows inside the segment store.
@@ -826,6 +827,35 @@ __device__ __forceinline__ void ld_half_flush(uint32_t t_acc, uint32_t lane_off,
       const float4 o = y[c0 / 4 + q];
       d4[c0 / 4 + q] = make_float4(fmaf(__uint_as_float(r[jj]), scale, o.x), fmaf(__uint_as_float(r[jj + 1]), scale, o.y),
                                    fmaf(__uint_as_float(r[jj + 2]), scale, o.z), fmaf(__uint_as_float(r[jj + 3]), scale, o.w));
+    }
+  }
+}
+
+// dst (+)= scale * (acc0 + acc1) (acc1 only when it was written in this flush group)
+template <int D>
+__device__ __forceinline__ void ld_half_flush2(uint32_t t_a, uint32_t t_b, bool use_b, uint32_t lane_off, int half,
+                                               float* __restrict__ dst, float scale, bool add, bool store) {
+  float4* d4 = reinterpret_cast<float4*>(dst + half * (D / 2));
+  float4 y[D / 8];
+#pragma unroll
+  for (int q = 0; q < D / 8; ++q) y[q] = (add && store) ? d4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int c0 = 0; c0 < D / 2; c0 += 32) {
+    uint32_t ra[32], rb[32];
+    tc::tmem_ld32(t_a + lane_off + half * (D / 2) + c0, ra);
+    tc::tmem_ld32(t_b + lane_off + half * (D / 2) + c0, rb);
+    tc::tmem_wait_ld();
+    if (!store) continue;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int jj = 4 * q;
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        v[e] = __uint_as_float(ra[jj + e]) + (use_b ? __uint_as_float(rb[jj + e]) : 0.f);
+      const float4 o = y[c0 / 4 + q];
+      d4[c0 / 4 + q] = make_float4(fmaf(v[0], scale, o.x), fmaf(v[1], scale, o.y), fmaf(v[2], scale, o.z),
+                                   fmaf(v[3], scale, o.w));
     }
   }
 }
@@ -1063,6 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // two dQ accumulators alternate by block (each sees half the MMAs between flushes: half the truncation drift)
   const uint32_t t_q = tmem, t_s = tmem + D, t_dp = t_s + 64, t_dq = t_dp + 64;
   const float sq = pow2_scale(amax[0]), sk = pow2_scale(amax[1]), sv = pow2_scale(amax[2]), sdo = pow2_scale(amax[3]);
   const float sds = pow2_scale(2.f * D * amax[3] * amax[2]);  // |dS| <= 2 max||dO|| max||V||
@@ -1168,15 +1199,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dq_kernel(
           const uint32_t kb = ya + kPb[c] * L::kYPiece;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
-            tc::mma_bf16_ts_warp(t_dq, pa + kk * 8, tc::sw128_desc(kb + kk * 16 * 128, L::kYChunk, 1024), kIdescQ,
-                                 (j % kFlushH != 0 || c > 0 || kk > 0) ? 1u : 0u);
+            tc::mma_bf16_ts_warp(t_dq + (j & 1) * D, pa + kk * 8, tc::sw128_desc(kb + kk * 16 * 128, L::kYChunk, 1024),
+                                 kIdescQ, (j % kFlushQ >= 2 || c > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit_warp(bar_o);
       }
       tc::mbar_wait(bar_o, ph);
       tc::tc_fence_after();
-      if (j % kFlushH == kFlushH - 1 || j + 1 == nblk)
-        ld_half_flush<D>(t_dq, lane_off, half, dq + (b0 + r) * rs + hd, fl_scale, j >= kFlushH, r < seg);
+      if (j % kFlushQ == kFlushQ - 1 || j + 1 == nblk)
+        ld_half_flush2<D>(t_dq, t_dq + D, j % kFlushQ >= 1, lane_off, half, dq + (b0 + r) * rs + hd, fl_scale,
+                          j >= kFlushQ, r < seg);
       tc::tc_fence_before();
       ph ^= 1;
     }
