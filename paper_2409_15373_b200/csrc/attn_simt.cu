@@ -584,12 +584,12 @@ static jg_status bwd_t(const int64_t* off, int64_t batch, int64_t total_rows, in
                        int64_t max_items, const int64_t* valid, bool x3, cudaStream_t st) {
   const int64_t units = total_rows * H;
   const int sms = device_sm_count();
+  if (x3 && items)  // fp32 on tcgen05 (attn_x3_sm100.cu; it computes Delta together with its operand maxima)
+    return launch_attn_bwd_x3(off, total_rows, H, D, q, k, v, go, o, lse, delta, dq, dk, dv, items, n_items,
+                              max_items, valid, st);
   attn_delta_kernel<T><<<(int)std::min<int64_t>((units + 7) / 8, 16 * sms), 256, 0, st>>>(
       units, H, D, (const T*)go, (const T*)o, total_rows, delta);
   JG_LAUNCHED("attn_delta_kernel");
-  if (x3 && items)  // fp32 on tcgen05 (attn_x3_sm100.cu)
-    return launch_attn_bwd_x3(off, total_rows, H, D, q, k, v, go, lse, delta, dq, dk, dv, items, n_items, max_items,
-                              valid, st);
   static const bool rowwise = std::getenv("JG_SIMT_ROWWISE") != nullptr;  // A/B knob: the row-per-warp kernels
   if (items && !rowwise) {
     if (D == 32)

@@ -512,6 +512,31 @@ struct Lay2 {
   static constexpr int kTmemCols = D == 128 ? 512 : 256;
 };
 
+// Delta = rowsum(dO * O) in fp64 (as attn_delta_kernel) fused with max |dO| into amax_go (the x2h scales)
+__global__ void delta_amax_kernel(int64_t units, int D, const float* __restrict__ go, const float* __restrict__ o,
+                                  int H, int64_t total_rows, float* __restrict__ delta, unsigned* __restrict__ amax_go) {
+  const int lane = threadIdx.x & 31;
+  float mx = 0.f;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < units;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = u / H;
+    const int h = (int)(u - r * H);
+    const int64_t base = u * D;
+    double acc = 0.0;
+    for (int d = lane; d < D; d += 32) {
+      const float g = go[base + d];
+      mx = fmaxf(mx, fabsf(g));
+      acc = fma((double)g, (double)o[base + d], acc);
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (lane == 0) delta[(int64_t)h * total_rows + r] = (float)acc;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  if (lane == 0 && mx > 0.f) atomicMax(amax_go, __float_as_uint(mx));
+}
+
 // max |x| of up to three fp32 tensors of n elements (n % 4 == 0) into amax[0..2] (zeroed; floats as ordered ints)
 __global__ void absmax3_kernel(const float4* __restrict__ a, const float4* __restrict__ b, const float4* __restrict__ c,
                                int64_t n4, unsigned* __restrict__ amax) {
@@ -1599,25 +1624,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_x2h_dkdv_kernel(
 
 template <int D>
 static jg_status bwd_x3(const int64_t* off, int64_t total_rows, int H, const void* q, const void* k, const void* v,
-                        const void* go, const float* lse, const float* delta, void* dq, void* dk, void* dv,
+                        const void* go, const void* o, const float* lse, float* delta, void* dq, void* dk, void* dv,
                         const int2* items, const int64_t* n_items, int64_t max_items, const int64_t* valid,
                         cudaStream_t st) {
   static const bool bf16x3 = std::getenv("JG_FP32_X3") != nullptr;  // A/B knob: the bf16 three-piece kernels
-  if (!bf16x3) {  // fp16 two-piece kernels with per-tensor power-of-two scales (one max pass over q, k, v, dO)
+  // Delta = rowsum(dO * O) (fp64 accumulation) fused with the max |dO| the fp16 scales need
+  unsigned* amax = nullptr;
+  JG_CUDA(cudaMallocAsync(&amax, 16, st));
+  scratch_note(16);
+  JG_CUDA(cudaMemsetAsync(amax, 0, 16, st));
+  {
+    const int64_t units = total_rows * H;
+    delta_amax_kernel<<<(int)std::min<int64_t>((units + 7) / 8, 16 * device_sm_count()), 256, 0, st>>>(
+        units, D, (const float*)go, (const float*)o, H, total_rows, delta, amax + 3);
+    JG_LAUNCHED("delta_amax_kernel");
+  }
+  struct FreeAmax {
+    unsigned* p;
+    cudaStream_t s;
+    ~FreeAmax() {
+      cudaFreeAsync(p, s);
+      scratch_note(-16);
+    }
+  } free_amax{amax, st};
+  if (!bf16x3) {  // fp16 two-piece kernels with per-tensor power-of-two scales (one max pass over q, k, v)
     const int sm_q2 = std::max<int>(BwdLay2<D, false>::kAlloc, 120 * 1024);
     const int sm_kv2 = std::max<int>(BwdLay2<D, true>::kAlloc, 120 * 1024);
     if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_x2h_dq_kernel<D>, sm_q2, "attn_bwd_x2h_dq_kernel"))
       return rc;
     if (jg_status rc = ensure_smem_attr((const void*)attn_bwd_x2h_dkdv_kernel<D>, sm_kv2, "attn_bwd_x2h_dkdv_kernel"))
       return rc;
-    unsigned* amax = nullptr;
-    JG_CUDA(cudaMallocAsync(&amax, 16, st));
-    scratch_note(16);
-    JG_CUDA(cudaMemsetAsync(amax, 0, 16, st));
     const int64_t n4 = total_rows * H * D / 4;
     const int mg = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 4 * device_sm_count()));
     absmax3_kernel<<<mg, 256, 0, st>>>((const float4*)q, (const float4*)k, (const float4*)v, n4, amax);
-    absmax3_kernel<<<mg, 256, 0, st>>>((const float4*)go, nullptr, nullptr, n4, amax + 3);
     JG_LAUNCHED("absmax3_kernel");
     const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>(max_items * H, (int64_t)device_sm_count()));
     const float scale2 = 1.0f / sqrtf((float)D);
@@ -1629,8 +1668,6 @@ static jg_status bwd_x3(const int64_t* off, int64_t total_rows, int H, const voi
         off, items, n_items, H, total_rows, (const float*)q, (const float*)k, (const float*)v, (const float*)go, lse,
         delta, (float*)dk, (float*)dv, kLog2e * scale2, scale2, valid, (const float*)amax);
     JG_LAUNCHED("attn_bwd_x2h_dkdv_kernel");
-    cudaFreeAsync(amax, st);
-    scratch_note(-16);
     return JG_OK;
   }
   // at least half the SM's shared memory: one CTA per SM, since each allocates all 512 TMEM columns
@@ -1669,15 +1706,15 @@ jg_status launch_attn_fwd_x3(const int64_t* off, int64_t total_rows, int H, int 
 }
 
 jg_status launch_attn_bwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
-                             const void* v, const void* go, const float* lse, const float* delta, void* dq, void* dk,
+                             const void* v, const void* go, const void* o, const float* lse, float* delta, void* dq, void* dk,
                              void* dv, const int2* items, const int64_t* n_items, int64_t max_items,
                              const int64_t* valid, cudaStream_t st) {
   if (total_rows == 0) return JG_OK;
   if (D == 64)
-    return x3::bwd_x3<64>(off, total_rows, H, q, k, v, go, lse, delta, dq, dk, dv, items, n_items, max_items, valid,
+    return x3::bwd_x3<64>(off, total_rows, H, q, k, v, go, o, lse, delta, dq, dk, dv, items, n_items, max_items, valid,
                           st);
   if (D == 128)
-    return x3::bwd_x3<128>(off, total_rows, H, q, k, v, go, lse, delta, dq, dk, dv, items, n_items, max_items, valid,
+    return x3::bwd_x3<128>(off, total_rows, H, q, k, v, go, o, lse, delta, dq, dk, dv, items, n_items, max_items, valid,
                            st);
   return fail(JG_UNSUPPORTED, "jagged_flash_attention_backward: split-bf16 path needs head_dim 64 or 128");
 }

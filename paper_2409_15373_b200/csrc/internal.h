@@ -133,7 +133,7 @@ jg_status launch_attn_fwd_x3(const int64_t* off, int64_t total_rows, int H, int 
                              const void* v, void* out, float* lse, const int2* items, const int64_t* n_items,
                              int64_t max_items, const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_x3(const int64_t* off, int64_t total_rows, int H, int D, const void* q, const void* k,
-                             const void* v, const void* go, const float* lse, const float* delta, void* dq, void* dk,
+                             const void* v, const void* go, const void* o, const float* lse, float* delta, void* dq, void* dk,
                              void* dv, const int2* items, const int64_t* n_items, int64_t max_items,
                              const int64_t* valid, cudaStream_t st);
 jg_status launch_attn_bwd_simt(const int64_t* off, int64_t batch, int64_t total_rows, int H, int D,
