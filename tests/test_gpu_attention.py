@@ -322,3 +322,29 @@ def test_full_size_cfg3_fp32_tensor_core_path():
     scale = segsum(go.abs()).clamp_min(1.0)
     assert float(((sdv - sdo).abs() / scale).max()) < 1e-5, "sum_k dV != sum_q dO"
     assert float((sdk.abs() / segsum(gr.dk.values.abs()).clamp_min(1.0)).max()) < 1e-5, "sum_k dK != 0"
+
+
+@pytest.mark.parametrize("scales", [(1e3, 1e-3, 1e2, 1e-2), (1e-3, 1e3, 1e-4, 1e4), (3e-2, 30.0, 5e3, 2e-3)])
+def test_fp32_tensor_core_path_operand_magnitudes(scales):
+    """The fp16 two-piece path rescales every operand by a power of two before splitting (fp16 covers ~6e-5 .. 65504):
+    q, k, v, dO of very different magnitudes must still match an fp64 torch reference at the fp32 tolerance."""
+    sq, sk, sv, sg = scales
+    ln = np.array([300, 1, 129, 0, 64], np.int64)
+    off = R.make_offsets(ln)
+    S, H, D = int(off[-1]), 2, 128
+    g = torch.Generator(device=DEV).manual_seed(17)
+    q, k, v, go = ((torch.rand(S, H, D, device=DEV, generator=g) * 2 - 1) * s for s in (sq, sk, sv, sg))
+    # sq * sk = 1 keeps the scores q.k / sqrt(D) O(1): a saturated softmax would make dq / dk vanish (ill-conditioned)
+    T = lambda a: J.JaggedTensor(torch.from_numpy(off).to(DEV), a, off)  # noqa: E731
+    Q, K, V, G = T(q), T(k), T(v), T(go)
+    saved = J.jagged_flash_attention_forward(Q, K, V)
+    gr = J.jagged_flash_attention_backward(Q, K, V, G, saved)
+    for i in np.nonzero(ln)[0]:
+        a, b = int(off[i]), int(off[i + 1])
+        o, lse, dq, dk, dv = _dense_sample_ref64(q[a:b], k[a:b], v[a:b], go[a:b])
+        assert_fp32_close(saved.output.values[a:b], o.cpu().numpy(), what=f"out sample {i} scales {scales}")
+        assert_fp32_close(saved.logsumexp[:, a:b], lse.cpu().numpy(), what=f"lse sample {i}")
+        for got, ref, nm in ((gr.dq, dq, "dq"), (gr.dk, dk, "dk"), (gr.dv, dv, "dv")):
+            if b - a == 1 and nm != "dv":  # a one-row sample's dq / dk are exactly 0 in the reference
+                continue
+            assert_fp32_close(got.values[a:b], ref.cpu().numpy(), what=f"{nm} sample {i} scales {scales}")
