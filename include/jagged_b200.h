@@ -23,7 +23,8 @@
  *     taken; block_q/block_k of the flash forward are validated (>= 1) exactly as the reference does
  *     and otherwise ignored (device tiles are fixed at 128x128).
  *
- * dtypes: JG_F32 (SIMT fp32 FFMA, "fp32 mode"), JG_BF16 (tcgen05 tensor cores where shapes allow,
+ * dtypes: JG_F32 ("fp32 mode": attention on tcgen05 via an fp16 two-piece split at head_dim 64/128, FFMA
+ * otherwise and for the bmm family), JG_BF16 (tcgen05 tensor cores where shapes allow,
  * fp32 accumulation). JG_F64 returns JG_UNSUPPORTED: there is no CPU fallback.
  * Attention tensors carry heads: [total_rows, num_heads, head_dim] row-major (token-major, the
  * reference's single-head layout when num_heads == 1); lse is float32 [num_heads, total_rows].

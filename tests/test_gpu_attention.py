@@ -150,27 +150,31 @@ def test_unfused_matches_flash(dtype):
         assert_bf16_close(got, ref, tol=3e-2, what="unfused (bf16 scores materialized)")
 
 
-def test_fwd_bwd_host_entry_matches_device_api():
-    """jg_jagged_flash_attention_fwd_bwd_host (pinned host buffers, chunked two-stream copy/compute pipeline)
-    gives the device API's results on every sample (the path bench.py's e2e measures)."""
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_fwd_bwd_host_entry_matches_device_api(dtype):
+    """jg_jagged_flash_attention_fwd_bwd_host (pinned host buffers, chunked three-stream copy/compute pipeline)
+    gives the device API's results on every sample (the path bench.py's e2e measures); fp32 runs the tcgen05
+    fp16 two-piece kernels on concurrent streams."""
     from paper_2409_15373_b200 import _lib
     ln = list(R.gen_lengths("half-mean", 300, 4, 40))
     H, D = 2, 128
-    off, (q, k, v, go), (Q, K, V, G) = make(ln, H, D, 9, torch.bfloat16)
+    off, (q, k, v, go), (Q, K, V, G) = make(ln, H, D, 9, dtype)
     saved = J.jagged_flash_attention_forward(Q, K, V)
     grads = J.jagged_flash_attention_backward(Q, K, V, G, saved)
     S = int(off[-1])
-    host = [torch.from_numpy(a).to(torch.bfloat16).pin_memory() for a in (q, k, v, go)]
-    outs = [torch.empty(S, H, D, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    host = [torch.from_numpy(a).to(dtype).pin_memory() for a in (q, k, v, go)]
+    outs = [torch.empty(S, H, D, dtype=dtype).pin_memory() for _ in range(4)]
     lse = torch.empty(H, S, dtype=torch.float32).pin_memory()
     hoff = np.ascontiguousarray(off, np.int64)
     _lib.check(_lib.lib().jg_jagged_flash_attention_fwd_bwd_host(
         hoff.ctypes.data, len(ln), H, D, *(t.data_ptr() for t in host), outs[0].data_ptr(), lse.data_ptr(),
-        outs[1].data_ptr(), outs[2].data_ptr(), outs[3].data_ptr(), 1, None))
-    assert_bf16_close(outs[0], saved.output.values.float().cpu().numpy(), tol=1e-2, what="out")
+        outs[1].data_ptr(), outs[2].data_ptr(), outs[3].data_ptr(), 1 if dtype == torch.bfloat16 else 0, None))
+    close = assert_bf16_close if dtype == torch.bfloat16 else assert_fp32_close
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-5
+    close(outs[0], saved.output.values.double().cpu().numpy(), tol=tol, what="out")
     np.testing.assert_allclose(lse.numpy(), saved.logsumexp.cpu().numpy(), rtol=1e-5, atol=1e-4)
     for got, ref, name in zip(outs[1:], (grads.dq, grads.dk, grads.dv), ("dq", "dk", "dv")):
-        assert_bf16_close(got, ref.values.float().cpu().numpy(), tol=1e-2, what=name)
+        close(got, ref.values.double().cpu().numpy(), tol=tol, what=name)
 
 
 def test_unfused_tensor_core_path_multihead():
